@@ -1,0 +1,537 @@
+#!/usr/bin/env python
+"""Benchmark of the DASH per-update step on B200 (BASELINE.json metric:
+"update-step latency and X elements/s at 1/2/4/8 B200; % of HBM roofline").
+
+Workload: the "large" stream of BASELINE.json configs[3] -- K0 = 50,000 slices,
+J = 128, R = 16, FP64, lambda = 0.95; every update appends U[1,8] rows to every
+active slice and registers 500 new slices of U[200,2000] rows (~0.79 M rows,
+~0.81 GB of X per update).  Synthetic data from the planted generator
+(workloads.py), drawn on the device; initial state planted in closed form.
+
+A "step" = one StreamState update (all kernels of the pass loop) over one
+batch already resident in HBM.  value = X elements (N*J) processed per second
+over the timed steps (whole job; max-over-ranks device time).  ms_per_step is
+the update-step latency.  Each step's batch is 0.81 GB > 126 MB L2, so the
+timed loop never re-reads a cached input ("inputs larger than L2").
+
+e2e: the same metric through the public API with host buffers: pinned host X
+-> H2D -> update -> D2H of U_new and v_used, all inside the timed region.
+
+--impl reference: the reference algorithm on the host CPU (oracle/ port of
+p2stream's update: numpy/OpenBLAS + the C restatement of the numba kernel),
+same workload and metric, rank 0 only.
+
+Multi-GPU (torchrun): slices are partitioned over ranks (slice k -> rank
+k % world); each rank runs the per-slice phase on its shard and the F/G fresh
+sums are all-reduced with NCCL once per pass before the replicated V solve
+(strong scaling: the total stream is fixed).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIG_NAME = "large"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="dash", choices=["dash", "reference"])
+    ap.add_argument("--config", default=CONFIG_NAME)
+    ap.add_argument("--K0", type=int, default=None, help="override K0 (smoke runs)")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=2)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# stream schedule shared by both arms (host RNG; identical for every rank)
+# ---------------------------------------------------------------------------
+class Schedule:
+    def __init__(self, cfg, steps, seed):
+        self.cfg = cfg
+        rng = np.random.default_rng([seed, 11])
+        from paper_2305_18376_b200.workloads import _draw
+        self.adds, self.new_len = [], []
+        active = cfg.K0
+        for _ in range(steps):
+            self.adds.append(_draw(rng, cfg.add_rows, active).astype(np.int64))
+            L = int(_draw(rng, cfg.new_slices, 1)[0])
+            self.new_len.append(_draw(rng, cfg.new_rows, L).astype(np.int64))
+            active += L
+
+
+def owned(k, rank, world):
+    return k % world == rank
+
+
+def algorithmic_bytes(N, J, R, M_old, L, b=8):
+    """bytes of one update (read X once, write U, per-slice
+    state r/w, new-slice state, F/V/G)."""
+    return b * (N * J + N * R + 2 * M_old * (R * R + 2 * R) + L * (R * R + 2 * R)
+                + 3 * J * R + 2 * R * R)
+
+
+def algorithmic_flops(N, J, R, M):
+    return 4 * N * J * R + N * (3 * R * R + 2 * R) + M * (4 * R ** 3 / 3 + 4 * R * R)
+
+
+def kernel_bytes(phase, N, J, R, M_old, L, nsplit, b=8):
+    """Algorithmic bytes per launch of each kernel (DESIGN.md table)."""
+    if phase == "xv":
+        return b * (N * J + N * R + J * R)
+    if phase == "fgemm":
+        return b * (N * J + N * R + nsplit * J * R) + 4 * N + b * (M_old + L) * R
+    if phase == "slices":
+        return b * (2 * N * R + 2 * M_old * (R * R + 2 * R) + L * (R * R + 2 * R))
+    if phase == "fused":
+        return algorithmic_bytes(N, J, R, M_old, L, b)
+    return 0
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def ncu_traffic(phase):
+    """dram bytes per launch from a committed `ncu --set full` capture."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    return d.get(phase)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2305_18376_b200 import _native as nat
+    from paper_2305_18376_b200 import workloads as wl
+    from paper_2305_18376_b200.distributed import ShardedStream
+    from paper_2305_18376_b200.stream import StreamState
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = wl.CONFIGS[args.config]
+    if args.K0:
+        cfg = wl.scaled(cfg, K0=args.K0)
+    J, R = cfg.J, cfg.R
+    total_steps = args.warmup + args.steps + args.e2e_steps
+    sched = Schedule(cfg, total_steps, cfg.seed)
+    H, V = wl.true_factors(cfg)
+    # true per-slice weights for every slice that will ever exist
+    n_all = cfg.K0 + sum(len(n) for n in sched.new_len)
+    w_true = np.random.default_rng([cfg.seed, 12]).uniform(size=(n_all, R))
+    # planted initial state (closed form, see workloads.planted_state) for owned slices
+    own0 = np.array([k for k in range(cfg.K0) if owned(k, rank, world)], dtype=np.int64)
+    D0 = H.T @ H
+    vtv = V.T @ V
+    Wl = w_true[own0]
+    G_all = np.einsum("kr,rz,kz->rz", w_true[:cfg.K0], D0, w_true[:cfg.K0])
+    G_all = (G_all + G_all.T) / 2.0
+    arrays = {
+        "slice_ids": [wl.slice_id(int(k)) for k in own0],
+        "W": Wl, "V": V, "C": np.einsum("rz,kz,zr->kr", D0, Wl, vtv),
+        "D": np.broadcast_to(D0, (len(own0), R, R)).copy(),
+        "F": V @ G_all, "G": G_all, "forgetting": cfg.forgetting, "passes": cfg.passes,
+    }
+    state = StreamState.from_arrays(arrays, device=dev)
+    engine = ShardedStream(state, rank=rank, world=world) if world > 1 else None
+
+    Hd = torch.as_tensor(H, device=dev)
+    Vd = torch.as_tensor(V, device=dev)
+    wd = torch.as_tensor(w_true, device=dev)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(cfg.seed * 1000 + 17)
+
+    # per-step local batches, generated on the device before timing
+    active = list(range(cfg.K0))
+    local_row = {int(k): i for i, k in enumerate(own0)}  # global slice -> local state row
+    batches = []
+    for t in range(total_steps):
+        add = sched.adds[t]
+        ex = [k for k in active if owned(k, rank, world)]
+        ex_counts = add[np.array(ex, dtype=np.int64)] if ex else np.zeros(0, np.int64)
+        base = len(active)
+        new = [base + i for i in range(len(sched.new_len[t])) if owned(base + i, rank, world)]
+        new_counts = sched.new_len[t][np.array(new, dtype=np.int64) - base] if new else np.zeros(0, np.int64)
+        active.extend(range(base, base + len(sched.new_len[t])))
+        ex_rows = np.array([local_row[k] for k in ex], dtype=np.int32)
+        for k in new:
+            local_row[k] = len(local_row)
+        counts = np.concatenate([ex_counts, new_counts]).astype(np.int64)
+        slices_of_rows = torch.as_tensor(np.repeat(np.array(ex + new, dtype=np.int64), counts), device=dev)
+        N = int(counts.sum())
+        q = torch.randn((N, R), generator=gen, device=dev, dtype=torch.float64) / np.sqrt(1100.0)
+        X = ((q @ Hd) * wd[slices_of_rows]) @ Vd.T
+        X += 0.1 * torch.randn((N, J), generator=gen, device=dev, dtype=torch.float64)
+        del q, slices_of_rows
+        batches.append({"X": X, "counts": counts, "ex_rows": ex_rows, "new": [wl.slice_id(k) for k in new],
+                        "N": N, "M_old": len(ex), "L": len(new)})
+
+    def step(b):
+        if engine is not None:
+            return engine.update_packed(b["X"], b["counts"], b["ex_rows"], b["new"])
+        return state.update_packed(b["X"], b["counts"], b["ex_rows"], b["new"])
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # warm-up
+    for t in range(args.warmup):
+        step(batches[t])
+    torch.cuda.synchronize()
+    state.check()
+
+    # timed region (device-resident batches)
+    L = nat.lib()
+    timed = batches[args.warmup:args.warmup + args.steps]
+    sampler = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    L.dash_ctx_set_profiling(state._ctx, 1)
+    sampler.start()
+    time.sleep(0.3)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
+    e0.record(stream)
+    for b in timed:
+        step(b)
+        launches += state.last_launches
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    import ctypes
+    nph = len(nat.PHASES)
+    ms_arr = (ctypes.c_double * nph)()
+    cnt_arr = (ctypes.c_int32 * nph)()
+    L.dash_ctx_phase_ms(state._ctx, ms_arr, cnt_arr, nph)
+    L.dash_ctx_set_profiling(state._ctx, 0)
+    state.check()
+    t_ms = e1.elapsed_time(e0) if False else e0.elapsed_time(e1)
+    t_max = t_ms
+    if world > 1:
+        tt = torch.tensor([t_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+    elems_local = sum(b["N"] for b in timed) * J
+    elems = elems_local
+    if world > 1:
+        te = torch.tensor([elems_local], device=dev, dtype=torch.float64)
+        dist.all_reduce(te)
+        elems = float(te.item())
+    value = elems / (t_max / 1e3)
+    ms_per_step = t_max / len(timed)
+
+    # e2e through the public API with host buffers
+    e2e_b = batches[args.warmup + args.steps:]
+    pins = []
+    for b in e2e_b:
+        hp = torch.empty_like(b["X"], device="cpu").pin_memory()
+        hp.copy_(b["X"])
+        pins.append(hp)
+    Uh = torch.empty((max(b["N"] for b in e2e_b), R), dtype=torch.float64).pin_memory() if e2e_b else None
+    vh = torch.empty((J, R), dtype=torch.float64).pin_memory()
+    Xd = torch.empty((max((b["N"] for b in e2e_b), default=1), J), dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
+    barrier()
+    h2d = d2h = 0
+    e2 = torch.cuda.Event(enable_timing=True)
+    e3 = torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for b, hp in zip(e2e_b, pins):
+        N = b["N"]
+        Xd[:N].copy_(hp, non_blocking=True)
+        b2 = dict(b, X=Xd[:N])
+        U, vu = step(b2)
+        Uh[:N].copy_(U, non_blocking=True)
+        vh.copy_(vu, non_blocking=True)
+        h2d += N * J * 8 + (b["M_old"] + b["L"]) * (8 + 4 + 1) + 8
+        d2h += N * R * 8 + J * R * 8
+    e3.record(stream)
+    torch.cuda.synchronize()
+    state.check()
+    e2e_ms = e2.elapsed_time(e3)
+    if world > 1:
+        tt = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e_elems = sum(b["N"] for b in e2e_b) * J
+    if world > 1:
+        te = torch.tensor([e2e_elems], device=dev, dtype=torch.float64)
+        dist.all_reduce(te)
+        e2e_elems = float(te.item())
+    e2e_value = e2e_elems / (e2e_ms / 1e3) if e2e_b else None
+
+    # roofline of the dominant kernel
+    phase_ms = {nat.PHASES[i]: ms_arr[i] for i in range(nph)}
+    phase_n = {nat.PHASES[i]: cnt_arr[i] for i in range(nph)}
+    dom = max(phase_ms, key=lambda k: phase_ms[k])
+    nb = len(timed)
+    N_avg = sum(b["N"] for b in timed) / nb
+    M_old_avg = sum(b["M_old"] for b in timed) / nb
+    L_avg = sum(b["L"] for b in timed) / nb
+    nsplit = int(np.clip(np.ceil(N_avg / 1024), 1, 148 * 4 // ((J + 63) // 64) + 1))
+    peak, peak_kind = peaks()
+    per_launch_ms = phase_ms[dom] / max(phase_n[dom], 1)
+    kb = kernel_bytes(dom, N_avg, J, R, M_old_avg, L_avg, nsplit)
+    achieved = kb / (per_launch_ms / 1e3) / 1e9
+    step_bytes = algorithmic_bytes(N_avg, J, R, M_old_avg, L_avg)
+    step_achieved = step_bytes / (ms_per_step / 1e3) / 1e9
+
+    out = None
+    if rank == 0:
+        out = {
+            "metric": f"X elements/s of the DASH update step ({cfg.name} stream, FP64)",
+            "value": value, "unit": "elements/s", "n_gpus": world, "steps": len(timed),
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (planted low-rank + N(0,0.1) noise, drawn on device; planted initial state)",
+            "config": {"workload": f"{cfg.name}: K0={cfg.K0} slices, J={J}, R={R}, lambda={cfg.forgetting}, "
+                                   f"+U[1,8] rows/slice and 500 new slices of U[200,2000] rows per update",
+                       "rows_per_update": N_avg, "slices_per_update": M_old_avg + L_avg,
+                       "passes": cfg.passes, "l2": "inputs larger than L2 (0.8 GB per step)",
+                       "parallelism": f"slice-sharded x{world}"},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": ncu_traffic(dom),
+                         "peak_source": peak_kind, "per_launch_ms": per_launch_ms,
+                         "alg_bytes_per_launch": kb},
+            "step_roofline": {"alg_bytes": step_bytes, "achieved_gbs": step_achieved,
+                              "frac": step_achieved / peak,
+                              "alg_flops": algorithmic_flops(N_avg, J, R, M_old_avg + L_avg),
+                              "tflops": algorithmic_flops(N_avg, J, R, M_old_avg + L_avg) / (ms_per_step / 1e3) / 1e12},
+            "phase_ms_per_step": {k: v / nb for k, v in phase_ms.items() if phase_n[k]},
+            "e2e": {"value": e2e_value, "unit": "elements/s", "h2d_bytes_per_step": h2d / max(len(e2e_b), 1),
+                    "d2h_bytes_per_step": d2h / max(len(e2e_b), 1),
+                    "ms_per_step": e2e_ms / max(len(e2e_b), 1), "steps": len(e2e_b)},
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+    del batches
+    if world > 1:
+        dist.barrier()
+    return out, cfg
+
+
+# ---------------------------------------------------------------------------
+# CPU arms (oracle port of the reference)
+# ---------------------------------------------------------------------------
+def host_stream(cfg, steps, seed_extra=0):
+    """Planted state + host batches for the CPU reference (same law as the
+    device generator)."""
+    from paper_2305_18376_b200 import workloads as wl
+    from paper_2305_18376_b200.tensor import NewSlice, UpdateBatch
+    sched = Schedule(cfg, steps, cfg.seed)
+    H, V = wl.true_factors(cfg)
+    R, J = cfg.R, cfg.J
+    n_all = cfg.K0 + sum(len(n) for n in sched.new_len)
+    w_true = np.random.default_rng([cfg.seed, 12]).uniform(size=(n_all, R))
+    D0 = H.T @ H
+    vtv = V.T @ V
+    W0 = w_true[:cfg.K0]
+    G0 = np.einsum("kr,rz,kz->rz", W0, D0, W0)
+    G0 = (G0 + G0.T) / 2.0
+    arrays = {"slice_ids": [wl.slice_id(k) for k in range(cfg.K0)], "W": W0, "V": V,
+              "C": np.einsum("rz,kz,zr->kr", D0, W0, vtv),
+              "D": np.broadcast_to(D0, (cfg.K0, R, R)).copy(), "F": V @ G0, "G": G0,
+              "forgetting": cfg.forgetting}
+    rng = np.random.default_rng([cfg.seed, 13, seed_extra])
+
+    def batches():
+        active = cfg.K0
+        for t in range(steps):
+            add = sched.adds[t]
+            new = sched.new_len[t]
+            counts = np.concatenate([add, new])
+            N = int(counts.sum())
+            ks = np.repeat(np.arange(active + len(new)), counts)
+            q = rng.standard_normal((N, R)) / np.sqrt(1100.0)
+            X = ((q @ H) * w_true[ks]) @ V.T + 0.1 * rng.standard_normal((N, J))
+            offs = np.concatenate([[0], np.cumsum(counts)])
+            existing = {wl.slice_id(k): X[offs[k]:offs[k + 1]] for k in range(active)}
+            fresh = [NewSlice(wl.slice_id(active + i), X[offs[active + i]:offs[active + i + 1]], t + 1)
+                     for i in range(len(new))]
+            active += len(new)
+            yield UpdateBatch(t + 1, existing, fresh, (t + 1, t + 1)), N
+    return arrays, batches
+
+
+def oracle_state(arrays):
+    from oracle import dash_oracle as orc
+    R = arrays["V"].shape[1]
+    return orc.OracleStreamState(arrays["slice_ids"], {s: [] for s in arrays["slice_ids"]},
+                                 arrays["W"], arrays["V"], arrays["C"], arrays["D"], arrays["F"],
+                                 arrays["G"], arrays["forgetting"])
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        return max([i.get("num_threads", 1) for i in info] or [1])
+    except Exception:
+        return 1
+
+
+def time_oracle(cfg, warm, steps):
+    """Time the CPU oracle on `steps` full updates after `warm` warm-ups."""
+    from oracle import dash_oracle as orc
+    orc.build_c()
+    arrays, gen = host_stream(cfg, warm + steps)
+    st = oracle_state(arrays)
+    times, elems = [], 0
+    for t, (batch, N) in enumerate(gen()):
+        t0 = time.perf_counter()
+        st.update(batch)
+        dt = time.perf_counter() - t0
+        if t >= warm:
+            times.append(dt)
+            elems += N * cfg.J
+    return elems, sum(times), len(times)
+
+
+def cpu_baseline(cfg, steps):
+    elems, secs, n = time_oracle(cfg, 1, steps)
+    return {"value": elems / secs, "unit": "elements/s", "cores": blas_threads(), "kind": "port",
+            "sample": f"{n} full {cfg.name} updates after 1 warm-up (oracle: numpy/OpenBLAS + C port of "
+                      f"the numba group_update; the per-slice kernel is single-threaded, BLAS uses "
+                      f"{blas_threads()} threads); {secs:.1f} s of CPU work",
+            "ms_per_step": 1e3 * secs / n}
+
+
+def run_reference(args):
+    from paper_2305_18376_b200 import workloads as wl
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    cfg = wl.CONFIGS[args.config]
+    if args.K0:
+        cfg = wl.scaled(cfg, K0=args.K0)
+    elems, secs, n = time_oracle(cfg, args.warmup, args.steps)
+    value = elems / secs
+    cores = blas_threads()
+    return {
+        "metric": f"X elements/s of the DASH update step ({cfg.name} stream, FP64)",
+        "value": value, "unit": "elements/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+        "steps": n, "warmup": args.warmup, "ms_per_step": 1e3 * secs / n,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (planted low-rank + N(0,0.1) noise, host numpy)",
+        "config": {"workload": f"{cfg.name}: K0={cfg.K0}, J={cfg.J}, R={cfg.R}", "parallelism": "cpu"},
+        "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": "elements/s", "cores": cores, "kind": "port",
+                         "sample": f"{n} full {cfg.name} updates of the oracle port of p2stream "
+                                   f"StreamState.update (numpy/OpenBLAS {cores} threads + C port of the "
+                                   f"numba kernel, single-threaded)"},
+        "e2e": {"value": value, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        out = run_reference(args)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+    out, cfg = run_gpu(args)
+    if out is not None:
+        world = out["n_gpus"]
+        if world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(cfg, args.cpu_steps)
+        else:
+            out["cpu_baseline"] = None
+        print(json.dumps(out), flush=True)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,148 @@
+/*
+ * dash_b200.h -- C ABI of the B200-native DASH (dual-way streaming PARAFAC2)
+ * per-update step.  Built as paper_2305_18376_b200/libdash_b200.so (sm_100a).
+ *
+ * Conventions (all entry points):
+ *   - every array argument is a DEVICE pointer unless its name ends in _host;
+ *     row-major, FP64 ("f64" suffix); the caller (torch) owns all of them;
+ *   - the library owns only the workspace arena inside a dash_ctx;
+ *   - work is enqueued on the given cudaStream_t (passed as void*) and is
+ *     stream-ordered; nothing synchronises the host except
+ *     dash_ctx_status(), which waits for the stream and reads the error slot;
+ *   - return value: 0 on success, a DASH_E* code otherwise (launch / shape
+ *     errors are reported immediately, numerical failures via
+ *     dash_ctx_status() because they are only known on the device).
+ *
+ * Reference interfaces replaced (paths under /root/reference/pkg/src/p2stream):
+ *   dash_update_f64         StreamState.update pass loop     stream.py:251-370
+ *   dash_group_update_f64   numba group_update seam          _kernels.py:62-149
+ *   dash_ridge_solve_f64    ridge_solve (V solve, update_v)   linalg.py:25-45,
+ *                                                             stream.py:158-160,346
+ *   dash_init_helpers_f64   init_helpers                      stream.py:56-82
+ *   dash_local_error_f64    local_error / slice_error         evaluate.py:93-118,
+ *                                                             anomaly.py:23-42
+ */
+#ifndef DASH_B200_H
+#define DASH_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DASH_OK 0
+#define DASH_E_ARG 1        /* bad shape / null pointer / unsupported rank   */
+#define DASH_E_CUDA 2       /* a CUDA launch or allocation failed            */
+#define DASH_E_SINGULAR 3   /* a ridge system was singular (LU zero pivot)  */
+#define DASH_E_NONFINITE 4  /* a solve produced a non-finite value          */
+
+#define DASH_MAX_RANK 32
+
+typedef struct dash_ctx dash_ctx;
+
+/* Create / destroy a context bound to the current CUDA device. */
+int dash_ctx_create(dash_ctx **out);
+void dash_ctx_destroy(dash_ctx *ctx);
+
+/* Wait for `stream`, then report the first numerical failure since the last
+ * call: returns DASH_OK or DASH_E_SINGULAR / DASH_E_NONFINITE, with
+ * *fail_slice_host = batch position of the failing slice (-1 = the V solve).
+ * Clears the slot. */
+int dash_ctx_status(dash_ctx *ctx, void *stream, int64_t *fail_slice_host);
+
+/* Kernel launches issued by the last dash_update_f64 call (for bench.py's
+ * gpu_launches figure). */
+int dash_ctx_last_launches(const dash_ctx *ctx);
+
+/* One update batch in CSR form: slice m (batch position) owns rows
+ * [row_ptr[m], row_ptr[m+1]) of X.  Order = UpdateBatch.items() order
+ * (tensor.py:166-171): existing slices, then new slices. */
+typedef struct {
+    const double *X;             /* N x ldx                                    */
+    int64_t ldx;                 /* >= J                                        */
+    int64_t N;                   /* total new rows                              */
+    int32_t M;                   /* slices in the batch                         */
+    const int64_t *row_ptr;      /* M+1 (device)                                */
+    const int64_t *row_ptr_host; /* M+1 (host copy, used for work planning)     */
+    const int32_t *state_row;    /* M: row of W/C/D owned by the slice          */
+    const uint8_t *is_new;       /* M: 1 = registered by this batch             */
+} dash_batch_f64;
+
+/* Stream state (StreamState fields, stream.py:196-206).  W/C/D have at least
+ * max(state_row)+1 rows.  F, G, V are updated in place. */
+typedef struct {
+    double *W;   /* K x R        */
+    double *C;   /* K x R        */
+    double *D;   /* K x R x R    */
+    double *V;   /* J x R        */
+    double *F;   /* J x R        */
+    double *G;   /* R x R        */
+    int32_t J;
+    int32_t R;
+    double forgetting;  /* lambda in (0, 1]                  */
+    int32_t passes;     /* ALS passes per update, >= 1       */
+} dash_state_f64;
+
+/* One full DASH update (stream.py:251-370): for each pass, U_new for every
+ * slice (pre-update V, W; new slices bootstrap W=1, C=0, D=0), c/D
+ * accumulation and the S-row (W) solve, F/G accumulation and the V solve.
+ * Writes U_out (N x R, batch row order) and v_used_out (J x R, V at the start
+ * of the last pass).  W rows are written every pass, C/D rows after the final
+ * pass; slices absent from the batch are untouched. */
+int dash_update_f64(dash_ctx *ctx, void *stream, const dash_batch_f64 *batch,
+                    dash_state_f64 *state, double *U_out, double *v_used_out,
+                    double eps);
+
+/* The same update split per pass, for the multi-GPU path: pass_begin runs
+ * U / c / D / W for the local slices and writes this rank's fresh sums
+ * fg_out = [f (J x R) | g (R x R)] (raw, not yet decayed); the caller
+ * all-reduces fg over ranks, then pass_finish forms F = lam F0 + f,
+ * G = sym(lam G0 + g) (F0/G0 = state at the start of the update) and solves V.
+ * dash_update_f64 == for each pass: pass_begin; pass_finish. */
+int dash_update_pass_begin_f64(dash_ctx *ctx, void *stream, const dash_batch_f64 *batch,
+                               dash_state_f64 *state, double *U_out, double *v_used_out,
+                               double eps, int32_t pass, double *fg_out);
+int dash_update_pass_finish_f64(dash_ctx *ctx, void *stream, dash_state_f64 *state,
+                                const double *fg, double eps);
+
+/* Phase timing for benchmarks: when enabled, CUDA events bracket every
+ * launch; dash_ctx_phase_ms syncs and returns the summed milliseconds (and
+ * launch counts) per phase id since the last call:
+ * 0 row_slice, 1 prologue, 2 xv, 3 slices, 4 fgemm, 5 sum_fg, 6 vsolve, 7 fused. */
+int dash_ctx_set_profiling(dash_ctx *ctx, int enable);
+int dash_ctx_phase_ms(dash_ctx *ctx, double *ms_out, int32_t *count_out, int32_t nphases);
+
+/* The reference's operator seam, same contract as _kernels.group_update:
+ * xv (G,I,R), vtv (R,R), s_used (G,R), c_old (G,R), d_old (G,R,R) ->
+ * u, us (G,I,R), c_new (G,R), d_new (G,R,R), w (G,R), g_fresh (R,R).
+ * *ok_host = 0 when some system needed the LU fallback or failed (the
+ * reference's ok=False); outputs are still the fallback solution. */
+int dash_group_update_f64(dash_ctx *ctx, void *stream, int32_t G, int32_t I, int32_t R,
+                          const double *xv, const double *vtv, const double *s_used,
+                          const double *c_old, const double *d_old, double lam, double eps,
+                          double *u, double *us, double *c_new, double *d_new, double *w,
+                          double *g_fresh, int32_t *ok_host);
+
+/* ridge_solve for a batch of systems: x_b = (lhs_b + eps*mean(diag lhs_b) I)^-1 rhs_b,
+ * lhs (B,n,n), rhs (B,n,m), x (B,n,m).  n <= DASH_MAX_RANK. */
+int dash_ridge_solve_f64(dash_ctx *ctx, void *stream, int32_t B, int32_t n, int32_t m,
+                         const double *lhs, const double *rhs, double *x, double eps);
+
+/* init_helpers over an initial tensor in CSR form (stream.py:56-82):
+ * C (K,R) = sum_i (X_k V) o U_k, D (K,R,R) = sym(U_k^T U_k),
+ * F (J,R) = sum_k X_k^T (U_k o w_k), G (R,R) = sym(sum_k U_k^T U_k o w_k w_k^T). */
+int dash_init_helpers_f64(dash_ctx *ctx, void *stream, const dash_batch_f64 *tensor,
+                          const double *U, const double *W, const double *V, int32_t J,
+                          int32_t R, double *C, double *D, double *F, double *G);
+
+/* local_error (evaluate.py:93-118): per-slice mean |X_k - (U_k o w_k) V^T|
+ * with post-update W, V; slice_err (M), tensor_err (1) = mean over slices. */
+int dash_local_error_f64(dash_ctx *ctx, void *stream, const dash_batch_f64 *batch,
+                         const double *U, const double *W, const double *V, int32_t J,
+                         int32_t R, double *slice_err, double *tensor_err);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DASH_B200_H */

@@ -1,0 +1,296 @@
+// Auxiliary entry points around the update step (included by dash_update.cu):
+//
+//   dash_init_helpers_f64   init_helpers        stream.py:56-82
+//   dash_local_error_f64    local_error         evaluate.py:93-118 (+ anomaly.py:23-27)
+//   dash_ridge_solve_f64    ridge_solve         linalg.py:25-45
+#pragma once
+
+namespace {
+
+// Per-slice c_k, D_k and the G contribution from (XV, U, W) -- init_helpers'
+// loop body (stream.py:71-81).  One warp per slice; slot per CTA.
+template <int RB, int NW>
+__global__ void __launch_bounds__(NW * 32) k_helpers(const int64_t *__restrict__ row_ptr, int M,
+                                                     const double *__restrict__ XV, const double *__restrict__ U,
+                                                     const double *__restrict__ W, int R, double *__restrict__ C,
+                                                     double *__restrict__ D, double *__restrict__ G_slots) {
+    constexpr int LD = RB + 1, NP = RB * (RB + 1) / 2, NPC = NP + RB, NPL = (NPC + 31) / 32;
+    __shared__ double Us_all[NW][32 * LD];
+    __shared__ double Xs_all[NW][32 * LD];
+    __shared__ double red[NW][NPC];
+    __shared__ int pr_s[NPC], pz_s[NPC];
+    const int lane = lane_id(), w = warp_id();
+    double *Us = Us_all[w], *Xs = Xs_all[w];
+    for (int i = threadIdx.x; i < NPC; i += blockDim.x) {
+        int r, z;
+        pair_rz(i, RB, r, z);
+        pr_s[i] = r;
+        pz_s[i] = z;
+    }
+    __syncthreads();
+    double g_loc[NPL];
+#pragma unroll
+    for (int q = 0; q < NPL; ++q) g_loc[q] = 0.0;
+    const int per_cta = (M + gridDim.x - 1) / gridDim.x;
+    const int m0 = blockIdx.x * per_cta, m1 = min(M, m0 + per_cta);
+    for (int m = m0 + w; m < m1; m += NW) {
+        const int64_t r0 = row_ptr[m], r1 = row_ptr[m + 1];
+        double gp[NPL];
+#pragma unroll
+        for (int q = 0; q < NPL; ++q) gp[q] = 0.0;
+        for (int64_t c0 = r0; c0 < r1; c0 += 32) {
+            const int64_t row = c0 + lane;
+            const bool valid = row < r1;
+#pragma unroll
+            for (int r = 0; r < RB; ++r) {
+                Us[lane * LD + r] = (valid && r < R) ? U[row * R + r] : 0.0;
+                Xs[lane * LD + r] = (valid && r < R) ? XV[row * R + r] : 0.0;
+            }
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < NPL; ++q) {
+                const int pp = lane + 32 * q;
+                if (pp < NPC) {
+                    const int a = pr_s[pp], c = pz_s[pp];
+                    const double *A = (pp < NP) ? Us : Xs;
+                    double acc = gp[q];
+                    for (int i = 0; i < 32; ++i) acc = fma(A[i * LD + a], Us[i * LD + c], acc);
+                    gp[q] = acc;
+                }
+            }
+            __syncwarp();
+        }
+#pragma unroll
+        for (int q = 0; q < NPL; ++q) {
+            const int pp = lane + 32 * q;
+            if (pp < NPC) {
+                const int r = pr_s[pp], z = pz_s[pp];
+                if (r < R && z < R) {
+                    if (pp < NP) {
+                        D[(int64_t)m * R * R + r * R + z] = gp[q];
+                        D[(int64_t)m * R * R + z * R + r] = gp[q];
+                        g_loc[q] = fma(gp[q] * W[(int64_t)m * R + r], W[(int64_t)m * R + z], g_loc[q]);
+                    } else {
+                        C[(int64_t)m * R + r] = gp[q];
+                    }
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < NPL; ++q)
+        if (lane + 32 * q < NPC) red[w][lane + 32 * q] = g_loc[q];
+    __syncthreads();
+    double *slot = G_slots + (int64_t)blockIdx.x * R * R;
+    for (int pp = threadIdx.x; pp < NP; pp += blockDim.x) {
+        double acc = 0.0;
+        for (int ww = 0; ww < NW; ++ww) acc += red[ww][pp];
+        const int r = pr_s[pp], z = pz_s[pp];
+        if (r < R && z < R) {
+            slot[r * R + z] = acc;
+            slot[z * R + r] = acc;
+        }
+    }
+}
+
+// Per-slice mean |X - (U o w) V^T| with post-update W, V; one warp per slice,
+// lanes over columns.  V is read through L1 (J x R may exceed shared memory).
+__global__ void __launch_bounds__(256) k_local_error(const double *__restrict__ X, int64_t ldx,
+                                                     const int64_t *__restrict__ row_ptr,
+                                                     const int32_t *__restrict__ state_row, int M,
+                                                     const double *__restrict__ U, const double *__restrict__ W,
+                                                     const double *__restrict__ V, int J, int R,
+                                                     double *__restrict__ slice_err) {
+    const int lane = lane_id();
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    __shared__ double us_s[8][DASH_MAX_RANK];
+    double *us = us_s[warp_id()];
+    for (int m = gw; m < M; m += nw) {
+        const int64_t r0 = row_ptr[m], r1 = row_ptr[m + 1];
+        const double *w = W + (int64_t)state_row[m] * R;
+        double acc = 0.0;
+        for (int64_t row = r0; row < r1; ++row) {
+            if (lane < R) us[lane] = U[row * R + lane] * w[lane];
+            __syncwarp();
+            for (int j = lane; j < J; j += 32) {
+                double rec = 0.0;
+                for (int r = 0; r < R; ++r) rec = fma(us[r], __ldg(V + (int64_t)j * R + r), rec);
+                acc += fabs(X[row * ldx + j] - rec);
+            }
+            __syncwarp();
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(FULL_MASK, acc, off);
+        if (lane == 0) slice_err[m] = acc / ((double)(r1 - r0) * J);
+    }
+}
+
+__global__ void k_mean(const double *__restrict__ v, int n, double *__restrict__ out) {
+    // fixed-order mean (single thread: n = slices per batch, small)
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double acc = 0.0;
+        for (int i = 0; i < n; ++i) acc += v[i];
+        *out = n > 0 ? acc / n : 0.0;
+    }
+}
+
+// Batched ridge_solve: system b = blockIdx.x, lanes over right-hand sides.
+template <int RB>
+__global__ void __launch_bounds__(32) k_ridge(const double *__restrict__ lhs, const double *__restrict__ rhs,
+                                              int n, int m, double eps, double *__restrict__ x,
+                                              unsigned long long *err) {
+    constexpr int LD = RB + 1;
+    __shared__ double Ls[RB * LD];
+    __shared__ double dinv[RB];
+    __shared__ int piv[RB];
+    __shared__ double scr[32][LD];
+    const int lane = lane_id();
+    const int64_t b = blockIdx.x;
+    const double *A = lhs + b * n * n;
+    double tr = 0.0;
+    for (int r = 0; r < n; ++r) tr += A[r * n + r];
+    const double sh = eps * (tr / n);
+    double row[RB];
+#pragma unroll
+    for (int z = 0; z < RB; ++z) {
+        double v = 0.0;
+        if (lane < n && z < n) {
+            v = A[lane * n + z];
+            if (z == lane) v += sh;
+        } else if (z == lane) {
+            v = 1.0;
+        }
+        row[z] = v;
+    }
+    bool ok = chol_regs<RB>(row, Ls, LD, dinv);
+    if (!ok) {
+        if (lane == 0) {
+            for (int r = 0; r < n; ++r)
+                for (int z = 0; z < n; ++z) Ls[r * LD + z] = A[r * n + z] + (r == z ? sh : 0.0);
+            if (!lu_factor_serial(Ls, LD, n, piv)) report_error(err, b, DASH_E_SINGULAR);
+        }
+        __syncwarp();
+    }
+    for (int c0 = 0; c0 < m; c0 += 32) {
+        const int c = c0 + lane;
+        const bool valid = c < m;
+        double v[RB];
+#pragma unroll
+        for (int r = 0; r < RB; ++r) v[r] = (valid && r < n) ? rhs[b * n * m + (int64_t)r * m + c] : 0.0;
+        if (ok) {
+            chol_solve_lane<RB>(Ls, LD, dinv, v);
+        } else {
+#pragma unroll
+            for (int r = 0; r < RB; ++r)
+                if (r < n) scr[lane][r] = v[r];
+            if (valid) lu_solve_serial(Ls, LD, n, piv, scr[lane]);
+#pragma unroll
+            for (int r = 0; r < RB; ++r) v[r] = (r < n) ? scr[lane][r] : 0.0;
+        }
+        bool fin = true;
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+            if (valid && r < n) {
+                x[b * n * m + (int64_t)r * m + c] = v[r];
+                fin = fin && finite_d(v[r]);
+            }
+        if (!fin) report_error(err, b, DASH_E_NONFINITE);
+        __syncwarp();
+    }
+}
+
+template <int RB>
+static void launch_helpers(cudaStream_t st, int nblocks, const int64_t *row_ptr, int M, const double *XV,
+                           const double *U, const double *W, int R, double *C, double *D, double *Gsl) {
+    constexpr int NW = RB <= 16 ? 4 : 2;
+    k_helpers<RB, NW><<<nblocks, NW * 32, 0, st>>>(row_ptr, M, XV, U, W, R, C, D, Gsl);
+}
+
+template <int RB>
+static void launch_ridge(cudaStream_t st, int B, const double *lhs, const double *rhs, int n, int m, double eps,
+                         double *x, unsigned long long *err) {
+    k_ridge<RB><<<B, 32, 0, st>>>(lhs, rhs, n, m, eps, x, err);
+}
+
+}  // namespace
+
+extern "C" {
+
+int dash_init_helpers_f64(dash_ctx *ctx, void *stream, const dash_batch_f64 *t, const double *U, const double *W,
+                          const double *V, int32_t J, int32_t R, double *C, double *D, double *F, double *G) {
+    if (!ctx || !t || R < 1 || R > DASH_MAX_RANK || J < 1) return DASH_E_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    ctx->last_launches = 0;
+    const int RB = rank_bucket(R);
+    const int64_t N = t->N;
+    const int M = t->M;
+    const int nblocks = std::max(1, std::min(M, ctx->num_sms * 8));
+    int64_t nsplit, rps;
+    plan_fsplit(ctx, N, J, nsplit, rps);
+    if (ensure(ctx->xv, sizeof(double) * std::max<int64_t>(N, 1) * R) ||
+        ensure(ctx->row_slice, sizeof(int32_t) * std::max<int64_t>(N, 1)) ||
+        ensure(ctx->gslots, sizeof(double) * nblocks * R * R) ||
+        ensure(ctx->fslots, sizeof(double) * nsplit * J * R) || ensure(ctx->fsnap, sizeof(double) * J * R) ||
+        ensure(ctx->gsnap, sizeof(double) * R * R) || ensure(ctx->scratch, sizeof(int32_t) * std::max(M, 1)))
+        return DASH_E_CUDA;
+    double *XV = (double *)ctx->xv.p;
+    int32_t *row_slice = (int32_t *)ctx->row_slice.p;
+    int32_t *ident = (int32_t *)ctx->scratch.p;
+    std::vector<int32_t> id(std::max(M, 1));
+    for (int i = 0; i < M; ++i) id[i] = i;
+    cudaMemcpyAsync(ident, id.data(), sizeof(int32_t) * M, cudaMemcpyHostToDevice, st);
+    cudaMemsetAsync(ctx->fsnap.p, 0, sizeof(double) * J * R, st);
+    cudaMemsetAsync(ctx->gsnap.p, 0, sizeof(double) * R * R, st);
+    dash_batch_f64 b = *t;
+    b.state_row = ident;
+    if (M > 0 && N > 0) {
+        k_row_slice<<<std::min(ctx->num_sms * 4, (M + 7) / 8 + 1), 256, 0, st>>>(t->row_ptr, M, row_slice);
+        launch_xv(ctx, st, &b, J, V, R, XV);
+        switch (RB) {
+            case 4: launch_helpers<4>(st, nblocks, t->row_ptr, M, XV, U, W, R, C, D, (double *)ctx->gslots.p); break;
+            case 8: launch_helpers<8>(st, nblocks, t->row_ptr, M, XV, U, W, R, C, D, (double *)ctx->gslots.p); break;
+            case 16: launch_helpers<16>(st, nblocks, t->row_ptr, M, XV, U, W, R, C, D, (double *)ctx->gslots.p); break;
+            default: launch_helpers<32>(st, nblocks, t->row_ptr, M, XV, U, W, R, C, D, (double *)ctx->gslots.p); break;
+        }
+        double *Fsl = (double *)ctx->fslots.p;
+        launch_fgemm(ctx, st, &b, J, U, row_slice, W, R, rps, (int)nsplit, Fsl);
+    }
+    const int64_t tot = (int64_t)J * R + R * R;
+    if (ensure(ctx->fg, sizeof(double) * tot)) return DASH_E_CUDA;
+    k_sum_fg<<<(int)((tot + 255) / 256), 256, 0, st>>>((double *)ctx->fslots.p, (M > 0 && N > 0) ? (int)nsplit : 0,
+                                                        (double *)ctx->gslots.p, (M > 0 && N > 0) ? nblocks : 0, J, R,
+                                                        (double *)ctx->fg.p);
+    k_finish_fg<<<(int)((tot + 255) / 256), 256, 0, st>>>((double *)ctx->fg.p, (double *)ctx->fsnap.p,
+                                                           (double *)ctx->gsnap.p, 0.0, J, R, F, G);
+    return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_E_CUDA;
+}
+
+int dash_local_error_f64(dash_ctx *ctx, void *stream, const dash_batch_f64 *b, const double *U, const double *W,
+                         const double *V, int32_t J, int32_t R, double *slice_err, double *tensor_err) {
+    if (!ctx || !b || R < 1 || R > DASH_MAX_RANK || J < 1) return DASH_E_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (b->M > 0) {
+        int blocks = std::max(1, std::min((b->M + 7) / 8, ctx->num_sms * 8));
+        k_local_error<<<blocks, 256, 0, st>>>(b->X, b->ldx, b->row_ptr, b->state_row, b->M, U, W, V, J, R,
+                                              slice_err);
+    }
+    k_mean<<<1, 32, 0, st>>>(slice_err, b->M, tensor_err);
+    return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_E_CUDA;
+}
+
+int dash_ridge_solve_f64(dash_ctx *ctx, void *stream, int32_t B, int32_t n, int32_t m, const double *lhs,
+                         const double *rhs, double *x, double eps) {
+    if (!ctx || B < 0 || n < 1 || n > DASH_MAX_RANK || m < 0) return DASH_E_ARG;
+    if (B == 0 || m == 0) return DASH_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (rank_bucket(n)) {
+        case 4: launch_ridge<4>(st, B, lhs, rhs, n, m, eps, x, ctx->err); break;
+        case 8: launch_ridge<8>(st, B, lhs, rhs, n, m, eps, x, ctx->err); break;
+        case 16: launch_ridge<16>(st, B, lhs, rhs, n, m, eps, x, ctx->err); break;
+        default: launch_ridge<32>(st, B, lhs, rhs, n, m, eps, x, ctx->err); break;
+    }
+    return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_E_CUDA;
+}
+
+}  // extern "C"

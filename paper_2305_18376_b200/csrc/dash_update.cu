@@ -1,0 +1,1105 @@
+// DASH per-update step on B200 (sm_100a), FP64.
+//
+// Reference being replaced: StreamState.update (stream.py:251-370) and its
+// numba kernel group_update (_kernels.py:62-144), paths under
+// /root/reference/pkg/src/p2stream.  One update = `passes` x
+//
+//   k_prologue   vtv = V^T V; snapshots of F, G (pass 0); v_used (last pass)
+//   k_xv         XV = X V                       (ragged-agnostic tall-skinny
+//                                                GEMM on FP64 DMMA tensor cores)
+//   k_slices     per slice: U = (XV o s) A^-1, c/D accumulation, W solve,
+//                G contribution  (warp-per-slice, CTA-per-big-slice; the two
+//                R x R ridge systems via warp Cholesky, LU fallback)
+//   k_fgemm      F partials = X^T (U o w_slice(row))   (DMMA, split over rows)
+//   k_sum_fg     fresh terms f, g = sums of the slots (fixed order)
+//   k_vsolve     F = lam F_snap + f, G = sym(lam G_snap + g), V = ridge_solve(G, F^T)^T
+//
+// All reductions use a fixed order (per-CTA slots summed in slot order), so
+// results are bit-reproducible run to run, as the reference's determinism
+// criterion requires (test_acceptance.py:416-475).
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "../../include/dash_b200.h"
+#include "dash_common.cuh"
+
+using namespace dash;
+
+namespace {
+
+constexpr int kSmallRows = 64;     // slices with more rows are "big" (one CTA each)
+constexpr int kSlicesPerItem = 16; // small slices grouped per CTA
+constexpr int kFSplitRows = 1024;  // target rows per F-GEMM split
+
+__host__ __device__ inline int rank_bucket(int R) {
+    return R <= 4 ? 4 : R <= 8 ? 8 : R <= 16 ? 16 : 32;
+}
+
+// ---------------------------------------------------------------------------
+// k_prologue: vtv, snapshots.  One CTA.
+// ---------------------------------------------------------------------------
+__global__ void k_prologue(const double *__restrict__ V, int J, int R, double *__restrict__ vtv,
+                           const double *__restrict__ F, const double *__restrict__ G,
+                           double *__restrict__ F_snap, double *__restrict__ G_snap,
+                           double *__restrict__ v_used, int snap, int last) {
+    for (int p = threadIdx.x; p < R * R; p += blockDim.x) {
+        int r = p / R, z = p % R;
+        double acc = 0.0;
+        for (int j = 0; j < J; ++j) acc = fma(V[j * R + r], V[j * R + z], acc);
+        vtv[p] = acc;
+    }
+    if (snap) {
+        for (int i = threadIdx.x; i < J * R; i += blockDim.x) F_snap[i] = F[i];
+        for (int i = threadIdx.x; i < R * R; i += blockDim.x) G_snap[i] = G[i];
+    }
+    if (last)
+        for (int i = threadIdx.x; i < J * R; i += blockDim.x) v_used[i] = V[i];
+}
+
+// row -> batch position of its slice
+__global__ void k_row_slice(const int64_t *__restrict__ row_ptr, int M, int32_t *__restrict__ row_slice) {
+    int warps = (gridDim.x * blockDim.x) >> 5;
+    int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    for (int m = gw; m < M; m += warps) {
+        int64_t a = row_ptr[m], b = row_ptr[m + 1];
+        for (int64_t r = a + lane_id(); r < b; r += 32) row_slice[r] = m;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k_xv: XV (N x R) = X (N x J, ld ldx) . V (J x R).  64-row tiles, 8 warps,
+// warp w owns rows 8w..8w+7 of the tile and all RP/8 column tiles.
+// ---------------------------------------------------------------------------
+template <int RP>
+__global__ void __launch_bounds__(256) k_xv(const double *__restrict__ X, int64_t ldx, int64_t N, int J,
+                                            const double *__restrict__ V, int R, double *__restrict__ XV) {
+    constexpr int BM = 64, BK = 32, LDXS = BK + 4;
+    constexpr int LDVS = (RP % 16 == 0) ? RP + 8 : RP;
+    constexpr int NT = RP / 8;
+    __shared__ double Xs[BM * LDXS];
+    __shared__ double Vs[BK * LDVS];
+    const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
+    const int g = lane >> 2, t = lane & 3;
+    const int64_t ntiles = (N + BM - 1) / BM;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t row0 = tile * BM;
+        double acc[NT][2];
+#pragma unroll
+        for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = 0.0;
+        for (int k0 = 0; k0 < J; k0 += BK) {
+#pragma unroll
+            for (int q = 0; q < (BM * BK) / 256; ++q) {
+                int i = tid + q * 256;
+                int r = i / BK, c = i % BK;
+                int64_t row = row0 + r;
+                int col = k0 + c;
+                Xs[r * LDXS + c] = (row < N && col < J) ? __ldg(X + row * ldx + col) : 0.0;
+            }
+            for (int i = tid; i < BK * RP; i += 256) {
+                int r = i / RP, c = i % RP;
+                int jj = k0 + r;
+                Vs[r * LDVS + c] = (jj < J && c < R) ? __ldg(V + jj * R + c) : 0.0;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int kk = 0; kk < BK / 4; ++kk) {
+                double a = Xs[(w * 8 + g) * LDXS + kk * 4 + t];
+#pragma unroll
+                for (int n = 0; n < NT; ++n) {
+                    double b = Vs[(kk * 4 + t) * LDVS + n * 8 + g];
+                    dmma884(acc[n], a, b);
+                }
+            }
+            __syncthreads();
+        }
+        const int64_t row = row0 + w * 8 + g;
+        if (row < N) {
+#pragma unroll
+            for (int n = 0; n < NT; ++n)
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    int col = n * 8 + t * 2 + i;
+                    if (col < R) XV[row * R + col] = acc[n][i];
+                }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k_slices: the per-slice phase (_kernels.py:62-144 semantics).
+// ---------------------------------------------------------------------------
+struct SliceParams {
+    const int4 *items;          // {slice0, nslices, big, 0}
+    const int64_t *row_ptr;
+    const int32_t *state_row;
+    const uint8_t *is_new;
+    const double *XV;           // N x R
+    double *U;                  // N x R
+    double *W, *C, *D;          // state rows
+    const double *vtv;          // R x R
+    double *G_slots;            // nitems x R x R
+    unsigned long long *err;
+    unsigned int *fallbacks;    // count of systems that needed LU
+    int R;
+    double lam, eps;
+    int pass, final_pass;
+};
+
+template <int RB>
+struct SliceSmem {
+    static constexpr int LD = RB + 1;
+    static constexpr int NP = RB * (RB + 1) / 2;  // gram pairs (upper triangle)
+    static constexpr int NPC = NP + RB;           // + the R entries of c
+    // per warp: L[RB*LD] | Us[32*LD] | Xs[32*LD] | gram[RB*LD] | dinv | svec | vec | piv
+    static constexpr int per_warp = RB * LD + 32 * LD + 32 * LD + RB * LD + 4 * RB;
+    __host__ __device__ static constexpr int shared(int nw) { return RB * LD + 2 * NPC + nw * NPC; }
+    __host__ __device__ static constexpr size_t bytes(int nw) {
+        return sizeof(double) * (shared(nw) + nw * per_warp);
+    }
+};
+
+// Pair index p -> (r, z).  p < NP: gram entry (r <= z, row-major upper
+// triangle); NP <= p < NP + RB: the c entry r = z = p - NP.
+__device__ __forceinline__ void pair_rz(int p, int RB, int &r, int &z) {
+    const int NP = RB * (RB + 1) / 2;
+    if (p >= NP) { r = z = p - NP; return; }
+    int rr = 0, base = 0;
+    while (p >= base + (RB - rr)) { base += RB - rr; ++rr; }
+    r = rr;
+    z = rr + (p - base);
+}
+
+template <int RB, int NW>
+__global__ void __launch_bounds__(NW * 32) k_slices(SliceParams p) {
+    using S = SliceSmem<RB>;
+    constexpr int LD = S::LD, NP = S::NP, NPC = S::NPC, NPL = (NPC + 31) / 32;
+    extern __shared__ double sm[];
+    double *vtv_s = sm;                               // RB x LD
+    int *pr_s = reinterpret_cast<int *>(vtv_s + RB * LD);  // NPC ints (stored in 2*NPC doubles)
+    int *pz_s = pr_s + NPC;
+    double *red = vtv_s + RB * LD + 2 * NPC;          // NW x NPC
+    const int lane = lane_id(), w = warp_id();
+    double *wbase = sm + S::shared(NW) + w * S::per_warp;
+    double *Ls = wbase;
+    double *Us = Ls + RB * LD;
+    double *Xs = Us + 32 * LD;
+    double *gram_s = Xs + 32 * LD;
+    double *dinv = gram_s + RB * LD;
+    double *svec = dinv + RB;
+    double *vec = svec + RB;
+    int *piv = reinterpret_cast<int *>(vec + RB);
+
+    const int R = p.R;
+    for (int i = threadIdx.x; i < RB * LD; i += blockDim.x) {
+        int r = i / LD, z = i % LD;
+        vtv_s[i] = (r < R && z < R) ? p.vtv[r * R + z] : 0.0;
+    }
+    for (int i = threadIdx.x; i < NPC; i += blockDim.x) {
+        int r, z;
+        pair_rz(i, RB, r, z);
+        pr_s[i] = r;
+        pz_s[i] = z;
+    }
+    __syncthreads();
+
+    double g_loc[NPL];
+#pragma unroll
+    for (int q = 0; q < NPL; ++q) g_loc[q] = 0.0;
+
+    const int4 item = p.items[blockIdx.x];
+    const bool big = item.z != 0;
+    const int nsl = item.y;
+
+    for (int si = big ? 0 : w; si < nsl; si += big ? nsl : NW) {
+        const int m = item.x + si;
+        const int64_t r0 = p.row_ptr[m], r1 = p.row_ptr[m + 1];
+        const int wrow = p.state_row[m];
+        const bool fresh = p.is_new[m] != 0;
+        if (lane < RB)
+            svec[lane] = (lane < R) ? ((fresh && p.pass == 0) ? 1.0 : p.W[(int64_t)wrow * R + lane]) : 0.0;
+        __syncwarp();
+
+        // ---- row-factor system A = vtv o s s^T + shift I (_kernels.py:86-97)
+        double sh = 0.0;
+        for (int r = 0; r < R; ++r) sh += vtv_s[r * LD + r] * svec[r] * svec[r];
+        sh = p.eps * sh / R;
+        bool cholA;
+        {
+            double row[RB];
+            const double sl = lane < RB ? svec[lane] : 0.0;
+#pragma unroll
+            for (int z = 0; z < RB; ++z) {
+                double v = 0.0;
+                if (lane < R && z < R) {
+                    v = vtv_s[lane * LD + z] * sl * svec[z];
+                    if (z == lane) v += sh;
+                } else if (z == lane) {
+                    v = 1.0;
+                }
+                row[z] = v;
+            }
+            cholA = chol_regs<RB>(row, Ls, LD, dinv);
+        }
+        if (!cholA) {
+            // LU fallback on the unpadded system (stream.py:324-329 -> np.linalg.solve)
+            if (lane == 0) {
+                atomicAdd(p.fallbacks, 1u);
+                for (int r = 0; r < R; ++r)
+                    for (int z = 0; z < R; ++z)
+                        Ls[r * LD + z] = vtv_s[r * LD + z] * svec[r] * svec[z] + (r == z ? sh : 0.0);
+                if (!lu_factor_serial(Ls, LD, R, piv)) report_error(p.err, m, DASH_E_SINGULAR);
+            }
+            __syncwarp();
+        }
+
+        // ---- rows: U, then c / gram partials from the staged rows
+        double gp[NPL];
+#pragma unroll
+        for (int q = 0; q < NPL; ++q) gp[q] = 0.0;
+        const int64_t nrows = r1 - r0;
+        const int nchunks = (int)((nrows + 31) / 32);
+        for (int ch = big ? w : 0; ch < nchunks; ch += big ? NW : 1) {
+            const int64_t row = r0 + (int64_t)ch * 32 + lane;
+            const bool valid = row < r1;
+            double b[RB];
+#pragma unroll
+            for (int r = 0; r < RB; ++r) {
+                double x = (valid && r < R) ? p.XV[row * R + r] : 0.0;
+                Xs[lane * LD + r] = x;
+                b[r] = x * svec[r];
+            }
+            if (cholA) {
+                chol_solve_lane<RB>(Ls, LD, dinv, b);
+            } else {
+                double *scr = Us + lane * LD;
+                
+#pragma unroll
+                for (int r = 0; r < RB; ++r) if (r < R) scr[r] = b[r];
+                if (valid) lu_solve_serial(Ls, LD, R, piv, scr);
+#pragma unroll
+                for (int r = 0; r < RB; ++r) b[r] = (r < R) ? scr[r] : 0.0;
+            }
+#pragma unroll
+            for (int r = 0; r < RB; ++r) {
+                if (!valid) b[r] = 0.0;
+                Us[lane * LD + r] = b[r];
+            }
+#pragma unroll
+            for (int r = 0; r < RB; ++r)
+                if (valid && r < R) p.U[row * R + r] = b[r];
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < NPL; ++q) {
+                const int pp = lane + 32 * q;
+                if (pp < NPC) {
+                    const int a = pr_s[pp], c = pz_s[pp];
+                    const double *A = (pp < NP) ? Us : Xs;
+                    double acc = gp[q];
+#pragma unroll 8
+                    for (int i = 0; i < 32; ++i) acc = fma(A[i * LD + a], Us[i * LD + c], acc);
+                    gp[q] = acc;
+                }
+            }
+            __syncwarp();
+        }
+
+        bool owner = true;
+        if (big) {
+            // combine the NW warps' partials in warp order
+            double *mine = red + w * NPC;
+#pragma unroll
+            for (int q = 0; q < NPL; ++q)
+                if (lane + 32 * q < NPC) mine[lane + 32 * q] = gp[q];
+            __syncthreads();
+            owner = (w == 0);
+            if (owner) {
+#pragma unroll
+                for (int q = 0; q < NPL; ++q) {
+                    int pp = lane + 32 * q;
+                    if (pp < NPC) {
+                        double acc = 0.0;
+                        for (int ww = 0; ww < NW; ++ww) acc += red[ww * NPC + pp];
+                        gp[q] = acc;
+                    }
+                }
+            }
+        }
+
+        if (owner) {
+            // gram (symmetric) and c to shared
+#pragma unroll
+            for (int q = 0; q < NPL; ++q) {
+                const int pp = lane + 32 * q;
+                if (pp < NP) {
+                    gram_s[pr_s[pp] * LD + pz_s[pp]] = gp[q];
+                    gram_s[pz_s[pp] * LD + pr_s[pp]] = gp[q];
+                } else if (pp < NPC) {
+                    vec[pp - NP] = gp[q];
+                }
+            }
+            __syncwarp();
+            // ---- c, D accumulation and the S-row system (_kernels.py:103-135)
+            double *dn = Us;  // reuse as d_new (RB x LD)
+            for (int i = lane; i < RB * RB; i += 32) {
+                int r = i / RB, z = i % RB;
+                double v = 0.0;
+                if (r < R && z < R) {
+                    double dold = fresh ? 0.0 : p.D[(int64_t)wrow * R * R + r * R + z];
+                    v = p.lam * dold + gram_s[r * LD + z];
+                }
+                dn[r * LD + z] = v;
+            }
+            double cn = 0.0;
+            if (lane < R) {
+                double cold = fresh ? 0.0 : p.C[(int64_t)wrow * R + lane];
+                cn = p.lam * cold + vec[lane];
+            }
+            __syncwarp();
+            double sh2 = 0.0;
+            for (int r = 0; r < R; ++r) sh2 += vtv_s[r * LD + r] * dn[r * LD + r];
+            sh2 = p.eps * sh2 / R;
+            double wv;
+            bool cholB;
+            {
+                double row[RB];
+#pragma unroll
+                for (int z = 0; z < RB; ++z) {
+                    double v = 0.0;
+                    if (lane < R && z < R) {
+                        v = vtv_s[lane * LD + z] * dn[lane * LD + z];
+                        if (z == lane) v += sh2;
+                    } else if (z == lane) {
+                        v = 1.0;
+                    }
+                    row[z] = v;
+                }
+                cholB = chol_regs<RB>(row, Ls, LD, dinv);
+                wv = chol_solve_dist<RB>(row, Ls, LD, dinv, cn);
+            }
+            bool fin = (lane >= R) || finite_d(wv);
+            bool good = cholB && __all_sync(FULL_MASK, fin);
+            if (!good) {
+                if (lane == 0) {
+                    atomicAdd(p.fallbacks, 1u);
+                    for (int r = 0; r < R; ++r)
+                        for (int z = 0; z < R; ++z)
+                            Ls[r * LD + z] = vtv_s[r * LD + z] * dn[r * LD + z] + (r == z ? sh2 : 0.0);
+                    if (!lu_factor_serial(Ls, LD, R, piv)) report_error(p.err, m, DASH_E_SINGULAR);
+                }
+                __syncwarp();
+                if (lane < R) vec[lane] = cn;
+                __syncwarp();
+                if (lane == 0) {
+                    lu_solve_serial(Ls, LD, R, piv, vec);
+                    for (int r = 0; r < R; ++r)
+                        if (!finite_d(vec[r])) { report_error(p.err, m, DASH_E_NONFINITE); break; }
+                }
+                __syncwarp();
+                wv = (lane < R) ? vec[lane] : 0.0;
+            }
+            if (lane < R) {
+                p.W[(int64_t)wrow * R + lane] = wv;
+                if (p.final_pass) p.C[(int64_t)wrow * R + lane] = cn;
+            }
+            if (p.final_pass)
+                for (int i = lane; i < R * R; i += 32)
+                    p.D[(int64_t)wrow * R * R + i] = dn[(i / R) * LD + (i % R)];
+            __syncwarp();
+            if (lane < RB) vec[lane] = (lane < R) ? wv : 0.0;
+            __syncwarp();
+            // ---- G contribution: gram o w w^T (_kernels.py:139-143)
+#pragma unroll
+            for (int q = 0; q < NPL; ++q) {
+                const int pp = lane + 32 * q;
+                if (pp < NP) g_loc[q] = fma(gp[q] * vec[pr_s[pp]], vec[pz_s[pp]], g_loc[q]);
+            }
+            __syncwarp();
+        }
+        if (big) __syncthreads();
+    }
+
+    // ---- per-item G slot: sum warps in order
+    __syncthreads();
+    {
+        double *mine = red + w * NPC;
+#pragma unroll
+        for (int q = 0; q < NPL; ++q)
+            if (lane + 32 * q < NPC) mine[lane + 32 * q] = g_loc[q];
+    }
+    __syncthreads();
+    double *slot = p.G_slots + (int64_t)blockIdx.x * R * R;
+    for (int pp = threadIdx.x; pp < NP; pp += blockDim.x) {
+        double acc = 0.0;
+        for (int ww = 0; ww < NW; ++ww) acc += red[ww * NPC + pp];
+        const int r = pr_s[pp], z = pz_s[pp];
+        if (r < R && z < R) {
+            slot[r * R + z] = acc;
+            slot[z * R + r] = acc;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k_fgemm: F partial slot s = X[rows_s]^T (U o w)[rows_s], J-block of 64.
+// ---------------------------------------------------------------------------
+template <int RP>
+__global__ void __launch_bounds__(256) k_fgemm(const double *__restrict__ X, int64_t ldx, int64_t N, int J,
+                                               const double *__restrict__ U, const int32_t *__restrict__ row_slice,
+                                               const int32_t *__restrict__ state_row, const double *__restrict__ W,
+                                               int R, int64_t rows_per_split, double *__restrict__ F_slots) {
+    constexpr int BJ = 64, BK = 32, LDXS = BJ + 8;
+    constexpr int LDUS = (RP % 16 == 0) ? RP + 8 : RP;
+    constexpr int NT = RP / 8;
+    __shared__ double Xs[BK * LDXS];
+    __shared__ double Ss[BK * LDUS];
+    const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
+    const int g = lane >> 2, t = lane & 3;
+    const int j0 = blockIdx.x * BJ;
+    const int64_t rbeg = (int64_t)blockIdx.y * rows_per_split;
+    const int64_t rend = min(N, rbeg + rows_per_split);
+    double acc[NT][2];
+#pragma unroll
+    for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = 0.0;
+    for (int64_t k0 = rbeg; k0 < rend; k0 += BK) {
+#pragma unroll
+        for (int q = 0; q < (BK * BJ) / 256; ++q) {
+            int i = tid + q * 256;
+            int r = i / BJ, c = i % BJ;
+            int64_t row = k0 + r;
+            int col = j0 + c;
+            Xs[r * LDXS + c] = (row < rend && col < J) ? __ldg(X + row * ldx + col) : 0.0;
+        }
+        for (int i = tid; i < BK * RP; i += 256) {
+            int r = i / RP, c = i % RP;
+            int64_t row = k0 + r;
+            double v = 0.0;
+            if (row < rend && c < R) {
+                int m = row_slice[row];
+                v = U[row * R + c] * W[(int64_t)state_row[m] * R + c];
+            }
+            Ss[r * LDUS + c] = v;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < BK / 4; ++kk) {
+            double a = Xs[(kk * 4 + t) * LDXS + w * 8 + g];
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+                double b = Ss[(kk * 4 + t) * LDUS + n * 8 + g];
+                dmma884(acc[n], a, b);
+            }
+        }
+        __syncthreads();
+    }
+    double *slot = F_slots + (int64_t)blockIdx.y * J * R;
+    const int j = j0 + w * 8 + g;
+    if (j < J) {
+#pragma unroll
+        for (int n = 0; n < NT; ++n)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                int col = n * 8 + t * 2 + i;
+                if (col < R) slot[j * R + col] = acc[n][i];
+            }
+    }
+}
+
+// fg = [sum_s F slots | sum_items G slots] in slot order (the fresh terms
+// f_fresh, g_fresh of stream.py:306-322; raw sums, not yet decayed).
+__global__ void k_sum_fg(const double *__restrict__ F_slots, int nfs, const double *__restrict__ G_slots, int ngs,
+                         int J, int R, double *__restrict__ fg) {
+    const int64_t JR = (int64_t)J * R;
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < JR) {
+        double acc = 0.0;
+        for (int s = 0; s < nfs; ++s) acc += F_slots[s * JR + i];
+        fg[i] = acc;
+    } else if (i < JR + R * R) {
+        const int64_t pidx = i - JR;
+        double acc = 0.0;
+        for (int s = 0; s < ngs; ++s) acc += G_slots[(int64_t)s * R * R + pidx];
+        fg[i] = acc;
+    }
+}
+
+// Finish one pass (stream.py:344-346): F = lam F_snap + f, G = sym(lam G_snap
+// + g), then V = ridge_solve(G, F^T)^T (linalg.py:25-45).  Every warp forms G
+// and factors it (identical result in every warp) and solves 32 rows of V;
+// block 0 / warp 0 writes G, each warp writes its F rows.
+template <int RB, int NWV>
+__global__ void __launch_bounds__(NWV * 32) k_vsolve(const double *__restrict__ fg, const double *__restrict__ F_snap,
+                                                     const double *__restrict__ G_snap, double lam, int J, int R,
+                                                     double eps, double *__restrict__ F, double *__restrict__ G,
+                                                     double *__restrict__ V, unsigned long long *err,
+                                                     unsigned int *fallbacks) {
+    constexpr int LD = RB + 1;
+    __shared__ double sL[NWV][RB * LD];
+    __shared__ double sG[NWV][RB * LD];
+    __shared__ double sd[NWV][RB];
+    __shared__ int spiv[NWV][RB];
+    __shared__ double sx[NWV][32][LD];
+    const int lane = lane_id(), w = warp_id();
+    double *Ls = sL[w], *Gs = sG[w], *dinv = sd[w];
+    const int64_t JR = (int64_t)J * R;
+    const double *g = fg + JR;
+    for (int i = lane; i < R * R; i += 32) {
+        const int r = i / R, z = i % R;
+        const double m1 = lam * G_snap[r * R + z] + g[r * R + z];
+        const double m2 = lam * G_snap[z * R + r] + g[z * R + r];
+        Gs[r * LD + z] = (m1 + m2) / 2.0;
+    }
+    __syncwarp();
+    if (blockIdx.x == 0 && w == 0)
+        for (int i = lane; i < R * R; i += 32) G[i] = Gs[(i / R) * LD + (i % R)];
+    double tr = 0.0;
+    for (int r = 0; r < R; ++r) tr += Gs[r * LD + r];
+    const double sh = eps * (tr / R);
+    double row[RB];
+#pragma unroll
+    for (int z = 0; z < RB; ++z) {
+        double v = 0.0;
+        if (lane < R && z < R) {
+            v = Gs[lane * LD + z];
+            if (z == lane) v += sh;
+        } else if (z == lane) {
+            v = 1.0;
+        }
+        row[z] = v;
+    }
+    bool ok = chol_regs<RB>(row, Ls, LD, dinv);
+    if (!ok) {
+        if (lane == 0) {
+            if (blockIdx.x == 0 && w == 0) atomicAdd(fallbacks, 1u);
+            for (int r = 0; r < R; ++r)
+                for (int z = 0; z < R; ++z) Ls[r * LD + z] = Gs[r * LD + z] + (r == z ? sh : 0.0);
+            if (!lu_factor_serial(Ls, LD, R, spiv[w])) report_error(err, -1, DASH_E_SINGULAR);
+        }
+        __syncwarp();
+    }
+    const int j = (blockIdx.x * NWV + w) * 32 + lane;
+    const bool valid = j < J;
+    double b[RB];
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+        double v = 0.0;
+        if (valid && r < R) {
+            v = lam * F_snap[(int64_t)j * R + r] + fg[(int64_t)j * R + r];
+            F[(int64_t)j * R + r] = v;
+        }
+        b[r] = v;
+    }
+    if (ok) {
+        chol_solve_lane<RB>(Ls, LD, dinv, b);
+    } else {
+        double *scr = sx[w][lane];
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+            if (r < R) scr[r] = b[r];
+        if (valid) lu_solve_serial(Ls, LD, R, spiv[w], scr);
+#pragma unroll
+        for (int r = 0; r < RB; ++r) b[r] = (r < R) ? scr[r] : 0.0;
+    }
+    if (valid) {
+        bool fin = true;
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+            if (r < R) {
+                V[(int64_t)j * R + r] = b[r];
+                fin = fin && finite_d(b[r]);
+            }
+        }
+        if (!fin) report_error(err, -1, DASH_E_NONFINITE);
+    }
+}
+
+// us = u o w  (group_update seam output)
+__global__ void k_us(const double *__restrict__ u, const double *__restrict__ w, int G, int I, int R,
+                     double *__restrict__ us) {
+    int64_t n = (int64_t)G * I * R;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t g = i / ((int64_t)I * R);
+        int r = (int)(i % R);
+        us[i] = u[i] * w[g * R + r];
+    }
+}
+
+// g_fresh = sum of item slots in order
+__global__ void k_sum_slots(const double *__restrict__ slots, int n, int RR, double *__restrict__ out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < RR) {
+        double acc = 0.0;
+        for (int s = 0; s < n; ++s) acc += slots[(int64_t)s * RR + i];
+        out[i] = acc;
+    }
+}
+
+}  // namespace
+
+// ===========================================================================
+// host side
+// ===========================================================================
+namespace {
+// F = lam F_snap + f, G = sym(lam G_snap + g)  (no V solve; init_helpers uses lam = 0)
+__global__ void k_finish_fg(const double *__restrict__ fg, const double *__restrict__ F_snap,
+                            const double *__restrict__ G_snap, double lam, int J, int R, double *__restrict__ F,
+                            double *__restrict__ G) {
+    const int64_t JR = (int64_t)J * R;
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < JR) {
+        F[i] = lam * F_snap[i] + fg[i];
+    } else if (i < JR + R * R) {
+        const int p = (int)(i - JR), r = p / R, z = p % R;
+        const double m1 = lam * G_snap[r * R + z] + fg[JR + r * R + z];
+        const double m2 = lam * G_snap[z * R + r] + fg[JR + z * R + r];
+        G[p] = (m1 + m2) / 2.0;
+    }
+}
+}  // namespace
+
+enum Phase { PH_ROWSLICE = 0, PH_PROLOGUE, PH_XV, PH_SLICES, PH_FGEMM, PH_SUMFG, PH_VSOLVE, PH_COUNT };
+
+struct dash_ctx {
+    struct Buf {
+        void *p = nullptr;
+        size_t cap = 0;
+    };
+    Buf xv, row_slice, items, gslots, fslots, vtv, fsnap, gsnap, fg, scratch;
+    unsigned long long *err = nullptr;
+    unsigned int *fallbacks = nullptr;
+    int4 *items_host[2] = {nullptr, nullptr};
+    size_t items_host_cap[2] = {0, 0};
+    cudaEvent_t staged[2] = {nullptr, nullptr};
+    int cur = 0;
+    int last_launches = 0;
+    int num_sms = 148;
+    // per-update plan, shared by the pass_begin calls of one update
+    int nitems = 0;
+    int64_t nsplit = 1, rps = 32;
+    // phase timing (bench): events around every launch when enabled
+    int prof = 0;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_recs;
+    size_t ev_used = 0;
+};
+
+namespace {
+
+cudaEvent_t prof_event(dash_ctx *ctx) {
+    if (ctx->ev_used == ctx->ev_pool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        ctx->ev_pool.push_back(e);
+    }
+    return ctx->ev_pool[ctx->ev_used++];
+}
+
+struct PhaseScope {
+    dash_ctx *ctx;
+    cudaStream_t st;
+    int id;
+    cudaEvent_t a = nullptr;
+    PhaseScope(dash_ctx *c, cudaStream_t s, int i) : ctx(c), st(s), id(i) {
+        if (ctx->prof) {
+            a = prof_event(ctx);
+            cudaEventRecord(a, st);
+        }
+        ctx->last_launches++;
+    }
+    ~PhaseScope() {
+        if (ctx->prof) {
+            cudaEvent_t b = prof_event(ctx);
+            cudaEventRecord(b, st);
+            ctx->ev_recs.push_back({id, {a, b}});
+        }
+    }
+};
+
+int ensure(dash_ctx::Buf &b, size_t bytes) {
+    if (b.cap >= bytes) return 0;
+    if (b.p) cudaFree(b.p);
+    size_t cap = std::max(bytes + bytes / 2, (size_t)256);
+    if (cudaMalloc(&b.p, cap) != cudaSuccess) {
+        b.p = nullptr;
+        b.cap = 0;
+        return DASH_E_CUDA;
+    }
+    b.cap = cap;
+    return 0;
+}
+
+int stage_items(dash_ctx *ctx, cudaStream_t st, const std::vector<int4> &items) {
+    int c = ctx->cur;
+    ctx->cur ^= 1;
+    cudaEventSynchronize(ctx->staged[c]);
+    size_t need = items.size() * sizeof(int4);
+    if (ctx->items_host_cap[c] < need) {
+        if (ctx->items_host[c]) cudaFreeHost(ctx->items_host[c]);
+        size_t cap = need + need / 2 + 64;
+        if (cudaMallocHost((void **)&ctx->items_host[c], cap) != cudaSuccess) return DASH_E_CUDA;
+        ctx->items_host_cap[c] = cap;
+    }
+    memcpy(ctx->items_host[c], items.data(), need);
+    if (ensure(ctx->items, need)) return DASH_E_CUDA;
+    cudaMemcpyAsync(ctx->items.p, ctx->items_host[c], need, cudaMemcpyHostToDevice, st);
+    cudaEventRecord(ctx->staged[c], st);
+    return 0;
+}
+
+// Host planning: contiguous batch positions -> CTA work items.
+void plan_items(const int64_t *row_ptr, int M, std::vector<int4> &items) {
+    items.clear();
+    int m = 0;
+    while (m < M) {
+        int64_t n = row_ptr[m + 1] - row_ptr[m];
+        if (n > kSmallRows) {
+            items.push_back(make_int4(m, 1, 1, 0));
+            ++m;
+            continue;
+        }
+        int start = m, cnt = 0;
+        while (m < M && cnt < kSlicesPerItem && (row_ptr[m + 1] - row_ptr[m]) <= kSmallRows) {
+            ++m;
+            ++cnt;
+        }
+        items.push_back(make_int4(start, cnt, 0, 0));
+    }
+}
+
+void plan_fsplit(dash_ctx *ctx, int64_t N, int J, int64_t &nsplit, int64_t &rps) {
+    nsplit = std::max<int64_t>(1, std::min<int64_t>((N + kFSplitRows - 1) / kFSplitRows,
+                                                    (int64_t)ctx->num_sms * 4 / ((J + 63) / 64) + 1));
+    rps = (N + nsplit - 1) / nsplit;
+    rps = std::max<int64_t>(32, (rps + 31) / 32 * 32);
+    nsplit = N > 0 ? (N + rps - 1) / rps : 1;
+}
+
+template <int RB>
+int launch_slices(dash_ctx *ctx, cudaStream_t st, int nitems, const SliceParams &sp) {
+    constexpr int NW = (RB <= 16) ? 8 : 4;
+    size_t smem = SliceSmem<RB>::bytes(NW);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_slices<RB, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    PhaseScope ps(ctx, st, PH_SLICES);
+    k_slices<RB, NW><<<nitems, NW * 32, smem, st>>>(sp);
+    return cudaGetLastError() == cudaSuccess ? 0 : DASH_E_CUDA;
+}
+
+int dispatch_slices(dash_ctx *ctx, cudaStream_t st, int RB, int nitems, const SliceParams &sp) {
+    switch (RB) {
+        case 4: return launch_slices<4>(ctx, st, nitems, sp);
+        case 8: return launch_slices<8>(ctx, st, nitems, sp);
+        case 16: return launch_slices<16>(ctx, st, nitems, sp);
+        default: return launch_slices<32>(ctx, st, nitems, sp);
+    }
+}
+
+template <int RP>
+void launch_xv_t(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, const double *V, int R,
+                 double *XV) {
+    int64_t ntiles = (b->N + 63) / 64;
+    int grid = (int)std::min<int64_t>(ntiles, (int64_t)ctx->num_sms * 8);
+    if (grid < 1) grid = 1;
+    PhaseScope ps(ctx, st, PH_XV);
+    k_xv<RP><<<grid, 256, 0, st>>>(b->X, b->ldx, b->N, J, V, R, XV);
+}
+
+void launch_xv(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, const double *V, int R,
+               double *XV) {
+    switch (rank_bucket(R) < 8 ? 8 : rank_bucket(R)) {
+        case 8: launch_xv_t<8>(ctx, st, b, J, V, R, XV); break;
+        case 16: launch_xv_t<16>(ctx, st, b, J, V, R, XV); break;
+        default: launch_xv_t<32>(ctx, st, b, J, V, R, XV); break;
+    }
+}
+
+template <int RP>
+void launch_fgemm_t(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, const double *U,
+                    const int32_t *row_slice, const double *W, int R, int64_t rps, int nsplit, double *F_slots) {
+    dim3 grid((J + 63) / 64, nsplit);
+    PhaseScope ps(ctx, st, PH_FGEMM);
+    k_fgemm<RP><<<grid, 256, 0, st>>>(b->X, b->ldx, b->N, J, U, row_slice, b->state_row, W, R, rps, F_slots);
+}
+
+void launch_fgemm(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, const double *U,
+                  const int32_t *row_slice, const double *W, int R, int64_t rps, int nsplit, double *F_slots) {
+    switch (rank_bucket(R) < 8 ? 8 : rank_bucket(R)) {
+        case 8: launch_fgemm_t<8>(ctx, st, b, J, U, row_slice, W, R, rps, nsplit, F_slots); break;
+        case 16: launch_fgemm_t<16>(ctx, st, b, J, U, row_slice, W, R, rps, nsplit, F_slots); break;
+        default: launch_fgemm_t<32>(ctx, st, b, J, U, row_slice, W, R, rps, nsplit, F_slots); break;
+    }
+}
+
+template <int RB>
+void launch_vsolve_t(dash_ctx *ctx, cudaStream_t st, const double *fg, double lam, int J, int R, double eps,
+                     double *F, double *G, double *V) {
+    constexpr int NWV = RB <= 16 ? 4 : 1;
+    int blocks = (J + NWV * 32 - 1) / (NWV * 32);
+    PhaseScope ps(ctx, st, PH_VSOLVE);
+    k_vsolve<RB, NWV><<<blocks, NWV * 32, 0, st>>>(fg, (const double *)ctx->fsnap.p, (const double *)ctx->gsnap.p,
+                                                    lam, J, R, eps, F, G, V, ctx->err, ctx->fallbacks);
+}
+
+bool valid_state(const dash_state_f64 *s) {
+    return s && s->R >= 1 && s->R <= DASH_MAX_RANK && s->J >= 1 && s->passes >= 1 && s->forgetting > 0.0 &&
+           s->forgetting <= 1.0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dash_ctx_create(dash_ctx **out) {
+    if (!out) return DASH_E_ARG;
+    dash_ctx *ctx = new dash_ctx();
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaMalloc(&ctx->err, sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc(&ctx->fallbacks, sizeof(unsigned int)) != cudaSuccess) {
+        delete ctx;
+        return DASH_E_CUDA;
+    }
+    unsigned long long none = ~0ull;
+    cudaMemcpy(ctx->err, &none, sizeof(none), cudaMemcpyHostToDevice);
+    cudaMemset(ctx->fallbacks, 0, sizeof(unsigned int));
+    for (int i = 0; i < 2; ++i) cudaEventCreateWithFlags(&ctx->staged[i], cudaEventDisableTiming);
+    *out = ctx;
+    return DASH_OK;
+}
+
+void dash_ctx_destroy(dash_ctx *ctx) {
+    if (!ctx) return;
+    cudaDeviceSynchronize();
+    dash_ctx::Buf *bufs[] = {&ctx->xv,  &ctx->row_slice, &ctx->items, &ctx->gslots, &ctx->fslots,
+                             &ctx->vtv, &ctx->fsnap,     &ctx->gsnap, &ctx->fg,     &ctx->scratch};
+    for (auto *b : bufs)
+        if (b->p) cudaFree(b->p);
+    cudaFree(ctx->err);
+    cudaFree(ctx->fallbacks);
+    for (int i = 0; i < 2; ++i) {
+        if (ctx->items_host[i]) cudaFreeHost(ctx->items_host[i]);
+        cudaEventDestroy(ctx->staged[i]);
+    }
+    for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+    delete ctx;
+}
+
+int dash_ctx_status(dash_ctx *ctx, void *stream, int64_t *fail_slice_host) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return DASH_E_CUDA;
+    unsigned long long key = 0;
+    if (cudaMemcpy(&key, ctx->err, sizeof(key), cudaMemcpyDeviceToHost) != cudaSuccess) return DASH_E_CUDA;
+    unsigned long long none = ~0ull;
+    cudaMemcpy(ctx->err, &none, sizeof(none), cudaMemcpyHostToDevice);
+    if (key == none) {
+        if (fail_slice_host) *fail_slice_host = 0;
+        return DASH_OK;
+    }
+    if (fail_slice_host) *fail_slice_host = (int64_t)(key >> 4) - 1;
+    return (int)(key & 15ull);
+}
+
+int dash_ctx_last_launches(const dash_ctx *ctx) { return ctx ? ctx->last_launches : 0; }
+
+int dash_ctx_set_profiling(dash_ctx *ctx, int enable) {
+    if (!ctx) return DASH_E_ARG;
+    ctx->prof = enable;
+    ctx->ev_recs.clear();
+    ctx->ev_used = 0;
+    return DASH_OK;
+}
+
+int dash_ctx_phase_ms(dash_ctx *ctx, double *ms_out, int32_t *count_out, int32_t nphases) {
+    if (!ctx || !ms_out) return DASH_E_ARG;
+    for (int i = 0; i < nphases; ++i) {
+        ms_out[i] = 0.0;
+        if (count_out) count_out[i] = 0;
+    }
+    for (auto &rec : ctx->ev_recs) {
+        cudaEventSynchronize(rec.second.second);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, rec.second.first, rec.second.second);
+        if (rec.first < nphases) {
+            ms_out[rec.first] += ms;
+            if (count_out) count_out[rec.first]++;
+        }
+    }
+    ctx->ev_recs.clear();
+    ctx->ev_used = 0;
+    return DASH_OK;
+}
+
+int dash_update_pass_begin_f64(dash_ctx *ctx, void *stream, const dash_batch_f64 *b, dash_state_f64 *s,
+                               double *U_out, double *v_used_out, double eps, int32_t pass, double *fg_out) {
+    if (!ctx || !b || !valid_state(s) || !U_out || !v_used_out || !fg_out) return DASH_E_ARG;
+    if (b->M < 0 || b->N < 0 || (b->N > 0 && b->ldx < s->J) || pass < 0 || pass >= s->passes) return DASH_E_ARG;
+    const int J = s->J, R = s->R;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int RB = rank_bucket(R);
+    const int64_t N = b->N;
+    const int M = b->M;
+    const int last = pass == s->passes - 1;
+    if (pass == 0) {
+        ctx->last_launches = 0;
+        std::vector<int4> items;
+        plan_items(b->row_ptr_host, M, items);
+        ctx->nitems = (int)items.size();
+        plan_fsplit(ctx, N, J, ctx->nsplit, ctx->rps);
+        if (ensure(ctx->xv, sizeof(double) * std::max<int64_t>(N, 1) * R) ||
+            ensure(ctx->row_slice, sizeof(int32_t) * std::max<int64_t>(N, 1)) ||
+            ensure(ctx->gslots, sizeof(double) * std::max(ctx->nitems, 1) * R * R) ||
+            ensure(ctx->fslots, sizeof(double) * ctx->nsplit * J * R) || ensure(ctx->vtv, sizeof(double) * R * R) ||
+            ensure(ctx->fsnap, sizeof(double) * J * R) || ensure(ctx->gsnap, sizeof(double) * R * R))
+            return DASH_E_CUDA;
+        if (ctx->nitems > 0 && stage_items(ctx, st, items)) return DASH_E_CUDA;
+        if (M > 0) {
+            PhaseScope ps(ctx, st, PH_ROWSLICE);
+            k_row_slice<<<std::min(ctx->num_sms * 4, (M + 7) / 8 + 1), 256, 0, st>>>(b->row_ptr, M,
+                                                                                    (int32_t *)ctx->row_slice.p);
+        }
+    }
+    double *XV = (double *)ctx->xv.p;
+    double *Fsl = (double *)ctx->fslots.p, *Gsl = (double *)ctx->gslots.p;
+    {
+        PhaseScope ps(ctx, st, PH_PROLOGUE);
+        k_prologue<<<1, 256, 0, st>>>(s->V, J, R, (double *)ctx->vtv.p, s->F, s->G, (double *)ctx->fsnap.p,
+                                      (double *)ctx->gsnap.p, v_used_out, pass == 0, last);
+    }
+    if (N > 0) {
+        launch_xv(ctx, st, b, J, s->V, R, XV);
+        SliceParams sp;
+        sp.items = (const int4 *)ctx->items.p;
+        sp.row_ptr = b->row_ptr;
+        sp.state_row = b->state_row;
+        sp.is_new = b->is_new;
+        sp.XV = XV;
+        sp.U = U_out;
+        sp.W = s->W;
+        sp.C = s->C;
+        sp.D = s->D;
+        sp.vtv = (const double *)ctx->vtv.p;
+        sp.G_slots = Gsl;
+        sp.err = ctx->err;
+        sp.fallbacks = ctx->fallbacks;
+        sp.R = R;
+        sp.lam = s->forgetting;
+        sp.eps = eps;
+        sp.pass = pass;
+        sp.final_pass = last;
+        if (dispatch_slices(ctx, st, RB, ctx->nitems, sp)) return DASH_E_CUDA;
+        launch_fgemm(ctx, st, b, J, U_out, (const int32_t *)ctx->row_slice.p, s->W, R, ctx->rps, (int)ctx->nsplit,
+                     Fsl);
+    }
+    {
+        const int64_t tot = (int64_t)J * R + R * R;
+        PhaseScope ps(ctx, st, PH_SUMFG);
+        k_sum_fg<<<(int)((tot + 255) / 256), 256, 0, st>>>(Fsl, N > 0 ? (int)ctx->nsplit : 0, Gsl,
+                                                            N > 0 ? ctx->nitems : 0, J, R, fg_out);
+    }
+    return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_E_CUDA;
+}
+
+int dash_update_pass_finish_f64(dash_ctx *ctx, void *stream, dash_state_f64 *s, const double *fg, double eps) {
+    if (!ctx || !valid_state(s) || !fg) return DASH_E_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int J = s->J, R = s->R;
+    switch (rank_bucket(R)) {
+        case 4: launch_vsolve_t<4>(ctx, st, fg, s->forgetting, J, R, eps, s->F, s->G, s->V); break;
+        case 8: launch_vsolve_t<8>(ctx, st, fg, s->forgetting, J, R, eps, s->F, s->G, s->V); break;
+        case 16: launch_vsolve_t<16>(ctx, st, fg, s->forgetting, J, R, eps, s->F, s->G, s->V); break;
+        default: launch_vsolve_t<32>(ctx, st, fg, s->forgetting, J, R, eps, s->F, s->G, s->V); break;
+    }
+    return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_E_CUDA;
+}
+
+int dash_update_f64(dash_ctx *ctx, void *stream, const dash_batch_f64 *b, dash_state_f64 *s, double *U_out,
+                    double *v_used_out, double eps) {
+    if (!ctx || !valid_state(s)) return DASH_E_ARG;
+    if (ensure(ctx->fg, sizeof(double) * ((size_t)s->J * s->R + s->R * s->R))) return DASH_E_CUDA;
+    double *fg = (double *)ctx->fg.p;
+    for (int pass = 0; pass < s->passes; ++pass) {
+        int rc = dash_update_pass_begin_f64(ctx, stream, b, s, U_out, v_used_out, eps, pass, fg);
+        if (rc) return rc;
+        rc = dash_update_pass_finish_f64(ctx, stream, s, fg, eps);
+        if (rc) return rc;
+    }
+    return DASH_OK;
+}
+
+int dash_group_update_f64(dash_ctx *ctx, void *stream, int32_t G, int32_t I, int32_t R, const double *xv,
+                          const double *vtv, const double *s_used, const double *c_old, const double *d_old,
+                          double lam, double eps, double *u, double *us, double *c_new, double *d_new, double *w,
+                          double *g_fresh, int32_t *ok_host) {
+    if (!ctx || G < 0 || I < 1 || R < 1 || R > DASH_MAX_RANK) return DASH_E_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    ctx->last_launches = 0;
+    const int RB = rank_bucket(R);
+    // synthetic batch: slice g owns rows g*I..(g+1)*I of xv; state row g
+    std::vector<int64_t> rp(G + 1);
+    for (int g = 0; g <= G; ++g) rp[g] = (int64_t)g * I;
+    std::vector<int4> items;
+    plan_items(rp.data(), G, items);
+    const int nitems = (int)items.size();
+    size_t need = sizeof(int64_t) * (G + 1) + sizeof(int32_t) * G + G + 64;
+    if (ensure(ctx->scratch, need) || ensure(ctx->gslots, sizeof(double) * std::max(nitems, 1) * R * R))
+        return DASH_E_CUDA;
+    int64_t *d_rp = (int64_t *)ctx->scratch.p;
+    int32_t *d_sr = (int32_t *)(d_rp + G + 1);
+    uint8_t *d_new_flag = (uint8_t *)(d_sr + G);
+    std::vector<int32_t> sr(G);
+    for (int g = 0; g < G; ++g) sr[g] = g;
+    cudaMemcpyAsync(d_rp, rp.data(), sizeof(int64_t) * (G + 1), cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_sr, sr.data(), sizeof(int32_t) * G, cudaMemcpyHostToDevice, st);
+    cudaMemsetAsync(d_new_flag, 0, G, st);
+    // state copies: W <- s_used, C <- c_old, D <- d_old (outputs double as state)
+    cudaMemcpyAsync(w, s_used, sizeof(double) * G * R, cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(c_new, c_old, sizeof(double) * G * R, cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(d_new, d_old, sizeof(double) * G * R * R, cudaMemcpyDeviceToDevice, st);
+    unsigned int zero = 0;
+    cudaMemcpyAsync(ctx->fallbacks, &zero, sizeof(zero), cudaMemcpyHostToDevice, st);
+    if (nitems > 0 && stage_items(ctx, st, items)) return DASH_E_CUDA;
+    if (G > 0) {
+        SliceParams sp;
+        sp.items = (const int4 *)ctx->items.p;
+        sp.row_ptr = d_rp;
+        sp.state_row = d_sr;
+        sp.is_new = d_new_flag;
+        sp.XV = xv;
+        sp.U = u;
+        sp.W = w;
+        sp.C = c_new;
+        sp.D = d_new;
+        sp.vtv = vtv;
+        sp.G_slots = (double *)ctx->gslots.p;
+        sp.err = ctx->err;
+        sp.fallbacks = ctx->fallbacks;
+        sp.R = R;
+        sp.lam = lam;
+        sp.eps = eps;
+        sp.pass = 1;  // read s from W (= s_used), not the new-slice bootstrap
+        sp.final_pass = 1;
+        if (dispatch_slices(ctx, st, RB, nitems, sp)) return DASH_E_CUDA;
+        k_us<<<std::max(1, std::min(1024, (int)(((int64_t)G * I * R + 255) / 256))), 256, 0, st>>>(u, w, G, I, R, us);
+        ctx->last_launches++;
+    }
+    k_sum_slots<<<(R * R + 255) / 256, 256, 0, st>>>((double *)ctx->gslots.p, G > 0 ? nitems : 0, R * R, g_fresh);
+    ctx->last_launches++;
+    unsigned int fb = 0;
+    cudaMemcpyAsync(&fb, ctx->fallbacks, sizeof(fb), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    if (ok_host) *ok_host = fb == 0 ? 1 : 0;
+    return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_E_CUDA;
+}
+
+}  // extern "C"
+
+#include "dash_aux.cuh"

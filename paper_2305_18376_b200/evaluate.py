@@ -1,0 +1,55 @@
+"""Per-update fitness on the GPU: ``local_error`` (evaluate.py:93-118 of the
+reference) -- per-slice mean |X_k - (U_k o w_k) V^T| with the post-update W
+and V, and the tensor-level mean over the slices in the batch
+(anomaly.py:23-42 ``slice_error`` / ``tensor_error``)."""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native as nat
+
+
+def local_error(batch_items, u_new, state):
+    """Same signature and return value as the reference: (te, {sid: mad})."""
+    ids = [sid for sid, _ in batch_items]
+    last = getattr(state, "_last", None)
+    dev = state.device
+    if (last is not None and last[0] == ids and hasattr(u_new, "device_tensor")
+            and u_new.device_tensor is last[5]):
+        _, row_ptr, state_row, X, N, U = last
+    else:
+        counts = np.array([np.asarray(r).shape[0] for _, r in batch_items], dtype=np.int64)
+        row_ptr = np.zeros(len(ids) + 1, dtype=np.int64)
+        np.cumsum(counts, out=row_ptr[1:])
+        X = torch.as_tensor(np.concatenate([np.asarray(r, dtype=float) for _, r in batch_items]),
+                            device=dev)
+        U = torch.as_tensor(np.concatenate([np.asarray(u_new[s], dtype=float) for s in ids]),
+                            device=dev)
+        state_row = np.array([state.row_of(s) for s in ids], dtype=np.int32)
+        N = int(row_ptr[-1])
+    slice_err, te = local_error_device(X, N, row_ptr, state_row, U, state)
+    se = slice_err.cpu().numpy()
+    return float(te.item()), {sid: float(se[k]) for k, sid in enumerate(ids)}
+
+
+def local_error_device(X, N, row_ptr, state_row, U, state):
+    """Device tensors in, device (slice_err (M,), tensor_err ()) out."""
+    dev = state.device
+    M = len(row_ptr) - 1
+    rp = torch.as_tensor(np.asarray(row_ptr, dtype=np.int64), device=dev)
+    sr = torch.as_tensor(np.asarray(state_row, dtype=np.int32), device=dev)
+    slice_err = torch.empty(max(M, 1), dtype=torch.float64, device=dev)
+    te = torch.empty((), dtype=torch.float64, device=dev)
+    b = nat.DashBatch(X=int(X.data_ptr()), ldx=int(X.stride(0)), N=N, M=M, row_ptr=int(rp.data_ptr()),
+                      row_ptr_host=np.asarray(row_ptr, dtype=np.int64).ctypes.data,
+                      state_row=int(sr.data_ptr()), is_new=0)
+    W = state.device_tensors["W"]
+    nat.check(nat.lib().dash_local_error_f64(state._ctx, nat.stream_ptr(), ctypes.byref(b),
+                                             int(U.data_ptr()), int(W.data_ptr()),
+                                             int(state._V.data_ptr()), state.J, state.rank,
+                                             int(slice_err.data_ptr()), int(te.data_ptr())),
+              "dash_local_error_f64")
+    return slice_err[:M], te

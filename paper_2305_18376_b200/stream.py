@@ -1,0 +1,593 @@
+"""Device-resident DASH stream state -- drop-in for the reference's
+``StreamState`` / ``initialize`` / ``init_helpers``
+(/root/reference/pkg/src/p2stream/stream.py:36-407).
+
+Layout in HBM (torch owns every buffer; the C ABI only sees pointers):
+
+  W (Kcap, R), C (Kcap, R), D (Kcap, R, R)   per-slice rows, slice order = the
+                                             reference's registration order;
+                                             capacity doubles on growth
+  V, F (J, R), G (R, R)                      shared factors / global summaries
+  U history                                  one (N_t, R) device block per
+                                             update (+ one for the initial
+                                             factors); u_blocks / u_matrix
+                                             gather lazily
+  X staging                                  (Ncap, J) device buffer reused by
+                                             every update, fed from a pinned
+                                             host buffer
+
+``update(batch)`` validates ids on the host, registers new slices, packs the
+batch into CSR (rows in ``batch.items()`` order), and launches the whole pass
+loop through ``dash_update_f64``.  It then synchronises once to turn a device
+solver failure into ``SolveError(slice_id)`` like the reference.  Host views
+(``W``, ``V``, ``C``, ``D``, ``F``, ``G``, ``u_blocks``, ``UpdateResult.u_new``)
+are lazy copies, cached until the next mutation.
+"""
+from __future__ import annotations
+
+import ctypes
+import time
+from collections.abc import Mapping
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .als import ALSInfo, FactorSet
+from .linalg import RIDGE_EPS, SolveError
+from .tensor import IrregularTensor, UpdateBatch
+
+F64 = torch.float64
+
+
+def _dev(device) -> torch.device:
+    if device is None:
+        if not torch.cuda.is_available():
+            raise nat.NativeUnavailable("the DASH engine needs a CUDA device (B200); none is visible")
+        return torch.device("cuda", torch.cuda.current_device())
+    d = torch.device(device)
+    if d.type != "cuda":
+        raise ValueError("the DASH engine runs on CUDA devices only")
+    if d.index is None:
+        d = torch.device("cuda", torch.cuda.current_device())
+    return d
+
+
+def _to_dev(a, device) -> torch.Tensor:
+    if isinstance(a, torch.Tensor):
+        return a.to(device=device, dtype=F64).contiguous()
+    return torch.as_tensor(np.ascontiguousarray(np.asarray(a, dtype=float)), device=device)
+
+
+def _ptr(t) -> int:
+    return int(t.data_ptr()) if t is not None else 0
+
+
+@dataclass
+class HelperState:
+    """Helper summaries in per-slice map form (stream.py:36-53)."""
+
+    c: dict
+    D: dict
+    F: np.ndarray
+    G: np.ndarray
+    forgetting: float
+
+    def __post_init__(self):
+        if not 0.0 < self.forgetting <= 1.0:
+            raise ValueError("forgetting factor must lie in (0, 1]")
+
+
+class _UNew(Mapping):
+    """``UpdateResult.u_new``: slice id -> (n_k, R) rows, copied from the
+    device on first access (one D2H for the whole update)."""
+
+    def __init__(self, ids, row_ptr, U_dev):
+        self._ids = ids
+        self._index = {sid: k for k, sid in enumerate(ids)}
+        self._row_ptr = row_ptr
+        self._dev = U_dev
+        self._host = None
+
+    def _h(self):
+        if self._host is None:
+            self._host = self._dev.cpu().numpy()
+        return self._host
+
+    def __getitem__(self, sid):
+        k = self._index[sid]
+        return self._h()[self._row_ptr[k]:self._row_ptr[k + 1]]
+
+    def __iter__(self):
+        return iter(self._ids)
+
+    def __len__(self):
+        return len(self._ids)
+
+    @property
+    def device_tensor(self) -> torch.Tensor:
+        return self._dev
+
+
+@dataclass
+class UpdateResult:
+    """What one consumed batch produced (stream.py:167-181)."""
+
+    update_index: int
+    u_new: Mapping
+    new_slice_ids: list
+    rows_new: int
+    seconds: float
+    v_used: np.ndarray = None
+
+
+class _UBlocks(Mapping):
+    """``StreamState.u_blocks``: slice id -> list of (rows, R) host blocks."""
+
+    def __init__(self, state):
+        self._s = state
+
+    def __getitem__(self, sid):
+        return [self._s._block_host(ref) for ref in self._s._ublk[sid]]
+
+    def __contains__(self, sid):
+        return sid in self._s._ublk
+
+    def __iter__(self):
+        return iter(self._s._ublk)
+
+    def __len__(self):
+        return len(self._s._ublk)
+
+
+class StreamState:
+    """Factors plus helper summaries of a live stream, resident on one GPU
+    (stream.py:184-247).  Exclusively owned during an update."""
+
+    def __init__(self, slice_ids, u_blocks, W, V, C, D, F, G, forgetting,
+                 update_index: int = 0, passes: int = 1, device=None):
+        if not 0.0 < forgetting <= 1.0:
+            raise ValueError("forgetting factor must lie in (0, 1]")
+        if passes < 1:
+            raise ValueError("passes must be at least 1")
+        self.device = _dev(device)
+        self.forgetting = float(forgetting)
+        self.update_index = int(update_index)
+        self.passes = int(passes)
+        self.slice_ids = list(slice_ids)
+        self._row_of = {sid: k for k, sid in enumerate(self.slice_ids)}
+        V = _to_dev(V, self.device)
+        self.J, R = V.shape
+        if R > nat.MAX_RANK:
+            raise ValueError(f"rank {R} exceeds the engine's maximum {nat.MAX_RANK}")
+        self._R = R
+        self._V, self._F, self._G = V, _to_dev(F, self.device), _to_dev(G, self.device)
+        K = len(self.slice_ids)
+        self._K = K
+        cap = max(16, K + K // 4)
+        self._Wd = torch.empty((cap, R), dtype=F64, device=self.device)
+        self._Cd = torch.empty((cap, R), dtype=F64, device=self.device)
+        self._Dd = torch.empty((cap, R, R), dtype=F64, device=self.device)
+        if K:
+            self._Wd[:K] = _to_dev(W, self.device).reshape(K, R)
+            self._Cd[:K] = _to_dev(C, self.device).reshape(K, R)
+            self._Dd[:K] = _to_dev(D, self.device).reshape(K, R, R)
+        # U history: list of device blocks; per slice a list of (block, lo, hi)
+        self._ustore: list = []
+        self._uhost: dict = {}
+        self._ublk: dict = {}
+        if u_blocks is not None:
+            self._ingest_u_blocks(u_blocks)
+        self._X = None
+        self._Xpin = None
+        self._pin_event = None
+        self._cache: dict = {}
+        self._last = None  # last update's device batch (for local_error)
+        self._ctx = nat.context(self.device.index)
+
+    # -- construction helpers ----------------------------------------------
+    def _ingest_u_blocks(self, u_blocks):
+        sids = [s for s in self.slice_ids if s in u_blocks]
+        arrs, spans = [], []
+        off = 0
+        for sid in sids:
+            for blk in u_blocks[sid]:
+                a = np.asarray(blk, dtype=float).reshape(-1, self._R)
+                arrs.append(a)
+                spans.append((sid, off, off + a.shape[0]))
+                off += a.shape[0]
+        for sid in sids:
+            self._ublk.setdefault(sid, [])
+        if off:
+            dev = torch.as_tensor(np.concatenate(arrs), device=self.device)
+            self._ustore.append(dev)
+            bi = len(self._ustore) - 1
+            for sid, lo, hi in spans:
+                self._ublk[sid].append((bi, lo, hi))
+
+    @classmethod
+    def from_arrays(cls, arrays: dict, device=None, u_blocks=None) -> "StreamState":
+        """Build from a dict with slice_ids, W, V, C, D, F, G, forgetting
+        (e.g. ``workloads.planted_state``); U history starts empty unless
+        ``u_blocks`` is given."""
+        R = np.asarray(arrays["V"]).shape[1]
+        if u_blocks is None:
+            u_blocks = {sid: [np.zeros((0, R))] for sid in arrays["slice_ids"]}
+        return cls(arrays["slice_ids"], u_blocks, arrays["W"], arrays["V"], arrays["C"],
+                   arrays["D"], arrays["F"], arrays["G"], arrays["forgetting"],
+                   passes=arrays.get("passes", 1), device=device)
+
+    # -- reference attribute API --------------------------------------------
+    @property
+    def rank(self) -> int:
+        return self._R
+
+    def row_of(self, slice_id) -> int:
+        return self._row_of[slice_id]
+
+    def has_slice(self, slice_id) -> bool:
+        return slice_id in self._row_of
+
+    def _host(self, name, t):
+        v = self._cache.get(name)
+        if v is None:
+            v = t.cpu().numpy()
+            self._cache[name] = v
+        return v
+
+    @property
+    def W(self) -> np.ndarray:
+        return self._host("W", self._Wd[:self._K])
+
+    @W.setter
+    def W(self, value):
+        self._Wd[:self._K] = _to_dev(value, self.device).reshape(self._K, self._R)
+        self._cache.clear()
+
+    @property
+    def C(self) -> np.ndarray:
+        return self._host("C", self._Cd[:self._K])
+
+    @C.setter
+    def C(self, value):
+        self._Cd[:self._K] = _to_dev(value, self.device).reshape(self._K, self._R)
+        self._cache.clear()
+
+    @property
+    def D(self) -> np.ndarray:
+        return self._host("D", self._Dd[:self._K])
+
+    @D.setter
+    def D(self, value):
+        self._Dd[:self._K] = _to_dev(value, self.device).reshape(self._K, self._R, self._R)
+        self._cache.clear()
+
+    @property
+    def V(self) -> np.ndarray:
+        return self._host("V", self._V)
+
+    @V.setter
+    def V(self, value):
+        self._V = _to_dev(value, self.device)
+        self._cache.clear()
+
+    @property
+    def F(self) -> np.ndarray:
+        return self._host("F", self._F)
+
+    @F.setter
+    def F(self, value):
+        self._F = _to_dev(value, self.device)
+        self._cache.clear()
+
+    @property
+    def G(self) -> np.ndarray:
+        return self._host("G", self._G)
+
+    @G.setter
+    def G(self, value):
+        self._G = _to_dev(value, self.device)
+        self._cache.clear()
+
+    # device views (no copy)
+    @property
+    def device_tensors(self) -> dict:
+        K = self._K
+        return {"W": self._Wd[:K], "C": self._Cd[:K], "D": self._Dd[:K],
+                "V": self._V, "F": self._F, "G": self._G}
+
+    @property
+    def u_blocks(self) -> Mapping:
+        return _UBlocks(self)
+
+    def _block_host(self, ref):
+        bi, lo, hi = ref
+        h = self._uhost.get(bi)
+        if h is None:
+            h = self._ustore[bi].cpu().numpy()
+            self._uhost[bi] = h
+        return h[lo:hi]
+
+    def u_matrix(self, slice_id) -> np.ndarray:
+        blocks = self.u_blocks[slice_id]
+        return blocks[0].copy() if len(blocks) == 1 else np.vstack(blocks)
+
+    def factor_set(self) -> FactorSet:
+        return FactorSet(slice_ids=list(self.slice_ids),
+                         U={sid: self.u_matrix(sid) for sid in self.slice_ids},
+                         W=self.W.copy(), V=self.V.copy())
+
+    @property
+    def helpers(self) -> HelperState:
+        C, D = self.C, self.D
+        return HelperState(c={sid: C[k].copy() for k, sid in enumerate(self.slice_ids)},
+                           D={sid: D[k].copy() for k, sid in enumerate(self.slice_ids)},
+                           F=self.F.copy(), G=self.G.copy(), forgetting=self.forgetting)
+
+    # -- growth ---------------------------------------------------------------
+    def _reserve(self, K_new: int):
+        cap = self._Wd.shape[0]
+        if K_new <= cap:
+            return
+        ncap = max(K_new, cap * 2)
+        R = self._R
+        for name, shape in (("_Wd", (ncap, R)), ("_Cd", (ncap, R)), ("_Dd", (ncap, R, R))):
+            old = getattr(self, name)
+            new = torch.empty(shape, dtype=F64, device=self.device)
+            new[:self._K] = old[:self._K]
+            setattr(self, name, new)
+
+    def _stage_x(self, N: int):
+        J = self.J
+        if self._X is None or self._X.shape[0] < N:
+            cap = max(N, 1024, int(N * 1.25))
+            self._X = torch.empty((cap, J), dtype=F64, device=self.device)
+        if self._Xpin is None or self._Xpin.shape[0] < N:
+            cap = max(N, 1024, int(N * 1.25))
+            self._Xpin = torch.empty((cap, J), dtype=F64, pin_memory=True)
+            self._pin_event = None
+        if self._pin_event is not None:
+            self._pin_event.synchronize()  # previous H2D from the staging buffer is done
+        return self._Xpin, self._X
+
+    # -- the update -----------------------------------------------------------
+    def update(self, batch: UpdateBatch) -> UpdateResult:
+        """Consume one batch (stream.py:251-370): same validation, same
+        registration order, same results within FP64 rounding."""
+        return self._update_items(batch.items())
+
+    def _update_items(self, items, allreduce=None) -> UpdateResult:
+        started = time.perf_counter()
+        entries = []
+        for sid, rows, is_new in items:
+            if is_new and sid in self._row_of:
+                raise ValueError(f"batch declares known slice {sid!r} as new")
+            if not is_new and sid not in self._row_of:
+                raise ValueError(f"batch references unknown existing slice {sid!r}")
+            rows = np.asarray(rows, dtype=float)
+            if rows.ndim != 2 or rows.shape[1] != self.J:
+                raise ValueError(f"slice {sid!r}: rows must be (n, {self.J})")
+            entries.append((sid, rows, is_new))
+        new_ids = [sid for sid, _, is_new in entries if is_new]
+        M = len(entries)
+        counts = np.fromiter((r.shape[0] for _, r, _ in entries), dtype=np.int64, count=M)
+        row_ptr = np.zeros(M + 1, dtype=np.int64)
+        np.cumsum(counts, out=row_ptr[1:])
+        N = int(row_ptr[-1])
+        # registration (stream.py:270-280): new rows appended in batch order
+        self._reserve(self._K + len(new_ids))
+        for sid in new_ids:
+            self._row_of[sid] = len(self.slice_ids)
+            self.slice_ids.append(sid)
+        state_row = np.fromiter((self._row_of[sid] for sid, _, _ in entries), dtype=np.int32, count=M)
+        is_new = np.fromiter((1 if n else 0 for _, _, n in entries), dtype=np.uint8, count=M)
+        self._K += len(new_ids)
+
+        pin, X = self._stage_x(N)
+        if N:
+            np.concatenate([r for _, r, _ in entries], axis=0, out=pin.numpy()[:N])
+            X[:N].copy_(pin[:N], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            self._pin_event = ev
+        res = self._run(X, N, row_ptr, state_row, is_new, check=True,
+                        ids=[sid for sid, _, _ in entries], allreduce=allreduce)
+        U_dev, v_used = res
+        # U history
+        self._ustore.append(U_dev)
+        bi = len(self._ustore) - 1
+        for k, (sid, _, n) in enumerate(entries):
+            ref = (bi, int(row_ptr[k]), int(row_ptr[k + 1]))
+            if n:
+                self._ublk[sid] = [ref]
+            else:
+                self._ublk[sid].append(ref)
+        self.update_index += 1
+        ids = [sid for sid, _, _ in entries]
+        self._last = (ids, row_ptr, state_row, X, N, U_dev)
+        return UpdateResult(
+            update_index=self.update_index,
+            u_new=_UNew(ids, row_ptr, U_dev),
+            new_slice_ids=new_ids,
+            rows_new=N,
+            seconds=time.perf_counter() - started,
+            v_used=v_used.cpu().numpy(),
+        )
+
+    def update_packed(self, X: torch.Tensor, counts: np.ndarray, existing_rows: np.ndarray,
+                      new_ids: list, check: bool = False, allreduce=None):
+        """Device-resident fast path: ``X`` (N, J) already on this GPU in
+        batch order -- existing slices (state rows ``existing_rows``) then the
+        ``len(new_ids)`` new slices; ``counts`` their row counts.  No host sync
+        unless ``check``.  Returns (U_new (N, R), v_used (J, R)) device tensors."""
+        M_old = len(existing_rows)
+        L = len(new_ids)
+        M = M_old + L
+        counts = np.asarray(counts, dtype=np.int64)
+        row_ptr = np.zeros(M + 1, dtype=np.int64)
+        np.cumsum(counts, out=row_ptr[1:])
+        N = int(row_ptr[-1])
+        self._reserve(self._K + L)
+        state_row = np.empty(M, dtype=np.int32)
+        state_row[:M_old] = existing_rows
+        state_row[M_old:] = np.arange(self._K, self._K + L, dtype=np.int32)
+        for sid in new_ids:
+            self._row_of[sid] = len(self.slice_ids)
+            self.slice_ids.append(sid)
+        self._K += L
+        is_new = np.zeros(M, dtype=np.uint8)
+        is_new[M_old:] = 1
+        U_dev, v_used = self._run(X, N, row_ptr, state_row, is_new, check=check, ids=None,
+                                  allreduce=allreduce)
+        self.update_index += 1
+        self._last = (None, row_ptr, state_row, X, N, U_dev)
+        return U_dev, v_used
+
+    def _run(self, X, N, row_ptr, state_row, is_new, check, ids, allreduce=None):
+        dev = self.device
+        M = len(state_row)
+        rp_d, sr_d, nw_d = self._stage_meta(row_ptr, state_row, is_new)
+        U = torch.empty((max(N, 0), self._R), dtype=F64, device=dev)
+        v_used = torch.empty((self.J, self._R), dtype=F64, device=dev)
+        b = nat.DashBatch(X=_ptr(X), ldx=int(X.stride(0)) if N else self.J, N=N, M=M,
+                          row_ptr=_ptr(rp_d), row_ptr_host=row_ptr.ctypes.data,
+                          state_row=_ptr(sr_d), is_new=_ptr(nw_d))
+        s = nat.DashState(W=_ptr(self._Wd), C=_ptr(self._Cd), D=_ptr(self._Dd), V=_ptr(self._V),
+                          F=_ptr(self._F), G=_ptr(self._G), J=self.J, R=self._R,
+                          forgetting=self.forgetting, passes=self.passes)
+        L = nat.lib()
+        st = nat.stream_ptr()
+        if allreduce is None:
+            nat.check(L.dash_update_f64(self._ctx, st, ctypes.byref(b), ctypes.byref(s), _ptr(U),
+                                        _ptr(v_used), RIDGE_EPS), "dash_update_f64")
+        else:
+            # sharded: per pass, local fresh sums -> all-reduce -> replicated finish
+            fg = torch.empty(self.J * self._R + self._R * self._R, dtype=F64, device=dev)
+            for p in range(self.passes):
+                nat.check(L.dash_update_pass_begin_f64(self._ctx, st, ctypes.byref(b), ctypes.byref(s),
+                                                       _ptr(U), _ptr(v_used), RIDGE_EPS, p, _ptr(fg)),
+                          "dash_update_pass_begin_f64")
+                allreduce(fg)
+                nat.check(L.dash_update_pass_finish_f64(self._ctx, st, ctypes.byref(s), _ptr(fg),
+                                                        RIDGE_EPS), "dash_update_pass_finish_f64")
+        self._cache.clear()
+        self.last_launches = L.dash_ctx_last_launches(self._ctx)
+        if ids is not None:
+            self._err_ids = ids
+        if check:
+            self.check()
+        return U, v_used
+
+    def _stage_meta(self, row_ptr, state_row, is_new):
+        """Copy the CSR index arrays through a double-buffered pinned ring, so
+        the host never blocks on the previous update."""
+        M = len(state_row)
+        ring = getattr(self, "_meta_ring", None)
+        if ring is None or ring[0][1].shape[0] < M:
+            cap = max(256, int(M * 1.25) + 2)
+            ring = []
+            for _ in range(2):
+                ring.append([torch.empty(cap + 1, dtype=torch.int64, pin_memory=True),
+                             torch.empty(cap, dtype=torch.int32, pin_memory=True),
+                             torch.empty(cap, dtype=torch.uint8, pin_memory=True),
+                             torch.empty(cap + 1, dtype=torch.int64, device=self.device),
+                             torch.empty(cap, dtype=torch.int32, device=self.device),
+                             torch.empty(cap, dtype=torch.uint8, device=self.device),
+                             None])
+            self._meta_ring = ring
+            self._meta_i = 0
+        slot = ring[self._meta_i]
+        self._meta_i ^= 1
+        if slot[6] is not None:
+            slot[6].synchronize()
+        slot[0][:M + 1].numpy()[:] = row_ptr
+        slot[1][:M].numpy()[:] = state_row
+        slot[2][:M].numpy()[:] = is_new
+        slot[3][:M + 1].copy_(slot[0][:M + 1], non_blocking=True)
+        slot[4][:M].copy_(slot[1][:M], non_blocking=True)
+        slot[5][:M].copy_(slot[2][:M], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        slot[6] = ev
+        return slot[3], slot[4], slot[5]
+
+    def check(self):
+        """Synchronise and raise SolveError for a device-side solver failure."""
+        pos = ctypes.c_int64(0)
+        rc = nat.lib().dash_ctx_status(self._ctx, nat.stream_ptr(), ctypes.byref(pos))
+        if rc == nat.DASH_OK:
+            return
+        if rc == nat.DASH_E_CUDA:
+            raise RuntimeError("CUDA error during the DASH update")
+        p = pos.value
+        ids = getattr(self, "_err_ids", None)
+        sid = None if p < 0 or ids is None or p >= len(ids) else ids[p]
+        msg = ("singular normal equations" if rc == nat.DASH_E_SINGULAR
+               else "non-finite solution from normal equations")
+        raise SolveError(msg, sid)
+
+
+
+def init_helpers(tensor: IrregularTensor, factors: FactorSet, forgetting: float = 0.7,
+                 device=None) -> HelperState:
+    """stream.py:56-82 on the GPU: c_k, D_k per slice and F, G."""
+    dev = _dev(device)
+    res = _init_helpers_device(tensor, factors, dev)
+    C, D, F, G = (t.cpu().numpy() for t in res)
+    ids = [s.slice_id for s in tensor.slices]
+    return HelperState(c={sid: C[k] for k, sid in enumerate(ids)},
+                       D={sid: D[k] for k, sid in enumerate(ids)}, F=F, G=G,
+                       forgetting=forgetting)
+
+
+def _init_helpers_device(tensor, factors, dev):
+    slices = list(tensor.slices)
+    J = tensor.column_count
+    R = factors.rank
+    for s in slices:
+        if factors.U[s.slice_id].shape[0] != s.row_count:
+            raise ValueError(f"factor block {s.slice_id!r} does not match slice rows")
+    counts = np.array([s.row_count for s in slices], dtype=np.int64)
+    row_ptr = np.zeros(len(slices) + 1, dtype=np.int64)
+    np.cumsum(counts, out=row_ptr[1:])
+    X = torch.as_tensor(np.concatenate([s.rows for s in slices]), device=dev)
+    U = torch.as_tensor(np.concatenate([factors.U[s.slice_id] for s in slices]), device=dev)
+    W = torch.as_tensor(np.stack([factors.s_row(s.slice_id) for s in slices]), device=dev)
+    V = torch.as_tensor(np.ascontiguousarray(factors.V), device=dev)
+    return init_helpers_packed(X, row_ptr, U, W, V)
+
+
+def init_helpers_packed(X, row_ptr, U, W, V):
+    """init_helpers on device-resident CSR data; returns device (C, D, F, G)."""
+    dev = X.device
+    K = len(row_ptr) - 1
+    J, R = V.shape
+    rp_d = torch.as_tensor(row_ptr, device=dev)
+    C = torch.empty((K, R), dtype=F64, device=dev)
+    D = torch.empty((K, R, R), dtype=F64, device=dev)
+    F = torch.empty((J, R), dtype=F64, device=dev)
+    G = torch.empty((R, R), dtype=F64, device=dev)
+    b = nat.DashBatch(X=_ptr(X), ldx=int(X.stride(0)), N=int(row_ptr[-1]), M=K, row_ptr=_ptr(rp_d),
+                      row_ptr_host=row_ptr.ctypes.data, state_row=0, is_new=0)
+    L = nat.lib()
+    ctx = nat.context(dev.index)
+    nat.check(L.dash_init_helpers_f64(ctx, nat.stream_ptr(), ctypes.byref(b), _ptr(U), _ptr(W),
+                                      _ptr(V), J, R, _ptr(C), _ptr(D), _ptr(F), _ptr(G)),
+              "dash_init_helpers_f64")
+    return C, D, F, G
+
+
+def initialize(tensor: IrregularTensor, rank: int, iters: int = 10, seed: int = 0,
+               forgetting: float = 0.7, passes: int = 1, device=None):
+    """stream.py:383-407: parafac2_als fit, init_helpers, wrap as stream state."""
+    from .als import parafac2_als
+    dev = _dev(device)
+    factors, info = parafac2_als(tensor, rank, iters=iters, seed=seed, return_info=True, device=dev)
+    C, D, F, G = _init_helpers_device(tensor, factors, dev)
+    return StreamState(
+        slice_ids=list(factors.slice_ids),
+        u_blocks={sid: [factors.U[sid]] for sid in factors.slice_ids},
+        W=factors.W, V=factors.V, C=C, D=D, F=F, G=G,
+        forgetting=forgetting, update_index=0, passes=passes, device=dev,
+    ), info

@@ -1,0 +1,48 @@
+"""CPU-side checks of the C ABI: the library loads and exports every symbol
+include/dash_b200.h declares (no compute calls -- no GPU here)."""
+import re
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def header_symbols():
+    text = (ROOT / "include" / "dash_b200.h").read_text()
+    return sorted(set(re.findall(r"^\s*(?:int|void)\s+\*?\s*(dash_\w+)\s*\(", text, re.M)))
+
+
+def test_header_declares_the_update_entry_points():
+    syms = header_symbols()
+    for name in ("dash_update_f64", "dash_group_update_f64", "dash_ridge_solve_f64",
+                 "dash_init_helpers_f64", "dash_local_error_f64", "dash_ctx_create"):
+        assert name in syms
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2305_18376_b200 import _native
+    from paper_2305_18376_b200.build import build_library
+    build_library()
+    lib = _native.load_library()
+    for name in header_symbols():
+        assert hasattr(lib, name), name
+    assert set(header_symbols()) == set(_native.SIGNATURES)
+
+
+def test_product_path_refuses_to_run_without_cuda():
+    import torch
+    from paper_2305_18376_b200 import _native
+    if torch.cuda.is_available():
+        pytest.skip("CUDA present")
+    with pytest.raises(_native.NativeUnavailable):
+        _native.lib()
+
+
+def test_sm100a_cubin_in_library():
+    import subprocess
+    from paper_2305_18376_b200.build import build_library
+    so = build_library()
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", str(so)],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
