@@ -294,6 +294,7 @@ def run_gpu(args):
     cnt_arr = (ctypes.c_int32 * nph)()
     L.dash_ctx_phase_ms(state._ctx, ms_arr, cnt_arr, nph)
     L.dash_ctx_set_profiling(state._ctx, 0)
+    fallbacks = L.dash_ctx_fallbacks(state._ctx, nat.stream_ptr(), 1)
     state.check()
     t_ms = e1.elapsed_time(e0) if False else e0.elapsed_time(e1)
     t_max = t_ms
@@ -392,6 +393,7 @@ def run_gpu(args):
                     "d2h_bytes_per_step": d2h / max(len(e2e_b), 1),
                     "ms_per_step": e2e_ms / max(len(e2e_b), 1), "steps": len(e2e_b)},
             "gpu_launches": launches,
+            "lu_fallbacks": fallbacks,
             "clocks": clocks,
         }
     del batches

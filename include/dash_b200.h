@@ -55,6 +55,10 @@ int dash_ctx_status(dash_ctx *ctx, void *stream, int64_t *fail_slice_host);
  * gpu_launches figure). */
 int dash_ctx_last_launches(const dash_ctx *ctx);
 
+/* Number of ridge systems that needed the LU fallback (Cholesky failed or a
+ * non-finite solution) since the last reset; syncs `stream`. */
+int dash_ctx_fallbacks(dash_ctx *ctx, void *stream, int32_t reset);
+
 /* One update batch in CSR form: slice m (batch position) owns rows
  * [row_ptr[m], row_ptr[m+1]) of X.  Order = UpdateBatch.items() order
  * (tensor.py:166-171): existing slices, then new slices. */

@@ -54,6 +54,7 @@ SIGNATURES = {
                                                   ctypes.c_int32, _c_dp]),
     "dash_update_pass_finish_f64": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(DashState),
                                                    _c_dp, ctypes.c_double]),
+    "dash_ctx_fallbacks": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32]),
     "dash_ctx_set_profiling": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "dash_ctx_phase_ms": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
                                          ctypes.POINTER(ctypes.c_int32), ctypes.c_int32]),

@@ -258,9 +258,11 @@ int dash_init_helpers_f64(dash_ctx *ctx, void *stream, const dash_batch_f64 *t, 
     }
     const int64_t tot = (int64_t)J * R + R * R;
     if (ensure(ctx->fg, sizeof(double) * tot)) return DASH_E_CUDA;
-    k_sum_fg<<<(int)((tot + 255) / 256), 256, 0, st>>>((double *)ctx->fslots.p, (M > 0 && N > 0) ? (int)nsplit : 0,
-                                                        (double *)ctx->gslots.p, (M > 0 && N > 0) ? nblocks : 0, J, R,
-                                                        (double *)ctx->fg.p);
+    if (colsum(ctx, st, (double *)ctx->fslots.p, (M > 0 && N > 0) ? (int)nsplit : 0, (int64_t)J * R,
+               (double *)ctx->fg.p) ||
+        colsum(ctx, st, (double *)ctx->gslots.p, (M > 0 && N > 0) ? nblocks : 0, (int64_t)R * R,
+               (double *)ctx->fg.p + (int64_t)J * R))
+        return DASH_E_CUDA;
     k_finish_fg<<<(int)((tot + 255) / 256), 256, 0, st>>>((double *)ctx->fg.p, (double *)ctx->fsnap.p,
                                                            (double *)ctx->gsnap.p, 0.0, J, R, F, G);
     return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_E_CUDA;

@@ -33,10 +33,13 @@ __device__ __forceinline__ int warp_id() { return threadIdx.x >> 5; }
 
 __device__ __forceinline__ bool finite_d(double x) { return isfinite(x); }
 
-// Error slot (one u64, ~0 = none): key = ((batch position + 1) << 4) | code,
-// so atomicMin keeps the first failing slice (position -1 = the V solve).
+// Error slot (one u64, ~0 = none): key = (position << 4) | code, so atomicMin
+// keeps the first failing slice in batch order; the V solve (pos = -1) maps
+// to kPosV, after every slice, as in the reference where the V solve runs last.
+constexpr long long kPosV = 1ll << 40;
 __device__ __forceinline__ void report_error(unsigned long long *err, long long pos, int code) {
-    unsigned long long key = ((unsigned long long)(pos + 1) << 4) | (unsigned long long)code;
+    if (pos < 0) pos = kPosV;
+    unsigned long long key = ((unsigned long long)pos << 4) | (unsigned long long)code;
     atomicMin(err, key);
 }
 

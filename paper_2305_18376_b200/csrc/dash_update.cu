@@ -11,7 +11,7 @@
 //                G contribution  (warp-per-slice, CTA-per-big-slice; the two
 //                R x R ridge systems via warp Cholesky, LU fallback)
 //   k_fgemm      F partials = X^T (U o w_slice(row))   (DMMA, split over rows)
-//   k_sum_fg     fresh terms f, g = sums of the slots (fixed order)
+//   colsum       fresh terms f, g = sums of the slots (fixed two-level order)
 //   k_vsolve     F = lam F_snap + f, G = sym(lam G_snap + g), V = ridge_solve(G, F^T)^T
 //
 // All reductions use a fixed order (per-CTA slots summed in slot order), so
@@ -510,22 +510,30 @@ __global__ void __launch_bounds__(256) k_fgemm(const double *__restrict__ X, int
     }
 }
 
-// fg = [sum_s F slots | sum_items G slots] in slot order (the fresh terms
-// f_fresh, g_fresh of stream.py:306-322; raw sums, not yet decayed).
-__global__ void k_sum_fg(const double *__restrict__ F_slots, int nfs, const double *__restrict__ G_slots, int ngs,
-                         int J, int R, double *__restrict__ fg) {
-    const int64_t JR = (int64_t)J * R;
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < JR) {
-        double acc = 0.0;
-        for (int s = 0; s < nfs; ++s) acc += F_slots[s * JR + i];
-        fg[i] = acc;
-    } else if (i < JR + R * R) {
-        const int64_t pidx = i - JR;
-        double acc = 0.0;
-        for (int s = 0; s < ngs; ++s) acc += G_slots[(int64_t)s * R * R + pidx];
-        fg[i] = acc;
-    }
+// Column sums of a (nslots x width) slot matrix in fixed order, two levels:
+// k_colsum_part sums segments of kSeg slots, k_colsum_final sums segments.
+// Used for fg = [sum F slots | sum G slots] (the fresh terms f_fresh, g_fresh
+// of stream.py:306-322; raw, not yet decayed).
+constexpr int kSeg = 32;
+
+__global__ void k_colsum_part(const double *__restrict__ slots, int nslots, int64_t width,
+                              double *__restrict__ part) {
+    const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int seg = blockIdx.y;
+    if (col >= width) return;
+    const int s0 = seg * kSeg, s1 = min(nslots, s0 + kSeg);
+    double acc = 0.0;
+    for (int s = s0; s < s1; ++s) acc += slots[(int64_t)s * width + col];
+    part[(int64_t)seg * width + col] = acc;
+}
+
+__global__ void k_colsum_final(const double *__restrict__ part, int nseg, int64_t width,
+                               double *__restrict__ out) {
+    const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (col >= width) return;
+    double acc = 0.0;
+    for (int s = 0; s < nseg; ++s) acc += part[(int64_t)s * width + col];
+    out[col] = acc;
 }
 
 // Finish one pass (stream.py:344-346): F = lam F_snap + f, G = sym(lam G_snap
@@ -669,7 +677,7 @@ struct dash_ctx {
         void *p = nullptr;
         size_t cap = 0;
     };
-    Buf xv, row_slice, items, gslots, fslots, vtv, fsnap, gsnap, fg, scratch;
+    Buf xv, row_slice, items, gslots, fslots, vtv, fsnap, gsnap, fg, part, scratch;
     unsigned long long *err = nullptr;
     unsigned int *fallbacks = nullptr;
     int4 *items_host[2] = {nullptr, nullptr};
@@ -848,6 +856,21 @@ void launch_vsolve_t(dash_ctx *ctx, cudaStream_t st, const double *fg, double la
                                                     lam, J, R, eps, F, G, V, ctx->err, ctx->fallbacks);
 }
 
+// out[0:width] = column sums of slots (nslots x width), deterministic order
+int colsum(dash_ctx *ctx, cudaStream_t st, const double *slots, int nslots, int64_t width, double *out) {
+    const int nseg = std::max(1, (nslots + kSeg - 1) / kSeg);
+    if (ensure(ctx->part, sizeof(double) * nseg * width)) return DASH_E_CUDA;
+    double *part = (double *)ctx->part.p;
+    const int bx = (int)((width + 127) / 128);
+    if (nslots == 0) {
+        cudaMemsetAsync(out, 0, sizeof(double) * width, st);
+        return 0;
+    }
+    k_colsum_part<<<dim3(bx, nseg), 128, 0, st>>>(slots, nslots, width, part);
+    k_colsum_final<<<bx, 128, 0, st>>>(part, nseg, width, out);
+    return 0;
+}
+
 bool valid_state(const dash_state_f64 *s) {
     return s && s->R >= 1 && s->R <= DASH_MAX_RANK && s->J >= 1 && s->passes >= 1 && s->forgetting > 0.0 &&
            s->forgetting <= 1.0;
@@ -880,7 +903,7 @@ void dash_ctx_destroy(dash_ctx *ctx) {
     if (!ctx) return;
     cudaDeviceSynchronize();
     dash_ctx::Buf *bufs[] = {&ctx->xv,  &ctx->row_slice, &ctx->items, &ctx->gslots, &ctx->fslots,
-                             &ctx->vtv, &ctx->fsnap,     &ctx->gsnap, &ctx->fg,     &ctx->scratch};
+                             &ctx->vtv, &ctx->fsnap,     &ctx->gsnap, &ctx->fg,     &ctx->part, &ctx->scratch};
     for (auto *b : bufs)
         if (b->p) cudaFree(b->p);
     cudaFree(ctx->err);
@@ -904,11 +927,24 @@ int dash_ctx_status(dash_ctx *ctx, void *stream, int64_t *fail_slice_host) {
         if (fail_slice_host) *fail_slice_host = 0;
         return DASH_OK;
     }
-    if (fail_slice_host) *fail_slice_host = (int64_t)(key >> 4) - 1;
+    if (fail_slice_host) {
+        long long pos = (long long)(key >> 4);
+        *fail_slice_host = pos >= kPosV ? -1 : pos;
+    }
     return (int)(key & 15ull);
 }
 
 int dash_ctx_last_launches(const dash_ctx *ctx) { return ctx ? ctx->last_launches : 0; }
+
+int dash_ctx_fallbacks(dash_ctx *ctx, void *stream, int32_t reset) {
+    if (!ctx) return -1;
+    unsigned int v = 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaMemcpyAsync(&v, ctx->fallbacks, sizeof(v), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    if (reset) cudaMemsetAsync(ctx->fallbacks, 0, sizeof(unsigned int), st);
+    return (int)v;
+}
 
 int dash_ctx_set_profiling(dash_ctx *ctx, int enable) {
     if (!ctx) return DASH_E_ARG;
@@ -1000,10 +1036,10 @@ int dash_update_pass_begin_f64(dash_ctx *ctx, void *stream, const dash_batch_f64
                      Fsl);
     }
     {
-        const int64_t tot = (int64_t)J * R + R * R;
         PhaseScope ps(ctx, st, PH_SUMFG);
-        k_sum_fg<<<(int)((tot + 255) / 256), 256, 0, st>>>(Fsl, N > 0 ? (int)ctx->nsplit : 0, Gsl,
-                                                            N > 0 ? ctx->nitems : 0, J, R, fg_out);
+        if (colsum(ctx, st, Fsl, N > 0 ? (int)ctx->nsplit : 0, (int64_t)J * R, fg_out) ||
+            colsum(ctx, st, Gsl, N > 0 ? ctx->nitems : 0, (int64_t)R * R, fg_out + (int64_t)J * R))
+            return DASH_E_CUDA;
     }
     return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_E_CUDA;
 }
