@@ -21,6 +21,7 @@
  *   dash_init_helpers_f64   init_helpers                      stream.py:56-82
  *   dash_local_error_f64    local_error / slice_error         evaluate.py:93-118,
  *                                                             anomaly.py:23-42
+ *   dash_als_sweep_f64      parafac2_als sweep (initialize)    als.py:102-201
  */
 #ifndef DASH_B200_H
 #define DASH_B200_H
@@ -145,6 +146,18 @@ int dash_init_helpers_f64(dash_ctx *ctx, void *stream, const dash_batch_f64 *ten
 int dash_local_error_f64(dash_ctx *ctx, void *stream, const dash_batch_f64 *batch,
                          const double *U, const double *W, const double *V, int32_t J,
                          int32_t R, double *slice_err, double *tensor_err);
+
+/* One sweep of parafac2_als (als.py:153-190) over a tensor in CSR form
+ * (row_ptr over K slices, state_row unused): updates V (J,R), H (R,R), W (K,R)
+ * in place, writes the sweep's bases Q (N,R) (ALSInfo.projections) and the
+ * direct-form loss sum_k ||X_k - Q_k (H o W_k) V^T||^2 to *loss (device). */
+int dash_als_sweep_f64(dash_ctx *ctx, void *stream, const dash_batch_f64 *tensor, int32_t J,
+                       int32_t R, double *V, double *H, double *W, double *Q, double *loss,
+                       double eps);
+
+/* U = Q H for N rows (the final U_k = Q_k H of als.py:191-195). */
+int dash_als_project_f64(dash_ctx *ctx, void *stream, int64_t N, int32_t R, const double *Q,
+                         const double *H, double *U);
 
 #ifdef __cplusplus
 }

@@ -71,6 +71,10 @@ SIGNATURES = {
     "dash_local_error_f64": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(DashBatch),
                                             _c_dp, _c_dp, _c_dp, ctypes.c_int32, ctypes.c_int32,
                                             _c_dp, _c_dp]),
+    "dash_als_sweep_f64": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(DashBatch),
+                                          ctypes.c_int32, ctypes.c_int32] + [_c_dp] * 5 + [ctypes.c_double]),
+    "dash_als_project_f64": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
+                                            _c_dp, _c_dp, _c_dp]),
 }
 
 _lib = None

@@ -136,10 +136,13 @@ __global__ void k_mean(const double *__restrict__ v, int n, double *__restrict__
 }
 
 // Batched ridge_solve: system b = blockIdx.x, lanes over right-hand sides.
+// rhs / x entry (r, c) of system b at [b*n*m + r*rs + c*cs] (rs = m, cs = 1 for
+// the contiguous (B, n, m) layout; rs = 1, cs = n for the transposed F^T-style
+// right-hand sides of the V solves).
 template <int RB>
 __global__ void __launch_bounds__(32) k_ridge(const double *__restrict__ lhs, const double *__restrict__ rhs,
-                                              int n, int m, double eps, double *__restrict__ x,
-                                              unsigned long long *err) {
+                                              int n, int m, int64_t rs, int64_t cs, double eps,
+                                              double *__restrict__ x, unsigned long long *err) {
     constexpr int LD = RB + 1;
     __shared__ double Ls[RB * LD];
     __shared__ double dinv[RB];
@@ -177,7 +180,7 @@ __global__ void __launch_bounds__(32) k_ridge(const double *__restrict__ lhs, co
         const bool valid = c < m;
         double v[RB];
 #pragma unroll
-        for (int r = 0; r < RB; ++r) v[r] = (valid && r < n) ? rhs[b * n * m + (int64_t)r * m + c] : 0.0;
+        for (int r = 0; r < RB; ++r) v[r] = (valid && r < n) ? rhs[b * n * m + r * rs + c * cs] : 0.0;
         if (ok) {
             chol_solve_lane<RB>(Ls, LD, dinv, v);
         } else {
@@ -192,7 +195,7 @@ __global__ void __launch_bounds__(32) k_ridge(const double *__restrict__ lhs, co
 #pragma unroll
         for (int r = 0; r < RB; ++r)
             if (valid && r < n) {
-                x[b * n * m + (int64_t)r * m + c] = v[r];
+                x[b * n * m + r * rs + c * cs] = v[r];
                 fin = fin && finite_d(v[r]);
             }
         if (!fin) report_error(err, b, DASH_E_NONFINITE);
@@ -210,7 +213,7 @@ static void launch_helpers(cudaStream_t st, int nblocks, const int64_t *row_ptr,
 template <int RB>
 static void launch_ridge(cudaStream_t st, int B, const double *lhs, const double *rhs, int n, int m, double eps,
                          double *x, unsigned long long *err) {
-    k_ridge<RB><<<B, 32, 0, st>>>(lhs, rhs, n, m, eps, x, err);
+    k_ridge<RB><<<B, 32, 0, st>>>(lhs, rhs, n, m, (int64_t)m, (int64_t)1, eps, x, err);
 }
 
 }  // namespace

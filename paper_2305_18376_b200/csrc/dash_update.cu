@@ -1139,3 +1139,4 @@ int dash_group_update_f64(dash_ctx *ctx, void *stream, int32_t G, int32_t I, int
 }  // extern "C"
 
 #include "dash_aux.cuh"
+#include "dash_als.cuh"
