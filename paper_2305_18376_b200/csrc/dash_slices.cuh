@@ -1,0 +1,343 @@
+// k_slices2: the per-slice phase of one DASH update (_kernels.py:62-144),
+// designed for latency hiding:
+//
+//  * one slice per GROUP of RB lanes (RB = rank bucket 4/8/16/32), lane r of a
+//    group owns index r of every per-slice vector and row r of every R x R
+//    matrix -> 32/RB slices per warp in flight, 4 warps per CTA, several CTAs
+//    per SM;
+//  * both R x R ridge systems are inverted in place with the symmetric SWEEP
+//    operator (Goodnight), one pivot per step: the pivot column is gathered
+//    through 8 bytes of shared memory per lane, so a step is 1 STS + RB/2
+//    LDS.128 + RB FMAs -- no serial triangular solves.  sweep(A) over all
+//    pivots = -A^{-1};  U rows are then u_i = -(A^{-1} diag(s)) xv_i, one dot
+//    product per lane, and w = -B^{-1} c.  SPD pivots are the same as
+//    Cholesky's; a non-positive / non-finite pivot (or non-finite w) takes the
+//    reference's fallback: LU with partial pivoting (numpy solve), then
+//    SolveError on a zero pivot (stream.py:319-339, linalg.py:25-45);
+//  * control flow is warp-uniform (row loops run to the warp's max row count
+//    with per-group predicates), so plain __syncwarp() is safe.
+//
+// Items: {slice0, nslices, big, 0}.  Small items: each group takes slices
+// g, g+NG, ... of the item.  Big item (one slice): every group inverts A
+// (identical result), rows are interleaved over the groups, c / gram
+// partials are reduced in group order, group 0 solves for w.
+#pragma once
+
+// (included inside dash_update.cu's anonymous namespace)
+
+template <int RB>
+struct S2 {
+    static constexpr int NW = 4;             // warps per CTA
+    static constexpr int GPW = 32 / RB;      // groups per warp
+    static constexpr int NG = NW * GPW;      // groups per CTA
+    static constexpr int LDV = RB + 2;       // vtv row pitch (16B aligned rows)
+    static constexpr int LDL = RB + 1;       // LU scratch pitch
+    // per group: buf[RB] | gacc[RB*RB] | lu[RB*LDL] | piv[RB] (as doubles) | dn[RB*RB]
+    static constexpr int per_group = RB + RB * RB + RB * LDL + RB + RB * RB;
+    // shared: vtv[RB*LDV] | red[NG * RB * (RB+1)]
+    static constexpr int shared = RB * LDV + NG * RB * (RB + 1);
+    __host__ __device__ static constexpr size_t bytes() { return sizeof(double) * (shared + NG * per_group); }
+};
+
+// all lanes of the group publish one value, every lane reads the RB-vector
+template <int RB>
+__device__ __forceinline__ void group_gather(double v, double *buf, int r, double (&out)[RB]) {
+    buf[r] = v;
+    __syncwarp();
+#pragma unroll
+    for (int z = 0; z < RB; ++z) out[z] = buf[z];
+    __syncwarp();
+}
+
+// In-place sweep of every pivot of the row-distributed symmetric matrix
+// (lane r holds row r in a[]): a <- -A^{-1}.  Returns false on a
+// non-positive or non-finite pivot.
+template <int RB>
+__device__ __forceinline__ bool sweep_inverse(double (&a)[RB], double *buf, int r) {
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < RB; ++k) {
+        double col[RB];
+        group_gather<RB>(a[k], buf, r, col);  // col[z] = A[z][k] = A[k][z]
+        const double d = col[k];
+        ok = ok && (d > 0.0) && isfinite(d);
+        const double id = 1.0 / d;
+        const bool piv = (r == k);
+        const double f = a[k] * id;
+#pragma unroll
+        for (int z = 0; z < RB; ++z) {
+            if (z == k) continue;
+            a[z] = piv ? a[z] * id : fma(-f, col[z], a[z]);
+        }
+        a[k] = piv ? -id : f;
+    }
+    return ok;
+}
+
+// Fallback: -A^{-1} by LU with partial pivoting on lane 0 of the group
+// (A given by a[] rows), written back into a[].  Returns false if singular.
+template <int RB>
+__device__ __noinline__ bool lu_neg_inverse(double (&a)[RB], double *lu, int *piv, double *buf, int r, int R,
+                                            bool do_it) {
+    // stage the matrix
+    if (do_it && r < RB)
+#pragma unroll
+        for (int z = 0; z < RB; ++z) lu[r * S2<RB>::LDL + z] = a[z];
+    __syncwarp();
+    bool ok = true;
+    if (do_it && r == 0) ok = lu_factor_serial(lu, S2<RB>::LDL, R, piv);
+    __syncwarp();
+    // column c of the inverse: lane c solves A x = e_c on its own scratch (buf is too small;
+    // reuse the gacc-free tail of lu: each lane solves serially into registers via a local copy)
+    double x[RB];
+#pragma unroll
+    for (int z = 0; z < RB; ++z) x[z] = (z == r) ? 1.0 : 0.0;
+    if (do_it && r < R) lu_solve_serial(lu, S2<RB>::LDL, R, piv, x);
+    // x = column r of A^{-1} = row r (symmetric); padded rows stay identity
+    if (do_it) {
+#pragma unroll
+        for (int z = 0; z < RB; ++z) a[z] = (r < R && z < R) ? -x[z] : (z == r ? -1.0 : 0.0);
+    }
+    (void)buf;
+    return ok;
+}
+
+template <int RB>
+__global__ void __launch_bounds__(S2<RB>::NW * 32) k_slices2(SliceParams p) {
+    using S = S2<RB>;
+    constexpr int NG = S::NG, LDV = S::LDV;
+    extern __shared__ double sm[];
+    double *vtv_s = sm;
+    double *red = vtv_s + RB * LDV;
+    const int lane = lane_id(), w = warp_id();
+    const int r = lane % RB;                 // index within the group
+    const int gid = w * S::GPW + lane / RB;  // group id in the CTA
+    double *gb = sm + S::shared + gid * S::per_group;
+    double *buf = gb;
+    double *gacc = buf + RB;
+    double *lu = gacc + RB * RB;
+    int *piv = reinterpret_cast<int *>(lu + RB * S::LDL);
+    double *dns = lu + RB * S::LDL + RB;  // d_new rows, lane r owns dns[r*RB ..]
+    const int R = p.R;
+    for (int i = threadIdx.x; i < RB * LDV; i += blockDim.x) {
+        const int a = i / LDV, b = i % LDV;
+        vtv_s[i] = (a < R && b < R) ? p.vtv[a * R + b] : 0.0;
+    }
+#pragma unroll
+    for (int z = 0; z < RB; ++z) gacc[r * RB + z] = 0.0;
+    __syncthreads();
+    const double *vrow = vtv_s + r * LDV;  // row r of vtv (shared)
+
+    const int4 item = p.items[blockIdx.x];
+    const bool big = item.z != 0;
+    const int nsl = item.y;
+    const int rounds = big ? 1 : (nsl + NG - 1) / NG;
+
+    for (int round = 0; round < rounds; ++round) {
+        const int j = big ? 0 : round * NG + gid;
+        const bool active = j < nsl;
+        const int m = item.x + (active ? j : 0);
+        const int64_t r0 = p.row_ptr[m];
+        const int64_t n = active ? p.row_ptr[m + 1] - r0 : 0;
+        const int wrow = p.state_row[m];
+        const bool fresh = p.is_new[m] != 0;
+        const bool real = active && r < R;
+
+        // ---- A = vtv o s s^T + shift I  (_kernels.py:86-96), then a <- -A^{-1} diag(s)
+        const double s_r = real ? ((fresh && p.pass == 0) ? 1.0 : p.W[(int64_t)wrow * R + r]) : 0.0;
+        double s_all[RB];
+        group_gather<RB>(s_r, buf, r, s_all);
+        double a[RB];
+        {
+            double sh = 0.0;
+            for (int z = 0; z < R; ++z) sh += vtv_s[z * LDV + z] * s_all[z] * s_all[z];
+            sh = p.eps * sh / R;
+#pragma unroll
+            for (int z = 0; z < RB; ++z) {
+                double v = (r < R && z < R) ? vrow[z] * s_r * s_all[z] : (z == r ? 1.0 : 0.0);
+                if (z == r && r < R) v += sh;
+                a[z] = active ? v : (z == r ? 1.0 : 0.0);
+            }
+        }
+        bool okA = sweep_inverse<RB>(a, buf, r);
+        if (__any_sync(FULL_MASK, !okA)) {
+            // rebuild A for the failing groups and invert by LU (reference: numpy solve)
+            double sh = 0.0;
+            for (int z = 0; z < R; ++z) sh += vtv_s[z * LDV + z] * s_all[z] * s_all[z];
+            sh = p.eps * sh / R;
+#pragma unroll
+            for (int z = 0; z < RB; ++z) {
+                double v = (r < R && z < R) ? vrow[z] * s_r * s_all[z] : (z == r ? 1.0 : 0.0);
+                if (z == r && r < R) v += sh;
+                if (!okA) a[z] = v;
+            }
+            if (!okA && r == 0) atomicAdd(p.fallbacks, 1u);
+            const bool okLU = lu_neg_inverse<RB>(a, lu, piv, buf, r, R, !okA);
+            if (!okA && r == 0 && !okLU) report_error(p.err, m, DASH_E_SINGULAR);
+        }
+        group_gather<RB>(s_r, buf, r, s_all);
+#pragma unroll
+        for (int z = 0; z < RB; ++z) a[z] *= s_all[z];  // a = -A^{-1} diag(s)
+
+        // ---- rows: u_i = A^{-1}(s o xv_i); c and gram partials (_kernels.py:98-115)
+        double c = 0.0, gram[RB];
+#pragma unroll
+        for (int z = 0; z < RB; ++z) gram[z] = 0.0;
+        const int G_rows = big ? NG : 1;
+        const int g_off = big ? gid : 0;
+        int64_t my_n = big ? (n > g_off ? (n - g_off + G_rows - 1) / G_rows : 0) : n;
+        int64_t nmax = my_n;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) nmax = max(nmax, (int64_t)__shfl_xor_sync(FULL_MASK, (long long)nmax, off));
+        for (int64_t i = 0; i < nmax; ++i) {
+            const bool valid = i < my_n;
+            const int64_t row = r0 + g_off + i * G_rows;
+            const double *xr = p.XV + row * R;
+            double u = 0.0;
+            if (valid) {
+#pragma unroll
+                for (int z = 0; z < RB; ++z)
+                    if (z < R) u = fma(-a[z], __ldg(xr + z), u);
+            }
+            if (!(valid && r < R)) u = 0.0;
+            if (valid && r < R) {
+                p.U[row * R + r] = u;
+                c = fma(__ldg(xr + r), u, c);
+            }
+            double ua[RB];
+            group_gather<RB>(u, buf, r, ua);
+#pragma unroll
+            for (int z = 0; z < RB; ++z) gram[z] = fma(u, ua[z], gram[z]);
+        }
+
+        bool owner = true;
+        if (big) {
+            double *mine = red + gid * RB * (RB + 1) + r * (RB + 1);
+#pragma unroll
+            for (int z = 0; z < RB; ++z) mine[z] = gram[z];
+            mine[RB] = c;
+            __syncthreads();
+            owner = (gid == 0);
+            if (owner) {
+                c = 0.0;
+#pragma unroll
+                for (int z = 0; z < RB; ++z) gram[z] = 0.0;
+                for (int g2 = 0; g2 < NG; ++g2) {
+                    const double *o = red + g2 * RB * (RB + 1) + r * (RB + 1);
+#pragma unroll
+                    for (int z = 0; z < RB; ++z) gram[z] += o[z];
+                    c += o[RB];
+                }
+            }
+        }
+        // ---- c, D accumulation and the S-row system (_kernels.py:103-135)
+        // (warp-uniform: for big items only group 0's lanes are `owner`, in warp 0)
+        if (!big || w == 0) {
+            const bool live = owner && active;
+            const bool lreal = live && r < R;
+            const double cold = (lreal && !fresh) ? p.C[(int64_t)wrow * R + r] : 0.0;
+            const double cn = lreal ? p.lam * cold + c : 0.0;
+            double *dn = dns + r * RB;
+            double drr = 0.0;
+#pragma unroll
+            for (int z = 0; z < RB; ++z) {
+                double v = 0.0;
+                if (lreal && z < R) {
+                    const double dold = fresh ? 0.0 : p.D[(int64_t)wrow * R * R + r * R + z];
+                    v = p.lam * dold + gram[z];
+                }
+                dn[z] = v;
+                if (z == r) drr = v;
+            }
+            // shift += vtv[r,r] * d_new[r,r] in the reference's order (_kernels.py:121-124)
+            const double vrr = vrow[r];
+            double sh2;
+            {
+                double vdd[RB];
+                group_gather<RB>(lreal ? vrr * drr : 0.0, buf, r, vdd);
+                double dsum = 0.0;
+#pragma unroll
+                for (int z = 0; z < RB; ++z)
+                    if (z < R) dsum += vdd[z];
+                sh2 = p.eps * dsum / R;
+            }
+#pragma unroll
+            for (int z = 0; z < RB; ++z) {
+                double v = (lreal && z < R) ? vrow[z] * dn[z] : (z == r ? 1.0 : 0.0);
+                if (z == r && lreal) v += sh2;
+                a[z] = v;
+            }
+            bool okB = sweep_inverse<RB>(a, buf, r);
+            double call[RB];
+            group_gather<RB>(cn, buf, r, call);
+            double wv = 0.0;
+#pragma unroll
+            for (int z = 0; z < RB; ++z) wv = fma(-a[z], call[z], wv);
+            if (!lreal) wv = 0.0;
+            bool fin = isfinite(wv);
+            // group-wide verdict
+            bool gok = okB && fin;
+            {
+                unsigned bal = __ballot_sync(FULL_MASK, !gok);
+                const unsigned gmask = (RB == 32) ? FULL_MASK : (((1u << RB) - 1u) << ((lane / RB) * RB));
+                gok = (bal & gmask) == 0;
+            }
+            if (__any_sync(FULL_MASK, !gok && live)) {
+                const bool need = !gok && live;
+#pragma unroll
+                for (int z = 0; z < RB; ++z) {
+                    double v = (lreal && z < R) ? vrow[z] * dn[z] : (z == r ? 1.0 : 0.0);
+                    if (z == r && lreal) v += sh2;
+                    if (need) a[z] = v;
+                }
+                if (need && r == 0) atomicAdd(p.fallbacks, 1u);
+                const bool okLU = lu_neg_inverse<RB>(a, lu, piv, buf, r, R, need);
+                if (need && r == 0 && !okLU) report_error(p.err, m, DASH_E_SINGULAR);
+                double wv2 = 0.0;
+#pragma unroll
+                for (int z = 0; z < RB; ++z) wv2 = fma(-a[z], call[z], wv2);
+                if (need) wv = lreal ? wv2 : 0.0;
+                if (need && lreal && !isfinite(wv)) report_error(p.err, m, DASH_E_NONFINITE);
+            }
+            if (lreal) {
+                p.W[(int64_t)wrow * R + r] = wv;
+                if (p.final_pass) {
+                    p.C[(int64_t)wrow * R + r] = cn;
+#pragma unroll
+                    for (int z = 0; z < RB; ++z)
+                        if (z < R) p.D[(int64_t)wrow * R * R + r * R + z] = dn[z];
+                }
+            }
+            // ---- G contribution gram o w w^T (_kernels.py:139-143)
+            double wa[RB];
+            group_gather<RB>(wv, buf, r, wa);
+            if (live) {
+#pragma unroll
+                for (int z = 0; z < RB; ++z) gacc[r * RB + z] = fma(gram[z] * wv, wa[z], gacc[r * RB + z]);
+            }
+        }
+        if (big) __syncthreads();
+    }
+
+    // ---- per-CTA G slot: groups summed in order
+    __syncthreads();
+    double *slot = p.G_slots + (int64_t)blockIdx.x * R * R;
+    for (int i = threadIdx.x; i < R * R; i += blockDim.x) {
+        const int a = i / R, b = i % R;
+        double acc = 0.0;
+        for (int g2 = 0; g2 < NG; ++g2) acc += sm[S::shared + g2 * S::per_group + RB + a * RB + b];
+        slot[i] = acc;
+    }
+}
+
+template <int RB>
+int launch_slices2(cudaStream_t st, int nitems, const SliceParams &sp) {
+    const size_t smem = S2<RB>::bytes();
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_slices2<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    k_slices2<RB><<<nitems, S2<RB>::NW * 32, smem, st>>>(sp);
+    return cudaGetLastError() == cudaSuccess ? 0 : DASH_E_CUDA;
+}

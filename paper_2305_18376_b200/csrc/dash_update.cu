@@ -445,6 +445,8 @@ __global__ void __launch_bounds__(NW * 32) k_slices(SliceParams p) {
     }
 }
 
+#include "dash_slices.cuh"
+
 // ---------------------------------------------------------------------------
 // k_fgemm: F partial slot s = X[rows_s]^T (U o w)[rows_s], J-block of 64.
 // ---------------------------------------------------------------------------
@@ -760,7 +762,7 @@ int stage_items(dash_ctx *ctx, cudaStream_t st, const std::vector<int4> &items) 
 }
 
 // Host planning: contiguous batch positions -> CTA work items.
-void plan_items(const int64_t *row_ptr, int M, std::vector<int4> &items) {
+void plan_items(const int64_t *row_ptr, int M, std::vector<int4> &items, int per_item = kSlicesPerItem) {
     items.clear();
     int m = 0;
     while (m < M) {
@@ -771,7 +773,7 @@ void plan_items(const int64_t *row_ptr, int M, std::vector<int4> &items) {
             continue;
         }
         int start = m, cnt = 0;
-        while (m < M && cnt < kSlicesPerItem && (row_ptr[m + 1] - row_ptr[m]) <= kSmallRows) {
+        while (m < M && cnt < per_item && (row_ptr[m + 1] - row_ptr[m]) <= kSmallRows) {
             ++m;
             ++cnt;
         }
@@ -801,13 +803,18 @@ int launch_slices(dash_ctx *ctx, cudaStream_t st, int nitems, const SliceParams 
     return cudaGetLastError() == cudaSuccess ? 0 : DASH_E_CUDA;
 }
 
+int slices_per_item(int RB) { return RB <= 16 ? 2 * S2<16>::NW * (32 / RB) : kSlicesPerItem; }
+
 int dispatch_slices(dash_ctx *ctx, cudaStream_t st, int RB, int nitems, const SliceParams &sp) {
-    switch (RB) {
-        case 4: return launch_slices<4>(ctx, st, nitems, sp);
-        case 8: return launch_slices<8>(ctx, st, nitems, sp);
-        case 16: return launch_slices<16>(ctx, st, nitems, sp);
-        default: return launch_slices<32>(ctx, st, nitems, sp);
+    if (RB <= 16) {
+        PhaseScope ps(ctx, st, PH_SLICES);
+        switch (RB) {
+            case 4: return launch_slices2<4>(st, nitems, sp);
+            case 8: return launch_slices2<8>(st, nitems, sp);
+            default: return launch_slices2<16>(st, nitems, sp);
+        }
     }
+    return launch_slices<32>(ctx, st, nitems, sp);
 }
 
 template <int RP>
@@ -987,7 +994,7 @@ int dash_update_pass_begin_f64(dash_ctx *ctx, void *stream, const dash_batch_f64
     if (pass == 0) {
         ctx->last_launches = 0;
         std::vector<int4> items;
-        plan_items(b->row_ptr_host, M, items);
+        plan_items(b->row_ptr_host, M, items, slices_per_item(RB));
         ctx->nitems = (int)items.size();
         plan_fsplit(ctx, N, J, ctx->nsplit, ctx->rps);
         if (ensure(ctx->xv, sizeof(double) * std::max<int64_t>(N, 1) * R) ||
@@ -1083,7 +1090,7 @@ int dash_group_update_f64(dash_ctx *ctx, void *stream, int32_t G, int32_t I, int
     std::vector<int64_t> rp(G + 1);
     for (int g = 0; g <= G; ++g) rp[g] = (int64_t)g * I;
     std::vector<int4> items;
-    plan_items(rp.data(), G, items);
+    plan_items(rp.data(), G, items, slices_per_item(RB));
     const int nitems = (int)items.size();
     size_t need = sizeof(int64_t) * (G + 1) + sizeof(int32_t) * G + G + 64;
     if (ensure(ctx->scratch, need) || ensure(ctx->gslots, sizeof(double) * std::max(nitems, 1) * R * R))
