@@ -32,10 +32,15 @@ struct S2 {
     static constexpr int NG = NW * GPW;      // groups per CTA
     static constexpr int LDV = RB + 2;       // vtv row pitch (16B aligned rows)
     static constexpr int LDL = RB + 1;       // LU scratch pitch
-    // per group: buf[RB] | gacc[RB*RB] | lu[RB*LDL] | piv[RB] (as doubles) | dn[RB*RB]
-    static constexpr int per_group = RB + RB * RB + RB * LDL + RB + RB * RB;
-    // shared: vtv[RB*LDV] | red[NG * RB * (RB+1)]
-    static constexpr int shared = RB * LDV + NG * RB * (RB + 1);
+    static constexpr int CAPR = 128;         // XV rows staged per block
+    // per group: buf[RB] | gacc[RB*RB] | piv[RB] (as doubles) | dn[RB*RB]
+    static constexpr int per_group = RB + RB * RB + RB + RB * RB;
+    // union region (never live at the same time): staged XV rows [CAPR*RB] |
+    // big-item partials red[NG*RB*(RB+1)] | per-group LU scratch [NG*RB*LDL]
+    static constexpr int cmax(int a, int b) { return a > b ? a : b; }
+    static constexpr int uni = cmax(CAPR * RB, cmax(NG * RB * (RB + 1), NG * RB * LDL));
+    // shared: vtv[RB*LDV] | union | wsh[RB] (big item: w broadcast)
+    static constexpr int shared = RB * LDV + uni + RB;
     __host__ __device__ static constexpr size_t bytes() { return sizeof(double) * (shared + NG * per_group); }
 };
 
@@ -44,9 +49,32 @@ template <int RB>
 __device__ __forceinline__ void group_gather(double v, double *buf, int r, double (&out)[RB]) {
     buf[r] = v;
     __syncwarp();
+    const double2 *b2 = reinterpret_cast<const double2 *>(buf);  // buf is 16-byte aligned
 #pragma unroll
-    for (int z = 0; z < RB; ++z) out[z] = buf[z];
+    for (int z = 0; z < RB / 2; ++z) {
+        const double2 t = b2[z];
+        out[2 * z] = t.x;
+        out[2 * z + 1] = t.y;
+    }
     __syncwarp();
+}
+
+// 8-byte async global->shared copy (no register staging); completes at cp_async_wait()
+__device__ __forceinline__ void cp_async8(double *dst, const double *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+                 "l"(src));
+}
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_all;\n" ::); }
+
+// 1/d to within 1 ulp: hardware reciprocal seed + two Newton steps (no IEEE
+// division subroutine on the sweep's critical path)
+__device__ __forceinline__ double rcp_nr(double d) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+    double e = fma(-d, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-d, r, 1.0);
+    return fma(r, e, r);
 }
 
 // In-place sweep of every pivot of the row-distributed symmetric matrix
@@ -61,13 +89,16 @@ __device__ __forceinline__ bool sweep_inverse(double (&a)[RB], double *buf, int 
         group_gather<RB>(a[k], buf, r, col);  // col[z] = A[z][k] = A[k][z]
         const double d = col[k];
         ok = ok && (d > 0.0) && isfinite(d);
-        const double id = 1.0 / d;
+        const double id = rcp_nr(d);
         const bool piv = (r == k);
         const double f = a[k] * id;
+        // pivot row: a *= 1/d ; other rows: a -= (a_k/d) col   (one DMUL + one DFMA each)
+        const double alpha = piv ? id : 1.0;
+        const double beta = piv ? 0.0 : f;
 #pragma unroll
         for (int z = 0; z < RB; ++z) {
             if (z == k) continue;
-            a[z] = piv ? a[z] * id : fma(-f, col[z], a[z]);
+            a[z] = fma(-beta, col[z], a[z] * alpha);
         }
         a[k] = piv ? -id : f;
     }
@@ -102,8 +133,16 @@ __device__ __noinline__ bool lu_neg_inverse(double (&a)[RB], double *lu, int *pi
     return ok;
 }
 
+#ifdef DASH_DEBUG_TIMING
+__device__ long long g_dbg[8192 * 8];
+#define DBG_T(slot) do { if (threadIdx.x == 0 && blockIdx.x < 8192) g_dbg[blockIdx.x * 8 + (slot)] = clock64(); } while (0)
+#else
+#define DBG_T(slot) do {} while (0)
+#endif
+
 template <int RB>
-__global__ void __launch_bounds__(S2<RB>::NW * 32) k_slices2(SliceParams p) {
+__global__ void __launch_bounds__(S2<RB>::NW * 32, 3) k_slices2(SliceParams p) {
+    DBG_T(0);
     using S = S2<RB>;
     constexpr int NG = S::NG, LDV = S::LDV;
     extern __shared__ double sm[];
@@ -115,9 +154,11 @@ __global__ void __launch_bounds__(S2<RB>::NW * 32) k_slices2(SliceParams p) {
     double *gb = sm + S::shared + gid * S::per_group;
     double *buf = gb;
     double *gacc = buf + RB;
-    double *lu = gacc + RB * RB;
-    int *piv = reinterpret_cast<int *>(lu + RB * S::LDL);
-    double *dns = lu + RB * S::LDL + RB;  // d_new rows, lane r owns dns[r*RB ..]
+    int *piv = reinterpret_cast<int *>(gacc + RB * RB);
+    double *dns = gacc + RB * RB + RB;  // d_new rows, lane r owns dns[r*RB ..]
+    double *xs = red;                   // staged XV rows (union)
+    double *wsh = red + S::uni;         // big item: w broadcast to all groups
+    double *lu = red + gid * RB * S::LDL;  // LU scratch (union; used only outside the row phase)
     const int R = p.R;
     for (int i = threadIdx.x; i < RB * LDV; i += blockDim.x) {
         const int a = i / LDV, b = i % LDV;
@@ -132,6 +173,7 @@ __global__ void __launch_bounds__(S2<RB>::NW * 32) k_slices2(SliceParams p) {
     const bool big = item.z != 0;
     const int nsl = item.y;
     const int rounds = big ? 1 : (nsl + NG - 1) / NG;
+    DBG_T(1);
 
     for (int round = 0; round < rounds; ++round) {
         const int j = big ? 0 : round * NG + gid;
@@ -143,6 +185,15 @@ __global__ void __launch_bounds__(S2<RB>::NW * 32) k_slices2(SliceParams p) {
         const bool fresh = p.is_new[m] != 0;
         const bool real = active && r < R;
 
+        // prefetch this slice's D row (cp.async -> dns) and c_old; consumed after the rows
+        if (real && !fresh && (!big || gid == 0)) {
+            // D is exactly symmetric: lane r reads COLUMN r (= row r), so the 16 lanes
+            // of a group read 16 consecutive doubles per step (coalesced 128 B)
+            const double *dcol = p.D + (int64_t)wrow * R * R + r;
+            for (int z = 0; z < R; ++z) cp_async8(dns + r * RB + z, dcol + (int64_t)z * R);
+        }
+        const double cold_pf = (real && !fresh) ? p.C[(int64_t)wrow * R + r] : 0.0;
+
         // ---- A = vtv o s s^T + shift I  (_kernels.py:86-96), then a <- -A^{-1} diag(s)
         const double s_r = real ? ((fresh && p.pass == 0) ? 1.0 : p.W[(int64_t)wrow * R + r]) : 0.0;
         double s_all[RB];
@@ -152,14 +203,13 @@ __global__ void __launch_bounds__(S2<RB>::NW * 32) k_slices2(SliceParams p) {
             double sh = 0.0;
             for (int z = 0; z < R; ++z) sh += vtv_s[z * LDV + z] * s_all[z] * s_all[z];
             sh = p.eps * sh / R;
+            const double dg = real ? sh : 1.0;  // padded / idle rows: identity
 #pragma unroll
-            for (int z = 0; z < RB; ++z) {
-                double v = (r < R && z < R) ? vrow[z] * s_r * s_all[z] : (z == r ? 1.0 : 0.0);
-                if (z == r && r < R) v += sh;
-                a[z] = active ? v : (z == r ? 1.0 : 0.0);
-            }
+            for (int z = 0; z < RB; ++z) a[z] = vrow[z] * s_r * s_all[z] + ((z == r) ? dg : 0.0);
         }
+        if (round == 0) DBG_T(2);
         bool okA = sweep_inverse<RB>(a, buf, r);
+        if (round == 0) DBG_T(3);
         if (__any_sync(FULL_MASK, !okA)) {
             // rebuild A for the failing groups and invert by LU (reference: numpy solve)
             double sh = 0.0;
@@ -183,33 +233,91 @@ __global__ void __launch_bounds__(S2<RB>::NW * 32) k_slices2(SliceParams p) {
         double c = 0.0, gram[RB];
 #pragma unroll
         for (int z = 0; z < RB; ++z) gram[z] = 0.0;
-        const int G_rows = big ? NG : 1;
-        const int g_off = big ? gid : 0;
-        int64_t my_n = big ? (n > g_off ? (n - g_off + G_rows - 1) / G_rows : 0) : n;
-        int64_t nmax = my_n;
+        // rows of this round are contiguous in XV: stage them in blocks of CAPR
+        // rows with coalesced loads, then every group reads its rows from smem
+        const int64_t blk_lo = big ? r0 : p.row_ptr[item.x + round * NG];
+        const int64_t blk_hi = big ? r0 + n : p.row_ptr[min(item.x + (round + 1) * NG, item.x + nsl)];
+        for (int64_t base = blk_lo; base < blk_hi; base += S::CAPR) {
+            const int64_t hi = min(blk_hi, base + (int64_t)S::CAPR);
+            __syncthreads();
+            {
+                // rows staged with pitch RB (zero-padded when R < RB): 8 loads in flight per thread
+                const double *src = p.XV + base * R;
+                const int nrow = (int)(hi - base);
+                constexpr int NT = S::NW * 32, UNR = 8;
+                if (R == RB) {
+                    const int tot = nrow * RB;
+                    for (int e0 = threadIdx.x; e0 < tot; e0 += NT * UNR) {
+                        double v[UNR];
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) nmax = max(nmax, (int64_t)__shfl_xor_sync(FULL_MASK, (long long)nmax, off));
-        for (int64_t i = 0; i < nmax; ++i) {
-            const bool valid = i < my_n;
-            const int64_t row = r0 + g_off + i * G_rows;
-            const double *xr = p.XV + row * R;
-            double u = 0.0;
-            if (valid) {
+                        for (int q = 0; q < UNR; ++q) {
+                            const int e = e0 + q * NT;
+                            v[q] = e < tot ? __ldg(src + e) : 0.0;
+                        }
 #pragma unroll
-                for (int z = 0; z < RB; ++z)
-                    if (z < R) u = fma(-a[z], __ldg(xr + z), u);
+                        for (int q = 0; q < UNR; ++q) {
+                            const int e = e0 + q * NT;
+                            if (e < tot) xs[e] = v[q];
+                        }
+                    }
+                } else {
+                    const int tot = nrow * RB;
+                    for (int e0 = threadIdx.x; e0 < tot; e0 += NT * UNR) {
+                        double v[UNR];
+#pragma unroll
+                        for (int q = 0; q < UNR; ++q) {
+                            const int e = e0 + q * NT;
+                            const int rr = e / RB, z = e % RB;
+                            v[q] = (e < tot && z < R) ? __ldg(src + rr * R + z) : 0.0;
+                        }
+#pragma unroll
+                        for (int q = 0; q < UNR; ++q) {
+                            const int e = e0 + q * NT;
+                            if (e < tot) xs[e] = v[q];
+                        }
+                    }
+                }
             }
-            if (!(valid && r < R)) u = 0.0;
-            if (valid && r < R) {
-                p.U[row * R + r] = u;
-                c = fma(__ldg(xr + r), u, c);
+            __syncthreads();
+            int64_t lo_g, cnt;
+            if (big) {
+                lo_g = base + gid;
+                cnt = (hi > lo_g) ? (hi - lo_g + NG - 1) / NG : 0;
+            } else {
+                lo_g = max(r0, base);
+                cnt = max((int64_t)0, min(r0 + n, hi) - lo_g);
             }
-            double ua[RB];
-            group_gather<RB>(u, buf, r, ua);
+            int64_t nmax = cnt;
 #pragma unroll
-            for (int z = 0; z < RB; ++z) gram[z] = fma(u, ua[z], gram[z]);
+            for (int off = 16; off > 0; off >>= 1)
+                nmax = max(nmax, (int64_t)__shfl_xor_sync(FULL_MASK, (long long)nmax, off));
+            for (int64_t i = 0; i < nmax; ++i) {
+                const bool valid = i < cnt;
+                const int64_t row = big ? lo_g + i * NG : lo_g + i;
+                const double2 *xr2 = reinterpret_cast<const double2 *>(xs + (valid ? (row - base) * RB : 0));
+                double u = 0.0, xrr = 0.0;
+#pragma unroll
+                for (int z = 0; z < RB / 2; ++z) {
+                    const double2 t = xr2[z];
+                    u = fma(-a[2 * z], t.x, u);
+                    u = fma(-a[2 * z + 1], t.y, u);
+                    if (2 * z == r) xrr = t.x;
+                    if (2 * z + 1 == r) xrr = t.y;
+                }
+                if (!(valid && r < R)) u = 0.0;
+                if (valid && r < R) {
+                    p.U[row * R + r] = u;
+                    c = fma(xrr, u, c);
+                }
+                double ua[RB];
+                group_gather<RB>(u, buf, r, ua);
+#pragma unroll
+                for (int z = 0; z < RB; ++z) gram[z] = fma(u, ua[z], gram[z]);
+            }
         }
+        __syncthreads();
 
+        if (round == 0) DBG_T(4);
         bool owner = true;
         if (big) {
             double *mine = red + gid * RB * (RB + 1) + r * (RB + 1);
@@ -235,15 +343,17 @@ __global__ void __launch_bounds__(S2<RB>::NW * 32) k_slices2(SliceParams p) {
         if (!big || w == 0) {
             const bool live = owner && active;
             const bool lreal = live && r < R;
-            const double cold = (lreal && !fresh) ? p.C[(int64_t)wrow * R + r] : 0.0;
+            const double cold = (lreal && !fresh) ? cold_pf : 0.0;
             const double cn = lreal ? p.lam * cold + c : 0.0;
+            cp_async_wait();
+            __syncwarp();
             double *dn = dns + r * RB;
             double drr = 0.0;
 #pragma unroll
             for (int z = 0; z < RB; ++z) {
                 double v = 0.0;
                 if (lreal && z < R) {
-                    const double dold = fresh ? 0.0 : p.D[(int64_t)wrow * R * R + r * R + z];
+                    const double dold = fresh ? 0.0 : dn[z];
                     v = p.lam * dold + gram[z];
                 }
                 dn[z] = v;
@@ -261,13 +371,14 @@ __global__ void __launch_bounds__(S2<RB>::NW * 32) k_slices2(SliceParams p) {
                     if (z < R) dsum += vdd[z];
                 sh2 = p.eps * dsum / R;
             }
+            {
+                const double dg2 = lreal ? sh2 : 1.0;
 #pragma unroll
-            for (int z = 0; z < RB; ++z) {
-                double v = (lreal && z < R) ? vrow[z] * dn[z] : (z == r ? 1.0 : 0.0);
-                if (z == r && lreal) v += sh2;
-                a[z] = v;
+                for (int z = 0; z < RB; ++z) a[z] = vrow[z] * dn[z] + ((z == r) ? dg2 : 0.0);
             }
+            if (round == 0) DBG_T(5);
             bool okB = sweep_inverse<RB>(a, buf, r);
+            if (round == 0) DBG_T(6);
             double call[RB];
             group_gather<RB>(cn, buf, r, call);
             double wv = 0.0;
@@ -305,9 +416,20 @@ __global__ void __launch_bounds__(S2<RB>::NW * 32) k_slices2(SliceParams p) {
                     p.C[(int64_t)wrow * R + r] = cn;
 #pragma unroll
                     for (int z = 0; z < RB; ++z)
-                        if (z < R) p.D[(int64_t)wrow * R * R + r * R + z] = dn[z];
+                        if (z < R) p.D[(int64_t)wrow * R * R + (int64_t)z * R + r] = dn[z];  // column r (= row r)
                 }
             }
+            // ---- US = U o w for the F GEMM (small items: this group's own rows,
+            // re-read from the U it wrote; big items: after the w broadcast below)
+            if (p.US != nullptr && !big) {
+                int64_t nm = live ? n : 0, nmx = nm;
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1)
+                    nmx = max(nmx, (int64_t)__shfl_xor_sync(FULL_MASK, (long long)nmx, off));
+                for (int64_t i = 0; i < nmx; ++i)
+                    if (i < nm && lreal) p.US[(r0 + i) * R + r] = p.U[(r0 + i) * R + r] * wv;
+            }
+            if (big && owner && r < RB) wsh[r] = lreal ? wv : 0.0;
             // ---- G contribution gram o w w^T (_kernels.py:139-143)
             double wa[RB];
             group_gather<RB>(wv, buf, r, wa);
@@ -316,11 +438,19 @@ __global__ void __launch_bounds__(S2<RB>::NW * 32) k_slices2(SliceParams p) {
                 for (int z = 0; z < RB; ++z) gacc[r * RB + z] = fma(gram[z] * wv, wa[z], gacc[r * RB + z]);
             }
         }
-        if (big) __syncthreads();
+        if (big) {
+            __syncthreads();
+            if (p.US != nullptr) {
+                const double wr = (r < R) ? wsh[r] : 0.0;
+                for (int64_t row = r0 + gid; row < r0 + n; row += NG)
+                    if (r < R) p.US[row * R + r] = p.U[row * R + r] * wr;
+            }
+        }
     }
 
     // ---- per-CTA G slot: groups summed in order
     __syncthreads();
+    DBG_T(7);
     double *slot = p.G_slots + (int64_t)blockIdx.x * R * R;
     for (int i = threadIdx.x; i < R * R; i += blockDim.x) {
         const int a = i / R, b = i % R;

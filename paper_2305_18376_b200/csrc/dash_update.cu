@@ -141,6 +141,7 @@ struct SliceParams {
     const uint8_t *is_new;
     const double *XV;           // N x R
     double *U;                  // N x R
+    double *US;                 // N x R: U o w_slice (F-GEMM operand), may be null
     double *W, *C, *D;          // state rows
     const double *vtv;          // R x R
     double *G_slots;            // nitems x R x R
@@ -446,6 +447,7 @@ __global__ void __launch_bounds__(NW * 32) k_slices(SliceParams p) {
 }
 
 #include "dash_slices.cuh"
+#include "dash_stream.cuh"
 
 // ---------------------------------------------------------------------------
 // k_fgemm: F partial slot s = X[rows_s]^T (U o w)[rows_s], J-block of 64.
@@ -679,7 +681,7 @@ struct dash_ctx {
         void *p = nullptr;
         size_t cap = 0;
     };
-    Buf xv, row_slice, items, gslots, fslots, vtv, fsnap, gsnap, fg, part, scratch;
+    Buf xv, row_slice, items, gslots, fslots, vtv, fsnap, gsnap, fg, part, us, scratch;
     unsigned long long *err = nullptr;
     unsigned int *fallbacks = nullptr;
     int4 *items_host[2] = {nullptr, nullptr};
@@ -691,6 +693,7 @@ struct dash_ctx {
     // per-update plan, shared by the pass_begin calls of one update
     int nitems = 0;
     int64_t nsplit = 1, rps = 32;
+    bool stream = false;  // TMA-ring GEMM path for this update
     // phase timing (bench): events around every launch when enabled
     int prof = 0;
     std::vector<cudaEvent_t> ev_pool;
@@ -779,6 +782,8 @@ void plan_items(const int64_t *row_ptr, int M, std::vector<int4> &items, int per
         }
         items.push_back(make_int4(start, cnt, 0, 0));
     }
+    // big (one-CTA, long) items first so they do not form the grid's tail
+    std::stable_partition(items.begin(), items.end(), [](const int4 &it) { return it.z != 0; });
 }
 
 void plan_fsplit(dash_ctx *ctx, int64_t N, int J, int64_t &nsplit, int64_t &rps) {
@@ -878,6 +883,48 @@ int colsum(dash_ctx *ctx, cudaStream_t st, const double *slots, int nslots, int6
     return 0;
 }
 
+// ---- streaming (TMA ring) GEMM path: J, ldx, R even; ring fits in shared memory
+template <int RP>
+bool stream_ok_t(int J, int64_t ldx, int R) {
+    if ((J & 1) || (ldx & 1) || (R & 1)) return false;
+    const int JP = ((J + 7) / 8) * 8;
+    if ((JP / 8) * (RP / 8) > 64) return false;
+    const size_t lim = 220 * 1024;
+    return StreamSmem<RP>::xv_bytes(J) <= lim && StreamSmem<RP>::f_bytes(J) <= lim;
+}
+bool stream_ok(int J, int64_t ldx, int R) {
+    const int RB = rank_bucket(R);
+    if (RB > 16) return false;  // US is produced by k_slices2 (R <= 16)
+    return RB <= 8 ? stream_ok_t<8>(J, ldx, R) : stream_ok_t<16>(J, ldx, R);
+}
+
+template <int RP>
+void launch_xv2_t(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, const double *V, int R, double *XV) {
+    const size_t smem = StreamSmem<RP>::xv_bytes(J);
+    cudaFuncSetAttribute(k_xv2<RP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    PhaseScope ps(ctx, st, PH_XV);
+    k_xv2<RP><<<ctx->num_sms, kCW * 32 + 32, smem, st>>>(b->X, b->ldx, b->N, J, V, R, XV);
+}
+
+template <int RP, int MAXT>
+void launch_f2_tt(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, const double *US, int R,
+                  double *F_slots) {
+    const size_t smem = StreamSmem<RP>::f_bytes(J);
+    cudaFuncSetAttribute(k_fgemm2<RP, MAXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    PhaseScope ps(ctx, st, PH_FGEMM);
+    k_fgemm2<RP, MAXT><<<ctx->num_sms, kCW * 32 + 32, smem, st>>>(b->X, b->ldx, b->N, J, US, R, F_slots);
+}
+
+template <int RP>
+void launch_f2_t(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, const double *US, int R,
+                 double *F_slots) {
+    const int need = ((((J + 7) / 8) * (RP / 8)) + 7) / 8;
+    if (need <= 1) launch_f2_tt<RP, 1>(ctx, st, b, J, US, R, F_slots);
+    else if (need <= 2) launch_f2_tt<RP, 2>(ctx, st, b, J, US, R, F_slots);
+    else if (need <= 4) launch_f2_tt<RP, 4>(ctx, st, b, J, US, R, F_slots);
+    else launch_f2_tt<RP, 8>(ctx, st, b, J, US, R, F_slots);
+}
+
 bool valid_state(const dash_state_f64 *s) {
     return s && s->R >= 1 && s->R <= DASH_MAX_RANK && s->J >= 1 && s->passes >= 1 && s->forgetting > 0.0 &&
            s->forgetting <= 1.0;
@@ -910,7 +957,7 @@ void dash_ctx_destroy(dash_ctx *ctx) {
     if (!ctx) return;
     cudaDeviceSynchronize();
     dash_ctx::Buf *bufs[] = {&ctx->xv,  &ctx->row_slice, &ctx->items, &ctx->gslots, &ctx->fslots,
-                             &ctx->vtv, &ctx->fsnap,     &ctx->gsnap, &ctx->fg,     &ctx->part, &ctx->scratch};
+                             &ctx->vtv, &ctx->fsnap,     &ctx->gsnap, &ctx->fg,     &ctx->part, &ctx->us, &ctx->scratch};
     for (auto *b : bufs)
         if (b->p) cudaFree(b->p);
     cudaFree(ctx->err);
@@ -942,6 +989,13 @@ int dash_ctx_status(dash_ctx *ctx, void *stream, int64_t *fail_slice_host) {
 }
 
 int dash_ctx_last_launches(const dash_ctx *ctx) { return ctx ? ctx->last_launches : 0; }
+
+#ifdef DASH_DEBUG_TIMING
+int dash_debug_timing(long long *host, int n) {
+    cudaDeviceSynchronize();
+    return cudaMemcpyFromSymbol(host, g_dbg, sizeof(long long) * n) == cudaSuccess ? 0 : 2;
+}
+#endif
 
 int dash_ctx_fallbacks(dash_ctx *ctx, void *stream, int32_t reset) {
     if (!ctx) return -1;
@@ -996,12 +1050,15 @@ int dash_update_pass_begin_f64(dash_ctx *ctx, void *stream, const dash_batch_f64
         std::vector<int4> items;
         plan_items(b->row_ptr_host, M, items, slices_per_item(RB));
         ctx->nitems = (int)items.size();
+        ctx->stream = stream_ok(J, b->ldx, R) && N > 0;
         plan_fsplit(ctx, N, J, ctx->nsplit, ctx->rps);
+        if (ctx->stream) ctx->nsplit = ctx->num_sms;
         if (ensure(ctx->xv, sizeof(double) * std::max<int64_t>(N, 1) * R) ||
             ensure(ctx->row_slice, sizeof(int32_t) * std::max<int64_t>(N, 1)) ||
             ensure(ctx->gslots, sizeof(double) * std::max(ctx->nitems, 1) * R * R) ||
             ensure(ctx->fslots, sizeof(double) * ctx->nsplit * J * R) || ensure(ctx->vtv, sizeof(double) * R * R) ||
-            ensure(ctx->fsnap, sizeof(double) * J * R) || ensure(ctx->gsnap, sizeof(double) * R * R))
+            ensure(ctx->fsnap, sizeof(double) * J * R) || ensure(ctx->gsnap, sizeof(double) * R * R) ||
+            (ctx->stream && ensure(ctx->us, sizeof(double) * std::max<int64_t>(N, 1) * R)))
             return DASH_E_CUDA;
         if (ctx->nitems > 0 && stage_items(ctx, st, items)) return DASH_E_CUDA;
         if (M > 0) {
@@ -1018,7 +1075,12 @@ int dash_update_pass_begin_f64(dash_ctx *ctx, void *stream, const dash_batch_f64
                                       (double *)ctx->gsnap.p, v_used_out, pass == 0, last);
     }
     if (N > 0) {
-        launch_xv(ctx, st, b, J, s->V, R, XV);
+        if (ctx->stream) {
+            if (rank_bucket(R) <= 8) launch_xv2_t<8>(ctx, st, b, J, s->V, R, XV);
+            else launch_xv2_t<16>(ctx, st, b, J, s->V, R, XV);
+        } else {
+            launch_xv(ctx, st, b, J, s->V, R, XV);
+        }
         SliceParams sp;
         sp.items = (const int4 *)ctx->items.p;
         sp.row_ptr = b->row_ptr;
@@ -1026,6 +1088,7 @@ int dash_update_pass_begin_f64(dash_ctx *ctx, void *stream, const dash_batch_f64
         sp.is_new = b->is_new;
         sp.XV = XV;
         sp.U = U_out;
+        sp.US = ctx->stream ? (double *)ctx->us.p : nullptr;
         sp.W = s->W;
         sp.C = s->C;
         sp.D = s->D;
@@ -1039,8 +1102,13 @@ int dash_update_pass_begin_f64(dash_ctx *ctx, void *stream, const dash_batch_f64
         sp.pass = pass;
         sp.final_pass = last;
         if (dispatch_slices(ctx, st, RB, ctx->nitems, sp)) return DASH_E_CUDA;
-        launch_fgemm(ctx, st, b, J, U_out, (const int32_t *)ctx->row_slice.p, s->W, R, ctx->rps, (int)ctx->nsplit,
-                     Fsl);
+        if (ctx->stream) {
+            if (rank_bucket(R) <= 8) launch_f2_t<8>(ctx, st, b, J, (const double *)ctx->us.p, R, Fsl);
+            else launch_f2_t<16>(ctx, st, b, J, (const double *)ctx->us.p, R, Fsl);
+        } else {
+            launch_fgemm(ctx, st, b, J, U_out, (const int32_t *)ctx->row_slice.p, s->W, R, ctx->rps,
+                         (int)ctx->nsplit, Fsl);
+        }
     }
     {
         PhaseScope ps(ctx, st, PH_SUMFG);
@@ -1118,6 +1186,7 @@ int dash_group_update_f64(dash_ctx *ctx, void *stream, int32_t G, int32_t I, int
         sp.is_new = d_new_flag;
         sp.XV = xv;
         sp.U = u;
+        sp.US = nullptr;
         sp.W = w;
         sp.C = c_new;
         sp.D = d_new;
