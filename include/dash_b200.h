@@ -38,7 +38,8 @@ extern "C" {
 #define DASH_E_SINGULAR 3   /* a ridge system was singular (LU zero pivot)  */
 #define DASH_E_NONFINITE 4  /* a solve produced a non-finite value          */
 
-#define DASH_MAX_RANK 32
+#define DASH_MAX_RANK 64      /* update path (dash_update*, group_update)      */
+#define DASH_MAX_RANK_ALS 32  /* ALS sweep, init_helpers, ridge_solve           */
 
 typedef struct dash_ctx dash_ctx;
 
@@ -130,7 +131,7 @@ int dash_group_update_f64(dash_ctx *ctx, void *stream, int32_t G, int32_t I, int
                           double *g_fresh, int32_t *ok_host);
 
 /* ridge_solve for a batch of systems: x_b = (lhs_b + eps*mean(diag lhs_b) I)^-1 rhs_b,
- * lhs (B,n,n), rhs (B,n,m), x (B,n,m).  n <= DASH_MAX_RANK. */
+ * lhs (B,n,n), rhs (B,n,m), x (B,n,m).  n <= DASH_MAX_RANK_ALS. */
 int dash_ridge_solve_f64(dash_ctx *ctx, void *stream, int32_t B, int32_t n, int32_t m,
                          const double *lhs, const double *rhs, double *x, double eps);
 

@@ -30,8 +30,8 @@ def parafac2_als_gpu(tensor, rank: int, iters: int = 10, seed: int = 0, tol: flo
         raise ValueError(f"rank {rank} exceeds min(columns, shortest slice) = {min(J, min_rows)}")
     if iters < 1:
         raise ValueError("iters must be at least 1")
-    if rank > nat.MAX_RANK:
-        raise ValueError(f"rank {rank} exceeds the engine's maximum {nat.MAX_RANK}")
+    if rank > nat.MAX_RANK_ALS:
+        raise ValueError(f"rank {rank} exceeds the ALS engine's maximum {nat.MAX_RANK_ALS}")
     from .stream import _dev
     dev = _dev(device)
     K = len(slices)

@@ -485,7 +485,7 @@ extern "C" {
 
 int dash_als_sweep_f64(dash_ctx *ctx, void *stream, const dash_batch_f64 *t, int32_t J, int32_t R, double *V,
                        double *H, double *W, double *Q, double *loss, double eps) {
-    if (!ctx || !t || R < 1 || R > DASH_MAX_RANK || J < 1 || t->M < 1) return DASH_E_ARG;
+    if (!ctx || !t || R < 1 || R > DASH_MAX_RANK_ALS || J < 1 || t->M < 1) return DASH_E_ARG;
     cudaStream_t st = (cudaStream_t)stream;
     ctx->last_launches = 0;
     const int K = t->M;

@@ -222,7 +222,7 @@ extern "C" {
 
 int dash_init_helpers_f64(dash_ctx *ctx, void *stream, const dash_batch_f64 *t, const double *U, const double *W,
                           const double *V, int32_t J, int32_t R, double *C, double *D, double *F, double *G) {
-    if (!ctx || !t || R < 1 || R > DASH_MAX_RANK || J < 1) return DASH_E_ARG;
+    if (!ctx || !t || R < 1 || R > DASH_MAX_RANK_ALS || J < 1) return DASH_E_ARG;
     cudaStream_t st = (cudaStream_t)stream;
     ctx->last_launches = 0;
     const int RB = rank_bucket(R);
@@ -286,7 +286,7 @@ int dash_local_error_f64(dash_ctx *ctx, void *stream, const dash_batch_f64 *b, c
 
 int dash_ridge_solve_f64(dash_ctx *ctx, void *stream, int32_t B, int32_t n, int32_t m, const double *lhs,
                          const double *rhs, double *x, double eps) {
-    if (!ctx || B < 0 || n < 1 || n > DASH_MAX_RANK || m < 0) return DASH_E_ARG;
+    if (!ctx || B < 0 || n < 1 || n > DASH_MAX_RANK_ALS || m < 0) return DASH_E_ARG;
     if (B == 0 || m == 0) return DASH_OK;
     cudaStream_t st = (cudaStream_t)stream;
     switch (rank_bucket(n)) {

@@ -33,8 +33,9 @@ struct S2 {
     static constexpr int LDV = RB + 2;       // vtv row pitch (16B aligned rows)
     static constexpr int LDL = RB + 1;       // LU scratch pitch
     static constexpr int CAPR = 128;         // XV rows staged per block
-    // per group: buf[RB] | gacc[RB*RB] | piv[RB] (as doubles) | dn[RB*RB]
-    static constexpr int per_group = RB + RB * RB + RB + RB * RB;
+    static constexpr int CAPU = 16;          // u rows stashed per group (US write without re-reading U)
+    // per group: buf[RB] | gacc[RB*RB] | piv[RB] (as doubles) | dn[RB*RB] | ust[CAPU*RB]
+    static constexpr int per_group = RB + RB * RB + RB + RB * RB + CAPU * RB;
     // union region (never live at the same time): staged XV rows [CAPR*RB] |
     // big-item partials red[NG*RB*(RB+1)] | per-group LU scratch [NG*RB*LDL]
     static constexpr int cmax(int a, int b) { return a > b ? a : b; }
@@ -156,6 +157,7 @@ __global__ void __launch_bounds__(S2<RB>::NW * 32, 3) k_slices2(SliceParams p) {
     double *gacc = buf + RB;
     int *piv = reinterpret_cast<int *>(gacc + RB * RB);
     double *dns = gacc + RB * RB + RB;  // d_new rows, lane r owns dns[r*RB ..]
+    double *ust = dns + RB * RB;         // stashed u rows of a small slice
     double *xs = red;                   // staged XV rows (union)
     double *wsh = red + S::uni;         // big item: w broadcast to all groups
     double *lu = red + gid * RB * S::LDL;  // LU scratch (union; used only outside the row phase)
@@ -309,6 +311,7 @@ __global__ void __launch_bounds__(S2<RB>::NW * 32, 3) k_slices2(SliceParams p) {
                     p.U[row * R + r] = u;
                     c = fma(xrr, u, c);
                 }
+                if (!big && valid && row - r0 < S::CAPU) ust[(row - r0) * RB + r] = u;
                 double ua[RB];
                 group_gather<RB>(u, buf, r, ua);
 #pragma unroll
@@ -427,7 +430,8 @@ __global__ void __launch_bounds__(S2<RB>::NW * 32, 3) k_slices2(SliceParams p) {
                 for (int off = 16; off > 0; off >>= 1)
                     nmx = max(nmx, (int64_t)__shfl_xor_sync(FULL_MASK, (long long)nmx, off));
                 for (int64_t i = 0; i < nmx; ++i)
-                    if (i < nm && lreal) p.US[(r0 + i) * R + r] = p.U[(r0 + i) * R + r] * wv;
+                    if (i < nm && lreal)
+                        p.US[(r0 + i) * R + r] = (i < S::CAPU ? ust[i * RB + r] : p.U[(r0 + i) * R + r]) * wv;
             }
             if (big && owner && r < RB) wsh[r] = lreal ? wv : 0.0;
             // ---- G contribution gram o w w^T (_kernels.py:139-143)
@@ -442,6 +446,7 @@ __global__ void __launch_bounds__(S2<RB>::NW * 32, 3) k_slices2(SliceParams p) {
             __syncthreads();
             if (p.US != nullptr) {
                 const double wr = (r < R) ? wsh[r] : 0.0;
+#pragma unroll 8
                 for (int64_t row = r0 + gid; row < r0 + n; row += NG)
                     if (r < R) p.US[row * R + r] = p.U[row * R + r] * wr;
             }

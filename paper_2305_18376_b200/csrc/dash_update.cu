@@ -38,7 +38,7 @@ constexpr int kSlicesPerItem = 16; // small slices grouped per CTA
 constexpr int kFSplitRows = 1024;  // target rows per F-GEMM split
 
 __host__ __device__ inline int rank_bucket(int R) {
-    return R <= 4 ? 4 : R <= 8 ? 8 : R <= 16 ? 16 : 32;
+    return R <= 4 ? 4 : R <= 8 ? 8 : R <= 16 ? 16 : R <= 32 ? 32 : 64;
 }
 
 // ---------------------------------------------------------------------------
@@ -448,6 +448,7 @@ __global__ void __launch_bounds__(NW * 32) k_slices(SliceParams p) {
 
 #include "dash_slices.cuh"
 #include "dash_stream.cuh"
+#include "dash_slices_cta.cuh"
 
 // ---------------------------------------------------------------------------
 // k_fgemm: F partial slot s = X[rows_s]^T (U o w)[rows_s], J-block of 64.
@@ -808,7 +809,7 @@ int launch_slices(dash_ctx *ctx, cudaStream_t st, int nitems, const SliceParams 
     return cudaGetLastError() == cudaSuccess ? 0 : DASH_E_CUDA;
 }
 
-int slices_per_item(int RB) { return RB <= 16 ? 2 * S2<16>::NW * (32 / RB) : kSlicesPerItem; }
+int slices_per_item(int RB) { return RB <= 16 ? 2 * S2<16>::NW * (32 / RB) : RB <= 32 ? kSlicesPerItem : 1; }
 
 int dispatch_slices(dash_ctx *ctx, cudaStream_t st, int RB, int nitems, const SliceParams &sp) {
     if (RB <= 16) {
@@ -818,6 +819,17 @@ int dispatch_slices(dash_ctx *ctx, cudaStream_t st, int RB, int nitems, const Sl
             case 8: return launch_slices2<8>(st, nitems, sp);
             default: return launch_slices2<16>(st, nitems, sp);
         }
+    }
+    if (RB == 64) {
+        const size_t smem = SC<64>::bytes();
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_slices_cta<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            attr = true;
+        }
+        PhaseScope ps(ctx, st, PH_SLICES);
+        k_slices_cta<64><<<nitems, 256, smem, st>>>(sp);
+        return cudaGetLastError() == cudaSuccess ? 0 : DASH_E_CUDA;
     }
     return launch_slices<32>(ctx, st, nitems, sp);
 }
@@ -837,7 +849,8 @@ void launch_xv(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, c
     switch (rank_bucket(R) < 8 ? 8 : rank_bucket(R)) {
         case 8: launch_xv_t<8>(ctx, st, b, J, V, R, XV); break;
         case 16: launch_xv_t<16>(ctx, st, b, J, V, R, XV); break;
-        default: launch_xv_t<32>(ctx, st, b, J, V, R, XV); break;
+        case 32: launch_xv_t<32>(ctx, st, b, J, V, R, XV); break;
+        default: launch_xv_t<64>(ctx, st, b, J, V, R, XV); break;
     }
 }
 
@@ -854,7 +867,8 @@ void launch_fgemm(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J
     switch (rank_bucket(R) < 8 ? 8 : rank_bucket(R)) {
         case 8: launch_fgemm_t<8>(ctx, st, b, J, U, row_slice, W, R, rps, nsplit, F_slots); break;
         case 16: launch_fgemm_t<16>(ctx, st, b, J, U, row_slice, W, R, rps, nsplit, F_slots); break;
-        default: launch_fgemm_t<32>(ctx, st, b, J, U, row_slice, W, R, rps, nsplit, F_slots); break;
+        case 32: launch_fgemm_t<32>(ctx, st, b, J, U, row_slice, W, R, rps, nsplit, F_slots); break;
+        default: launch_fgemm_t<64>(ctx, st, b, J, U, row_slice, W, R, rps, nsplit, F_slots); break;
     }
 }
 
@@ -1127,7 +1141,16 @@ int dash_update_pass_finish_f64(dash_ctx *ctx, void *stream, dash_state_f64 *s, 
         case 4: launch_vsolve_t<4>(ctx, st, fg, s->forgetting, J, R, eps, s->F, s->G, s->V); break;
         case 8: launch_vsolve_t<8>(ctx, st, fg, s->forgetting, J, R, eps, s->F, s->G, s->V); break;
         case 16: launch_vsolve_t<16>(ctx, st, fg, s->forgetting, J, R, eps, s->F, s->G, s->V); break;
-        default: launch_vsolve_t<32>(ctx, st, fg, s->forgetting, J, R, eps, s->F, s->G, s->V); break;
+        case 32: launch_vsolve_t<32>(ctx, st, fg, s->forgetting, J, R, eps, s->F, s->G, s->V); break;
+        default: {
+            const size_t smem = sizeof(double) * (64 * SC<64>::LDM + SC<64>::NT + 64);
+            cudaFuncSetAttribute(k_vsolve_cta<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            PhaseScope ps(ctx, st, PH_VSOLVE);
+            k_vsolve_cta<64><<<(J + 31) / 32, 256, smem, st>>>(fg, (const double *)ctx->fsnap.p,
+                                                               (const double *)ctx->gsnap.p, s->forgetting, J, R, eps,
+                                                               s->F, s->G, s->V, ctx->err, ctx->fallbacks);
+            break;
+        }
     }
     return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_E_CUDA;
 }

@@ -127,6 +127,7 @@ def stream_parity(cfg, steps_check=None):
     ("large", dict(K0=120, steps=2, new_slices=3)),
     ("wide10", dict(K0=40, steps=2, new_slices=2)),
     ("wide32", dict(K0=40, steps=2, new_slices=2)),
+    ("wide64", dict(K0=30, steps=2, new_slices=2)),
 ])
 def test_config_shaped_streams_match_oracle(name, kw):
     from paper_2305_18376_b200 import workloads as wl
