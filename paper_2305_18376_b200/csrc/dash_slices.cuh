@@ -34,8 +34,9 @@ struct S2 {
     static constexpr int LDL = RB + 1;       // LU scratch pitch
     static constexpr int CAPR = 128;         // XV rows staged per block
     static constexpr int CAPU = 16;          // u rows stashed per group (US write without re-reading U)
-    // per group: buf[RB] | gacc[RB*RB] | piv[RB] (as doubles) | dn[RB*RB] | ust[CAPU*RB]
-    static constexpr int per_group = RB + RB * RB + RB + RB * RB + CAPU * RB;
+    // per group: buf[RB] | gacc[RB*LDL] | piv[RB] (as doubles) | dn[RB*LDL] | ust[CAPU*RB]
+    // (per-lane rows at the odd pitch LDL: conflict-free; +pad keeps group bases 16B-aligned)
+    static constexpr int per_group = RB + RB * LDL + RB + RB * LDL + CAPU * RB + ((RB * LDL * 2) & 1 ? 1 : 0);
     // union region (never live at the same time): staged XV rows [CAPR*RB] |
     // big-item partials red[NG*RB*(RB+1)] | per-group LU scratch [NG*RB*LDL]
     static constexpr int cmax(int a, int b) { return a > b ? a : b; }
@@ -106,31 +107,41 @@ __device__ __forceinline__ bool sweep_inverse(double (&a)[RB], double *buf, int 
     return ok;
 }
 
-// Fallback: -A^{-1} by LU with partial pivoting on lane 0 of the group
-// (A given by a[] rows), written back into a[].  Returns false if singular.
+// Fallback: -A^{-1} by LU with partial pivoting, for the groups with need
+// set.  The caller stages the RB x RB matrix rows into lu (lane r -> row r,
+// pitch LDL) and reads row r of the result back from lu afterwards; only
+// shared-memory pointers cross the call, so no register array is ever
+// materialised on the stack on the (common) path that never calls this.
 template <int RB>
-__device__ __noinline__ bool lu_neg_inverse(double (&a)[RB], double *lu, int *piv, double *buf, int r, int R,
-                                            bool do_it) {
-    // stage the matrix
-    if (do_it && r < RB)
-#pragma unroll
-        for (int z = 0; z < RB; ++z) lu[r * S2<RB>::LDL + z] = a[z];
+__device__ __noinline__ bool lu_neg_inverse_smem(double *lu, int *piv, int r, int R, bool need) {
+    constexpr int LDL = RB + 1;
     __syncwarp();
     bool ok = true;
-    if (do_it && r == 0) ok = lu_factor_serial(lu, S2<RB>::LDL, R, piv);
+    if (need && r == 0) ok = lu_factor_serial(lu, LDL, R, piv);
     __syncwarp();
-    // column c of the inverse: lane c solves A x = e_c on its own scratch (buf is too small;
-    // reuse the gacc-free tail of lu: each lane solves serially into registers via a local copy)
-    double x[RB];
-#pragma unroll
+    double x[RB];  // column r of A^{-1} (= row r, symmetric); local memory, fallback path only
     for (int z = 0; z < RB; ++z) x[z] = (z == r) ? 1.0 : 0.0;
-    if (do_it && r < R) lu_solve_serial(lu, S2<RB>::LDL, R, piv, x);
-    // x = column r of A^{-1} = row r (symmetric); padded rows stay identity
-    if (do_it) {
+    if (need && r < R) lu_solve_serial(lu, LDL, R, piv, x);
+    __syncwarp();
+    if (need)
+        for (int z = 0; z < RB; ++z) lu[r * LDL + z] = (r < R && z < R) ? -x[z] : (z == r ? -1.0 : 0.0);
+    __syncwarp();
+    return __shfl_sync(FULL_MASK, ok ? 1 : 0, (lane_id() / RB) * RB) != 0;
+}
+
+// stage a[] rows -> lu, invert (LU fallback), read back; warp-uniform call sites only
+template <int RB>
+__device__ __forceinline__ bool lu_fallback(double (&a)[RB], double *lu, int *piv, int r, int R, bool need) {
+    constexpr int LDL = RB + 1;
+    if (need) {
 #pragma unroll
-        for (int z = 0; z < RB; ++z) a[z] = (r < R && z < R) ? -x[z] : (z == r ? -1.0 : 0.0);
+        for (int z = 0; z < RB; ++z) lu[r * LDL + z] = a[z];
     }
-    (void)buf;
+    const bool ok = lu_neg_inverse_smem<RB>(lu, piv, r, R, need);
+    if (need) {
+#pragma unroll
+        for (int z = 0; z < RB; ++z) a[z] = lu[r * LDL + z];
+    }
     return ok;
 }
 
@@ -155,9 +166,9 @@ __global__ void __launch_bounds__(S2<RB>::NW * 32, 3) k_slices2(SliceParams p) {
     double *gb = sm + S::shared + gid * S::per_group;
     double *buf = gb;
     double *gacc = buf + RB;
-    int *piv = reinterpret_cast<int *>(gacc + RB * RB);
-    double *dns = gacc + RB * RB + RB;  // d_new rows, lane r owns dns[r*RB ..]
-    double *ust = dns + RB * RB;         // stashed u rows of a small slice
+    int *piv = reinterpret_cast<int *>(gacc + RB * S::LDL);
+    double *dns = gacc + RB * S::LDL + RB;  // d_new rows, lane r owns dns[r*LDL ..]
+    double *ust = dns + RB * S::LDL;     // stashed u rows of a small slice
     double *xs = red;                   // staged XV rows (union)
     double *wsh = red + S::uni;         // big item: w broadcast to all groups
     double *lu = red + gid * RB * S::LDL;  // LU scratch (union; used only outside the row phase)
@@ -167,7 +178,7 @@ __global__ void __launch_bounds__(S2<RB>::NW * 32, 3) k_slices2(SliceParams p) {
         vtv_s[i] = (a < R && b < R) ? p.vtv[a * R + b] : 0.0;
     }
 #pragma unroll
-    for (int z = 0; z < RB; ++z) gacc[r * RB + z] = 0.0;
+    for (int z = 0; z < RB; ++z) gacc[r * S::LDL + z] = 0.0;
     __syncthreads();
     const double *vrow = vtv_s + r * LDV;  // row r of vtv (shared)
 
@@ -192,7 +203,7 @@ __global__ void __launch_bounds__(S2<RB>::NW * 32, 3) k_slices2(SliceParams p) {
             // D is exactly symmetric: lane r reads COLUMN r (= row r), so the 16 lanes
             // of a group read 16 consecutive doubles per step (coalesced 128 B)
             const double *dcol = p.D + (int64_t)wrow * R * R + r;
-            for (int z = 0; z < R; ++z) cp_async8(dns + r * RB + z, dcol + (int64_t)z * R);
+            for (int z = 0; z < R; ++z) cp_async8(dns + r * S::LDL + z, dcol + (int64_t)z * R);
         }
         const double cold_pf = (real && !fresh) ? p.C[(int64_t)wrow * R + r] : 0.0;
 
@@ -203,7 +214,8 @@ __global__ void __launch_bounds__(S2<RB>::NW * 32, 3) k_slices2(SliceParams p) {
         double a[RB];
         {
             double sh = 0.0;
-            for (int z = 0; z < R; ++z) sh += vtv_s[z * LDV + z] * s_all[z] * s_all[z];
+            _Pragma("unroll") for (int z = 0; z < RB; ++z)  // compile-time bound: s_all stays in registers
+                if (z < R) sh += vtv_s[z * LDV + z] * s_all[z] * s_all[z];
             sh = p.eps * sh / R;
             const double dg = real ? sh : 1.0;  // padded / idle rows: identity
 #pragma unroll
@@ -215,7 +227,8 @@ __global__ void __launch_bounds__(S2<RB>::NW * 32, 3) k_slices2(SliceParams p) {
         if (__any_sync(FULL_MASK, !okA)) {
             // rebuild A for the failing groups and invert by LU (reference: numpy solve)
             double sh = 0.0;
-            for (int z = 0; z < R; ++z) sh += vtv_s[z * LDV + z] * s_all[z] * s_all[z];
+            _Pragma("unroll") for (int z = 0; z < RB; ++z)  // compile-time bound: s_all stays in registers
+                if (z < R) sh += vtv_s[z * LDV + z] * s_all[z] * s_all[z];
             sh = p.eps * sh / R;
 #pragma unroll
             for (int z = 0; z < RB; ++z) {
@@ -224,7 +237,7 @@ __global__ void __launch_bounds__(S2<RB>::NW * 32, 3) k_slices2(SliceParams p) {
                 if (!okA) a[z] = v;
             }
             if (!okA && r == 0) atomicAdd(p.fallbacks, 1u);
-            const bool okLU = lu_neg_inverse<RB>(a, lu, piv, buf, r, R, !okA);
+            const bool okLU = lu_fallback<RB>(a, lu, piv, r, R, !okA);
             if (!okA && r == 0 && !okLU) report_error(p.err, m, DASH_E_SINGULAR);
         }
         group_gather<RB>(s_r, buf, r, s_all);
@@ -350,7 +363,7 @@ __global__ void __launch_bounds__(S2<RB>::NW * 32, 3) k_slices2(SliceParams p) {
             const double cn = lreal ? p.lam * cold + c : 0.0;
             cp_async_wait();
             __syncwarp();
-            double *dn = dns + r * RB;
+            double *dn = dns + r * S::LDL;
             double drr = 0.0;
 #pragma unroll
             for (int z = 0; z < RB; ++z) {
@@ -405,7 +418,7 @@ __global__ void __launch_bounds__(S2<RB>::NW * 32, 3) k_slices2(SliceParams p) {
                     if (need) a[z] = v;
                 }
                 if (need && r == 0) atomicAdd(p.fallbacks, 1u);
-                const bool okLU = lu_neg_inverse<RB>(a, lu, piv, buf, r, R, need);
+                const bool okLU = lu_fallback<RB>(a, lu, piv, r, R, need);
                 if (need && r == 0 && !okLU) report_error(p.err, m, DASH_E_SINGULAR);
                 double wv2 = 0.0;
 #pragma unroll
@@ -439,7 +452,7 @@ __global__ void __launch_bounds__(S2<RB>::NW * 32, 3) k_slices2(SliceParams p) {
             group_gather<RB>(wv, buf, r, wa);
             if (live) {
 #pragma unroll
-                for (int z = 0; z < RB; ++z) gacc[r * RB + z] = fma(gram[z] * wv, wa[z], gacc[r * RB + z]);
+                for (int z = 0; z < RB; ++z) gacc[r * S::LDL + z] = fma(gram[z] * wv, wa[z], gacc[r * S::LDL + z]);
             }
         }
         if (big) {
@@ -460,7 +473,7 @@ __global__ void __launch_bounds__(S2<RB>::NW * 32, 3) k_slices2(SliceParams p) {
     for (int i = threadIdx.x; i < R * R; i += blockDim.x) {
         const int a = i / R, b = i % R;
         double acc = 0.0;
-        for (int g2 = 0; g2 < NG; ++g2) acc += sm[S::shared + g2 * S::per_group + RB + a * RB + b];
+        for (int g2 = 0; g2 < NG; ++g2) acc += sm[S::shared + g2 * S::per_group + RB + a * S::LDL + b];
         slot[i] = acc;
     }
 }

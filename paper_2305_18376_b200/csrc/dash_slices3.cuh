@@ -1,0 +1,241 @@
+// k_slices3: the per-slice phase (_kernels.py:62-144) for SMALL slices
+// (<= kSmallRows rows), persistent and warp-autonomous.
+//
+// k_slices2 ran every CTA in lock-step rounds separated by __syncthreads, so
+// each round's global-load latencies (metadata, W, D, XV) were exposed while
+// the FP64 pipe idled.  Here every warp owns a static stream of units (one
+// slice per RB-lane group, 32/RB slices per unit) and never waits for another
+// warp: it loads the unit's metadata, issues cp.async copies of the slices'
+// D columns and XV rows into its own shared staging, and runs the A-system
+// sweep while those copies are in flight.  CTA barriers appear only in the
+// prologue (vtv) and epilogue (per-CTA G slot, summed in fixed group order ->
+// deterministic).  Same sweep / LU-fallback / SolveError chain as k_slices2.
+// (included inside dash_update.cu's anonymous namespace)
+#pragma once
+
+template <int RB>
+struct S3 {
+    static constexpr int NW = 4;
+    static constexpr int GPW = 32 / RB;
+    static constexpr int NG = NW * GPW;
+    static constexpr int LDV = RB + 2;
+    static constexpr int LDL = RB + 1;
+    static constexpr int CAPW = 16;  // XV rows staged per group (longer slices read XV directly)
+    // per group: buf[RB] | gacc[RB*LDL] | dn[RB*LDL] | xs[CAPW*RB] | lu[RB*LDL] | piv[RB]
+    // (per-lane rows use the odd pitch LDL = RB+1: lane r's row r hits distinct banks)
+    static constexpr int per_group = RB + RB * LDL + RB * LDL + CAPW * RB + RB * LDL + RB + 2;  // even: 16B-aligned group bases
+    static constexpr int shared = RB * LDV;
+    __host__ __device__ static constexpr size_t bytes() { return sizeof(double) * (shared + NG * per_group); }
+};
+
+template <int RB>
+__global__ void __launch_bounds__(S3<RB>::NW * 32, 3) k_slices3(SliceParams p, const int32_t *__restrict__ small_pos,
+                                                                 int nsmall) {
+    using S = S3<RB>;
+    constexpr int LDV = S::LDV, GPW = S::GPW, CAPW = S::CAPW;
+    extern __shared__ __align__(16) double sm[];
+    double *vtv_s = sm;
+    const int lane = lane_id(), w = warp_id();
+    const int r = lane % RB;
+    const int gid = w * GPW + lane / RB;
+    double *buf = sm + S::shared + gid * S::per_group;
+    double *gacc = buf + RB;
+    double *dns = gacc + RB * S::LDL;
+    double *xs = dns + RB * S::LDL + 1;  // +1: keep xs 16-byte aligned
+    double *lu = xs + CAPW * RB;
+    int *piv = reinterpret_cast<int *>(lu + RB * S::LDL);
+    const int R = p.R;
+    for (int i = threadIdx.x; i < RB * LDV; i += blockDim.x) {
+        const int a = i / LDV, b = i % LDV;
+        vtv_s[i] = (a < R && b < R) ? p.vtv[a * R + b] : 0.0;
+    }
+#pragma unroll
+    for (int z = 0; z < RB; ++z) gacc[r * S::LDL + z] = 0.0;
+    __syncthreads();
+    const double *vrow = vtv_s + r * LDV;
+
+    const int nunits = (nsmall + GPW - 1) / GPW;
+    const int nwarps = gridDim.x * S::NW;
+    for (int unit = blockIdx.x * S::NW + w; unit < nunits; unit += nwarps) {
+        const int j = unit * GPW + lane / RB;
+        const bool active = j < nsmall;
+        const int m = small_pos[active ? j : 0];
+        const int64_t r0 = p.row_ptr[m];
+        const int64_t n = active ? p.row_ptr[m + 1] - r0 : 0;
+        const int wrow = p.state_row[m];
+        const bool fresh = p.is_new[m] != 0;
+        const bool real = active && r < R;
+        const bool staged = n <= CAPW;
+        // ---- async prefetch: D column r (D symmetric; coalesced) and the XV rows
+        if (real && !fresh) {
+            const double *dcol = p.D + (int64_t)wrow * R * R + r;
+            for (int z = 0; z < R; ++z) cp_async8(dns + r * S::LDL + z, dcol + (int64_t)z * R);
+        }
+        if (real && staged)
+            for (int i = 0; i < (int)n; ++i) cp_async8(xs + i * RB + r, p.XV + (r0 + i) * R + r);
+        const double cold = (real && !fresh) ? p.C[(int64_t)wrow * R + r] : 0.0;
+
+        // ---- A = vtv o s s^T + shift I, a <- -A^{-1} diag(s)  (_kernels.py:86-97)
+        const double s_r = real ? ((fresh && p.pass == 0) ? 1.0 : p.W[(int64_t)wrow * R + r]) : 0.0;
+        double s_all[RB];
+        group_gather<RB>(s_r, buf, r, s_all);
+        double sh = 0.0;
+        _Pragma("unroll") for (int z = 0; z < RB; ++z)  // compile-time bound: s_all stays in registers
+                if (z < R) sh += vtv_s[z * LDV + z] * s_all[z] * s_all[z];
+        sh = p.eps * sh / R;
+        double a[RB];
+        {
+            const double dg = real ? sh : 1.0;
+#pragma unroll
+            for (int z = 0; z < RB; ++z) a[z] = vrow[z] * s_r * s_all[z] + ((z == r) ? dg : 0.0);
+        }
+        const bool okA = sweep_inverse<RB>(a, buf, r);
+        if (__any_sync(FULL_MASK, !okA)) {
+            const double dg = real ? sh : 1.0;
+#pragma unroll
+            for (int z = 0; z < RB; ++z)
+                if (!okA) a[z] = vrow[z] * s_r * s_all[z] + ((z == r) ? dg : 0.0);
+            if (!okA && r == 0) atomicAdd(p.fallbacks, 1u);
+            const bool okLU = lu_fallback<RB>(a, lu, piv, r, R, !okA);
+            if (!okA && r == 0 && !okLU) report_error(p.err, m, DASH_E_SINGULAR);
+        }
+        group_gather<RB>(s_r, buf, r, s_all);
+#pragma unroll
+        for (int z = 0; z < RB; ++z) a[z] *= s_all[z];
+        cp_async_wait();
+        __syncwarp();
+
+        // ---- rows (_kernels.py:98-115): u, U, c, gram; u stashed over its xs row
+        double c = 0.0, gram[RB];
+#pragma unroll
+        for (int z = 0; z < RB; ++z) gram[z] = 0.0;
+        int64_t nmax = n;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1)
+            nmax = max(nmax, (int64_t)__shfl_xor_sync(FULL_MASK, (long long)nmax, off));
+        for (int64_t i = 0; i < nmax; ++i) {
+            const bool valid = i < n;
+            double u = 0.0, xrr = 0.0;
+            if (valid) {
+                if (staged) {
+                    const double *xr = xs + i * RB;
+#pragma unroll
+                    for (int z = 0; z < RB; ++z)
+                        if (z < R) u = fma(-a[z], xr[z], u);
+                    xrr = r < R ? xr[r] : 0.0;
+                } else {
+                    const double *xr = p.XV + (r0 + i) * R;
+#pragma unroll
+                    for (int z = 0; z < RB; ++z)
+                        if (z < R) u = fma(-a[z], __ldg(xr + z), u);
+                    xrr = r < R ? __ldg(xr + r) : 0.0;
+                }
+            }
+            if (!(valid && r < R)) u = 0.0;
+            if (valid && r < R) {
+                p.U[(r0 + i) * R + r] = u;
+                c = fma(xrr, u, c);
+            }
+            double ua[RB];
+            group_gather<RB>(u, buf, r, ua);
+#pragma unroll
+            for (int z = 0; z < RB; ++z) gram[z] = fma(u, ua[z], gram[z]);
+            if (valid && staged) xs[i * RB + r] = u;  // all lanes read row i before the gather's sync
+        }
+
+        // ---- c, D accumulation and the S-row system (_kernels.py:103-135)
+        const double cn = real ? p.lam * cold + c : 0.0;
+        double *dn = dns + r * S::LDL;
+        double drr = 0.0;
+#pragma unroll
+        for (int z = 0; z < RB; ++z) {
+            double v = 0.0;
+            if (real && z < R) v = p.lam * (fresh ? 0.0 : dn[z]) + gram[z];
+            dn[z] = v;
+            if (z == r) drr = v;
+        }
+        double sh2;
+        {
+            double vdd[RB];
+            group_gather<RB>(real ? vrow[r] * drr : 0.0, buf, r, vdd);
+            double dsum = 0.0;
+#pragma unroll
+            for (int z = 0; z < RB; ++z)
+                if (z < R) dsum += vdd[z];
+            sh2 = p.eps * dsum / R;
+        }
+        {
+            const double dg2 = real ? sh2 : 1.0;
+#pragma unroll
+            for (int z = 0; z < RB; ++z) a[z] = vrow[z] * dn[z] + ((z == r) ? dg2 : 0.0);
+        }
+        const bool okB = sweep_inverse<RB>(a, buf, r);
+        double call[RB];
+        group_gather<RB>(cn, buf, r, call);
+        double wv = 0.0;
+#pragma unroll
+        for (int z = 0; z < RB; ++z) wv = fma(-a[z], call[z], wv);
+        if (!real) wv = 0.0;
+        bool gok = okB && isfinite(wv);
+        {
+            const unsigned bal = __ballot_sync(FULL_MASK, !gok);
+            const unsigned gmask = (RB == 32) ? FULL_MASK : (((1u << RB) - 1u) << ((lane / RB) * RB));
+            gok = (bal & gmask) == 0;
+        }
+        if (__any_sync(FULL_MASK, !gok && active)) {
+            const bool need = !gok && active;
+            const double dg2 = real ? sh2 : 1.0;
+#pragma unroll
+            for (int z = 0; z < RB; ++z)
+                if (need) a[z] = vrow[z] * dn[z] + ((z == r) ? dg2 : 0.0);
+            if (need && r == 0) atomicAdd(p.fallbacks, 1u);
+            const bool okLU = lu_fallback<RB>(a, lu, piv, r, R, need);
+            if (need && r == 0 && !okLU) report_error(p.err, m, DASH_E_SINGULAR);
+            double wv2 = 0.0;
+#pragma unroll
+            for (int z = 0; z < RB; ++z) wv2 = fma(-a[z], call[z], wv2);
+            if (need) wv = real ? wv2 : 0.0;
+            if (need && real && !isfinite(wv)) report_error(p.err, m, DASH_E_NONFINITE);
+        }
+        if (real) {
+            p.W[(int64_t)wrow * R + r] = wv;
+            if (p.final_pass) {
+                p.C[(int64_t)wrow * R + r] = cn;
+#pragma unroll
+                for (int z = 0; z < RB; ++z)
+                    if (z < R) p.D[(int64_t)wrow * R * R + (int64_t)z * R + r] = dn[z];  // column r
+            }
+            if (p.US != nullptr)
+                for (int64_t i = 0; i < n; ++i)
+                    p.US[(r0 + i) * R + r] = (staged ? xs[i * RB + r] : p.U[(r0 + i) * R + r]) * wv;
+        }
+        double wa[RB];
+        group_gather<RB>(wv, buf, r, wa);
+        if (active) {
+#pragma unroll
+            for (int z = 0; z < RB; ++z) gacc[r * S::LDL + z] = fma(gram[z] * wv, wa[z], gacc[r * S::LDL + z]);
+        }
+        __syncwarp();
+    }
+    // ---- per-CTA G slot, groups in order
+    __syncthreads();
+    double *slot = p.G_slots + (int64_t)blockIdx.x * R * R;
+    for (int i = threadIdx.x; i < R * R; i += blockDim.x) {
+        const int a = i / R, b = i % R;
+        double acc = 0.0;
+        for (int g2 = 0; g2 < S::NG; ++g2) acc += sm[S::shared + g2 * S::per_group + RB + a * S::LDL + b];
+        slot[i] = acc;
+    }
+}
+
+template <int RB>
+int launch_slices3(cudaStream_t st, int grid, const SliceParams &sp, const int32_t *small_pos, int nsmall) {
+    const size_t smem = S3<RB>::bytes();
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_slices3<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    k_slices3<RB><<<grid, S3<RB>::NW * 32, smem, st>>>(sp, small_pos, nsmall);
+    return cudaGetLastError() == cudaSuccess ? 0 : DASH_E_CUDA;
+}

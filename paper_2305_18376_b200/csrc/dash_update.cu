@@ -449,6 +449,7 @@ __global__ void __launch_bounds__(NW * 32) k_slices(SliceParams p) {
 #include "dash_slices.cuh"
 #include "dash_stream.cuh"
 #include "dash_slices_cta.cuh"
+#include "dash_slices3.cuh"
 
 // ---------------------------------------------------------------------------
 // k_fgemm: F partial slot s = X[rows_s]^T (U o w)[rows_s], J-block of 64.
@@ -695,6 +696,7 @@ struct dash_ctx {
     int nitems = 0;
     int64_t nsplit = 1, rps = 32;
     bool stream = false;  // TMA-ring GEMM path for this update
+    void *plan_p = nullptr;  // SlicePlan of the update in flight
     // phase timing (bench): events around every launch when enabled
     int prof = 0;
     std::vector<cudaEvent_t> ev_pool;
@@ -832,6 +834,68 @@ int dispatch_slices(dash_ctx *ctx, cudaStream_t st, int RB, int nitems, const Sl
         return cudaGetLastError() == cudaSuccess ? 0 : DASH_E_CUDA;
     }
     return launch_slices<32>(ctx, st, nitems, sp);
+}
+
+// Slice-phase plan.  R <= 16: small slices (<= kSmallRows) go to the
+// persistent warp-autonomous k_slices3 (G slots [0, g3)), big slices to
+// CTA-cooperative k_slices2 items (slots [g3, g3 + nbig)).  Larger ranks keep
+// one item list.  items = [big items..., small positions packed 4 per int4].
+struct SlicePlan {
+    std::vector<int4> items;
+    int nbig = 0, nsmall = 0, g3 = 0, nslots = 0;
+    bool split = false;
+};
+
+SlicePlan make_plan(const int64_t *row_ptr, int M, int RB, int num_sms) {
+    SlicePlan pl;
+    if (RB > 16) {
+        plan_items(row_ptr, M, pl.items, slices_per_item(RB));
+        pl.nslots = (int)pl.items.size();
+        return pl;
+    }
+    pl.split = true;
+    std::vector<int32_t> small;
+    small.reserve(M);
+    for (int m = 0; m < M; ++m) {
+        if (row_ptr[m + 1] - row_ptr[m] > kSmallRows) pl.items.push_back(make_int4(m, 1, 1, 0));
+        else small.push_back(m);
+    }
+    pl.nbig = (int)pl.items.size();
+    pl.nsmall = (int)small.size();
+    for (size_t i = 0; i < small.size(); i += 4) {
+        int v[4] = {0, 0, 0, 0};
+        for (size_t k = 0; k < 4 && i + k < small.size(); ++k) v[k] = small[i + k];
+        pl.items.push_back(make_int4(v[0], v[1], v[2], v[3]));
+    }
+    const int gpw = 32 / RB, units = (pl.nsmall + gpw - 1) / gpw;
+    pl.g3 = pl.nsmall > 0 ? std::max(1, std::min(3 * num_sms, (units + S3<16>::NW - 1) / S3<16>::NW)) : 0;
+    pl.nslots = pl.g3 + pl.nbig;
+    return pl;
+}
+
+SlicePlan &plan_of(dash_ctx *ctx) { return *reinterpret_cast<SlicePlan *>(ctx->plan_p); }
+
+int launch_plan(dash_ctx *ctx, cudaStream_t st, int RB, const SlicePlan &pl, SliceParams sp) {
+    if (!pl.split) return dispatch_slices(ctx, st, RB, (int)pl.items.size(), sp);
+    PhaseScope ps(ctx, st, PH_SLICES);
+    const int32_t *small_pos = reinterpret_cast<const int32_t *>(sp.items + pl.nbig);
+    if (pl.nsmall > 0) {
+        int rc = RB == 4 ? launch_slices3<4>(st, pl.g3, sp, small_pos, pl.nsmall)
+                 : RB == 8 ? launch_slices3<8>(st, pl.g3, sp, small_pos, pl.nsmall)
+                           : launch_slices3<16>(st, pl.g3, sp, small_pos, pl.nsmall);
+        if (rc) return rc;
+    }
+    if (pl.nbig > 0) {
+        if (pl.nsmall > 0) ctx->last_launches++;  // two kernels under one phase
+        SliceParams sb = sp;
+        sb.G_slots = sp.G_slots + (int64_t)pl.g3 * sp.R * sp.R;
+        switch (RB) {
+            case 4: return launch_slices2<4>(st, pl.nbig, sb);
+            case 8: return launch_slices2<8>(st, pl.nbig, sb);
+            default: return launch_slices2<16>(st, pl.nbig, sb);
+        }
+    }
+    return 0;
 }
 
 template <int RP>
@@ -981,6 +1045,7 @@ void dash_ctx_destroy(dash_ctx *ctx) {
         cudaEventDestroy(ctx->staged[i]);
     }
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+    delete reinterpret_cast<SlicePlan *>(ctx->plan_p);
     delete ctx;
 }
 
@@ -1061,9 +1126,10 @@ int dash_update_pass_begin_f64(dash_ctx *ctx, void *stream, const dash_batch_f64
     const int last = pass == s->passes - 1;
     if (pass == 0) {
         ctx->last_launches = 0;
-        std::vector<int4> items;
-        plan_items(b->row_ptr_host, M, items, slices_per_item(RB));
-        ctx->nitems = (int)items.size();
+        if (!ctx->plan_p) ctx->plan_p = new SlicePlan();
+        plan_of(ctx) = make_plan(b->row_ptr_host, M, RB, ctx->num_sms);
+        ctx->nitems = plan_of(ctx).nslots;
+        const std::vector<int4> &items = plan_of(ctx).items;
         ctx->stream = stream_ok(J, b->ldx, R) && N > 0;
         plan_fsplit(ctx, N, J, ctx->nsplit, ctx->rps);
         if (ctx->stream) ctx->nsplit = ctx->num_sms;
@@ -1074,7 +1140,7 @@ int dash_update_pass_begin_f64(dash_ctx *ctx, void *stream, const dash_batch_f64
             ensure(ctx->fsnap, sizeof(double) * J * R) || ensure(ctx->gsnap, sizeof(double) * R * R) ||
             (ctx->stream && ensure(ctx->us, sizeof(double) * std::max<int64_t>(N, 1) * R)))
             return DASH_E_CUDA;
-        if (ctx->nitems > 0 && stage_items(ctx, st, items)) return DASH_E_CUDA;
+        if (!items.empty() && stage_items(ctx, st, items)) return DASH_E_CUDA;
         if (M > 0) {
             PhaseScope ps(ctx, st, PH_ROWSLICE);
             k_row_slice<<<std::min(ctx->num_sms * 4, (M + 7) / 8 + 1), 256, 0, st>>>(b->row_ptr, M,
@@ -1115,7 +1181,7 @@ int dash_update_pass_begin_f64(dash_ctx *ctx, void *stream, const dash_batch_f64
         sp.eps = eps;
         sp.pass = pass;
         sp.final_pass = last;
-        if (dispatch_slices(ctx, st, RB, ctx->nitems, sp)) return DASH_E_CUDA;
+        if (launch_plan(ctx, st, RB, plan_of(ctx), sp)) return DASH_E_CUDA;
         if (ctx->stream) {
             if (rank_bucket(R) <= 8) launch_f2_t<8>(ctx, st, b, J, (const double *)ctx->us.p, R, Fsl);
             else launch_f2_t<16>(ctx, st, b, J, (const double *)ctx->us.p, R, Fsl);
