@@ -1,0 +1,296 @@
+// k_big: the per-slice phase for BIG slices (> kSmallRows rows), R <= 16,
+// one CTA (8 warps) per slice, the row work on the FP64 tensor pipe:
+//
+//   M      = -A^{-1} diag(s)          (group sweep, warp 0)        _kernels.py:86-97
+//   per 64-row block of XV (cp.async double-buffered):
+//     U    = XV M^T        (DMMA 64x16x16)  -> U_out               _kernels.py:97-101
+//     c   += diag(XV^T U)  (fragment FMAs)                         _kernels.py:104-108
+//     gram+= U^T U         (DMMA 16x16x64)                          _kernels.py:109-115
+//   w = B^{-1} c_new, B = vtv o (lam D + gram) + shift (group sweep, warp 0)
+//   US = U o w  (L2-hot re-read of the rows just written), G slot = gram o w w^T.
+//
+// The reference sums c / gram row by row; here the sums run in DMMA / block
+// order (fixed -> deterministic; differences are rounding-level).
+// (included inside dash_update.cu's anonymous namespace)
+#pragma once
+
+struct BigSmem {
+    static constexpr int RB = 16, RP = 16;
+    static constexpr int BR = 64;           // rows per block
+    static constexpr int XPI = RP + 4;      // XV staging pitch (A-frag reads conflict-free)
+    static constexpr int UPI = RP + 8;      // U block pitch (gram frags conflict-free)
+    static constexpr int MPI = RP + 4;      // M pitch (B-frag reads)
+    static constexpr int LDV = RB + 2;
+    static constexpr int LDL = RB + 1;
+    static constexpr int NS = 3;            // XV staging ring depth
+    // xs[NS][BR*XPI] | us[BR*UPI] | Ms[RP*MPI] | vtv[RB*LDV] | red[8*64] | gram_s[RB*LDL] | buf[RB] | dn[RB*LDL]
+    // | lu[RB*LDL] | vec[4*RB] | piv[RB]
+    static constexpr int doubles =
+        NS * BR * XPI + BR * UPI + RP * MPI + RB * LDV + 8 * 64 + RB * LDL + RB + RB * LDL + RB * LDL + 4 * RB + RB;
+    static constexpr size_t bytes() { return sizeof(double) * doubles + 64; }
+};
+
+__device__ __forceinline__ void cp_async16(double *dst, const double *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+                 "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+__device__ __forceinline__ void cp_async_wait2() { asm volatile("cp.async.wait_group 2;\n" ::); }
+
+// stage XV rows [row0, row0+nr) into xs (pitch XPI); R must be even (16-byte chunks)
+__device__ __forceinline__ void big_stage(double *xs, const double *XV, int64_t row0, int nr, int R) {
+    using B = BigSmem;
+    const int chunks = R / 2;
+    for (int e = threadIdx.x; e < B::BR * chunks; e += blockDim.x) {
+        const int i = e / chunks, c2 = e % chunks;
+        if (i < nr) cp_async16(xs + i * B::XPI + 2 * c2, XV + (row0 + i) * R + 2 * c2);
+    }
+}
+
+__global__ void __launch_bounds__(256, 2) k_big(SliceParams p, const int4 *__restrict__ bigs) {
+    using B = BigSmem;
+    constexpr int RB = B::RB, RP = B::RP, BR = B::BR, XPI = B::XPI, UPI = B::UPI, MPI = B::MPI, LDV = B::LDV,
+                  LDL = B::LDL;
+    extern __shared__ __align__(16) double sm[];
+    double *xs0 = sm;
+    double *us = xs0 + B::NS * BR * XPI;
+    double *Ms = us + BR * UPI;
+    double *vtv_s = Ms + RP * MPI;
+    double *red = vtv_s + RB * LDV;      // 8 warps x 64
+    double *gram_s = red + 8 * 64;
+    double *buf = gram_s + RB * LDL;
+    double *dns = buf + RB;
+    double *lu = dns + RB * LDL;
+    double *vec = lu + RB * LDL;         // s | c | w | spare
+    int *piv = reinterpret_cast<int *>(vec + 4 * RB);
+    const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
+    const int g = lane >> 2, t = lane & 3;
+    const int R = p.R;
+    const int m = bigs[blockIdx.x].x;
+    const int64_t r0 = p.row_ptr[m], n = p.row_ptr[m + 1] - r0;
+    const int wrow = p.state_row[m];
+    const bool fresh = p.is_new[m] != 0;
+    // prefetch the first two XV blocks while the A system is solved
+    const int nblk = (int)((n + BR - 1) / BR);
+    for (int q = 0; q < B::NS - 1; ++q) {
+        if (q < nblk) big_stage(xs0 + q * BR * XPI, p.XV, r0 + (int64_t)q * BR, (int)min((int64_t)BR, n - (int64_t)q * BR), R);
+        cp_async_commit();
+    }
+    for (int i = tid; i < RB * LDV; i += blockDim.x) {
+        const int a = i / LDV, b = i % LDV;
+        vtv_s[i] = (a < R && b < R) ? p.vtv[a * R + b] : 0.0;
+    }
+    if (tid < RB) vec[tid] = tid < R ? ((fresh && p.pass == 0) ? 1.0 : p.W[(int64_t)wrow * R + tid]) : 0.0;
+    if (tid < RB && !fresh)
+        for (int z = 0; z < R; ++z) dns[tid * LDL + z] = tid < R ? p.D[(int64_t)wrow * R * R + (int64_t)z * R + tid] : 0.0;
+    const double cold = (tid < R && !fresh) ? p.C[(int64_t)wrow * R + tid] : 0.0;
+    __syncthreads();
+    // ---- A sweep by warp 0, lanes 0..15 (lanes 16..31 run a harmless identity copy)
+    if (w == 0) {
+        const int r = lane % RB;
+        const bool real = lane < RB && r < R;
+        const double s_r = real ? vec[r] : 0.0;
+        double s_all[RB];
+#pragma unroll
+        for (int z = 0; z < RB; ++z) s_all[z] = vec[z];
+        double sh = 0.0;
+#pragma unroll
+        for (int z = 0; z < RB; ++z)
+            if (z < R) sh += vtv_s[z * LDV + z] * s_all[z] * s_all[z];
+        sh = p.eps * sh / R;
+        const double dg = real ? sh : 1.0;
+        const double *vrow = vtv_s + r * LDV;
+        double a2[RB];
+#pragma unroll
+        for (int z = 0; z < RB; ++z) a2[z] = (lane < RB ? vrow[z] * s_r * s_all[z] : 0.0) + ((z == r) ? dg : 0.0);
+        // lanes 0..15 sweep A; lanes 16..31 sweep a harmless identity (own gather buffer)
+        const bool okA = sweep_inverse<RB>(a2, lane < RB ? buf : red + 7 * 64, r);
+        const unsigned badA = __ballot_sync(FULL_MASK, !okA) & 0xffffu;
+        if (badA) {
+            const bool need = lane < RB;
+#pragma unroll
+            for (int z = 0; z < RB; ++z)
+                if (need) a2[z] = vrow[z] * s_r * s_all[z] + ((z == r) ? dg : 0.0);
+            if (lane == 0) atomicAdd(p.fallbacks, 1u);
+            const bool okLU = lu_fallback<RB>(a2, lu, piv, r, R, need);
+            if (lane == 0 && !okLU) report_error(p.err, m, DASH_E_SINGULAR);
+        }
+        // Ms[n][k] = A^{-1}[n][k] s_k, so U = XV Ms^T  (a2 holds -A^{-1})
+        if (lane < RB) {
+#pragma unroll
+            for (int z = 0; z < RB; ++z) Ms[r * MPI + z] = -a2[z] * s_all[z];
+        }
+    }
+    __syncthreads();
+
+    // ---- rows, one 64-row block at a time (double-buffered XV)
+    double cacc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // c partials for cols (nb*8 + 2t + e)
+    double gacc[2] = {0.0, 0.0};                   // gram tile (mi, ni) = (w >> 1, w & 1), warps 0..3
+    for (int bi = 0; bi < nblk; ++bi) {
+        double *xs = xs0 + (bi % B::NS) * BR * XPI;
+        const int64_t b0 = r0 + (int64_t)bi * BR;
+        const int nr = (int)min((int64_t)BR, n - (int64_t)bi * BR);
+        {
+            const int q = bi + B::NS - 1;  // refill the stage consumed two blocks ago
+            if (q < nblk)
+                big_stage(xs0 + (q % B::NS) * BR * XPI, p.XV, r0 + (int64_t)q * BR,
+                          (int)min((int64_t)BR, n - (int64_t)q * BR), R);
+            cp_async_commit();
+        }
+        cp_async_wait2();
+        __syncthreads();
+        if (nr < BR || R < RP) {  // zero padded columns / tail rows of the staged block
+            for (int e = tid; e < BR * XPI; e += blockDim.x) {
+                const int i = e / XPI, z = e % XPI;
+                if (i >= nr || z >= R) xs[e] = 0.0;
+            }
+            __syncthreads();
+        }
+        // U = XV Ms^T: warp w -> rows 8w..8w+7, both n-tiles
+        double uacc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+        for (int kk = 0; kk < RP / 4; ++kk) {
+            const double a = xs[(8 * w + g) * XPI + 4 * kk + t];
+#pragma unroll
+            for (int nb = 0; nb < 2; ++nb) dmma884(uacc[nb], a, Ms[(8 * nb + g) * MPI + 4 * kk + t]);
+        }
+        const int row = 8 * w + g;
+#pragma unroll
+        for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int col = 8 * nb + 2 * t + e;
+                const double u = (row < nr && col < R) ? uacc[nb][e] : 0.0;
+                us[row * UPI + col] = u;
+                if (row < nr && col < R) p.U[(b0 + row) * R + col] = u;
+                cacc[nb][e] = fma(xs[row * XPI + col], u, cacc[nb][e]);
+            }
+        __syncthreads();
+        // gram += U^T U : warps 0..3, tile (w>>1, w&1), 16 k-steps over the 64 rows
+        if (w < 4) {
+            const int mi = w >> 1, ni = w & 1;
+#pragma unroll
+            for (int kk = 0; kk < BR / 4; ++kk) {
+                const double a = us[(4 * kk + t) * UPI + 8 * mi + g];
+                const double b = us[(4 * kk + t) * UPI + 8 * ni + g];
+                dmma884(gacc, a, b);
+            }
+        }
+        __syncthreads();
+    }
+    // ---- reduce c (over lanes g and warps) and gram tiles into shared
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            double v = cacc[nb][e];
+            v += __shfl_xor_sync(FULL_MASK, v, 4);
+            v += __shfl_xor_sync(FULL_MASK, v, 8);
+            v += __shfl_xor_sync(FULL_MASK, v, 16);
+            cacc[nb][e] = v;
+        }
+    if (g == 0) {
+#pragma unroll
+        for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) red[w * 64 + 8 * nb + 2 * t + e] = cacc[nb][e];
+    }
+    if (w < 4) {
+        const int mi = w >> 1, ni = w & 1;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) gram_s[(8 * mi + g) * LDL + 8 * ni + 2 * t + e] = gacc[e];
+    }
+    __syncthreads();
+    if (tid < RB) {
+        double cs = 0.0;
+        for (int ww = 0; ww < 8; ++ww) cs += red[ww * 64 + tid];
+        vec[RB + tid] = tid < R ? p.lam * cold + cs : 0.0;  // c_new
+    }
+    __syncthreads();
+    // ---- D accumulation and the S-row system by warp 0 lanes 0..15
+    if (w == 0) {
+        const int r = lane % RB;
+        const bool lreal = lane < RB && r < R;
+        double *dn = dns + r * LDL;
+        double drr = 0.0;
+        double dnr[RB];
+#pragma unroll
+        for (int z = 0; z < RB; ++z) {
+            double v = 0.0;
+            if (lreal && z < R) v = p.lam * (fresh ? 0.0 : dn[z]) + gram_s[r * LDL + z];
+            dnr[z] = v;
+            if (z == r) drr = v;
+        }
+        __syncwarp();
+        if (lane < RB) {
+#pragma unroll
+            for (int z = 0; z < RB; ++z) dn[z] = dnr[z];
+        }
+        double vdd[RB];
+        group_gather<RB>(lreal ? vtv_s[r * LDV + r] * drr : 0.0, lane < RB ? buf : red + 7 * 64, r, vdd);
+        double dsum = 0.0;
+#pragma unroll
+        for (int z = 0; z < RB; ++z)
+            if (z < R) dsum += vdd[z];
+        const double sh2 = p.eps * dsum / R;
+        const double dg2 = lreal ? sh2 : 1.0;
+        double a[RB];
+#pragma unroll
+        for (int z = 0; z < RB; ++z) a[z] = (lane < RB ? vtv_s[r * LDV + z] * dnr[z] : 0.0) + ((z == r) ? dg2 : 0.0);
+        bool okB = sweep_inverse<RB>(a, lane < RB ? buf : red + 7 * 64, r);
+        double wv = 0.0;
+#pragma unroll
+        for (int z = 0; z < RB; ++z) wv = fma(-a[z], vec[RB + z], wv);
+        if (!lreal) wv = 0.0;
+        const bool good = __all_sync(FULL_MASK, (okB && isfinite(wv)) || lane >= RB);
+        if (!good) {
+            const bool need = lane < RB;
+#pragma unroll
+            for (int z = 0; z < RB; ++z) a[z] = (lane < RB ? vtv_s[r * LDV + z] * dnr[z] : 0.0) + ((z == r) ? dg2 : 0.0);
+            if (lane == 0) atomicAdd(p.fallbacks, 1u);
+            const bool okLU = lu_fallback<RB>(a, lu, piv, r, R, need);
+            if (lane == 0 && !okLU) report_error(p.err, m, DASH_E_SINGULAR);
+            wv = 0.0;
+#pragma unroll
+            for (int z = 0; z < RB; ++z) wv = fma(-a[z], vec[RB + z], wv);
+            if (!lreal) wv = 0.0;
+            if (lreal && !isfinite(wv)) report_error(p.err, m, DASH_E_NONFINITE);
+        }
+        if (lreal) {
+            p.W[(int64_t)wrow * R + r] = wv;
+            if (p.final_pass) {
+                p.C[(int64_t)wrow * R + r] = vec[RB + r];
+#pragma unroll
+                for (int z = 0; z < RB; ++z)
+                    if (z < R) p.D[(int64_t)wrow * R * R + (int64_t)z * R + r] = dnr[z];
+            }
+        }
+        if (lane < RB) vec[2 * RB + lane] = lreal ? wv : 0.0;
+    }
+    __syncthreads();
+    // ---- G slot (gram o w w^T) and US = U o w (rows just written: L2-hot)
+    double *slot = p.G_slots + (int64_t)blockIdx.x * R * R;
+    for (int i = tid; i < R * R; i += blockDim.x) {
+        const int a = i / R, b = i % R;
+        slot[i] = gram_s[a * LDL + b] * vec[2 * RB + a] * vec[2 * RB + b];
+    }
+    if (p.US != nullptr) {
+        const int64_t tot = n * R;
+        const double *Ur = p.U + r0 * R;
+        double *USr = p.US + r0 * R;
+#pragma unroll 4
+        for (int64_t e = tid; e < tot; e += blockDim.x) USr[e] = Ur[e] * vec[2 * RB + (int)(e % R)];
+    }
+}
+
+int launch_big(cudaStream_t st, int nbig, const SliceParams &sp, const int4 *bigs) {
+    const size_t smem = BigSmem::bytes();
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    k_big<<<nbig, 256, smem, st>>>(sp, bigs);
+    return cudaGetLastError() == cudaSuccess ? 0 : DASH_E_CUDA;
+}

@@ -48,18 +48,26 @@ __global__ void k_prologue(const double *__restrict__ V, int J, int R, double *_
                            const double *__restrict__ F, const double *__restrict__ G,
                            double *__restrict__ F_snap, double *__restrict__ G_snap,
                            double *__restrict__ v_used, int snap, int last) {
-    for (int p = threadIdx.x; p < R * R; p += blockDim.x) {
-        int r = p / R, z = p % R;
-        double acc = 0.0;
-        for (int j = 0; j < J; ++j) acc = fma(V[j * R + r], V[j * R + z], acc);
-        vtv[p] = acc;
+    if (blockIdx.x == 0) {
+        // vtv: 4 threads per (r, z) split J, combined in fixed order (unrolled: loads in flight)
+        for (int p = threadIdx.x >> 2; p < R * R; p += blockDim.x >> 2) {
+            const int r = p / R, z = p % R, q = threadIdx.x & 3;
+            double acc = 0.0;
+#pragma unroll 8
+            for (int j = q; j < J; j += 4) acc = fma(V[j * R + r], V[j * R + z], acc);
+            acc += __shfl_xor_sync(FULL_MASK, acc, 1);
+            acc += __shfl_xor_sync(FULL_MASK, acc, 2);
+            if (q == 0) vtv[p] = acc;
+        }
+        return;
     }
+    const int tid = (blockIdx.x - 1) * blockDim.x + threadIdx.x, nt = (gridDim.x - 1) * blockDim.x;
     if (snap) {
-        for (int i = threadIdx.x; i < J * R; i += blockDim.x) F_snap[i] = F[i];
-        for (int i = threadIdx.x; i < R * R; i += blockDim.x) G_snap[i] = G[i];
+        for (int i = tid; i < J * R; i += nt) F_snap[i] = F[i];
+        for (int i = tid; i < R * R; i += nt) G_snap[i] = G[i];
     }
     if (last)
-        for (int i = threadIdx.x; i < J * R; i += blockDim.x) v_used[i] = V[i];
+        for (int i = tid; i < J * R; i += nt) v_used[i] = V[i];
 }
 
 // row -> batch position of its slice
@@ -450,6 +458,7 @@ __global__ void __launch_bounds__(NW * 32) k_slices(SliceParams p) {
 #include "dash_stream.cuh"
 #include "dash_slices_cta.cuh"
 #include "dash_slices3.cuh"
+#include "dash_big.cuh"
 
 // ---------------------------------------------------------------------------
 // k_fgemm: F partial slot s = X[rows_s]^T (U o w)[rows_s], J-block of 64.
@@ -889,6 +898,7 @@ int launch_plan(dash_ctx *ctx, cudaStream_t st, int RB, const SlicePlan &pl, Sli
         if (pl.nsmall > 0) ctx->last_launches++;  // two kernels under one phase
         SliceParams sb = sp;
         sb.G_slots = sp.G_slots + (int64_t)pl.g3 * sp.R * sp.R;
+        if (RB == 16 && (sp.R % 2) == 0) return launch_big(st, pl.nbig, sb, sp.items);  // DMMA big-slice kernel
         switch (RB) {
             case 4: return launch_slices2<4>(st, pl.nbig, sb);
             case 8: return launch_slices2<8>(st, pl.nbig, sb);
@@ -1141,7 +1151,7 @@ int dash_update_pass_begin_f64(dash_ctx *ctx, void *stream, const dash_batch_f64
             (ctx->stream && ensure(ctx->us, sizeof(double) * std::max<int64_t>(N, 1) * R)))
             return DASH_E_CUDA;
         if (!items.empty() && stage_items(ctx, st, items)) return DASH_E_CUDA;
-        if (M > 0) {
+        if (M > 0 && !ctx->stream) {  // row -> slice map: only the generic F GEMM needs it
             PhaseScope ps(ctx, st, PH_ROWSLICE);
             k_row_slice<<<std::min(ctx->num_sms * 4, (M + 7) / 8 + 1), 256, 0, st>>>(b->row_ptr, M,
                                                                                     (int32_t *)ctx->row_slice.p);
@@ -1151,7 +1161,8 @@ int dash_update_pass_begin_f64(dash_ctx *ctx, void *stream, const dash_batch_f64
     double *Fsl = (double *)ctx->fslots.p, *Gsl = (double *)ctx->gslots.p;
     {
         PhaseScope ps(ctx, st, PH_PROLOGUE);
-        k_prologue<<<1, 256, 0, st>>>(s->V, J, R, (double *)ctx->vtv.p, s->F, s->G, (double *)ctx->fsnap.p,
+        k_prologue<<<1 + std::max(1, std::min(16, (J * R + 255) / 256)), 256, 0, st>>>(
+            s->V, J, R, (double *)ctx->vtv.p, s->F, s->G, (double *)ctx->fsnap.p,
                                       (double *)ctx->gsnap.p, v_used_out, pass == 0, last);
     }
     if (N > 0) {
