@@ -88,22 +88,21 @@ __global__ void __launch_bounds__(256, 2) k_big(SliceParams p, const int4 *__res
     __syncthreads();
     // ---- A sweep by warp 0, lanes 0..15 (lanes 16..31 run a harmless identity copy)
     if (w == 0) {
+        // s is read from shared (vec) rather than held in a register array: keeps
+        // the sweep's live set at a[] + the gathered column (no spills)
         const int r = lane % RB;
         const bool real = lane < RB && r < R;
         const double s_r = real ? vec[r] : 0.0;
-        double s_all[RB];
-#pragma unroll
-        for (int z = 0; z < RB; ++z) s_all[z] = vec[z];
         double sh = 0.0;
 #pragma unroll
         for (int z = 0; z < RB; ++z)
-            if (z < R) sh += vtv_s[z * LDV + z] * s_all[z] * s_all[z];
+            if (z < R) sh += vtv_s[z * LDV + z] * vec[z] * vec[z];
         sh = p.eps * sh / R;
         const double dg = real ? sh : 1.0;
         const double *vrow = vtv_s + r * LDV;
         double a2[RB];
 #pragma unroll
-        for (int z = 0; z < RB; ++z) a2[z] = (lane < RB ? vrow[z] * s_r * s_all[z] : 0.0) + ((z == r) ? dg : 0.0);
+        for (int z = 0; z < RB; ++z) a2[z] = (lane < RB ? vrow[z] * s_r * vec[z] : 0.0) + ((z == r) ? dg : 0.0);
         // lanes 0..15 sweep A; lanes 16..31 sweep a harmless identity (own gather buffer)
         const bool okA = sweep_inverse<RB>(a2, lane < RB ? buf : red + 7 * 64, r);
         const unsigned badA = __ballot_sync(FULL_MASK, !okA) & 0xffffu;
@@ -111,7 +110,7 @@ __global__ void __launch_bounds__(256, 2) k_big(SliceParams p, const int4 *__res
             const bool need = lane < RB;
 #pragma unroll
             for (int z = 0; z < RB; ++z)
-                if (need) a2[z] = vrow[z] * s_r * s_all[z] + ((z == r) ? dg : 0.0);
+                if (need) a2[z] = vrow[z] * s_r * vec[z] + ((z == r) ? dg : 0.0);
             if (lane == 0) atomicAdd(p.fallbacks, 1u);
             const bool okLU = lu_fallback<RB>(a2, lu, piv, r, R, need);
             if (lane == 0 && !okLU) report_error(p.err, m, DASH_E_SINGULAR);
@@ -119,14 +118,14 @@ __global__ void __launch_bounds__(256, 2) k_big(SliceParams p, const int4 *__res
         // Ms[n][k] = A^{-1}[n][k] s_k, so U = XV Ms^T  (a2 holds -A^{-1})
         if (lane < RB) {
 #pragma unroll
-            for (int z = 0; z < RB; ++z) Ms[r * MPI + z] = -a2[z] * s_all[z];
+            for (int z = 0; z < RB; ++z) Ms[r * MPI + z] = -a2[z] * vec[z];
         }
     }
     __syncthreads();
 
     // ---- rows, one 64-row block at a time (double-buffered XV)
     double cacc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // c partials for cols (nb*8 + 2t + e)
-    double gacc[2] = {0.0, 0.0};                   // gram tile (mi, ni) = (w >> 1, w & 1), warps 0..3
+    double gacc[2] = {0.0, 0.0};  // gram tile (mi, ni) = ((w&3) >> 1, w & 1), K half w >> 2
     for (int bi = 0; bi < nblk; ++bi) {
         double *xs = xs0 + (bi % B::NS) * BR * XPI;
         const int64_t b0 = r0 + (int64_t)bi * BR;
@@ -167,13 +166,14 @@ __global__ void __launch_bounds__(256, 2) k_big(SliceParams p, const int4 *__res
                 cacc[nb][e] = fma(xs[row * XPI + col], u, cacc[nb][e]);
             }
         __syncthreads();
-        // gram += U^T U : warps 0..3, tile (w>>1, w&1), 16 k-steps over the 64 rows
-        if (w < 4) {
-            const int mi = w >> 1, ni = w & 1;
+        // gram += U^T U : 8 warps = 4 tiles x 2 K-halves (8-deep DMMA chains)
+        {
+            const int mi = (w & 3) >> 1, ni = w & 1, kh = w >> 2;
 #pragma unroll
-            for (int kk = 0; kk < BR / 4; ++kk) {
-                const double a = us[(4 * kk + t) * UPI + 8 * mi + g];
-                const double b = us[(4 * kk + t) * UPI + 8 * ni + g];
+            for (int kk = 0; kk < BR / 8; ++kk) {
+                const int row = 4 * (kk + kh * (BR / 8)) + t;
+                const double a = us[row * UPI + 8 * mi + g];
+                const double b = us[row * UPI + 8 * ni + g];
                 dmma884(gacc, a, b);
             }
         }
@@ -196,10 +196,20 @@ __global__ void __launch_bounds__(256, 2) k_big(SliceParams p, const int4 *__res
 #pragma unroll
             for (int e = 0; e < 2; ++e) red[w * 64 + 8 * nb + 2 * t + e] = cacc[nb][e];
     }
-    if (w < 4) {
-        const int mi = w >> 1, ni = w & 1;
+    {
+        const int mi = (w & 3) >> 1, ni = w & 1;
+        if (w >= 4) {
 #pragma unroll
-        for (int e = 0; e < 2; ++e) gram_s[(8 * mi + g) * LDL + 8 * ni + 2 * t + e] = gacc[e];
+            for (int e = 0; e < 2; ++e) gram_s[(8 * mi + g) * LDL + 8 * ni + 2 * t + e] = gacc[e];
+        }
+        __syncthreads();
+        if (w < 4) {  // fixed order: (first K half) + (second K half)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                double *gp = gram_s + (8 * mi + g) * LDL + 8 * ni + 2 * t + e;
+                *gp = gacc[e] + *gp;
+            }
+        }
     }
     __syncthreads();
     if (tid < RB) {
@@ -208,36 +218,26 @@ __global__ void __launch_bounds__(256, 2) k_big(SliceParams p, const int4 *__res
         vec[RB + tid] = tid < R ? p.lam * cold + cs : 0.0;  // c_new
     }
     __syncthreads();
-    // ---- D accumulation and the S-row system by warp 0 lanes 0..15
+    // ---- D accumulation and the S-row system by warp 0 lanes 0..15 (D row in shared dns)
     if (w == 0) {
         const int r = lane % RB;
         const bool lreal = lane < RB && r < R;
         double *dn = dns + r * LDL;
-        double drr = 0.0;
-        double dnr[RB];
-#pragma unroll
-        for (int z = 0; z < RB; ++z) {
-            double v = 0.0;
-            if (lreal && z < R) v = p.lam * (fresh ? 0.0 : dn[z]) + gram_s[r * LDL + z];
-            dnr[z] = v;
-            if (z == r) drr = v;
-        }
-        __syncwarp();
         if (lane < RB) {
 #pragma unroll
-            for (int z = 0; z < RB; ++z) dn[z] = dnr[z];
+            for (int z = 0; z < RB; ++z)
+                dn[z] = (lreal && z < R) ? p.lam * (fresh ? 0.0 : dn[z]) + gram_s[r * LDL + z] : 0.0;
         }
-        double vdd[RB];
-        group_gather<RB>(lreal ? vtv_s[r * LDV + r] * drr : 0.0, lane < RB ? buf : red + 7 * 64, r, vdd);
+        __syncwarp();
         double dsum = 0.0;
 #pragma unroll
         for (int z = 0; z < RB; ++z)
-            if (z < R) dsum += vdd[z];
+            if (z < R) dsum += vtv_s[z * LDV + z] * dns[z * LDL + z];
         const double sh2 = p.eps * dsum / R;
         const double dg2 = lreal ? sh2 : 1.0;
         double a[RB];
 #pragma unroll
-        for (int z = 0; z < RB; ++z) a[z] = (lane < RB ? vtv_s[r * LDV + z] * dnr[z] : 0.0) + ((z == r) ? dg2 : 0.0);
+        for (int z = 0; z < RB; ++z) a[z] = (lane < RB ? vtv_s[r * LDV + z] * dn[z] : 0.0) + ((z == r) ? dg2 : 0.0);
         bool okB = sweep_inverse<RB>(a, lane < RB ? buf : red + 7 * 64, r);
         double wv = 0.0;
 #pragma unroll
@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(256, 2) k_big(SliceParams p, const int4 *__res
         if (!good) {
             const bool need = lane < RB;
 #pragma unroll
-            for (int z = 0; z < RB; ++z) a[z] = (lane < RB ? vtv_s[r * LDV + z] * dnr[z] : 0.0) + ((z == r) ? dg2 : 0.0);
+            for (int z = 0; z < RB; ++z) a[z] = (lane < RB ? vtv_s[r * LDV + z] * dn[z] : 0.0) + ((z == r) ? dg2 : 0.0);
             if (lane == 0) atomicAdd(p.fallbacks, 1u);
             const bool okLU = lu_fallback<RB>(a, lu, piv, r, R, need);
             if (lane == 0 && !okLU) report_error(p.err, m, DASH_E_SINGULAR);
@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(256, 2) k_big(SliceParams p, const int4 *__res
                 p.C[(int64_t)wrow * R + r] = vec[RB + r];
 #pragma unroll
                 for (int z = 0; z < RB; ++z)
-                    if (z < R) p.D[(int64_t)wrow * R * R + (int64_t)z * R + r] = dnr[z];
+                    if (z < R) p.D[(int64_t)wrow * R * R + (int64_t)z * R + r] = dn[z];
             }
         }
         if (lane < RB) vec[2 * RB + lane] = lreal ? wv : 0.0;
@@ -276,11 +276,34 @@ __global__ void __launch_bounds__(256, 2) k_big(SliceParams p, const int4 *__res
         slot[i] = gram_s[a * LDL + b] * vec[2 * RB + a] * vec[2 * RB + b];
     }
     if (p.US != nullptr) {
-        const int64_t tot = n * R;
-        const double *Ur = p.U + r0 * R;
-        double *USr = p.US + r0 * R;
-#pragma unroll 4
-        for (int64_t e = tid; e < tot; e += blockDim.x) USr[e] = Ur[e] * vec[2 * RB + (int)(e % R)];
+        // 16-byte chunks (R even); a thread's column pair advances by a fixed step
+        // per iteration, so no per-element division.  Loads are batched ahead of
+        // the stores (U and US never alias).
+        const int half = R / 2;
+        const int64_t tot = n * half;
+        const double2 *__restrict__ Ur = reinterpret_cast<const double2 *>(p.U + r0 * R);
+        double2 *__restrict__ USr = reinterpret_cast<double2 *>(p.US + r0 * R);
+        const double *wv = vec + 2 * RB;
+        const int step = blockDim.x % half;
+        int col = tid % half;
+        constexpr int UNR = 2;
+        for (int64_t e0 = tid; e0 < tot; e0 += (int64_t)UNR * blockDim.x) {
+            double2 v[UNR];
+            int cc[UNR];
+#pragma unroll
+            for (int k = 0; k < UNR; ++k) {
+                const int64_t e = e0 + (int64_t)k * blockDim.x;
+                if (e < tot) v[k] = __ldcg(Ur + e);
+                cc[k] = col;
+                col += step;
+                if (col >= half) col -= half;
+            }
+#pragma unroll
+            for (int k = 0; k < UNR; ++k) {
+                const int64_t e = e0 + (int64_t)k * blockDim.x;
+                if (e < tot) USr[e] = make_double2(v[k].x * wv[2 * cc[k]], v[k].y * wv[2 * cc[k] + 1]);
+            }
+        }
     }
 }
 

@@ -1,0 +1,209 @@
+// TMA-tensor streaming GEMMs (R bucket 16): the same two contractions as
+// dash_stream.cuh, but each 32-row tile arrives as ceil(J/16) tensor copies
+// (cp.async.bulk.tensor.2d, box 16 doubles x 32 rows, 128-byte swizzle)
+// instead of 32 one-row bulk copies -- the per-copy cost of small bulk copies
+// capped the v2 kernels at ~4.9 TB/s (tools/bulk_probe.cu: 6.9 TB/s with one
+// large copy per tile).
+//
+// Fragment loads are LDS.128 pairs on the swizzled layout:
+//   k_xv3    XV = X V: each lane reads X[row][2c, 2c+1] and feeds two DMMA
+//            k-steps whose K orders are the even / odd columns of an 8-column
+//            group; V is staged transposed (Vt[n][k]) so the matching B pair is
+//            one LDS.128 too.
+//   k_fgemm3 F = X^T US: the M (=j) and N (=r) dimensions are split into even
+//            / odd halves, so one LDS.128 of X and one of US feed a 2x2 block of
+//            DMMA tiles; the permutation is undone when the slot is written.
+// With the 128B swizzle (16-byte chunk c of row r stored at c ^ (r & 7)) all
+// these reads are bank-conflict-free.  Rows past N are zero-filled by TMA.
+// (included inside dash_update.cu's anonymous namespace)
+#pragma once
+
+#include <cuda.h>
+
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int r0, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(r0), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void prefetch_map(const CUtensorMap *map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+
+// double offset of the 16-byte chunk `c` (0..7) of row `r` inside a swizzled 32x16 box
+__device__ __forceinline__ int swz(int r, int c) { return r * 16 + ((c ^ (r & 7)) << 1); }
+
+struct TmaSmem {
+    static __host__ __device__ int strips(int J) { return (J + 15) / 16; }
+    static __host__ __device__ int vtp(int J) { return strips(J) * 16 + 8; }  // Vt pitch (== 8 mod 16)
+    static __host__ __device__ size_t stage_doubles(int J) { return (size_t)strips(J) * 512; }
+    static __host__ __device__ size_t xv_bytes(int J) {
+        return 1024 + sizeof(double) * (kStages * stage_doubles(J) + 16 * (size_t)vtp(J)) + 16 * kStages;
+    }
+    static __host__ __device__ size_t f_bytes(int J) {
+        return 1024 + sizeof(double) * (kStages * (stage_doubles(J) + 512)) + 16 * kStages;
+    }
+};
+
+// 1024-byte alignment for the swizzled boxes; pointer arithmetic (not an integer
+// round trip) so the compiler keeps the shared address space and emits LDS.
+__device__ __forceinline__ double *align1k(double *p) {
+    return p + (((1024u - (smem_u32(p) & 1023u)) & 1023u) >> 3);
+}
+
+__global__ void __launch_bounds__(kCW * 32 + 32, 1) k_xv3(const __grid_constant__ CUtensorMap tmX, int64_t N, int J,
+                                                          const double *__restrict__ V, int R, double *__restrict__ XV) {
+    extern __shared__ __align__(16) double sm_raw[];
+    double *sm = align1k(sm_raw);
+    const int JS = TmaSmem::strips(J), VTP = TmaSmem::vtp(J);
+    const size_t SD = TmaSmem::stage_doubles(J);
+    double *xs = sm;                               // kStages x JS x 512 (swizzled 32x16 boxes)
+    double *vt = xs + kStages * SD;                // 16 x VTP: vt[n][k] = V[k][n]
+    uint64_t *full = reinterpret_cast<uint64_t *>(vt + 16 * VTP);
+    uint64_t *empty = full + kStages;
+    const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
+    const int g = lane >> 2, t = lane & 3;
+    for (int i = tid; i < 16 * VTP; i += blockDim.x) {
+        const int nn = i / VTP, k = i % VTP;
+        vt[i] = (nn < R && k < J) ? V[k * R + nn] : 0.0;
+    }
+    if (tid == 0) {
+        prefetch_map(&tmX);
+        for (int s2 = 0; s2 < kStages; ++s2) {
+            mbar_init(&full[s2], 1);
+            mbar_init(&empty[s2], kCW);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int64_t ntiles = (N + kTR - 1) / kTR;
+    const int64_t mine = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    if (w == kCW) {
+        if (lane == 0) {
+            for (int64_t i = 0; i < mine; ++i) {
+                const int st = (int)(i % kStages);
+                if (i >= kStages) mbar_wait(&empty[st], (uint32_t)(((i / kStages) - 1) & 1));
+                const int r0 = (int)((blockIdx.x + i * gridDim.x) * kTR);
+                mbar_arrive_expect_tx(&full[st], (uint32_t)JS * 4096u);
+                for (int s = 0; s < JS; ++s) tma_load_2d(xs + st * SD + s * 512, &tmX, 16 * s, r0, &full[st]);
+            }
+        }
+        return;
+    }
+    const int mb = w & 3, nb = w >> 2;  // 8-row block, 8-column block of the 32 x 16 output tile
+    const double *vrow = vt + (8 * nb + g) * VTP + 2 * t;
+    for (int64_t i = 0; i < mine; ++i) {
+        const int st = (int)(i % kStages);
+        mbar_wait(&full[st], (uint32_t)((i / kStages) & 1));
+        const double *xt = xs + st * SD;
+        const int row = 8 * mb + g;
+        double acc[2] = {0.0, 0.0}, acc2[2] = {0.0, 0.0};
+        for (int s = 0; s < JS; ++s) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {  // 8-column group h of the strip
+                const double2 a = *reinterpret_cast<const double2 *>(xt + s * 512 + swz(row, 4 * h + t));
+                const double2 b = *reinterpret_cast<const double2 *>(vrow + 16 * s + 8 * h);
+                dmma884(acc, a.x, b.x);   // k-order: even columns of the group
+                dmma884(acc2, a.y, b.y);  // odd columns
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+        const int64_t grow = (blockIdx.x + i * gridDim.x) * kTR + row;
+        if (grow < N) {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int col = 8 * nb + 2 * t + e;
+                if (col < R) XV[grow * R + col] = acc[e] + acc2[e];
+            }
+        }
+    }
+}
+
+// F slot = sum over this CTA's tiles of X^T US.  Warp w owns J-strips w, w+8, ...
+// (MAXS strips); per strip a 2x2 block of 8x8 DMMA tiles (even/odd j x even/odd r).
+template <int MAXS>
+__global__ void __launch_bounds__(kCW * 32 + 32, 1) k_fgemm3(const __grid_constant__ CUtensorMap tmX,
+                                                             const __grid_constant__ CUtensorMap tmU, int64_t N, int J,
+                                                             int R, double *__restrict__ F_slots) {
+    extern __shared__ __align__(16) double sm_raw[];
+    double *sm = align1k(sm_raw);
+    const int JS = TmaSmem::strips(J);
+    const size_t SD = TmaSmem::stage_doubles(J) + 512;  // X boxes + the US box
+    double *xs = sm;
+    uint64_t *full = reinterpret_cast<uint64_t *>(xs + kStages * SD);
+    uint64_t *empty = full + kStages;
+    const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
+    const int g = lane >> 2, t = lane & 3;
+    if (tid == 0) {
+        prefetch_map(&tmX);
+        prefetch_map(&tmU);
+        for (int s2 = 0; s2 < kStages; ++s2) {
+            mbar_init(&full[s2], 1);
+            mbar_init(&empty[s2], kCW);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int64_t ntiles = (N + kTR - 1) / kTR;
+    const int64_t mine = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    if (w == kCW) {
+        if (lane == 0) {
+            for (int64_t i = 0; i < mine; ++i) {
+                const int st = (int)(i % kStages);
+                if (i >= kStages) mbar_wait(&empty[st], (uint32_t)(((i / kStages) - 1) & 1));
+                const int r0 = (int)((blockIdx.x + i * gridDim.x) * kTR);
+                mbar_arrive_expect_tx(&full[st], (uint32_t)(JS + 1) * 4096u);
+                for (int s = 0; s < JS; ++s) tma_load_2d(xs + st * SD + s * 512, &tmX, 16 * s, r0, &full[st]);
+                tma_load_2d(xs + st * SD + JS * 512, &tmU, 0, r0, &full[st]);
+            }
+        }
+        return;
+    }
+    double acc[MAXS][4][2];
+#pragma unroll
+    for (int q = 0; q < MAXS; ++q)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[q][k][0] = acc[q][k][1] = 0.0;
+    for (int64_t i = 0; i < mine; ++i) {
+        const int st = (int)(i % kStages);
+        mbar_wait(&full[st], (uint32_t)((i / kStages) & 1));
+        const double *xt = xs + st * SD;
+        const double *ut = xt + JS * 512;
+#pragma unroll
+        for (int kk = 0; kk < kTR / 4; ++kk) {
+            const int row = 4 * kk + t;
+            const double2 b = *reinterpret_cast<const double2 *>(ut + swz(row, g));  // US[row][2g], [2g+1]
+#pragma unroll
+            for (int q = 0; q < MAXS; ++q) {
+                const int s = w + kCW * q;
+                if (s < JS) {
+                    const double2 a = *reinterpret_cast<const double2 *>(xt + s * 512 + swz(row, g));
+                    dmma884(acc[q][0], a.x, b.x);  // even j, even r
+                    dmma884(acc[q][1], a.x, b.y);  // even j, odd r
+                    dmma884(acc[q][2], a.y, b.x);  // odd j, even r
+                    dmma884(acc[q][3], a.y, b.y);  // odd j, odd r
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+    }
+    double *slot = F_slots + (int64_t)blockIdx.x * J * R;
+#pragma unroll
+    for (int q = 0; q < MAXS; ++q) {
+        const int s = w + kCW * q;
+        if (s < JS) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int j = 16 * s + 2 * g + (k >> 1);
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int r = 2 * (2 * t + e) + (k & 1);
+                    if (j < J && r < R) slot[j * R + r] = acc[q][k][e];
+                }
+            }
+        }
+    }
+}

@@ -17,6 +17,8 @@
 // All reductions use a fixed order (per-CTA slots summed in slot order), so
 // results are bit-reproducible run to run, as the reference's determinism
 // criterion requires (test_acceptance.py:416-475).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -456,6 +458,7 @@ __global__ void __launch_bounds__(NW * 32) k_slices(SliceParams p) {
 
 #include "dash_slices.cuh"
 #include "dash_stream.cuh"
+#include "dash_tma.cuh"
 #include "dash_slices_cta.cuh"
 #include "dash_slices3.cuh"
 #include "dash_big.cuh"
@@ -705,6 +708,7 @@ struct dash_ctx {
     int nitems = 0;
     int64_t nsplit = 1, rps = 32;
     bool stream = false;  // TMA-ring GEMM path for this update
+    bool tma = false;     // ... with tensor-map (swizzled box) copies: k_xv3 / k_fgemm3
     void *plan_p = nullptr;  // SlicePlan of the update in flight
     // phase timing (bench): events around every launch when enabled
     int prof = 0;
@@ -869,6 +873,10 @@ SlicePlan make_plan(const int64_t *row_ptr, int M, int RB, int num_sms) {
         if (row_ptr[m + 1] - row_ptr[m] > kSmallRows) pl.items.push_back(make_int4(m, 1, 1, 0));
         else small.push_back(m);
     }
+    // longest first: one CTA per big slice, ~2 waves -> shorter tail (stable: deterministic slot order)
+    std::stable_sort(pl.items.begin(), pl.items.end(), [row_ptr](const int4 &a, const int4 &b) {
+        return row_ptr[a.x + 1] - row_ptr[a.x] > row_ptr[b.x + 1] - row_ptr[b.x];
+    });
     pl.nbig = (int)pl.items.size();
     pl.nsmall = (int)small.size();
     for (size_t i = 0; i < small.size(); i += 4) {
@@ -984,6 +992,70 @@ bool stream_ok(int J, int64_t ldx, int R) {
     const int RB = rank_bucket(R);
     if (RB > 16) return false;  // US is produced by k_slices2 (R <= 16)
     return RB <= 8 ? stream_ok_t<8>(J, ldx, R) : stream_ok_t<16>(J, ldx, R);
+}
+
+// ---- tensor-map path (R bucket 16): box 16 doubles x 32 rows, 128B swizzle, OOB rows zero-filled
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        cudaDriverEntryPointQueryResult q;
+        void *f = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+        else
+            cudaGetLastError();
+    }
+    return fn;
+}
+
+bool make_box_map(CUtensorMap *map, const double *base, int64_t cols, int64_t rows, int64_t ld) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
+    cuuint32_t box[2] = {16, (cuuint32_t)kTR};
+    cuuint32_t es[2] = {1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool tma_ok(const dash_batch_f64 *b, int J, int R) {
+    const size_t lim = 220 * 1024;
+    return rank_bucket(R) == 16 && !(R & 1) && !(b->ldx & 1) && (reinterpret_cast<uintptr_t>(b->X) & 15) == 0 &&
+           b->N < (int64_t)1 << 31 && TmaSmem::strips(J) <= 16 && TmaSmem::xv_bytes(J) <= lim &&
+           TmaSmem::f_bytes(J) <= lim && encode_fn() != nullptr;
+}
+
+int launch_xv3(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, const double *V, int R, double *XV) {
+    CUtensorMap mx;
+    if (!make_box_map(&mx, b->X, J, b->N, b->ldx)) return DASH_E_CUDA;
+    const size_t smem = TmaSmem::xv_bytes(J);
+    cudaFuncSetAttribute(k_xv3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    PhaseScope ps(ctx, st, PH_XV);
+    k_xv3<<<ctx->num_sms, kCW * 32 + 32, smem, st>>>(mx, b->N, J, V, R, XV);
+    return 0;
+}
+
+template <int MAXS>
+void launch_f3_t(dash_ctx *ctx, cudaStream_t st, const CUtensorMap &mx, const CUtensorMap &mu, int64_t N, int J,
+                 int R, double *F_slots) {
+    const size_t smem = TmaSmem::f_bytes(J);
+    cudaFuncSetAttribute(k_fgemm3<MAXS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    PhaseScope ps(ctx, st, PH_FGEMM);
+    k_fgemm3<MAXS><<<ctx->num_sms, kCW * 32 + 32, smem, st>>>(mx, mu, N, J, R, F_slots);
+}
+
+int launch_f3(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, const double *US, int R,
+              double *F_slots) {
+    CUtensorMap mx, mu;
+    if (!make_box_map(&mx, b->X, J, b->N, b->ldx) || !make_box_map(&mu, US, R, b->N, R)) return DASH_E_CUDA;
+    if (TmaSmem::strips(J) <= kCW) launch_f3_t<1>(ctx, st, mx, mu, b->N, J, R, F_slots);
+    else launch_f3_t<2>(ctx, st, mx, mu, b->N, J, R, F_slots);
+    return 0;
 }
 
 template <int RP>
@@ -1143,6 +1215,7 @@ int dash_update_pass_begin_f64(dash_ctx *ctx, void *stream, const dash_batch_f64
         ctx->stream = stream_ok(J, b->ldx, R) && N > 0;
         plan_fsplit(ctx, N, J, ctx->nsplit, ctx->rps);
         if (ctx->stream) ctx->nsplit = ctx->num_sms;
+        ctx->tma = ctx->stream && tma_ok(b, J, R);
         if (ensure(ctx->xv, sizeof(double) * std::max<int64_t>(N, 1) * R) ||
             ensure(ctx->row_slice, sizeof(int32_t) * std::max<int64_t>(N, 1)) ||
             ensure(ctx->gslots, sizeof(double) * std::max(ctx->nitems, 1) * R * R) ||
@@ -1166,7 +1239,9 @@ int dash_update_pass_begin_f64(dash_ctx *ctx, void *stream, const dash_batch_f64
                                       (double *)ctx->gsnap.p, v_used_out, pass == 0, last);
     }
     if (N > 0) {
-        if (ctx->stream) {
+        if (ctx->tma) {
+            if (launch_xv3(ctx, st, b, J, s->V, R, XV)) return DASH_E_CUDA;
+        } else if (ctx->stream) {
             if (rank_bucket(R) <= 8) launch_xv2_t<8>(ctx, st, b, J, s->V, R, XV);
             else launch_xv2_t<16>(ctx, st, b, J, s->V, R, XV);
         } else {
@@ -1193,7 +1268,9 @@ int dash_update_pass_begin_f64(dash_ctx *ctx, void *stream, const dash_batch_f64
         sp.pass = pass;
         sp.final_pass = last;
         if (launch_plan(ctx, st, RB, plan_of(ctx), sp)) return DASH_E_CUDA;
-        if (ctx->stream) {
+        if (ctx->tma) {
+            if (launch_f3(ctx, st, b, J, (const double *)ctx->us.p, R, Fsl)) return DASH_E_CUDA;
+        } else if (ctx->stream) {
             if (rank_bucket(R) <= 8) launch_f2_t<8>(ctx, st, b, J, (const double *)ctx->us.p, R, Fsl);
             else launch_f2_t<16>(ctx, st, b, J, (const double *)ctx->us.p, R, Fsl);
         } else {
