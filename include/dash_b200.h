@@ -64,6 +64,9 @@ int dash_ctx_fallbacks(dash_ctx *ctx, void *stream, int32_t reset);
 /* One update batch in CSR form: slice m (batch position) owns rows
  * [row_ptr[m], row_ptr[m+1]) of X.  Order = UpdateBatch.items() order
  * (tensor.py:166-171): existing slices, then new slices. */
+/* Rows per batch are addressed with 32-bit offsets inside the kernels. */
+#define DASH_MAX_BATCH_ROWS 2147483647LL
+
 typedef struct {
     const double *X;             /* N x ldx                                    */
     int64_t ldx;                 /* >= J                                        */

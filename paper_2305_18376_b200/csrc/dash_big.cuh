@@ -238,10 +238,8 @@ __global__ void __launch_bounds__(256, 2) k_big(SliceParams p, const int4 *__res
         double a[RB];
 #pragma unroll
         for (int z = 0; z < RB; ++z) a[z] = (lane < RB ? vtv_s[r * LDV + z] * dn[z] : 0.0) + ((z == r) ? dg2 : 0.0);
-        bool okB = sweep_inverse<RB>(a, lane < RB ? buf : red + 7 * 64, r);
-        double wv = 0.0;
-#pragma unroll
-        for (int z = 0; z < RB; ++z) wv = fma(-a[z], vec[RB + z], wv);
+        double wv;  // w = B^{-1} c  (lu: scratch until a fallback; lanes 16..31 solve a harmless identity)
+        bool okB = gj_solve<RB>(a, lreal ? vec[RB + r] : 0.0, lane < RB ? lu : red + 7 * 64, r, wv);
         if (!lreal) wv = 0.0;
         const bool good = __all_sync(FULL_MASK, (okB && isfinite(wv)) || lane >= RB);
         if (!good) {

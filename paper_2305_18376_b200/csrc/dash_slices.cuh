@@ -107,6 +107,51 @@ __device__ __forceinline__ bool sweep_inverse(double (&a)[RB], double *buf, int 
     return ok;
 }
 
+// x = B^{-1} rhs for one right-hand side (lane r holds row r of the SPD B in
+// a[] and rhs_r), by Gauss-Jordan elimination without normalising the pivot
+// row: step k subtracts (a_i[k] / d_k) x (pivot row) from every other row,
+// touching only the columns right of k; after RB steps the matrix is
+// diag(d) and x_i = rhs_i / d_i.  The pivot row's trailing entries are read
+// from the gathered column k (the trailing Schur complement is symmetric), so
+// each step costs one shared store per lane and ~(RB-k)/2 LDS.128.  The
+// pivot's reciprocal is computed one step ahead (off the critical path).
+// Same success test as the sweep / Cholesky: every pivot > 0 and finite.
+// pb: per-group scratch of >= RB + 2 doubles, 16-byte aligned.  a[] is
+// destroyed.  ~136 DFMA per lane vs ~480 DP ops for the full sweep.
+template <int RB>
+__device__ __forceinline__ bool gj_solve(double (&a)[RB], double rhs, double *pb, int r, double &x) {
+    bool ok = true;
+    double idown = 0.0;
+    double idn = rcp_nr(a[0]);  // lane 0's value is the first pivot's reciprocal
+#pragma unroll
+    for (int k = 0; k < RB; ++k) {
+        const bool piv = (r == k);
+        pb[r] = a[k];
+        if (piv) *reinterpret_cast<double2 *>(pb + RB) = make_double2(rhs, idn);
+        __syncwarp();
+        const double2 ri = *reinterpret_cast<const double2 *>(pb + RB);  // (rhs_k, 1/d_k)
+        const double2 *p2 = reinterpret_cast<const double2 *>(pb);
+        double col[RB];
+#pragma unroll
+        for (int z = (k / 2) * 2; z < RB; z += 2) {
+            const double2 v = p2[z / 2];
+            col[z] = v.x;
+            col[z + 1] = v.y;
+        }
+        const double d = col[k];
+        ok = ok && (d > 0.0) && isfinite(d);
+        if (piv) idown = ri.y;
+        const double f = piv ? 0.0 : a[k] * ri.y;
+#pragma unroll
+        for (int z = k + 1; z < RB; ++z) a[z] = fma(-f, col[z], a[z]);
+        rhs = fma(-f, ri.x, rhs);
+        if (k + 1 < RB) idn = rcp_nr(a[k + 1]);
+        __syncwarp();
+    }
+    x = rhs * idown;
+    return ok;
+}
+
 // Fallback: -A^{-1} by LU with partial pivoting, for the groups with need
 // set.  The caller stages the RB x RB matrix rows into lu (lane r -> row r,
 // pitch LDL) and reads row r of the result back from lu afterwards; only

@@ -26,10 +26,24 @@ struct S3 {
     static constexpr int per_group = RB + RB * LDL + RB * LDL + CAPW * RB + RB * LDL + RB + 2;  // even: 16B-aligned group bases
     static constexpr int shared = RB * LDV;
     __host__ __device__ static constexpr size_t bytes() { return sizeof(double) * (shared + NG * per_group); }
+    static_assert(shared % 2 == 0 && per_group % 2 == 0 && (RB + 2 * RB * LDL + CAPW * RB) % 2 == 0,
+                  "group scratch must stay 16-byte aligned");
 };
 
+// small-slice metadata, packed once per update: (r0, n, wrow | fresh << 31, m)
+__global__ void k_pack_small(const int32_t *__restrict__ small_pos, int nsmall, const int64_t *__restrict__ row_ptr,
+                             const int32_t *__restrict__ state_row, const uint8_t *__restrict__ is_new,
+                             int4 *__restrict__ meta) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nsmall; j += gridDim.x * blockDim.x) {
+        const int m = small_pos[j];
+        const int64_t r0 = row_ptr[m];
+        meta[j] = make_int4((int)r0, (int)(row_ptr[m + 1] - r0),
+                            (int)((unsigned)state_row[m] | (is_new[m] ? 0x80000000u : 0u)), m);
+    }
+}
+
 template <int RB>
-__global__ void __launch_bounds__(S3<RB>::NW * 32, 3) k_slices3(SliceParams p, const int32_t *__restrict__ small_pos,
+__global__ void __launch_bounds__(S3<RB>::NW * 32, 3) k_slices3(SliceParams p, const int4 *__restrict__ meta,
                                                                  int nsmall) {
     using S = S3<RB>;
     constexpr int LDV = S::LDV, GPW = S::GPW, CAPW = S::CAPW;
@@ -41,7 +55,7 @@ __global__ void __launch_bounds__(S3<RB>::NW * 32, 3) k_slices3(SliceParams p, c
     double *buf = sm + S::shared + gid * S::per_group;
     double *gacc = buf + RB;
     double *dns = gacc + RB * S::LDL;
-    double *xs = dns + RB * S::LDL + 1;  // +1: keep xs 16-byte aligned
+    double *xs = dns + RB * S::LDL;  // RB*LDL is even: xs and lu stay 16-byte aligned (gj_solve scratch)
     double *lu = xs + CAPW * RB;
     int *piv = reinterpret_cast<int *>(lu + RB * S::LDL);
     const int R = p.R;
@@ -56,16 +70,38 @@ __global__ void __launch_bounds__(S3<RB>::NW * 32, 3) k_slices3(SliceParams p, c
 
     const int nunits = (nsmall + GPW - 1) / GPW;
     const int nwarps = gridDim.x * S::NW;
-    for (int unit = blockIdx.x * S::NW + w; unit < nunits; unit += nwarps) {
+    // software pipeline: the next unit's metadata and W / C values are loaded
+    // while the current unit computes, so a unit starts with one dependent
+    // global round trip (the D / XV copies) instead of three.
+    const int4 none = make_int4(0, 0, 0, 0);
+    auto meta_of = [&](int unit) {
+        const int j = unit * GPW + lane / RB;
+        return (unit < nunits && j < nsmall) ? __ldg(meta + j) : none;
+    };
+    auto sw_of = [&](const int4 &mt, bool act, double &sw, double &cw) {
+        const int wr = mt.z & 0x7fffffff;
+        const bool fr = mt.z < 0;
+        sw = (act && r < R) ? ((fr && p.pass == 0) ? 1.0 : p.W[(int64_t)wr * R + r]) : 0.0;
+        cw = (act && r < R && !fr) ? p.C[(int64_t)wr * R + r] : 0.0;
+    };
+    int unit = blockIdx.x * S::NW + w;
+    int4 nmeta = meta_of(unit);
+    double nsw = 0.0, ncw = 0.0;
+    sw_of(nmeta, unit < nunits && unit * GPW + lane / RB < nsmall, nsw, ncw);
+    for (; unit < nunits; unit += nwarps) {
         const int j = unit * GPW + lane / RB;
         const bool active = j < nsmall;
-        const int m = small_pos[active ? j : 0];
-        const int64_t r0 = p.row_ptr[m];
-        const int64_t n = active ? p.row_ptr[m + 1] - r0 : 0;
-        const int wrow = p.state_row[m];
-        const bool fresh = p.is_new[m] != 0;
+        const int4 mt = nmeta;
+        const int m = mt.w;
+        const int64_t r0 = mt.x;
+        const int64_t n = active ? mt.y : 0;
+        const int wrow = mt.z & 0x7fffffff;
+        const bool fresh = mt.z < 0;
         const bool real = active && r < R;
         const bool staged = n <= CAPW;
+        const double s_r = nsw, cold = ncw;
+        const int nxt = unit + nwarps;
+        nmeta = meta_of(nxt);
         // ---- async prefetch: D column r (D symmetric; coalesced) and the XV rows
         if (real && !fresh) {
             const double *dcol = p.D + (int64_t)wrow * R * R + r;
@@ -73,10 +109,8 @@ __global__ void __launch_bounds__(S3<RB>::NW * 32, 3) k_slices3(SliceParams p, c
         }
         if (real && staged)
             for (int i = 0; i < (int)n; ++i) cp_async8(xs + i * RB + r, p.XV + (r0 + i) * R + r);
-        const double cold = (real && !fresh) ? p.C[(int64_t)wrow * R + r] : 0.0;
 
         // ---- A = vtv o s s^T + shift I, a <- -A^{-1} diag(s)  (_kernels.py:86-97)
-        const double s_r = real ? ((fresh && p.pass == 0) ? 1.0 : p.W[(int64_t)wrow * R + r]) : 0.0;
         double s_all[RB];
         group_gather<RB>(s_r, buf, r, s_all);
         double sh = 0.0;
@@ -99,6 +133,7 @@ __global__ void __launch_bounds__(S3<RB>::NW * 32, 3) k_slices3(SliceParams p, c
             const bool okLU = lu_fallback<RB>(a, lu, piv, r, R, !okA);
             if (!okA && r == 0 && !okLU) report_error(p.err, m, DASH_E_SINGULAR);
         }
+        sw_of(nmeta, nxt < nunits && nxt * GPW + lane / RB < nsmall, nsw, ncw);  // next unit's s, c_old
         group_gather<RB>(s_r, buf, r, s_all);
 #pragma unroll
         for (int z = 0; z < RB; ++z) a[z] *= s_all[z];
@@ -169,12 +204,8 @@ __global__ void __launch_bounds__(S3<RB>::NW * 32, 3) k_slices3(SliceParams p, c
 #pragma unroll
             for (int z = 0; z < RB; ++z) a[z] = vrow[z] * dn[z] + ((z == r) ? dg2 : 0.0);
         }
-        const bool okB = sweep_inverse<RB>(a, buf, r);
-        double call[RB];
-        group_gather<RB>(cn, buf, r, call);
-        double wv = 0.0;
-#pragma unroll
-        for (int z = 0; z < RB; ++z) wv = fma(-a[z], call[z], wv);
+        double wv;
+        const bool okB = gj_solve<RB>(a, cn, lu, r, wv);  // w = B^{-1} c (lu: scratch until a fallback)
         if (!real) wv = 0.0;
         bool gok = okB && isfinite(wv);
         {
@@ -191,6 +222,8 @@ __global__ void __launch_bounds__(S3<RB>::NW * 32, 3) k_slices3(SliceParams p, c
             if (need && r == 0) atomicAdd(p.fallbacks, 1u);
             const bool okLU = lu_fallback<RB>(a, lu, piv, r, R, need);
             if (need && r == 0 && !okLU) report_error(p.err, m, DASH_E_SINGULAR);
+            double call[RB];
+            group_gather<RB>(cn, buf, r, call);
             double wv2 = 0.0;
 #pragma unroll
             for (int z = 0; z < RB; ++z) wv2 = fma(-a[z], call[z], wv2);
@@ -229,13 +262,13 @@ __global__ void __launch_bounds__(S3<RB>::NW * 32, 3) k_slices3(SliceParams p, c
 }
 
 template <int RB>
-int launch_slices3(cudaStream_t st, int grid, const SliceParams &sp, const int32_t *small_pos, int nsmall) {
+int launch_slices3(cudaStream_t st, int grid, const SliceParams &sp, const int4 *meta, int nsmall) {
     const size_t smem = S3<RB>::bytes();
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_slices3<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    k_slices3<RB><<<grid, S3<RB>::NW * 32, smem, st>>>(sp, small_pos, nsmall);
+    k_slices3<RB><<<grid, S3<RB>::NW * 32, smem, st>>>(sp, meta, nsmall);
     return cudaGetLastError() == cudaSuccess ? 0 : DASH_E_CUDA;
 }

@@ -695,7 +695,7 @@ struct dash_ctx {
         void *p = nullptr;
         size_t cap = 0;
     };
-    Buf xv, row_slice, items, gslots, fslots, vtv, fsnap, gsnap, fg, part, us, scratch;
+    Buf xv, row_slice, items, gslots, fslots, vtv, fsnap, gsnap, fg, part, us, scratch, smeta;
     unsigned long long *err = nullptr;
     unsigned int *fallbacks = nullptr;
     int4 *items_host[2] = {nullptr, nullptr};
@@ -895,11 +895,11 @@ SlicePlan &plan_of(dash_ctx *ctx) { return *reinterpret_cast<SlicePlan *>(ctx->p
 int launch_plan(dash_ctx *ctx, cudaStream_t st, int RB, const SlicePlan &pl, SliceParams sp) {
     if (!pl.split) return dispatch_slices(ctx, st, RB, (int)pl.items.size(), sp);
     PhaseScope ps(ctx, st, PH_SLICES);
-    const int32_t *small_pos = reinterpret_cast<const int32_t *>(sp.items + pl.nbig);
+    const int4 *meta = (const int4 *)ctx->smeta.p;  // packed by k_pack_small at pass 0
     if (pl.nsmall > 0) {
-        int rc = RB == 4 ? launch_slices3<4>(st, pl.g3, sp, small_pos, pl.nsmall)
-                 : RB == 8 ? launch_slices3<8>(st, pl.g3, sp, small_pos, pl.nsmall)
-                           : launch_slices3<16>(st, pl.g3, sp, small_pos, pl.nsmall);
+        int rc = RB == 4 ? launch_slices3<4>(st, pl.g3, sp, meta, pl.nsmall)
+                 : RB == 8 ? launch_slices3<8>(st, pl.g3, sp, meta, pl.nsmall)
+                           : launch_slices3<16>(st, pl.g3, sp, meta, pl.nsmall);
         if (rc) return rc;
     }
     if (pl.nbig > 0) {
@@ -1117,7 +1117,8 @@ void dash_ctx_destroy(dash_ctx *ctx) {
     if (!ctx) return;
     cudaDeviceSynchronize();
     dash_ctx::Buf *bufs[] = {&ctx->xv,  &ctx->row_slice, &ctx->items, &ctx->gslots, &ctx->fslots,
-                             &ctx->vtv, &ctx->fsnap,     &ctx->gsnap, &ctx->fg,     &ctx->part, &ctx->us, &ctx->scratch};
+                             &ctx->vtv, &ctx->fsnap,     &ctx->gsnap, &ctx->fg,     &ctx->part, &ctx->us, &ctx->scratch,
+                             &ctx->smeta};
     for (auto *b : bufs)
         if (b->p) cudaFree(b->p);
     cudaFree(ctx->err);
@@ -1199,7 +1200,9 @@ int dash_ctx_phase_ms(dash_ctx *ctx, double *ms_out, int32_t *count_out, int32_t
 int dash_update_pass_begin_f64(dash_ctx *ctx, void *stream, const dash_batch_f64 *b, dash_state_f64 *s,
                                double *U_out, double *v_used_out, double eps, int32_t pass, double *fg_out) {
     if (!ctx || !b || !valid_state(s) || !U_out || !v_used_out || !fg_out) return DASH_E_ARG;
-    if (b->M < 0 || b->N < 0 || (b->N > 0 && b->ldx < s->J) || pass < 0 || pass >= s->passes) return DASH_E_ARG;
+    if (b->M < 0 || b->N < 0 || b->N > DASH_MAX_BATCH_ROWS || (b->N > 0 && b->ldx < s->J) || pass < 0 ||
+        pass >= s->passes)
+        return DASH_E_ARG;
     const int J = s->J, R = s->R;
     cudaStream_t st = (cudaStream_t)stream;
     const int RB = rank_bucket(R);
@@ -1224,6 +1227,14 @@ int dash_update_pass_begin_f64(dash_ctx *ctx, void *stream, const dash_batch_f64
             (ctx->stream && ensure(ctx->us, sizeof(double) * std::max<int64_t>(N, 1) * R)))
             return DASH_E_CUDA;
         if (!items.empty() && stage_items(ctx, st, items)) return DASH_E_CUDA;
+        const SlicePlan &pl = plan_of(ctx);
+        if (pl.split && pl.nsmall > 0) {
+            if (ensure(ctx->smeta, sizeof(int4) * pl.nsmall)) return DASH_E_CUDA;
+            PhaseScope ps(ctx, st, PH_ROWSLICE);
+            k_pack_small<<<std::min(ctx->num_sms * 2, (pl.nsmall + 255) / 256), 256, 0, st>>>(
+                reinterpret_cast<const int32_t *>((const int4 *)ctx->items.p + pl.nbig), pl.nsmall, b->row_ptr,
+                b->state_row, b->is_new, (int4 *)ctx->smeta.p);
+        }
         if (M > 0 && !ctx->stream) {  // row -> slice map: only the generic F GEMM needs it
             PhaseScope ps(ctx, st, PH_ROWSLICE);
             k_row_slice<<<std::min(ctx->num_sms * 4, (M + 7) / 8 + 1), 256, 0, st>>>(b->row_ptr, M,
