@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--impl", default="dash", choices=["dash", "reference"])
     ap.add_argument("--config", default=CONFIG_NAME)
     ap.add_argument("--K0", type=int, default=None, help="override K0 (smoke runs)")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=2)
     return ap.parse_args()
@@ -92,16 +92,34 @@ def algorithmic_flops(N, J, R, M):
     return 4 * N * J * R + N * (3 * R * R + 2 * R) + M * (4 * R ** 3 / 3 + 4 * R * R)
 
 
-def kernel_bytes(phase, N, J, R, M_old, L, nsplit, b=8):
+SMALL_ROWS = 64  # csrc/dash_update.cu kSmallRows: slices with more rows go to k_big
+
+
+def batch_stats(batches):
+    """Average rows / existing / new slices per update, split small vs big."""
+    acc = dict(N=0.0, Ns=0.0, Mos=0.0, Ls=0.0, Nb=0.0, Mob=0.0, Lb=0.0)
+    for b in batches:
+        c = np.asarray(b["counts"])
+        new = np.arange(len(c)) >= b["M_old"]
+        small = c <= SMALL_ROWS
+        acc["N"] += c.sum()
+        for k, m in (("s", small), ("b", ~small)):
+            acc["N" + k] += c[m].sum()
+            acc["Mo" + k] += (m & ~new).sum()
+            acc["L" + k] += (m & new).sum()
+    return {k: v / max(len(batches), 1) for k, v in acc.items()}
+
+
+def kernel_bytes(phase, st, J, R, nsplit, b=8):
     """Algorithmic bytes per launch of each kernel (DESIGN.md table)."""
-    if phase == "xv":
+    N = st["N"]
+    if phase == "xv":        # read X, V; write XV
         return b * (N * J + N * R + J * R)
-    if phase == "fgemm":
-        return b * (N * J + N * R + nsplit * J * R) + 4 * N + b * (M_old + L) * R
-    if phase == "slices":
-        return b * (2 * N * R + 2 * M_old * (R * R + 2 * R) + L * (R * R + 2 * R))
-    if phase == "fused":
-        return algorithmic_bytes(N, J, R, M_old, L, b)
+    if phase == "fgemm":     # read X, US; write one J x R slot per CTA
+        return b * (N * J + N * R + nsplit * J * R)
+    if phase in ("slices", "big"):  # read XV; write U, US; per-slice W/C/D r/w (new: write only)
+        k = "s" if phase == "slices" else "b"
+        return b * (3 * st["N" + k] * R + st["Mo" + k] * (2 * R * R + 4 * R) + st["L" + k] * (R * R + 2 * R))
     return 0
 
 
@@ -200,7 +218,8 @@ def run_gpu(args):
     if args.K0:
         cfg = wl.scaled(cfg, K0=args.K0)
     J, R = cfg.J, cfg.R
-    total_steps = args.warmup + args.steps + args.e2e_steps
+    prof_steps = 3  # separate profiled steps for the per-phase breakdown (events kept out of the timed loop)
+    total_steps = args.warmup + args.steps + prof_steps + args.e2e_steps
     sched = Schedule(cfg, total_steps, cfg.seed)
     H, V = wl.true_factors(cfg)
     # true per-slice weights for every slice that will ever exist
@@ -274,7 +293,6 @@ def run_gpu(args):
     sampler = ClockSampler(local)
     barrier()
     torch.cuda.synchronize()
-    L.dash_ctx_set_profiling(state._ctx, 1)
     sampler.start()
     time.sleep(0.3)
     stream = torch.cuda.current_stream()
@@ -288,13 +306,20 @@ def run_gpu(args):
     torch.cuda.synchronize()
     barrier()
     clocks = sampler.stop()
+    fallbacks = L.dash_ctx_fallbacks(state._ctx, nat.stream_ptr(), 1)
+    # per-phase breakdown: separate steps with CUDA events around every launch
     import ctypes
+    profiled = batches[args.warmup + args.steps:args.warmup + args.steps + prof_steps]
+    torch.cuda.synchronize()
+    L.dash_ctx_set_profiling(state._ctx, 1)
+    for b in profiled:
+        step(b)
+    torch.cuda.synchronize()
     nph = len(nat.PHASES)
     ms_arr = (ctypes.c_double * nph)()
     cnt_arr = (ctypes.c_int32 * nph)()
     L.dash_ctx_phase_ms(state._ctx, ms_arr, cnt_arr, nph)
     L.dash_ctx_set_profiling(state._ctx, 0)
-    fallbacks = L.dash_ctx_fallbacks(state._ctx, nat.stream_ptr(), 1)
     state.check()
     t_ms = e1.elapsed_time(e0) if False else e0.elapsed_time(e1)
     t_max = t_ms
@@ -311,31 +336,37 @@ def run_gpu(args):
     value = elems / (t_max / 1e3)
     ms_per_step = t_max / len(timed)
 
-    # e2e through the public API with host buffers
-    e2e_b = batches[args.warmup + args.steps:]
+    # e2e through the public API with host buffers: HostPipeline uploads batch
+    # t+1 (pinned host -> HBM) and reads back batch t-1's U / v_used while
+    # batch t is updated; every step's H2D and D2H lie inside the timed region.
+    from paper_2305_18376_b200.stream import HostPipeline
+    e2e_b = batches[args.warmup + args.steps + prof_steps:]
     pins = []
     for b in e2e_b:
         hp = torch.empty_like(b["X"], device="cpu").pin_memory()
         hp.copy_(b["X"])
         pins.append(hp)
-    Uh = torch.empty((max(b["N"] for b in e2e_b), R), dtype=torch.float64).pin_memory() if e2e_b else None
-    vh = torch.empty((J, R), dtype=torch.float64).pin_memory()
-    Xd = torch.empty((max((b["N"] for b in e2e_b), default=1), J), dtype=torch.float64, device=dev)
+        b["X"] = None  # device copy no longer needed
+    maxN = max((b["N"] for b in e2e_b), default=1)
+    Uh = [torch.empty((maxN, R), dtype=torch.float64).pin_memory() for _ in range(2)]
+    vh = [torch.empty((J, R), dtype=torch.float64).pin_memory() for _ in range(2)]
+    pipe = HostPipeline(engine if engine is not None else state, maxN, J, device=dev)
     torch.cuda.synchronize()
     barrier()
     h2d = d2h = 0
     e2 = torch.cuda.Event(enable_timing=True)
     e3 = torch.cuda.Event(enable_timing=True)
     e2.record(stream)
-    for b, hp in zip(e2e_b, pins):
+    pipe.start()
+    staged = pipe.put(pins[0]) if e2e_b else None
+    for k, b in enumerate(e2e_b):
+        nxt = pipe.put(pins[k + 1]) if k + 1 < len(e2e_b) else None
+        pipe.update(staged, b["counts"], b["ex_rows"], b["new"], U_host=Uh[k % 2], v_host=vh[k % 2])
+        staged = nxt
         N = b["N"]
-        Xd[:N].copy_(hp, non_blocking=True)
-        b2 = dict(b, X=Xd[:N])
-        U, vu = step(b2)
-        Uh[:N].copy_(U, non_blocking=True)
-        vh.copy_(vu, non_blocking=True)
         h2d += N * J * 8 + (b["M_old"] + b["L"]) * (8 + 4 + 1) + 8
         d2h += N * R * 8 + J * R * 8
+    pipe.finish()
     e3.record(stream)
     torch.cuda.synchronize()
     state.check()
@@ -355,14 +386,24 @@ def run_gpu(args):
     phase_ms = {nat.PHASES[i]: ms_arr[i] for i in range(nph)}
     phase_n = {nat.PHASES[i]: cnt_arr[i] for i in range(nph)}
     dom = max(phase_ms, key=lambda k: phase_ms[k])
-    nb = len(timed)
-    N_avg = sum(b["N"] for b in timed) / nb
-    M_old_avg = sum(b["M_old"] for b in timed) / nb
-    L_avg = sum(b["L"] for b in timed) / nb
-    nsplit = int(np.clip(np.ceil(N_avg / 1024), 1, 148 * 4 // ((J + 63) // 64) + 1))
+    nb = len(profiled)
+    nt = len(timed)
+    N_avg = sum(b["N"] for b in timed) / nt
+    M_old_avg = sum(b["M_old"] for b in timed) / nt
+    L_avg = sum(b["L"] for b in timed) / nt
+    nsplit = torch.cuda.get_device_properties(dev).multi_processor_count  # streaming GEMM: one slot per CTA
     peak, peak_kind = peaks()
     per_launch_ms = phase_ms[dom] / max(phase_n[dom], 1)
-    kb = kernel_bytes(dom, N_avg, J, R, M_old_avg, L_avg, nsplit)
+    stt = batch_stats(profiled)
+    kb = kernel_bytes(dom, stt, J, R, nsplit)
+    per_kernel = {}
+    for ph in phase_ms:
+        if phase_n[ph]:
+            ms1 = phase_ms[ph] / phase_n[ph]
+            kb1 = kernel_bytes(ph, stt, J, R, nsplit)
+            per_kernel[ph] = {"ms_per_launch": ms1, "alg_bytes": kb1,
+                              "gbs": kb1 / (ms1 / 1e3) / 1e9 if kb1 else None,
+                              "frac_hbm": kb1 / (ms1 / 1e3) / 1e9 / peak if kb1 else None}
     achieved = kb / (per_launch_ms / 1e3) / 1e9
     step_bytes = algorithmic_bytes(N_avg, J, R, M_old_avg, L_avg)
     step_achieved = step_bytes / (ms_per_step / 1e3) / 1e9
@@ -389,6 +430,7 @@ def run_gpu(args):
                               "alg_flops": algorithmic_flops(N_avg, J, R, M_old_avg + L_avg),
                               "tflops": algorithmic_flops(N_avg, J, R, M_old_avg + L_avg) / (ms_per_step / 1e3) / 1e12},
             "phase_ms_per_step": {k: v / nb for k, v in phase_ms.items() if phase_n[k]},
+            "per_kernel_roofline": per_kernel,
             "e2e": {"value": e2e_value, "unit": "elements/s", "h2d_bytes_per_step": h2d / max(len(e2e_b), 1),
                     "d2h_bytes_per_step": d2h / max(len(e2e_b), 1),
                     "ms_per_step": e2e_ms / max(len(e2e_b), 1), "steps": len(e2e_b)},

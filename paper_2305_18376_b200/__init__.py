@@ -13,7 +13,7 @@ from .tensor import DatasetError, IrregularTensor, NewSlice, SliceMatrix, Update
 
 def __getattr__(name):
     # torch-dependent pieces load on first use (keeps `import` light on CPU-only hosts)
-    if name in ("StreamState", "UpdateResult", "HelperState", "initialize", "init_helpers"):
+    if name in ("StreamState", "UpdateResult", "HelperState", "HostPipeline", "initialize", "init_helpers"):
         from . import stream
         return getattr(stream, name)
     if name == "local_error":
@@ -26,7 +26,8 @@ def __getattr__(name):
 
 
 __all__ = [
-    "ALSInfo", "DatasetError", "FactorSet", "FactorizationError", "HelperState", "IrregularTensor",
+    "ALSInfo", "DatasetError", "FactorSet", "FactorizationError", "HelperState", "HostPipeline",
+    "IrregularTensor",
     "NewSlice", "RIDGE_EPS", "ShardedStream", "SliceMatrix", "SolveError", "StreamState",
     "UpdateBatch", "UpdateResult", "init_helpers", "initialize", "local_error", "parafac2_als",
     "reconstruct", "relative_error",

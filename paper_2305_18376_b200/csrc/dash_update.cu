@@ -688,7 +688,7 @@ __global__ void k_finish_fg(const double *__restrict__ fg, const double *__restr
 }
 }  // namespace
 
-enum Phase { PH_ROWSLICE = 0, PH_PROLOGUE, PH_XV, PH_SLICES, PH_FGEMM, PH_SUMFG, PH_VSOLVE, PH_COUNT };
+enum Phase { PH_ROWSLICE = 0, PH_PROLOGUE, PH_XV, PH_SLICES, PH_FGEMM, PH_SUMFG, PH_VSOLVE, PH_BIG, PH_COUNT };
 
 struct dash_ctx {
     struct Buf {
@@ -894,16 +894,16 @@ SlicePlan &plan_of(dash_ctx *ctx) { return *reinterpret_cast<SlicePlan *>(ctx->p
 
 int launch_plan(dash_ctx *ctx, cudaStream_t st, int RB, const SlicePlan &pl, SliceParams sp) {
     if (!pl.split) return dispatch_slices(ctx, st, RB, (int)pl.items.size(), sp);
-    PhaseScope ps(ctx, st, PH_SLICES);
     const int4 *meta = (const int4 *)ctx->smeta.p;  // packed by k_pack_small at pass 0
     if (pl.nsmall > 0) {
+        PhaseScope ps(ctx, st, PH_SLICES);
         int rc = RB == 4 ? launch_slices3<4>(st, pl.g3, sp, meta, pl.nsmall)
                  : RB == 8 ? launch_slices3<8>(st, pl.g3, sp, meta, pl.nsmall)
                            : launch_slices3<16>(st, pl.g3, sp, meta, pl.nsmall);
         if (rc) return rc;
     }
     if (pl.nbig > 0) {
-        if (pl.nsmall > 0) ctx->last_launches++;  // two kernels under one phase
+        PhaseScope ps(ctx, st, PH_BIG);
         SliceParams sb = sp;
         sb.G_slots = sp.G_slots + (int64_t)pl.g3 * sp.R * sp.R;
         if (RB == 16 && (sp.R % 2) == 0) return launch_big(st, pl.nbig, sb, sp.items);  // DMMA big-slice kernel

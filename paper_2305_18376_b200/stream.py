@@ -528,6 +528,79 @@ class StreamState:
         raise SolveError(msg, sid)
 
 
+class HostPipeline:
+    """Overlapped host-memory feeding of ``update_packed`` (serving loop).
+
+    ``put(X_host)`` copies a pinned host batch into one of ``depth`` device
+    buffers on a dedicated H2D stream; ``update(staged, ...)`` makes the
+    compute stream wait for that copy (an event, no host sync), runs the
+    update, and starts the read-back of U_new / v_used into caller-provided
+    pinned buffers on a D2H stream.  So batch t+1's upload and batch t-1's
+    read-back run while batch t is being updated; a buffer is reused only
+    after the update that read it has finished (event-ordered).  ``engine`` is
+    a StreamState or a ShardedStream (anything with ``update_packed``).
+    """
+
+    class Staged:
+        __slots__ = ("slot", "X", "ready")
+
+        def __init__(self, slot, X, ready):
+            self.slot, self.X, self.ready = slot, X, ready
+
+    def __init__(self, engine, max_rows: int, J: int, device=None, depth: int = 2):
+        self.engine = engine
+        dev = _dev(device)
+        self.device = dev
+        self.depth = depth
+        self.bufs = [torch.empty((max(int(max_rows), 1), J), dtype=F64, device=dev) for _ in range(depth)]
+        self.h2d = torch.cuda.Stream(dev)
+        self.d2h = torch.cuda.Stream(dev)
+        self._free = [None] * depth
+        self._k = 0
+
+    def start(self):
+        """Order the side streams after everything already queued on the compute stream."""
+        cur = torch.cuda.current_stream(self.device)
+        self.h2d.wait_stream(cur)
+        self.d2h.wait_stream(cur)
+
+    def put(self, X_host: torch.Tensor) -> "HostPipeline.Staged":
+        slot = self._k % self.depth
+        self._k += 1
+        N = int(X_host.shape[0])
+        if N > self.bufs[slot].shape[0]:
+            raise ValueError(f"batch of {N} rows exceeds the pipeline's max_rows {self.bufs[slot].shape[0]}")
+        X = self.bufs[slot][:N]
+        with torch.cuda.stream(self.h2d):
+            if self._free[slot] is not None:
+                self.h2d.wait_event(self._free[slot])
+            X.copy_(X_host, non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record(self.h2d)
+        return HostPipeline.Staged(slot, X, ready)
+
+    def update(self, staged, counts, existing_rows, new_ids, U_host=None, v_host=None):
+        cur = torch.cuda.current_stream(self.device)
+        cur.wait_event(staged.ready)
+        U, v_used = self.engine.update_packed(staged.X, counts, existing_rows, new_ids)
+        done = torch.cuda.Event()
+        done.record(cur)
+        self._free[staged.slot] = done
+        if U_host is not None or v_host is not None:
+            with torch.cuda.stream(self.d2h):
+                self.d2h.wait_event(done)
+                if U_host is not None:
+                    U_host[:U.shape[0]].copy_(U, non_blocking=True)
+                if v_host is not None:
+                    v_host.copy_(v_used, non_blocking=True)
+        return U, v_used
+
+    def finish(self):
+        """Make the compute stream wait for every queued copy (no host sync)."""
+        cur = torch.cuda.current_stream(self.device)
+        cur.wait_stream(self.h2d)
+        cur.wait_stream(self.d2h)
+
 
 def init_helpers(tensor: IrregularTensor, factors: FactorSet, forgetting: float = 0.7,
                  device=None) -> HelperState:

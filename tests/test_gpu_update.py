@@ -223,3 +223,52 @@ def test_ridge_solve_matches_oracle():
         lhs = base @ base.transpose(0, 2, 1)
         rhs = rng.standard_normal((4, n, m))
         assert rel(ridge_solve(lhs, rhs), orc.ridge_solve(lhs, rhs)) < 1e-10
+
+
+def _packed(state, batch):
+    """UpdateBatch -> update_packed arguments (items() order: existing, then new)."""
+    ex = list(batch.existing_rows.items())
+    X = np.concatenate([r for _, r in ex] + [ns.rows for ns in batch.new_slices])
+    counts = np.array([r.shape[0] for _, r in ex] + [ns.rows.shape[0] for ns in batch.new_slices])
+    rows = np.array([state.row_of(s) for s, _ in ex], dtype=np.int32)
+    return X, counts, rows, [ns.slice_id for ns in batch.new_slices]
+
+
+def test_host_pipeline_matches_device_resident_updates():
+    """HostPipeline (overlapped pinned H2D / update / D2H) is bit-identical to
+    update_packed on device-resident batches."""
+    from paper_2305_18376_b200 import workloads as wl
+    from paper_2305_18376_b200.stream import HostPipeline
+    cfg = wl.scaled(wl.CONFIGS["large"], K0=200, steps=4, new_slices=3)
+    stream = wl.make_stream(cfg)
+    ps = wl.planted_state(stream)
+    a = gpu_state_from_planted(ps)
+    b = gpu_state_from_planted(ps)
+    batches = list(stream.batches())
+    ref = []
+    for bt in batches:
+        X, counts, rows, new = _packed(a, bt)
+        U, vu = a.update_packed(torch.as_tensor(X, device="cuda"), counts, rows, new)
+        ref.append((U.cpu().numpy(), vu.cpu().numpy()))
+    Xs = [np.concatenate([r for _, r in bt.existing_rows.items()] + [ns.rows for ns in bt.new_slices])
+          for bt in batches]
+    pins = [torch.as_tensor(X).pin_memory() for X in Xs]
+    maxN = max(X.shape[0] for X in Xs)
+    R = ps["V"].shape[1]
+    Uh = [torch.empty((maxN, R), dtype=torch.float64).pin_memory() for _ in batches]
+    vh = [torch.empty((cfg.J, R), dtype=torch.float64).pin_memory() for _ in batches]
+    pipe = HostPipeline(b, maxN, cfg.J)
+    pipe.start()
+    staged = pipe.put(pins[0])
+    for k, bt in enumerate(batches):
+        nxt = pipe.put(pins[k + 1]) if k + 1 < len(batches) else None
+        _, counts, rows, new = _packed(b, bt)  # state rows: after the previous update registered its slices
+        pipe.update(staged, counts, rows, new, U_host=Uh[k], v_host=vh[k])
+        staged = nxt
+    pipe.finish()
+    torch.cuda.synchronize()
+    for k, (U, vu) in enumerate(ref):
+        assert np.array_equal(Uh[k][:U.shape[0]].numpy(), U), k
+        assert np.array_equal(vh[k].numpy(), vu), k
+    for name in ("W", "C", "D", "F", "G", "V"):
+        assert np.array_equal(getattr(a, name), getattr(b, name)), name

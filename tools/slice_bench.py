@@ -29,7 +29,7 @@ def run(K0, J, R, rows_existing, n_new, rows_new, reps=5):
         ms = (ctypes.c_double * 8)(); cnt = (ctypes.c_int32 * 8)()
         L.dash_ctx_phase_ms(st._ctx, ms, cnt, 8)
         if rep >= 1:
-            out.append({nat.PHASES[i]: ms[i] for i in range(8) if cnt[i]})
+            out.append({nat.PHASES[i]: ms[i] for i in range(len(nat.PHASES)) if cnt[i]})
     avg = {k: float(np.mean([o[k] for o in out])) for k in out[0]}
     return avg
 
