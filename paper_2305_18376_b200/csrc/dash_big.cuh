@@ -37,6 +37,7 @@ __device__ __forceinline__ void cp_async16(double *dst, const double *src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 __device__ __forceinline__ void cp_async_wait2() { asm volatile("cp.async.wait_group 2;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
 // stage XV rows [row0, row0+nr) into xs (pitch XPI); R must be even (16-byte chunks)
 __device__ __forceinline__ void big_stage(double *xs, const double *XV, int64_t row0, int nr, int R) {
@@ -48,7 +49,11 @@ __device__ __forceinline__ void big_stage(double *xs, const double *XV, int64_t 
     }
 }
 
-__global__ void __launch_bounds__(256, 2) k_big(SliceParams p, const int4 *__restrict__ bigs) {
+// CTA b processes big slices b, b + gridDim.x, ... of the device plan (meta +
+// nsmall, longest size class first; launched with one CTA per big slice) and
+// accumulates their gram o w w^T into its own G slot (deterministic).
+__global__ void __launch_bounds__(256, 2) k_big(SliceParams p, const int4 *__restrict__ meta,
+                                                const int *__restrict__ plan_counts) {
     using B = BigSmem;
     constexpr int RB = B::RB, RP = B::RP, BR = B::BR, XPI = B::XPI, UPI = B::UPI, MPI = B::MPI, LDV = B::LDV,
                   LDL = B::LDL;
@@ -67,251 +72,258 @@ __global__ void __launch_bounds__(256, 2) k_big(SliceParams p, const int4 *__res
     const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
     const int g = lane >> 2, t = lane & 3;
     const int R = p.R;
-    const int m = bigs[blockIdx.x].x;
-    const int64_t r0 = p.row_ptr[m], n = p.row_ptr[m + 1] - r0;
-    const int wrow = p.state_row[m];
-    const bool fresh = p.is_new[m] != 0;
-    // prefetch the first two XV blocks while the A system is solved
-    const int nblk = (int)((n + BR - 1) / BR);
-    for (int q = 0; q < B::NS - 1; ++q) {
-        if (q < nblk) big_stage(xs0 + q * BR * XPI, p.XV, r0 + (int64_t)q * BR, (int)min((int64_t)BR, n - (int64_t)q * BR), R);
-        cp_async_commit();
-    }
+    const int nsmall = plan_counts[0], nbig = plan_counts[1];
     for (int i = tid; i < RB * LDV; i += blockDim.x) {
         const int a = i / LDV, b = i % LDV;
         vtv_s[i] = (a < R && b < R) ? p.vtv[a * R + b] : 0.0;
     }
-    if (tid < RB) vec[tid] = tid < R ? ((fresh && p.pass == 0) ? 1.0 : p.W[(int64_t)wrow * R + tid]) : 0.0;
-    if (tid < RB && !fresh)
-        for (int z = 0; z < R; ++z) dns[tid * LDL + z] = tid < R ? p.D[(int64_t)wrow * R * R + (int64_t)z * R + tid] : 0.0;
-    const double cold = (tid < R && !fresh) ? p.C[(int64_t)wrow * R + tid] : 0.0;
-    __syncthreads();
-    // ---- A sweep by warp 0, lanes 0..15 (lanes 16..31 run a harmless identity copy)
-    if (w == 0) {
-        // s is read from shared (vec) rather than held in a register array: keeps
-        // the sweep's live set at a[] + the gathered column (no spills)
-        const int r = lane % RB;
-        const bool real = lane < RB && r < R;
-        const double s_r = real ? vec[r] : 0.0;
-        double sh = 0.0;
-#pragma unroll
-        for (int z = 0; z < RB; ++z)
-            if (z < R) sh += vtv_s[z * LDV + z] * vec[z] * vec[z];
-        sh = p.eps * sh / R;
-        const double dg = real ? sh : 1.0;
-        const double *vrow = vtv_s + r * LDV;
-        double a2[RB];
-#pragma unroll
-        for (int z = 0; z < RB; ++z) a2[z] = (lane < RB ? vrow[z] * s_r * vec[z] : 0.0) + ((z == r) ? dg : 0.0);
-        // lanes 0..15 sweep A; lanes 16..31 sweep a harmless identity (own gather buffer)
-        const bool okA = sweep_inverse<RB>(a2, lane < RB ? buf : red + 7 * 64, r);
-        const unsigned badA = __ballot_sync(FULL_MASK, !okA) & 0xffffu;
-        if (badA) {
-            const bool need = lane < RB;
-#pragma unroll
-            for (int z = 0; z < RB; ++z)
-                if (need) a2[z] = vrow[z] * s_r * vec[z] + ((z == r) ? dg : 0.0);
-            if (lane == 0) atomicAdd(p.fallbacks, 1u);
-            const bool okLU = lu_fallback<RB>(a2, lu, piv, r, R, need);
-            if (lane == 0 && !okLU) report_error(p.err, m, DASH_E_SINGULAR);
-        }
-        // Ms[n][k] = A^{-1}[n][k] s_k, so U = XV Ms^T  (a2 holds -A^{-1})
-        if (lane < RB) {
-#pragma unroll
-            for (int z = 0; z < RB; ++z) Ms[r * MPI + z] = -a2[z] * vec[z];
-        }
-    }
-    __syncthreads();
-
-    // ---- rows, one 64-row block at a time (double-buffered XV)
-    double cacc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // c partials for cols (nb*8 + 2t + e)
-    double gacc[2] = {0.0, 0.0};  // gram tile (mi, ni) = ((w&3) >> 1, w & 1), K half w >> 2
-    for (int bi = 0; bi < nblk; ++bi) {
-        double *xs = xs0 + (bi % B::NS) * BR * XPI;
-        const int64_t b0 = r0 + (int64_t)bi * BR;
-        const int nr = (int)min((int64_t)BR, n - (int64_t)bi * BR);
-        {
-            const int q = bi + B::NS - 1;  // refill the stage consumed two blocks ago
-            if (q < nblk)
-                big_stage(xs0 + (q % B::NS) * BR * XPI, p.XV, r0 + (int64_t)q * BR,
-                          (int)min((int64_t)BR, n - (int64_t)q * BR), R);
+    double gslot = 0.0;  // this thread's entry (tid) of the CTA's G slot
+    for (int bi = blockIdx.x; bi < nbig; bi += gridDim.x) {
+        __syncthreads();  // previous slice done with the shared buffers
+        const int4 mt = meta[nsmall + bi];
+        const int m = mt.w;
+        const int64_t r0 = mt.x, n = mt.y;
+        const int wrow = mt.z & 0x7fffffff;
+        const bool fresh = mt.z < 0;
+        // prefetch the first two XV blocks while the A system is solved
+        const int nblk = (int)((n + BR - 1) / BR);
+        for (int q = 0; q < B::NS - 1; ++q) {
+            if (q < nblk) big_stage(xs0 + q * BR * XPI, p.XV, r0 + (int64_t)q * BR, (int)min((int64_t)BR, n - (int64_t)q * BR), R);
             cp_async_commit();
         }
-        cp_async_wait2();
+        if (tid < RB) vec[tid] = tid < R ? ((fresh && p.pass == 0) ? 1.0 : p.W[(int64_t)wrow * R + tid]) : 0.0;
+        if (tid < RB && !fresh)
+            for (int z = 0; z < R; ++z) dns[tid * LDL + z] = tid < R ? p.D[(int64_t)wrow * R * R + (int64_t)z * R + tid] : 0.0;
+        const double cold = (tid < R && !fresh) ? p.C[(int64_t)wrow * R + tid] : 0.0;
         __syncthreads();
-        if (nr < BR || R < RP) {  // zero padded columns / tail rows of the staged block
-            for (int e = tid; e < BR * XPI; e += blockDim.x) {
-                const int i = e / XPI, z = e % XPI;
-                if (i >= nr || z >= R) xs[e] = 0.0;
+        // ---- A sweep by warp 0, lanes 0..15 (lanes 16..31 run a harmless identity copy)
+        if (w == 0) {
+            // s is read from shared (vec) rather than held in a register array: keeps
+            // the sweep's live set at a[] + the gathered column (no spills)
+            const int r = lane % RB;
+            const bool real = lane < RB && r < R;
+            const double s_r = real ? vec[r] : 0.0;
+            double sh = 0.0;
+    #pragma unroll
+            for (int z = 0; z < RB; ++z)
+                if (z < R) sh += vtv_s[z * LDV + z] * vec[z] * vec[z];
+            sh = p.eps * sh / R;
+            const double dg = real ? sh : 1.0;
+            const double *vrow = vtv_s + r * LDV;
+            double a2[RB];
+    #pragma unroll
+            for (int z = 0; z < RB; ++z) a2[z] = (lane < RB ? vrow[z] * s_r * vec[z] : 0.0) + ((z == r) ? dg : 0.0);
+            // lanes 0..15 sweep A; lanes 16..31 sweep a harmless identity (own gather buffer)
+            const bool okA = sweep_inverse<RB>(a2, lane < RB ? buf : red + 7 * 64, r);
+            const unsigned badA = __ballot_sync(FULL_MASK, !okA) & 0xffffu;
+            if (badA) {
+                const bool need = lane < RB;
+    #pragma unroll
+                for (int z = 0; z < RB; ++z)
+                    if (need) a2[z] = vrow[z] * s_r * vec[z] + ((z == r) ? dg : 0.0);
+                if (lane == 0) atomicAdd(p.fallbacks, 1u);
+                const bool okLU = lu_fallback<RB>(a2, lu, piv, r, R, need);
+                if (lane == 0 && !okLU) report_error(p.err, m, DASH_E_SINGULAR);
+            }
+            // Ms[n][k] = A^{-1}[n][k] s_k, so U = XV Ms^T  (a2 holds -A^{-1})
+            if (lane < RB) {
+    #pragma unroll
+                for (int z = 0; z < RB; ++z) Ms[r * MPI + z] = -a2[z] * vec[z];
+            }
+        }
+        __syncthreads();
+
+        // ---- rows, one 64-row block at a time (double-buffered XV)
+        double cacc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // c partials for cols (nb*8 + 2t + e)
+        double gacc[2] = {0.0, 0.0};  // gram tile (mi, ni) = ((w&3) >> 1, w & 1), K half w >> 2
+        for (int bi = 0; bi < nblk; ++bi) {
+            double *xs = xs0 + (bi % B::NS) * BR * XPI;
+            const int64_t b0 = r0 + (int64_t)bi * BR;
+            const int nr = (int)min((int64_t)BR, n - (int64_t)bi * BR);
+            {
+                const int q = bi + B::NS - 1;  // refill the stage consumed two blocks ago
+                if (q < nblk)
+                    big_stage(xs0 + (q % B::NS) * BR * XPI, p.XV, r0 + (int64_t)q * BR,
+                              (int)min((int64_t)BR, n - (int64_t)q * BR), R);
+                cp_async_commit();
+            }
+            cp_async_wait2();
+            __syncthreads();
+            if (nr < BR || R < RP) {  // zero padded columns / tail rows of the staged block
+                for (int e = tid; e < BR * XPI; e += blockDim.x) {
+                    const int i = e / XPI, z = e % XPI;
+                    if (i >= nr || z >= R) xs[e] = 0.0;
+                }
+                __syncthreads();
+            }
+            // U = XV Ms^T: warp w -> rows 8w..8w+7, both n-tiles
+            double uacc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    #pragma unroll
+            for (int kk = 0; kk < RP / 4; ++kk) {
+                const double a = xs[(8 * w + g) * XPI + 4 * kk + t];
+    #pragma unroll
+                for (int nb = 0; nb < 2; ++nb) dmma884(uacc[nb], a, Ms[(8 * nb + g) * MPI + 4 * kk + t]);
+            }
+            const int row = 8 * w + g;
+    #pragma unroll
+            for (int nb = 0; nb < 2; ++nb)
+    #pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int col = 8 * nb + 2 * t + e;
+                    const double u = (row < nr && col < R) ? uacc[nb][e] : 0.0;
+                    us[row * UPI + col] = u;
+                    if (row < nr && col < R) p.U[(b0 + row) * R + col] = u;
+                    cacc[nb][e] = fma(xs[row * XPI + col], u, cacc[nb][e]);
+                }
+            __syncthreads();
+            // gram += U^T U : 8 warps = 4 tiles x 2 K-halves (8-deep DMMA chains)
+            {
+                const int mi = (w & 3) >> 1, ni = w & 1, kh = w >> 2;
+    #pragma unroll
+                for (int kk = 0; kk < BR / 8; ++kk) {
+                    const int row = 4 * (kk + kh * (BR / 8)) + t;
+                    const double a = us[row * UPI + 8 * mi + g];
+                    const double b = us[row * UPI + 8 * ni + g];
+                    dmma884(gacc, a, b);
+                }
             }
             __syncthreads();
         }
-        // U = XV Ms^T: warp w -> rows 8w..8w+7, both n-tiles
-        double uacc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-#pragma unroll
-        for (int kk = 0; kk < RP / 4; ++kk) {
-            const double a = xs[(8 * w + g) * XPI + 4 * kk + t];
-#pragma unroll
-            for (int nb = 0; nb < 2; ++nb) dmma884(uacc[nb], a, Ms[(8 * nb + g) * MPI + 4 * kk + t]);
-        }
-        const int row = 8 * w + g;
-#pragma unroll
+        // ---- reduce c (over lanes g and warps) and gram tiles into shared
+    #pragma unroll
         for (int nb = 0; nb < 2; ++nb)
-#pragma unroll
+    #pragma unroll
             for (int e = 0; e < 2; ++e) {
-                const int col = 8 * nb + 2 * t + e;
-                const double u = (row < nr && col < R) ? uacc[nb][e] : 0.0;
-                us[row * UPI + col] = u;
-                if (row < nr && col < R) p.U[(b0 + row) * R + col] = u;
-                cacc[nb][e] = fma(xs[row * XPI + col], u, cacc[nb][e]);
+                double v = cacc[nb][e];
+                v += __shfl_xor_sync(FULL_MASK, v, 4);
+                v += __shfl_xor_sync(FULL_MASK, v, 8);
+                v += __shfl_xor_sync(FULL_MASK, v, 16);
+                cacc[nb][e] = v;
             }
-        __syncthreads();
-        // gram += U^T U : 8 warps = 4 tiles x 2 K-halves (8-deep DMMA chains)
+        if (g == 0) {
+    #pragma unroll
+            for (int nb = 0; nb < 2; ++nb)
+    #pragma unroll
+                for (int e = 0; e < 2; ++e) red[w * 64 + 8 * nb + 2 * t + e] = cacc[nb][e];
+        }
         {
-            const int mi = (w & 3) >> 1, ni = w & 1, kh = w >> 2;
-#pragma unroll
-            for (int kk = 0; kk < BR / 8; ++kk) {
-                const int row = 4 * (kk + kh * (BR / 8)) + t;
-                const double a = us[row * UPI + 8 * mi + g];
-                const double b = us[row * UPI + 8 * ni + g];
-                dmma884(gacc, a, b);
+            const int mi = (w & 3) >> 1, ni = w & 1;
+            if (w >= 4) {
+    #pragma unroll
+                for (int e = 0; e < 2; ++e) gram_s[(8 * mi + g) * LDL + 8 * ni + 2 * t + e] = gacc[e];
+            }
+            __syncthreads();
+            if (w < 4) {  // fixed order: (first K half) + (second K half)
+    #pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    double *gp = gram_s + (8 * mi + g) * LDL + 8 * ni + 2 * t + e;
+                    *gp = gacc[e] + *gp;
+                }
             }
         }
         __syncthreads();
-    }
-    // ---- reduce c (over lanes g and warps) and gram tiles into shared
-#pragma unroll
-    for (int nb = 0; nb < 2; ++nb)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            double v = cacc[nb][e];
-            v += __shfl_xor_sync(FULL_MASK, v, 4);
-            v += __shfl_xor_sync(FULL_MASK, v, 8);
-            v += __shfl_xor_sync(FULL_MASK, v, 16);
-            cacc[nb][e] = v;
-        }
-    if (g == 0) {
-#pragma unroll
-        for (int nb = 0; nb < 2; ++nb)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) red[w * 64 + 8 * nb + 2 * t + e] = cacc[nb][e];
-    }
-    {
-        const int mi = (w & 3) >> 1, ni = w & 1;
-        if (w >= 4) {
-#pragma unroll
-            for (int e = 0; e < 2; ++e) gram_s[(8 * mi + g) * LDL + 8 * ni + 2 * t + e] = gacc[e];
+        if (tid < RB) {
+            double cs = 0.0;
+            for (int ww = 0; ww < 8; ++ww) cs += red[ww * 64 + tid];
+            vec[RB + tid] = tid < R ? p.lam * cold + cs : 0.0;  // c_new
         }
         __syncthreads();
-        if (w < 4) {  // fixed order: (first K half) + (second K half)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                double *gp = gram_s + (8 * mi + g) * LDL + 8 * ni + 2 * t + e;
-                *gp = gacc[e] + *gp;
-            }
-        }
-    }
-    __syncthreads();
-    if (tid < RB) {
-        double cs = 0.0;
-        for (int ww = 0; ww < 8; ++ww) cs += red[ww * 64 + tid];
-        vec[RB + tid] = tid < R ? p.lam * cold + cs : 0.0;  // c_new
-    }
-    __syncthreads();
-    // ---- D accumulation and the S-row system by warp 0 lanes 0..15 (D row in shared dns)
-    if (w == 0) {
-        const int r = lane % RB;
-        const bool lreal = lane < RB && r < R;
-        double *dn = dns + r * LDL;
-        if (lane < RB) {
-#pragma unroll
-            for (int z = 0; z < RB; ++z)
-                dn[z] = (lreal && z < R) ? p.lam * (fresh ? 0.0 : dn[z]) + gram_s[r * LDL + z] : 0.0;
-        }
-        __syncwarp();
-        double dsum = 0.0;
-#pragma unroll
-        for (int z = 0; z < RB; ++z)
-            if (z < R) dsum += vtv_s[z * LDV + z] * dns[z * LDL + z];
-        const double sh2 = p.eps * dsum / R;
-        const double dg2 = lreal ? sh2 : 1.0;
-        double a[RB];
-#pragma unroll
-        for (int z = 0; z < RB; ++z) a[z] = (lane < RB ? vtv_s[r * LDV + z] * dn[z] : 0.0) + ((z == r) ? dg2 : 0.0);
-        double wv;  // w = B^{-1} c  (lu: scratch until a fallback; lanes 16..31 solve a harmless identity)
-        bool okB = gj_solve<RB>(a, lreal ? vec[RB + r] : 0.0, lane < RB ? lu : red + 7 * 64, r, wv);
-        if (!lreal) wv = 0.0;
-        const bool good = __all_sync(FULL_MASK, (okB && isfinite(wv)) || lane >= RB);
-        if (!good) {
-            const bool need = lane < RB;
-#pragma unroll
-            for (int z = 0; z < RB; ++z) a[z] = (lane < RB ? vtv_s[r * LDV + z] * dn[z] : 0.0) + ((z == r) ? dg2 : 0.0);
-            if (lane == 0) atomicAdd(p.fallbacks, 1u);
-            const bool okLU = lu_fallback<RB>(a, lu, piv, r, R, need);
-            if (lane == 0 && !okLU) report_error(p.err, m, DASH_E_SINGULAR);
-            wv = 0.0;
-#pragma unroll
-            for (int z = 0; z < RB; ++z) wv = fma(-a[z], vec[RB + z], wv);
-            if (!lreal) wv = 0.0;
-            if (lreal && !isfinite(wv)) report_error(p.err, m, DASH_E_NONFINITE);
-        }
-        if (lreal) {
-            p.W[(int64_t)wrow * R + r] = wv;
-            if (p.final_pass) {
-                p.C[(int64_t)wrow * R + r] = vec[RB + r];
-#pragma unroll
+        // ---- D accumulation and the S-row system by warp 0 lanes 0..15 (D row in shared dns)
+        if (w == 0) {
+            const int r = lane % RB;
+            const bool lreal = lane < RB && r < R;
+            double *dn = dns + r * LDL;
+            if (lane < RB) {
+    #pragma unroll
                 for (int z = 0; z < RB; ++z)
-                    if (z < R) p.D[(int64_t)wrow * R * R + (int64_t)z * R + r] = dn[z];
+                    dn[z] = (lreal && z < R) ? p.lam * (fresh ? 0.0 : dn[z]) + gram_s[r * LDL + z] : 0.0;
+            }
+            __syncwarp();
+            double dsum = 0.0;
+    #pragma unroll
+            for (int z = 0; z < RB; ++z)
+                if (z < R) dsum += vtv_s[z * LDV + z] * dns[z * LDL + z];
+            const double sh2 = p.eps * dsum / R;
+            const double dg2 = lreal ? sh2 : 1.0;
+            double a[RB];
+    #pragma unroll
+            for (int z = 0; z < RB; ++z) a[z] = (lane < RB ? vtv_s[r * LDV + z] * dn[z] : 0.0) + ((z == r) ? dg2 : 0.0);
+            double wv;  // w = B^{-1} c  (lu: scratch until a fallback; lanes 16..31 solve a harmless identity)
+            bool okB = gj_solve<RB>(a, lreal ? vec[RB + r] : 0.0, lane < RB ? lu : red + 7 * 64, r, wv);
+            if (!lreal) wv = 0.0;
+            const bool good = __all_sync(FULL_MASK, (okB && isfinite(wv)) || lane >= RB);
+            if (!good) {
+                const bool need = lane < RB;
+    #pragma unroll
+                for (int z = 0; z < RB; ++z) a[z] = (lane < RB ? vtv_s[r * LDV + z] * dn[z] : 0.0) + ((z == r) ? dg2 : 0.0);
+                if (lane == 0) atomicAdd(p.fallbacks, 1u);
+                const bool okLU = lu_fallback<RB>(a, lu, piv, r, R, need);
+                if (lane == 0 && !okLU) report_error(p.err, m, DASH_E_SINGULAR);
+                wv = 0.0;
+    #pragma unroll
+                for (int z = 0; z < RB; ++z) wv = fma(-a[z], vec[RB + z], wv);
+                if (!lreal) wv = 0.0;
+                if (lreal && !isfinite(wv)) report_error(p.err, m, DASH_E_NONFINITE);
+            }
+            if (lreal) {
+                p.W[(int64_t)wrow * R + r] = wv;
+                if (p.final_pass) {
+                    p.C[(int64_t)wrow * R + r] = vec[RB + r];
+    #pragma unroll
+                    for (int z = 0; z < RB; ++z)
+                        if (z < R) p.D[(int64_t)wrow * R * R + (int64_t)z * R + r] = dn[z];
+                }
+            }
+            if (lane < RB) vec[2 * RB + lane] = lreal ? wv : 0.0;
+        }
+        __syncthreads();
+        // ---- G slot (gram o w w^T) and US = U o w (rows just written: L2-hot)
+        if (tid < R * R) {
+            const int a = tid / R, b = tid % R;
+            gslot += gram_s[a * LDL + b] * vec[2 * RB + a] * vec[2 * RB + b];
+        }
+        if (p.US != nullptr) {
+            // 16-byte chunks (R even); a thread's column pair advances by a fixed step
+            // per iteration, so no per-element division.  Loads are batched ahead of
+            // the stores (U and US never alias).
+            const int half = R / 2;
+            const int64_t tot = n * half;
+            const double2 *__restrict__ Ur = reinterpret_cast<const double2 *>(p.U + r0 * R);
+            double2 *__restrict__ USr = reinterpret_cast<double2 *>(p.US + r0 * R);
+            const double *wv = vec + 2 * RB;
+            const int step = blockDim.x % half;
+            int col = tid % half;
+            constexpr int UNR = 2;
+            for (int64_t e0 = tid; e0 < tot; e0 += (int64_t)UNR * blockDim.x) {
+                double2 v[UNR];
+                int cc[UNR];
+    #pragma unroll
+                for (int k = 0; k < UNR; ++k) {
+                    const int64_t e = e0 + (int64_t)k * blockDim.x;
+                    if (e < tot) v[k] = __ldcg(Ur + e);
+                    cc[k] = col;
+                    col += step;
+                    if (col >= half) col -= half;
+                }
+    #pragma unroll
+                for (int k = 0; k < UNR; ++k) {
+                    const int64_t e = e0 + (int64_t)k * blockDim.x;
+                    if (e < tot) USr[e] = make_double2(v[k].x * wv[2 * cc[k]], v[k].y * wv[2 * cc[k] + 1]);
+                }
             }
         }
-        if (lane < RB) vec[2 * RB + lane] = lreal ? wv : 0.0;
-    }
-    __syncthreads();
-    // ---- G slot (gram o w w^T) and US = U o w (rows just written: L2-hot)
-    double *slot = p.G_slots + (int64_t)blockIdx.x * R * R;
-    for (int i = tid; i < R * R; i += blockDim.x) {
-        const int a = i / R, b = i % R;
-        slot[i] = gram_s[a * LDL + b] * vec[2 * RB + a] * vec[2 * RB + b];
-    }
-    if (p.US != nullptr) {
-        // 16-byte chunks (R even); a thread's column pair advances by a fixed step
-        // per iteration, so no per-element division.  Loads are batched ahead of
-        // the stores (U and US never alias).
-        const int half = R / 2;
-        const int64_t tot = n * half;
-        const double2 *__restrict__ Ur = reinterpret_cast<const double2 *>(p.U + r0 * R);
-        double2 *__restrict__ USr = reinterpret_cast<double2 *>(p.US + r0 * R);
-        const double *wv = vec + 2 * RB;
-        const int step = blockDim.x % half;
-        int col = tid % half;
-        constexpr int UNR = 2;
-        for (int64_t e0 = tid; e0 < tot; e0 += (int64_t)UNR * blockDim.x) {
-            double2 v[UNR];
-            int cc[UNR];
-#pragma unroll
-            for (int k = 0; k < UNR; ++k) {
-                const int64_t e = e0 + (int64_t)k * blockDim.x;
-                if (e < tot) v[k] = __ldcg(Ur + e);
-                cc[k] = col;
-                col += step;
-                if (col >= half) col -= half;
-            }
-#pragma unroll
-            for (int k = 0; k < UNR; ++k) {
-                const int64_t e = e0 + (int64_t)k * blockDim.x;
-                if (e < tot) USr[e] = make_double2(v[k].x * wv[2 * cc[k]], v[k].y * wv[2 * cc[k] + 1]);
-            }
-        }
-    }
+        cp_async_wait_all();
+    }  // big slices of this CTA
+    if (tid < R * R) p.G_slots[(int64_t)blockIdx.x * R * R + tid] = gslot;
 }
 
-int launch_big(cudaStream_t st, int nbig, const SliceParams &sp, const int4 *bigs) {
+int launch_big(cudaStream_t st, int grid, const SliceParams &sp, const int4 *meta, const int *plan_counts) {
     const size_t smem = BigSmem::bytes();
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    k_big<<<nbig, 256, smem, st>>>(sp, bigs);
+    k_big<<<grid, 256, smem, st>>>(sp, meta, plan_counts);
     return cudaGetLastError() == cudaSuccess ? 0 : DASH_E_CUDA;
 }

@@ -21,53 +21,210 @@ struct S3 {
     static constexpr int LDV = RB + 2;
     static constexpr int LDL = RB + 1;
     static constexpr int CAPW = 16;  // XV rows staged per group (longer slices read XV directly)
-    // per group: buf[RB] | gacc[RB*LDL] | dn[RB*LDL] | xs[CAPW*RB] | lu[RB*LDL] | piv[RB]
-    // (per-lane rows use the odd pitch LDL = RB+1: lane r's row r hits distinct banks)
-    static constexpr int per_group = RB + RB * LDL + RB * LDL + CAPW * RB + RB * LDL + RB + 2;  // even: 16B-aligned group bases
+    // per group: buf[RB+2] (gathers; gj_solve scratch) | dn[RB*LDL] | xs[CAPW*RB]
+    // per warp : gacc[RB*LDL] (the warp's groups accumulate in turn) | lu[RB*LDL] | piv[RB]
+    //            (LU fallback scratch, used by one group at a time)
+    // Per-lane rows use the odd pitch LDL = RB+1 (lane r's row r hits distinct banks).
+    // ~55 KB for RB = 16: four CTAs (16 warps) per SM.
+    static constexpr int per_group = (RB + 2) + RB * LDL + CAPW * RB;
+    static constexpr int per_warp = GPW * per_group + 2 * RB * LDL + RB;
     static constexpr int shared = RB * LDV;
-    __host__ __device__ static constexpr size_t bytes() { return sizeof(double) * (shared + NG * per_group); }
-    static_assert(shared % 2 == 0 && per_group % 2 == 0 && (RB + 2 * RB * LDL + CAPW * RB) % 2 == 0,
+    __host__ __device__ static constexpr size_t bytes() { return sizeof(double) * (shared + NW * per_warp); }
+    static_assert(shared % 2 == 0 && per_group % 2 == 0 && per_warp % 2 == 0 && (RB * LDL) % 2 == 0,
                   "group scratch must stay 16-byte aligned");
 };
 
-// small-slice metadata, packed once per update: (r0, n, wrow | fresh << 31, m)
-__global__ void k_pack_small(const int32_t *__restrict__ small_pos, int nsmall, const int64_t *__restrict__ row_ptr,
-                             const int32_t *__restrict__ state_row, const uint8_t *__restrict__ is_new,
-                             int4 *__restrict__ meta) {
-    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nsmall; j += gridDim.x * blockDim.x) {
-        const int m = small_pos[j];
-        const int64_t r0 = row_ptr[m];
-        meta[j] = make_int4((int)r0, (int)(row_ptr[m + 1] - r0),
-                            (int)((unsigned)state_row[m] | (is_new[m] ? 0x80000000u : 0u)), m);
+// lu_fallback for the groups with `need`, one group of the warp at a time (the
+// LU scratch is per warp).  Rare path.
+template <int RB>
+__device__ __forceinline__ bool lu_fallback_seq(double (&a)[RB], double *lu, int *piv, int r, int R, bool need) {
+    constexpr int GPW = 32 / RB;
+    const int gme = lane_id() / RB;
+    bool ok = true;
+#pragma unroll 1
+    for (int gi = 0; gi < GPW; ++gi) {
+        const bool ng = need && gme == gi;
+        if (__any_sync(FULL_MASK, ng)) {
+            const bool o = lu_fallback<RB>(a, lu, piv, r, R, ng);
+            if (gme == gi) ok = o;
+        }
+    }
+    return ok;
+}
+
+// ---- device-side slice plan (R <= 16), once per update --------------------
+// Stable counting sort of the batch positions by bucket: small slices
+// (n <= kSmallRows) longest first (bucket kSmallRows - n), then big slices by
+// 64-row size class, largest first.  Output: meta[M] = (r0, n, wrow | fresh <<
+// 31, m) in plan order and plan_counts = {nsmall, nbig}.  Deterministic: per
+// chunk histograms, a sequential scan, and a warp-ordered scatter.  No host
+// work and no host round trip: the slice kernels read the counts on device.
+constexpr int kPlanChunk = 256;                   // batch positions per chunk (one warp scatters a chunk)
+constexpr int kBigClasses = 128;                  // 64-row classes, (64, 8192+]
+constexpr int kPlanBuckets = kSmallRows + 1 + kBigClasses;
+
+__device__ __forceinline__ int plan_bucket(int64_t n) {
+    if (n <= kSmallRows) return kSmallRows - (int)n;
+    const int64_t q = (n - 1) / 64;
+    const int c = q < kBigClasses ? (int)q : kBigClasses;  // 1..kBigClasses
+    return kSmallRows + 1 + (kBigClasses - c);
+}
+
+// hist[b][c]: bucket-b count of chunk c (bucket-major; one CTA of kPlanChunk threads per chunk)
+__global__ void __launch_bounds__(kPlanChunk) k_plan_count(const int64_t *__restrict__ row_ptr, int M,
+                                                           int *__restrict__ hist) {
+    __shared__ int h[kPlanBuckets];
+    for (int i = threadIdx.x; i < kPlanBuckets; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    const int m = blockIdx.x * kPlanChunk + threadIdx.x;
+    if (m < M) atomicAdd(&h[plan_bucket(row_ptr[m + 1] - row_ptr[m])], 1);
+    __syncthreads();
+    for (int i = threadIdx.x; i < kPlanBuckets; i += blockDim.x) hist[(size_t)i * gridDim.x + blockIdx.x] = h[i];
+}
+
+// One CTA per bucket b: off[b][c] = bucket-b positions in chunks < c
+// (coalesced block scan over the chunks, tiles of 256 with a carry) and
+// tot[b] = all bucket-b positions.  The bucket bases are a scan of tot,
+// taken by each scatter warp itself.
+constexpr int kScanThreads = 256;
+__global__ void __launch_bounds__(kScanThreads) k_plan_scan(const int *__restrict__ hist, int nch,
+                                                            int *__restrict__ off, int *__restrict__ tot) {
+    __shared__ int wsum[kScanThreads / 32];
+    const int tid = threadIdx.x, lane = tid & 31, wq = tid >> 5;
+    const int *h = hist + (size_t)blockIdx.x * nch;
+    int *o = off + (size_t)blockIdx.x * nch;
+    int carry = 0;
+    for (int c0 = 0; c0 < nch; c0 += kScanThreads) {
+        const int c = c0 + tid;
+        const int v = c < nch ? h[c] : 0;
+        int inc = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int u = __shfl_up_sync(FULL_MASK, inc, d);
+            if (lane >= d) inc += u;
+        }
+        if (lane == 31) wsum[wq] = inc;
+        __syncthreads();
+        int wbase = 0, all = 0;
+#pragma unroll
+        for (int k = 0; k < kScanThreads / 32; ++k) {
+            const int x = wsum[k];
+            if (k < wq) wbase += x;
+            all += x;
+        }
+        if (c < nch) o[c] = carry + wbase + inc - v;
+        carry += all;
+        __syncthreads();
+    }
+    if (tid == 0) tot[blockIdx.x] = carry;
+}
+
+// exclusive scan of tot[0..kPlanBuckets) by one warp into base[] (shared)
+__device__ __forceinline__ void plan_bases(const int *__restrict__ tot, int *base, int lane) {
+    constexpr int PER = (kPlanBuckets + 31) / 32;
+    int v[PER], s = 0;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        const int b = lane * PER + k;
+        v[k] = b < kPlanBuckets ? tot[b] : 0;
+        s += v[k];
+    }
+    int inc = s;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int u = __shfl_up_sync(FULL_MASK, inc, d);
+        if (lane >= d) inc += u;
+    }
+    int run = inc - s;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        const int b = lane * PER + k;
+        if (b < kPlanBuckets) base[b] = run;
+        run += v[k];
+    }
+}
+
+// one warp per chunk (4 chunks per CTA): the chunk's loads are issued up
+// front, then 32 positions at a time are ranked in order -> stable
+__global__ void __launch_bounds__(128) k_plan_scatter(const int64_t *__restrict__ row_ptr,
+                                                      const int32_t *__restrict__ state_row,
+                                                      const uint8_t *__restrict__ is_new, int M, int nch,
+                                                      const int *__restrict__ off, const int *__restrict__ tot,
+                                                      int4 *__restrict__ meta, int *__restrict__ counts) {
+    constexpr int ROUNDS = kPlanChunk / 32;
+    __shared__ int run_s[4][kPlanBuckets];
+    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    const int chunk = blockIdx.x * 4 + wq;
+    if (chunk >= nch) return;
+    int *run = run_s[wq];
+    plan_bases(tot, run, lane);
+    __syncwarp();
+    if (chunk == 0 && lane == 0) {  // {nsmall, nbig}
+        const int nsmall = run[kSmallRows + 1];
+        counts[0] = nsmall;
+        counts[1] = run[kPlanBuckets - 1] + tot[kPlanBuckets - 1] - nsmall;
+    }
+    for (int b = lane; b < kPlanBuckets; b += 32) run[b] += off[(size_t)b * nch + chunk];
+    const int c0 = chunk * kPlanChunk;
+    int64_t r0[ROUNDS];
+    int nn[ROUNDS], sr[ROUNDS];
+#pragma unroll
+    for (int k = 0; k < ROUNDS; ++k) {
+        const int m = c0 + 32 * k + lane;
+        r0[k] = 0;
+        nn[k] = -1;
+        sr[k] = 0;
+        if (m < M) {
+            r0[k] = row_ptr[m];
+            nn[k] = (int)(row_ptr[m + 1] - r0[k]);
+            sr[k] = (int)((unsigned)state_row[m] | (is_new[m] ? 0x80000000u : 0u));
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < ROUNDS; ++k) {
+        const bool v = nn[k] >= 0;
+        const int b = v ? plan_bucket(nn[k]) : -1 - lane;  // invalid lanes: unique keys
+        const unsigned peers = __match_any_sync(FULL_MASK, b);
+        const int rank = __popc(peers & ((1u << lane) - 1u));
+        const int pos = v ? run[b] + rank : 0;
+        __syncwarp();
+        if (v && rank == 0) run[b] += __popc(peers);
+        __syncwarp();
+        if (v) meta[pos] = make_int4((int)r0[k], nn[k], sr[k], c0 + 32 * k + lane);
     }
 }
 
 template <int RB>
-__global__ void __launch_bounds__(S3<RB>::NW * 32, 3) k_slices3(SliceParams p, const int4 *__restrict__ meta,
-                                                                 int nsmall) {
+__global__ void __launch_bounds__(S3<RB>::NW * 32, 4) k_slices3(SliceParams p, const int4 *__restrict__ meta,
+                                                                 const int *__restrict__ plan_counts) {
     using S = S3<RB>;
     constexpr int LDV = S::LDV, GPW = S::GPW, CAPW = S::CAPW;
     extern __shared__ __align__(16) double sm[];
     double *vtv_s = sm;
     const int lane = lane_id(), w = warp_id();
     const int r = lane % RB;
-    const int gid = w * GPW + lane / RB;
-    double *buf = sm + S::shared + gid * S::per_group;
-    double *gacc = buf + RB;
-    double *dns = gacc + RB * S::LDL;
-    double *xs = dns + RB * S::LDL;  // RB*LDL is even: xs and lu stay 16-byte aligned (gj_solve scratch)
-    double *lu = xs + CAPW * RB;
+    const int gl = lane / RB;  // group within the warp
+    double *wbase = sm + S::shared + w * S::per_warp;
+    double *buf = wbase + gl * S::per_group;
+    double *dns = buf + RB + 2;
+    double *xs = dns + RB * S::LDL;
+    double *gacc = wbase + GPW * S::per_group;
+    double *lu = gacc + RB * S::LDL;
     int *piv = reinterpret_cast<int *>(lu + RB * S::LDL);
     const int R = p.R;
     for (int i = threadIdx.x; i < RB * LDV; i += blockDim.x) {
         const int a = i / LDV, b = i % LDV;
         vtv_s[i] = (a < R && b < R) ? p.vtv[a * R + b] : 0.0;
     }
+    if (gl == 0) {
 #pragma unroll
-    for (int z = 0; z < RB; ++z) gacc[r * S::LDL + z] = 0.0;
+        for (int z = 0; z < RB; ++z) gacc[r * S::LDL + z] = 0.0;
+    }
     __syncthreads();
     const double *vrow = vtv_s + r * LDV;
 
+    const int nsmall = plan_counts[0];
     const int nunits = (nsmall + GPW - 1) / GPW;
     const int nwarps = gridDim.x * S::NW;
     // software pipeline: the next unit's metadata and W / C values are loaded
@@ -130,7 +287,7 @@ __global__ void __launch_bounds__(S3<RB>::NW * 32, 3) k_slices3(SliceParams p, c
             for (int z = 0; z < RB; ++z)
                 if (!okA) a[z] = vrow[z] * s_r * s_all[z] + ((z == r) ? dg : 0.0);
             if (!okA && r == 0) atomicAdd(p.fallbacks, 1u);
-            const bool okLU = lu_fallback<RB>(a, lu, piv, r, R, !okA);
+            const bool okLU = lu_fallback_seq<RB>(a, lu, piv, r, R, !okA);
             if (!okA && r == 0 && !okLU) report_error(p.err, m, DASH_E_SINGULAR);
         }
         sw_of(nmeta, nxt < nunits && nxt * GPW + lane / RB < nsmall, nsw, ncw);  // next unit's s, c_old
@@ -205,7 +362,7 @@ __global__ void __launch_bounds__(S3<RB>::NW * 32, 3) k_slices3(SliceParams p, c
             for (int z = 0; z < RB; ++z) a[z] = vrow[z] * dn[z] + ((z == r) ? dg2 : 0.0);
         }
         double wv;
-        const bool okB = gj_solve<RB>(a, cn, lu, r, wv);  // w = B^{-1} c (lu: scratch until a fallback)
+        const bool okB = gj_solve<RB>(a, cn, buf, r, wv);  // w = B^{-1} c (buf: RB+2 scratch)
         if (!real) wv = 0.0;
         bool gok = okB && isfinite(wv);
         {
@@ -220,7 +377,7 @@ __global__ void __launch_bounds__(S3<RB>::NW * 32, 3) k_slices3(SliceParams p, c
             for (int z = 0; z < RB; ++z)
                 if (need) a[z] = vrow[z] * dn[z] + ((z == r) ? dg2 : 0.0);
             if (need && r == 0) atomicAdd(p.fallbacks, 1u);
-            const bool okLU = lu_fallback<RB>(a, lu, piv, r, R, need);
+            const bool okLU = lu_fallback_seq<RB>(a, lu, piv, r, R, need);
             if (need && r == 0 && !okLU) report_error(p.err, m, DASH_E_SINGULAR);
             double call[RB];
             group_gather<RB>(cn, buf, r, call);
@@ -244,11 +401,14 @@ __global__ void __launch_bounds__(S3<RB>::NW * 32, 3) k_slices3(SliceParams p, c
         }
         double wa[RB];
         group_gather<RB>(wv, buf, r, wa);
-        if (active) {
 #pragma unroll
-            for (int z = 0; z < RB; ++z) gacc[r * S::LDL + z] = fma(gram[z] * wv, wa[z], gacc[r * S::LDL + z]);
+        for (int gi = 0; gi < GPW; ++gi) {  // the warp's groups add into gacc in turn (fixed order)
+            if (active && gl == gi) {
+#pragma unroll
+                for (int z = 0; z < RB; ++z) gacc[r * S::LDL + z] = fma(gram[z] * wv, wa[z], gacc[r * S::LDL + z]);
+            }
+            __syncwarp();
         }
-        __syncwarp();
     }
     // ---- per-CTA G slot, groups in order
     __syncthreads();
@@ -256,19 +416,19 @@ __global__ void __launch_bounds__(S3<RB>::NW * 32, 3) k_slices3(SliceParams p, c
     for (int i = threadIdx.x; i < R * R; i += blockDim.x) {
         const int a = i / R, b = i % R;
         double acc = 0.0;
-        for (int g2 = 0; g2 < S::NG; ++g2) acc += sm[S::shared + g2 * S::per_group + RB + a * S::LDL + b];
+        for (int w2 = 0; w2 < S::NW; ++w2) acc += sm[S::shared + w2 * S::per_warp + GPW * S::per_group + a * S::LDL + b];
         slot[i] = acc;
     }
 }
 
 template <int RB>
-int launch_slices3(cudaStream_t st, int grid, const SliceParams &sp, const int4 *meta, int nsmall) {
+int launch_slices3(cudaStream_t st, int grid, const SliceParams &sp, const int4 *meta, const int *plan_counts) {
     const size_t smem = S3<RB>::bytes();
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_slices3<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    k_slices3<RB><<<grid, S3<RB>::NW * 32, smem, st>>>(sp, meta, nsmall);
+    k_slices3<RB><<<grid, S3<RB>::NW * 32, smem, st>>>(sp, meta, plan_counts);
     return cudaGetLastError() == cudaSuccess ? 0 : DASH_E_CUDA;
 }

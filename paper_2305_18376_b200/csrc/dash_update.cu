@@ -26,6 +26,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <vector>
 
 #include "../../include/dash_b200.h"
@@ -695,7 +696,7 @@ struct dash_ctx {
         void *p = nullptr;
         size_t cap = 0;
     };
-    Buf xv, row_slice, items, gslots, fslots, vtv, fsnap, gsnap, fg, part, us, scratch, smeta;
+    Buf xv, row_slice, items, gslots, fslots, vtv, fsnap, gsnap, fg, part, us, scratch, smeta, plan_hist;
     unsigned long long *err = nullptr;
     unsigned int *fallbacks = nullptr;
     int4 *items_host[2] = {nullptr, nullptr};
@@ -849,17 +850,19 @@ int dispatch_slices(dash_ctx *ctx, cudaStream_t st, int RB, int nitems, const Sl
     return launch_slices<32>(ctx, st, nitems, sp);
 }
 
-// Slice-phase plan.  R <= 16: small slices (<= kSmallRows) go to the
-// persistent warp-autonomous k_slices3 (G slots [0, g3)), big slices to
-// CTA-cooperative k_slices2 items (slots [g3, g3 + nbig)).  Larger ranks keep
-// one item list.  items = [big items..., small positions packed 4 per int4].
+// Slice-phase plan.  R <= 16: the slice order is planned ON DEVICE
+// (k_plan_*: small slices longest first, big slices by size class) and the
+// persistent k_slices3 (G slots [0, g3)) reads its work list from there.  Big
+// slices go to the persistent DMMA kernel k_big (RB == 16, R even; slots [g3,
+// g3 + gbig)), else to k_slices2 items planned on the host (slots [g3, g3 +
+// nbig)).  Larger ranks keep the host item list of k_slices / k_slices_cta.
 struct SlicePlan {
-    std::vector<int4> items;
-    int nbig = 0, nsmall = 0, g3 = 0, nslots = 0;
-    bool split = false;
+    std::vector<int4> items;  // host-planned items (k_slices2 big items, or all items for RB > 16)
+    int nbig = 0, g3 = 0, gbig = 0, nslots = 0;
+    bool split = false, big_dev = false;
 };
 
-SlicePlan make_plan(const int64_t *row_ptr, int M, int RB, int num_sms) {
+SlicePlan make_plan(const int64_t *row_ptr, int M, int RB, int R, int num_sms) {
     SlicePlan pl;
     if (RB > 16) {
         plan_items(row_ptr, M, pl.items, slices_per_item(RB));
@@ -867,46 +870,74 @@ SlicePlan make_plan(const int64_t *row_ptr, int M, int RB, int num_sms) {
         return pl;
     }
     pl.split = true;
-    std::vector<int32_t> small;
-    small.reserve(M);
-    for (int m = 0; m < M; ++m) {
-        if (row_ptr[m + 1] - row_ptr[m] > kSmallRows) pl.items.push_back(make_int4(m, 1, 1, 0));
-        else small.push_back(m);
+    pl.g3 = 4 * num_sms;
+    if (RB == 16 && (R % 2) == 0) {  // order on device; the host only counts big slices (grid size)
+        pl.big_dev = true;
+        int nbig = 0;
+        for (int m = 0; m < M; ++m) nbig += (row_ptr[m + 1] - row_ptr[m]) > kSmallRows;
+        pl.gbig = nbig;  // one CTA (and G slot) per big slice
+        pl.nslots = pl.g3 + pl.gbig;
+        return pl;
     }
-    // longest first: one CTA per big slice, ~2 waves -> shorter tail (stable: deterministic slot order)
+    for (int m = 0; m < M; ++m)
+        if (row_ptr[m + 1] - row_ptr[m] > kSmallRows) pl.items.push_back(make_int4(m, 1, 1, 0));
+    // longest first: one CTA per big slice -> shorter tail (stable: deterministic slot order)
     std::stable_sort(pl.items.begin(), pl.items.end(), [row_ptr](const int4 &a, const int4 &b) {
         return row_ptr[a.x + 1] - row_ptr[a.x] > row_ptr[b.x + 1] - row_ptr[b.x];
     });
     pl.nbig = (int)pl.items.size();
-    pl.nsmall = (int)small.size();
-    for (size_t i = 0; i < small.size(); i += 4) {
-        int v[4] = {0, 0, 0, 0};
-        for (size_t k = 0; k < 4 && i + k < small.size(); ++k) v[k] = small[i + k];
-        pl.items.push_back(make_int4(v[0], v[1], v[2], v[3]));
-    }
-    const int gpw = 32 / RB, units = (pl.nsmall + gpw - 1) / gpw;
-    pl.g3 = pl.nsmall > 0 ? std::max(1, std::min(3 * num_sms, (units + S3<16>::NW - 1) / S3<16>::NW)) : 0;
     pl.nslots = pl.g3 + pl.nbig;
     return pl;
 }
 
 SlicePlan &plan_of(dash_ctx *ctx) { return *reinterpret_cast<SlicePlan *>(ctx->plan_p); }
 
-int launch_plan(dash_ctx *ctx, cudaStream_t st, int RB, const SlicePlan &pl, SliceParams sp) {
+// device plan (R <= 16): meta[M] in plan order + plan_counts {nsmall, nbig}
+int device_plan(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b) {
+    const int M = b->M;
+    const int nch = std::max(1, (M + kPlanChunk - 1) / kPlanChunk);
+    // hist[B][nch] | off[B][nch] | tot[B] | counts[2]
+    if (ensure(ctx->smeta, sizeof(int4) * std::max(M, 1)) ||
+        ensure(ctx->plan_hist, sizeof(int) * (2 * (size_t)nch * kPlanBuckets + kPlanBuckets + 2)))
+        return DASH_E_CUDA;
+    int *hist = (int *)ctx->plan_hist.p;
+    int *off = hist + (size_t)nch * kPlanBuckets;
+    int *tot = off + (size_t)nch * kPlanBuckets;
+    int *counts = tot + kPlanBuckets;
+    PhaseScope ps(ctx, st, PH_ROWSLICE);
+    k_plan_count<<<nch, kPlanChunk, 0, st>>>(b->row_ptr, M, hist);
+    k_plan_scan<<<kPlanBuckets, kScanThreads, 0, st>>>(hist, nch, off, tot);
+    k_plan_scatter<<<(nch + 3) / 4, 128, 0, st>>>(b->row_ptr, b->state_row, b->is_new, M, nch, off, tot,
+                                                   (int4 *)ctx->smeta.p, counts);
+    ctx->last_launches += 2;  // three kernels under one phase
+    return cudaGetLastError() == cudaSuccess ? 0 : DASH_E_CUDA;
+}
+
+const int *plan_counts_of(dash_ctx *ctx, int M) {
+    const int nch = std::max(1, (M + kPlanChunk - 1) / kPlanChunk);
+    return (const int *)ctx->plan_hist.p + 2 * (size_t)nch * kPlanBuckets + kPlanBuckets;
+}
+
+int launch_plan(dash_ctx *ctx, cudaStream_t st, int RB, const SlicePlan &pl, SliceParams sp, int M) {
     if (!pl.split) return dispatch_slices(ctx, st, RB, (int)pl.items.size(), sp);
-    const int4 *meta = (const int4 *)ctx->smeta.p;  // packed by k_pack_small at pass 0
-    if (pl.nsmall > 0) {
+    const int4 *meta = (const int4 *)ctx->smeta.p;
+    const int *counts = plan_counts_of(ctx, M);
+    {
         PhaseScope ps(ctx, st, PH_SLICES);
-        int rc = RB == 4 ? launch_slices3<4>(st, pl.g3, sp, meta, pl.nsmall)
-                 : RB == 8 ? launch_slices3<8>(st, pl.g3, sp, meta, pl.nsmall)
-                           : launch_slices3<16>(st, pl.g3, sp, meta, pl.nsmall);
+        int rc = RB == 4 ? launch_slices3<4>(st, pl.g3, sp, meta, counts)
+                 : RB == 8 ? launch_slices3<8>(st, pl.g3, sp, meta, counts)
+                           : launch_slices3<16>(st, pl.g3, sp, meta, counts);
         if (rc) return rc;
+    }
+    SliceParams sb = sp;
+    sb.G_slots = sp.G_slots + (int64_t)pl.g3 * sp.R * sp.R;
+    if (pl.big_dev) {
+        if (pl.gbig == 0) return 0;
+        PhaseScope ps(ctx, st, PH_BIG);
+        return launch_big(st, pl.gbig, sb, meta, counts);  // DMMA big-slice kernel, plan order
     }
     if (pl.nbig > 0) {
         PhaseScope ps(ctx, st, PH_BIG);
-        SliceParams sb = sp;
-        sb.G_slots = sp.G_slots + (int64_t)pl.g3 * sp.R * sp.R;
-        if (RB == 16 && (sp.R % 2) == 0) return launch_big(st, pl.nbig, sb, sp.items);  // DMMA big-slice kernel
         switch (RB) {
             case 4: return launch_slices2<4>(st, pl.nbig, sb);
             case 8: return launch_slices2<8>(st, pl.nbig, sb);
@@ -1118,7 +1149,7 @@ void dash_ctx_destroy(dash_ctx *ctx) {
     cudaDeviceSynchronize();
     dash_ctx::Buf *bufs[] = {&ctx->xv,  &ctx->row_slice, &ctx->items, &ctx->gslots, &ctx->fslots,
                              &ctx->vtv, &ctx->fsnap,     &ctx->gsnap, &ctx->fg,     &ctx->part, &ctx->us, &ctx->scratch,
-                             &ctx->smeta};
+                             &ctx->smeta, &ctx->plan_hist};
     for (auto *b : bufs)
         if (b->p) cudaFree(b->p);
     cudaFree(ctx->err);
@@ -1209,10 +1240,14 @@ int dash_update_pass_begin_f64(dash_ctx *ctx, void *stream, const dash_batch_f64
     const int64_t N = b->N;
     const int M = b->M;
     const int last = pass == s->passes - 1;
+    static const bool host_timing = getenv("DASH_HOST_TIMING") != nullptr;
+    auto tnow = [] { return std::chrono::steady_clock::now(); };
+    auto t0 = tnow();
     if (pass == 0) {
         ctx->last_launches = 0;
         if (!ctx->plan_p) ctx->plan_p = new SlicePlan();
-        plan_of(ctx) = make_plan(b->row_ptr_host, M, RB, ctx->num_sms);
+        plan_of(ctx) = make_plan(b->row_ptr_host, M, RB, R, ctx->num_sms);
+        if (host_timing) fprintf(stderr, "[dash host] plan %.1f us\n", std::chrono::duration<double, std::micro>(tnow() - t0).count());
         ctx->nitems = plan_of(ctx).nslots;
         const std::vector<int4> &items = plan_of(ctx).items;
         ctx->stream = stream_ok(J, b->ldx, R) && N > 0;
@@ -1227,14 +1262,7 @@ int dash_update_pass_begin_f64(dash_ctx *ctx, void *stream, const dash_batch_f64
             (ctx->stream && ensure(ctx->us, sizeof(double) * std::max<int64_t>(N, 1) * R)))
             return DASH_E_CUDA;
         if (!items.empty() && stage_items(ctx, st, items)) return DASH_E_CUDA;
-        const SlicePlan &pl = plan_of(ctx);
-        if (pl.split && pl.nsmall > 0) {
-            if (ensure(ctx->smeta, sizeof(int4) * pl.nsmall)) return DASH_E_CUDA;
-            PhaseScope ps(ctx, st, PH_ROWSLICE);
-            k_pack_small<<<std::min(ctx->num_sms * 2, (pl.nsmall + 255) / 256), 256, 0, st>>>(
-                reinterpret_cast<const int32_t *>((const int4 *)ctx->items.p + pl.nbig), pl.nsmall, b->row_ptr,
-                b->state_row, b->is_new, (int4 *)ctx->smeta.p);
-        }
+        if (plan_of(ctx).split && M > 0 && N > 0 && device_plan(ctx, st, b)) return DASH_E_CUDA;
         if (M > 0 && !ctx->stream) {  // row -> slice map: only the generic F GEMM needs it
             PhaseScope ps(ctx, st, PH_ROWSLICE);
             k_row_slice<<<std::min(ctx->num_sms * 4, (M + 7) / 8 + 1), 256, 0, st>>>(b->row_ptr, M,
@@ -1278,7 +1306,7 @@ int dash_update_pass_begin_f64(dash_ctx *ctx, void *stream, const dash_batch_f64
         sp.eps = eps;
         sp.pass = pass;
         sp.final_pass = last;
-        if (launch_plan(ctx, st, RB, plan_of(ctx), sp)) return DASH_E_CUDA;
+        if (launch_plan(ctx, st, RB, plan_of(ctx), sp, M)) return DASH_E_CUDA;
         if (ctx->tma) {
             if (launch_f3(ctx, st, b, J, (const double *)ctx->us.p, R, Fsl)) return DASH_E_CUDA;
         } else if (ctx->stream) {
@@ -1289,6 +1317,7 @@ int dash_update_pass_begin_f64(dash_ctx *ctx, void *stream, const dash_batch_f64
                          (int)ctx->nsplit, Fsl);
         }
     }
+    if (host_timing) fprintf(stderr, "[dash host] pass_begin total %.1f us\n", std::chrono::duration<double, std::micro>(tnow() - t0).count());
     {
         PhaseScope ps(ctx, st, PH_SUMFG);
         if (colsum(ctx, st, Fsl, N > 0 ? (int)ctx->nsplit : 0, (int64_t)J * R, fg_out) ||
