@@ -52,8 +52,19 @@ __device__ __forceinline__ double *align1k(double *p) {
     return p + (((1024u - (smem_u32(p) & 1023u)) & 1023u) >> 3);
 }
 
+// Pass prologue fused into the XV kernel (no separate launch): CTA 0 forms
+// vtv = V^T V from its staged V^T, and all CTAs share the F / G snapshot and
+// v_used copies (what k_prologue does on the other paths).
+struct FusedPrologue {
+    double *vtv;
+    const double *F, *G;
+    double *F_snap, *G_snap, *v_used;
+    int snap, last;
+};
+
 __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_xv3(const __grid_constant__ CUtensorMap tmX, int64_t N, int J,
-                                                          const double *__restrict__ V, int R, double *__restrict__ XV) {
+                                                          const double *__restrict__ V, int R, double *__restrict__ XV,
+                                                          FusedPrologue pro) {
     extern __shared__ __align__(16) double sm_raw[];
     double *sm = align1k(sm_raw);
     const int JS = TmaSmem::strips(J), VTP = TmaSmem::vtp(J);
@@ -77,6 +88,23 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_xv3(const __grid_constant_
         fence_mbar_init();
     }
     __syncthreads();
+    {
+        const int gt = blockIdx.x * blockDim.x + tid, nt = gridDim.x * blockDim.x;
+        if (pro.snap) {
+            for (int i = gt; i < J * R; i += nt) pro.F_snap[i] = pro.F[i];
+            for (int i = gt; i < R * R; i += nt) pro.G_snap[i] = pro.G[i];
+        }
+        if (pro.last)
+            for (int i = gt; i < J * R; i += nt) pro.v_used[i] = V[i];
+        if (blockIdx.x == 0 && tid < R * R) {  // vtv[r][z] = sum_k V[k][r] V[k][z], 4 chains
+            const double *a = vt + (tid / R) * VTP, *b = vt + (tid % R) * VTP;
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int k = 0; k < J; k += 4)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[q] = fma(a[k + q], b[k + q], acc[q]);  // vt padded to 16
+            pro.vtv[tid] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+        }
+    }
     const int64_t ntiles = (N + kTR - 1) / kTR;
     const int64_t mine = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     if (w == kCW) {

@@ -555,6 +555,50 @@ __global__ void k_colsum_final(const double *__restrict__ part, int nseg, int64_
     out[col] = acc;
 }
 
+// Two slot arrays (F and G) summed by one pair of launches: blocks [0, a.nblk)
+// serve job a, the rest job b.  Same fixed segment order as k_colsum_part /
+// k_colsum_final (deterministic); loads unrolled so a segment's slots are in flight.
+struct ColSumJob {
+    const double *slots;
+    double *part, *out;
+    int64_t width;
+    int nslots, nseg, bx;
+};
+
+__global__ void __launch_bounds__(128) k_colsum_part2(ColSumJob a, ColSumJob b) {
+    int blk = blockIdx.x;
+    const bool second = blk >= a.bx * a.nseg;
+    const ColSumJob &j = second ? b : a;
+    if (second) blk -= a.bx * a.nseg;
+    const int64_t col = (int64_t)(blk % j.bx) * blockDim.x + threadIdx.x;
+    const int seg = blk / j.bx;
+    if (col >= j.width) return;
+    const int s0 = seg * kSeg, s1 = min(j.nslots, s0 + kSeg);
+    double acc = 0.0;
+    int s = s0;
+    for (; s + 8 <= s1; s += 8) {
+        double v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = j.slots[(int64_t)(s + k) * j.width + col];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc += v[k];
+    }
+    for (; s < s1; ++s) acc += j.slots[(int64_t)s * j.width + col];
+    j.part[(int64_t)seg * j.width + col] = acc;
+}
+
+__global__ void __launch_bounds__(128) k_colsum_final2(ColSumJob a, ColSumJob b) {
+    int blk = blockIdx.x;
+    const bool second = blk >= a.bx;
+    const ColSumJob &j = second ? b : a;
+    if (second) blk -= a.bx;
+    const int64_t col = (int64_t)blk * blockDim.x + threadIdx.x;
+    if (col >= j.width) return;
+    double acc = 0.0;
+    for (int s = 0; s < j.nseg; ++s) acc += j.part[(int64_t)s * j.width + col];
+    j.out[col] = acc;
+}
+
 // Finish one pass (stream.py:344-346): F = lam F_snap + f, G = sym(lam G_snap
 // + g), then V = ridge_solve(G, F^T)^T (linalg.py:25-45).  Every warp forms G
 // and factors it (identical result in every warp) and solves 32 rows of V;
@@ -1010,6 +1054,21 @@ int colsum(dash_ctx *ctx, cudaStream_t st, const double *slots, int nslots, int6
     return 0;
 }
 
+// column sums of two slot arrays (F slots and G slots) in two launches
+int colsum2(dash_ctx *ctx, cudaStream_t st, const double *sa, int na, int64_t wa, double *oa, const double *sb,
+            int nb, int64_t wb, double *ob) {
+    if (na == 0 || nb == 0) return colsum(ctx, st, sa, na, wa, oa) || colsum(ctx, st, sb, nb, wb, ob);
+    ColSumJob a{sa, nullptr, oa, wa, na, std::max(1, (na + kSeg - 1) / kSeg), (int)((wa + 127) / 128)};
+    ColSumJob b{sb, nullptr, ob, wb, nb, std::max(1, (nb + kSeg - 1) / kSeg), (int)((wb + 127) / 128)};
+    if (ensure(ctx->part, sizeof(double) * (a.nseg * wa + b.nseg * wb))) return DASH_E_CUDA;
+    a.part = (double *)ctx->part.p;
+    b.part = a.part + a.nseg * wa;
+    k_colsum_part2<<<a.bx * a.nseg + b.bx * b.nseg, 128, 0, st>>>(a, b);
+    k_colsum_final2<<<a.bx + b.bx, 128, 0, st>>>(a, b);
+    ctx->last_launches++;  // two kernels under one phase
+    return cudaGetLastError() == cudaSuccess ? 0 : DASH_E_CUDA;
+}
+
 // ---- streaming (TMA ring) GEMM path: J, ldx, R even; ring fits in shared memory
 template <int RP>
 bool stream_ok_t(int J, int64_t ldx, int R) {
@@ -1061,13 +1120,18 @@ bool tma_ok(const dash_batch_f64 *b, int J, int R) {
            TmaSmem::f_bytes(J) <= lim && encode_fn() != nullptr;
 }
 
-int launch_xv3(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, const double *V, int R, double *XV) {
+int launch_xv3(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, const double *V, int R, double *XV,
+               const FusedPrologue &pro) {
     CUtensorMap mx;
     if (!make_box_map(&mx, b->X, J, b->N, b->ldx)) return DASH_E_CUDA;
     const size_t smem = TmaSmem::xv_bytes(J);
-    cudaFuncSetAttribute(k_xv3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    static size_t attr = 0;
+    if (attr < smem) {
+        cudaFuncSetAttribute(k_xv3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = smem;
+    }
     PhaseScope ps(ctx, st, PH_XV);
-    k_xv3<<<ctx->num_sms, kCW * 32 + 32, smem, st>>>(mx, b->N, J, V, R, XV);
+    k_xv3<<<ctx->num_sms, kCW * 32 + 32, smem, st>>>(mx, b->N, J, V, R, XV, pro);
     return 0;
 }
 
@@ -1075,7 +1139,11 @@ template <int MAXS>
 void launch_f3_t(dash_ctx *ctx, cudaStream_t st, const CUtensorMap &mx, const CUtensorMap &mu, int64_t N, int J,
                  int R, double *F_slots) {
     const size_t smem = TmaSmem::f_bytes(J);
-    cudaFuncSetAttribute(k_fgemm3<MAXS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    static size_t attr = 0;
+    if (attr < smem) {
+        cudaFuncSetAttribute(k_fgemm3<MAXS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = smem;
+    }
     PhaseScope ps(ctx, st, PH_FGEMM);
     k_fgemm3<MAXS><<<ctx->num_sms, kCW * 32 + 32, smem, st>>>(mx, mu, N, J, R, F_slots);
 }
@@ -1271,7 +1339,8 @@ int dash_update_pass_begin_f64(dash_ctx *ctx, void *stream, const dash_batch_f64
     }
     double *XV = (double *)ctx->xv.p;
     double *Fsl = (double *)ctx->fslots.p, *Gsl = (double *)ctx->gslots.p;
-    {
+    const bool fused_pro = ctx->tma && N > 0;  // k_xv3 runs the prologue itself
+    if (!fused_pro) {
         PhaseScope ps(ctx, st, PH_PROLOGUE);
         k_prologue<<<1 + std::max(1, std::min(16, (J * R + 255) / 256)), 256, 0, st>>>(
             s->V, J, R, (double *)ctx->vtv.p, s->F, s->G, (double *)ctx->fsnap.p,
@@ -1279,7 +1348,9 @@ int dash_update_pass_begin_f64(dash_ctx *ctx, void *stream, const dash_batch_f64
     }
     if (N > 0) {
         if (ctx->tma) {
-            if (launch_xv3(ctx, st, b, J, s->V, R, XV)) return DASH_E_CUDA;
+            const FusedPrologue pro{(double *)ctx->vtv.p, s->F, s->G, (double *)ctx->fsnap.p, (double *)ctx->gsnap.p,
+                                    v_used_out, pass == 0, last};
+            if (launch_xv3(ctx, st, b, J, s->V, R, XV, pro)) return DASH_E_CUDA;
         } else if (ctx->stream) {
             if (rank_bucket(R) <= 8) launch_xv2_t<8>(ctx, st, b, J, s->V, R, XV);
             else launch_xv2_t<16>(ctx, st, b, J, s->V, R, XV);
@@ -1320,8 +1391,8 @@ int dash_update_pass_begin_f64(dash_ctx *ctx, void *stream, const dash_batch_f64
     if (host_timing) fprintf(stderr, "[dash host] pass_begin total %.1f us\n", std::chrono::duration<double, std::micro>(tnow() - t0).count());
     {
         PhaseScope ps(ctx, st, PH_SUMFG);
-        if (colsum(ctx, st, Fsl, N > 0 ? (int)ctx->nsplit : 0, (int64_t)J * R, fg_out) ||
-            colsum(ctx, st, Gsl, N > 0 ? ctx->nitems : 0, (int64_t)R * R, fg_out + (int64_t)J * R))
+        if (colsum2(ctx, st, Fsl, N > 0 ? (int)ctx->nsplit : 0, (int64_t)J * R, fg_out, Gsl,
+                    N > 0 ? ctx->nitems : 0, (int64_t)R * R, fg_out + (int64_t)J * R))
             return DASH_E_CUDA;
     }
     return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_E_CUDA;
