@@ -72,15 +72,20 @@ __global__ void __launch_bounds__(256, 2) k_big(SliceParams p, const int4 *__res
     const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
     const int g = lane >> 2, t = lane & 3;
     const int R = p.R;
-    const int nsmall = plan_counts[0], nbig = plan_counts[1];
+    // PDL: launched behind the small-slice kernel, whose CTAs trigger only
+    // after their own pdl_wait -- so XV, vtv and the plan are complete here.
+    // The two kernels touch disjoint slices / rows / G slots, so this one does
+    // not wait for the small-slice kernel until it exits (tail overlap).
+    pdl_trigger();
+    const int nsmall = __ldcg(plan_counts), nbig = __ldcg(plan_counts + 1);
     for (int i = tid; i < RB * LDV; i += blockDim.x) {
         const int a = i / LDV, b = i % LDV;
-        vtv_s[i] = (a < R && b < R) ? p.vtv[a * R + b] : 0.0;
+        vtv_s[i] = (a < R && b < R) ? __ldcg(p.vtv + a * R + b) : 0.0;  // L2: written by the XV kernel
     }
     double gslot = 0.0;  // this thread's entry (tid) of the CTA's G slot
     for (int bi = blockIdx.x; bi < nbig; bi += gridDim.x) {
         __syncthreads();  // previous slice done with the shared buffers
-        const int4 mt = meta[nsmall + bi];
+        const int4 mt = __ldcg(meta + nsmall + bi);
         const int m = mt.w;
         const int64_t r0 = mt.x, n = mt.y;
         const int wrow = mt.z & 0x7fffffff;
@@ -91,10 +96,10 @@ __global__ void __launch_bounds__(256, 2) k_big(SliceParams p, const int4 *__res
             if (q < nblk) big_stage(xs0 + q * BR * XPI, p.XV, r0 + (int64_t)q * BR, (int)min((int64_t)BR, n - (int64_t)q * BR), R);
             cp_async_commit();
         }
-        if (tid < RB) vec[tid] = tid < R ? ((fresh && p.pass == 0) ? 1.0 : p.W[(int64_t)wrow * R + tid]) : 0.0;
+        if (tid < RB) vec[tid] = tid < R ? ((fresh && p.pass == 0) ? 1.0 : __ldcg(p.W + (int64_t)wrow * R + tid)) : 0.0;
         if (tid < RB && !fresh)
-            for (int z = 0; z < R; ++z) dns[tid * LDL + z] = tid < R ? p.D[(int64_t)wrow * R * R + (int64_t)z * R + tid] : 0.0;
-        const double cold = (tid < R && !fresh) ? p.C[(int64_t)wrow * R + tid] : 0.0;
+            for (int z = 0; z < R; ++z) dns[tid * LDL + z] = tid < R ? __ldcg(p.D + (int64_t)wrow * R * R + (int64_t)z * R + tid) : 0.0;
+        const double cold = (tid < R && !fresh) ? __ldcg(p.C + (int64_t)wrow * R + tid) : 0.0;
         __syncthreads();
         // ---- A sweep by warp 0, lanes 0..15 (lanes 16..31 run a harmless identity copy)
         if (w == 0) {
@@ -315,6 +320,7 @@ __global__ void __launch_bounds__(256, 2) k_big(SliceParams p, const int4 *__res
         cp_async_wait_all();
     }  // big slices of this CTA
     if (tid < R * R) p.G_slots[(int64_t)blockIdx.x * R * R + tid] = gslot;
+    pdl_wait();  // completion of this grid implies completion of the small-slice kernel
 }
 
 int launch_big(cudaStream_t st, int grid, const SliceParams &sp, const int4 *meta, const int *plan_counts) {
@@ -324,6 +330,5 @@ int launch_big(cudaStream_t st, int grid, const SliceParams &sp, const int4 *met
         cudaFuncSetAttribute(k_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    k_big<<<grid, 256, smem, st>>>(sp, meta, plan_counts);
-    return cudaGetLastError() == cudaSuccess ? 0 : DASH_E_CUDA;
+    return launch_k(true, k_big, grid, 256, smem, st, sp, meta, plan_counts);
 }

@@ -29,6 +29,16 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
 }
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+// Programmatic dependent launch (sm_90+): a kernel launched with the
+// programmatic-serialization attribute may start while its predecessor in the
+// stream is still running; pdl_wait() blocks until that predecessor has
+// completed and its writes are visible, pdl_trigger() lets this kernel's own
+// successor begin launching.  Every kernel on the PDL chain calls pdl_wait()
+// in every CTA before it exits, so completion stays transitive.  Both are
+// no-ops for a normally launched kernel.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ int warp_id() { return threadIdx.x >> 5; }
 
 __device__ __forceinline__ bool finite_d(double x) { return isfinite(x); }

@@ -73,6 +73,7 @@ __device__ __forceinline__ int plan_bucket(int64_t n) {
 // hist[b][c]: bucket-b count of chunk c (bucket-major; one CTA of kPlanChunk threads per chunk)
 __global__ void __launch_bounds__(kPlanChunk) k_plan_count(const int64_t *__restrict__ row_ptr, int M,
                                                            int *__restrict__ hist) {
+    pdl_trigger();
     __shared__ int h[kPlanBuckets];
     for (int i = threadIdx.x; i < kPlanBuckets; i += blockDim.x) h[i] = 0;
     __syncthreads();
@@ -89,6 +90,8 @@ __global__ void __launch_bounds__(kPlanChunk) k_plan_count(const int64_t *__rest
 constexpr int kScanThreads = 256;
 __global__ void __launch_bounds__(kScanThreads) k_plan_scan(const int *__restrict__ hist, int nch,
                                                             int *__restrict__ off, int *__restrict__ tot) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ int wsum[kScanThreads / 32];
     const int tid = threadIdx.x, lane = tid & 31, wq = tid >> 5;
     const int *h = hist + (size_t)blockIdx.x * nch;
@@ -152,6 +155,8 @@ __global__ void __launch_bounds__(128) k_plan_scatter(const int64_t *__restrict_
                                                       const int *__restrict__ off, const int *__restrict__ tot,
                                                       int4 *__restrict__ meta, int *__restrict__ counts) {
     constexpr int ROUNDS = kPlanChunk / 32;
+    pdl_wait();
+    pdl_trigger();
     __shared__ int run_s[4][kPlanBuckets];
     const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
     const int chunk = blockIdx.x * 4 + wq;
@@ -213,13 +218,15 @@ __global__ void __launch_bounds__(S3<RB>::NW * 32, 4) k_slices3(SliceParams p, c
     double *lu = gacc + RB * S::LDL;
     int *piv = reinterpret_cast<int *>(lu + RB * S::LDL);
     const int R = p.R;
-    for (int i = threadIdx.x; i < RB * LDV; i += blockDim.x) {
-        const int a = i / LDV, b = i % LDV;
-        vtv_s[i] = (a < R && b < R) ? p.vtv[a * R + b] : 0.0;
-    }
     if (gl == 0) {
 #pragma unroll
         for (int z = 0; z < RB; ++z) gacc[r * S::LDL + z] = 0.0;
+    }
+    pdl_wait();     // XV, vtv (XV kernel) and the plan must be complete
+    pdl_trigger();  // only now: the big-slice kernel relies on the same inputs without waiting
+    for (int i = threadIdx.x; i < RB * LDV; i += blockDim.x) {
+        const int a = i / LDV, b = i % LDV;
+        vtv_s[i] = (a < R && b < R) ? p.vtv[a * R + b] : 0.0;
     }
     __syncthreads();
     const double *vrow = vtv_s + r * LDV;
@@ -429,6 +436,5 @@ int launch_slices3(cudaStream_t st, int grid, const SliceParams &sp, const int4 
         cudaFuncSetAttribute(k_slices3<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    k_slices3<RB><<<grid, S3<RB>::NW * 32, smem, st>>>(sp, meta, plan_counts);
-    return cudaGetLastError() == cudaSuccess ? 0 : DASH_E_CUDA;
+    return launch_k(true, k_slices3<RB>, grid, S3<RB>::NW * 32, smem, st, sp, meta, plan_counts);
 }

@@ -75,6 +75,10 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_xv3(const __grid_constant_
     uint64_t *empty = full + kStages;
     const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
     const int g = lane >> 2, t = lane & 3;
+    // PDL: needs nothing from the plan kernels before it (X, V are final once
+    // the update's first, normally launched kernel has started); waits only
+    // at exit so that its completion implies theirs.
+    pdl_trigger();
     for (int i = tid; i < 16 * VTP; i += blockDim.x) {
         const int nn = i / VTP, k = i % VTP;
         vt[i] = (nn < R && k < J) ? V[k * R + nn] : 0.0;
@@ -117,6 +121,7 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_xv3(const __grid_constant_
                 for (int s = 0; s < JS; ++s) tma_load_2d(xs + st * SD + s * 512, &tmX, 16 * s, r0, &full[st]);
             }
         }
+        pdl_wait();
         return;
     }
     const int mb = w & 3, nb = w >> 2;  // 8-row block, 8-column block of the 32 x 16 output tile
@@ -147,6 +152,7 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_xv3(const __grid_constant_
             }
         }
     }
+    pdl_wait();
 }
 
 // F slot = sum over this CTA's tiles of X^T US.  Warp w owns J-strips w, w+8, ...
@@ -164,6 +170,7 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_fgemm3(const __grid_consta
     uint64_t *empty = full + kStages;
     const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
     const int g = lane >> 2, t = lane & 3;
+    pdl_trigger();
     if (tid == 0) {
         prefetch_map(&tmX);
         prefetch_map(&tmU);
@@ -174,6 +181,7 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_fgemm3(const __grid_consta
         fence_mbar_init();
     }
     __syncthreads();
+    pdl_wait();  // US from the slice kernels
     const int64_t ntiles = (N + kTR - 1) / kTR;
     const int64_t mine = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     if (w == kCW) {

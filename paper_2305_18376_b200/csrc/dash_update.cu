@@ -457,6 +457,29 @@ __global__ void __launch_bounds__(NW * 32) k_slices(SliceParams p) {
     }
 }
 
+// Kernel launch, optionally with programmatic stream serialization (PDL):
+// only for kernels that call pdl_wait() before touching their predecessor's
+// data (dash_common.cuh).  DASH_NO_PDL=1 disables it (A/B timing).
+bool pdl_enabled() {
+    static const bool on = getenv("DASH_NO_PDL") == nullptr;
+    return on;
+}
+
+template <typename... KArgs, typename... Args>
+int launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = (pdl && pdl_enabled()) ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, args...) == cudaSuccess ? 0 : DASH_E_CUDA;
+}
+
 #include "dash_slices.cuh"
 #include "dash_stream.cuh"
 #include "dash_tma.cuh"
@@ -566,6 +589,8 @@ struct ColSumJob {
 };
 
 __global__ void __launch_bounds__(128) k_colsum_part2(ColSumJob a, ColSumJob b) {
+    pdl_wait();
+    pdl_trigger();
     int blk = blockIdx.x;
     const bool second = blk >= a.bx * a.nseg;
     const ColSumJob &j = second ? b : a;
@@ -588,6 +613,8 @@ __global__ void __launch_bounds__(128) k_colsum_part2(ColSumJob a, ColSumJob b) 
 }
 
 __global__ void __launch_bounds__(128) k_colsum_final2(ColSumJob a, ColSumJob b) {
+    pdl_wait();
+    pdl_trigger();
     int blk = blockIdx.x;
     const bool second = blk >= a.bx;
     const ColSumJob &j = second ? b : a;
@@ -610,6 +637,8 @@ __global__ void __launch_bounds__(NWV * 32) k_vsolve(const double *__restrict__ 
                                                      double *__restrict__ V, unsigned long long *err,
                                                      unsigned int *fallbacks) {
     constexpr int LD = RB + 1;
+    pdl_wait();
+    pdl_trigger();
     __shared__ double sL[NWV][RB * LD];
     __shared__ double sG[NWV][RB * LD];
     __shared__ double sd[NWV][RB];
@@ -949,12 +978,12 @@ int device_plan(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b) {
     int *tot = off + (size_t)nch * kPlanBuckets;
     int *counts = tot + kPlanBuckets;
     PhaseScope ps(ctx, st, PH_ROWSLICE);
+    // first kernel of the update: a normal launch (fully ordered after the previous update)
     k_plan_count<<<nch, kPlanChunk, 0, st>>>(b->row_ptr, M, hist);
-    k_plan_scan<<<kPlanBuckets, kScanThreads, 0, st>>>(hist, nch, off, tot);
-    k_plan_scatter<<<(nch + 3) / 4, 128, 0, st>>>(b->row_ptr, b->state_row, b->is_new, M, nch, off, tot,
-                                                   (int4 *)ctx->smeta.p, counts);
     ctx->last_launches += 2;  // three kernels under one phase
-    return cudaGetLastError() == cudaSuccess ? 0 : DASH_E_CUDA;
+    return launch_k(true, k_plan_scan, kPlanBuckets, kScanThreads, 0, st, (const int *)hist, nch, off, tot) ||
+           launch_k(true, k_plan_scatter, (nch + 3) / 4, 128, 0, st, (const int64_t *)b->row_ptr, b->state_row,
+                    b->is_new, M, nch, (const int *)off, (const int *)tot, (int4 *)ctx->smeta.p, counts);
 }
 
 const int *plan_counts_of(dash_ctx *ctx, int M) {
@@ -1035,8 +1064,8 @@ void launch_vsolve_t(dash_ctx *ctx, cudaStream_t st, const double *fg, double la
     constexpr int NWV = RB <= 16 ? 4 : 1;
     int blocks = (J + NWV * 32 - 1) / (NWV * 32);
     PhaseScope ps(ctx, st, PH_VSOLVE);
-    k_vsolve<RB, NWV><<<blocks, NWV * 32, 0, st>>>(fg, (const double *)ctx->fsnap.p, (const double *)ctx->gsnap.p,
-                                                    lam, J, R, eps, F, G, V, ctx->err, ctx->fallbacks);
+    launch_k(true, k_vsolve<RB, NWV>, blocks, NWV * 32, 0, st, fg, (const double *)ctx->fsnap.p,
+             (const double *)ctx->gsnap.p, lam, J, R, eps, F, G, V, ctx->err, ctx->fallbacks);
 }
 
 // out[0:width] = column sums of slots (nslots x width), deterministic order
@@ -1063,10 +1092,9 @@ int colsum2(dash_ctx *ctx, cudaStream_t st, const double *sa, int na, int64_t wa
     if (ensure(ctx->part, sizeof(double) * (a.nseg * wa + b.nseg * wb))) return DASH_E_CUDA;
     a.part = (double *)ctx->part.p;
     b.part = a.part + a.nseg * wa;
-    k_colsum_part2<<<a.bx * a.nseg + b.bx * b.nseg, 128, 0, st>>>(a, b);
-    k_colsum_final2<<<a.bx + b.bx, 128, 0, st>>>(a, b);
     ctx->last_launches++;  // two kernels under one phase
-    return cudaGetLastError() == cudaSuccess ? 0 : DASH_E_CUDA;
+    return launch_k(true, k_colsum_part2, a.bx * a.nseg + b.bx * b.nseg, 128, 0, st, a, b) ||
+           launch_k(true, k_colsum_final2, a.bx + b.bx, 128, 0, st, a, b);
 }
 
 // ---- streaming (TMA ring) GEMM path: J, ldx, R even; ring fits in shared memory
@@ -1121,7 +1149,7 @@ bool tma_ok(const dash_batch_f64 *b, int J, int R) {
 }
 
 int launch_xv3(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, const double *V, int R, double *XV,
-               const FusedPrologue &pro) {
+               const FusedPrologue &pro, bool pdl) {
     CUtensorMap mx;
     if (!make_box_map(&mx, b->X, J, b->N, b->ldx)) return DASH_E_CUDA;
     const size_t smem = TmaSmem::xv_bytes(J);
@@ -1131,8 +1159,7 @@ int launch_xv3(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, c
         attr = smem;
     }
     PhaseScope ps(ctx, st, PH_XV);
-    k_xv3<<<ctx->num_sms, kCW * 32 + 32, smem, st>>>(mx, b->N, J, V, R, XV, pro);
-    return 0;
+    return launch_k(pdl, k_xv3, ctx->num_sms, kCW * 32 + 32, smem, st, mx, b->N, J, V, R, XV, pro);
 }
 
 template <int MAXS>
@@ -1145,7 +1172,7 @@ void launch_f3_t(dash_ctx *ctx, cudaStream_t st, const CUtensorMap &mx, const CU
         attr = smem;
     }
     PhaseScope ps(ctx, st, PH_FGEMM);
-    k_fgemm3<MAXS><<<ctx->num_sms, kCW * 32 + 32, smem, st>>>(mx, mu, N, J, R, F_slots);
+    launch_k(true, k_fgemm3<MAXS>, ctx->num_sms, kCW * 32 + 32, smem, st, mx, mu, N, J, R, F_slots);
 }
 
 int launch_f3(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, const double *US, int R,
@@ -1350,7 +1377,8 @@ int dash_update_pass_begin_f64(dash_ctx *ctx, void *stream, const dash_batch_f64
         if (ctx->tma) {
             const FusedPrologue pro{(double *)ctx->vtv.p, s->F, s->G, (double *)ctx->fsnap.p, (double *)ctx->gsnap.p,
                                     v_used_out, pass == 0, last};
-            if (launch_xv3(ctx, st, b, J, s->V, R, XV, pro)) return DASH_E_CUDA;
+            // PDL only behind the plan kernels (pass 0); a later pass follows the V solve
+            if (launch_xv3(ctx, st, b, J, s->V, R, XV, pro, pass == 0)) return DASH_E_CUDA;
         } else if (ctx->stream) {
             if (rank_bucket(R) <= 8) launch_xv2_t<8>(ctx, st, b, J, s->V, R, XV);
             else launch_xv2_t<16>(ctx, st, b, J, s->V, R, XV);

@@ -1,0 +1,34 @@
+"""Programmatic dependent launch (PDL) does not change results: the update
+chain with PDL (kernels overlapping their predecessors' tails) is bit-identical
+to the fully serialised chain (DASH_NO_PDL=1) and across repeated runs, on a
+large-shaped stream (20k small slices + 300 big slices per update)."""
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _digest(no_pdl: bool) -> str:
+    env = dict(os.environ)
+    env.pop("DASH_NO_PDL", None)
+    if no_pdl:
+        env["DASH_NO_PDL"] = "1"
+    out = subprocess.run([sys.executable, str(ROOT / "tools" / "pdl_check.py")], cwd=ROOT, env=env,
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    return out.stdout.strip().splitlines()[-1]
+
+
+def test_pdl_chain_is_bit_identical_to_serialised_chain():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    a = _digest(False)
+    b = _digest(False)
+    c = _digest(True)
+    assert a == b == c, (a, b, c)
