@@ -34,6 +34,12 @@ __device__ __forceinline__ void prefetch_map(const CUtensorMap *map) {
 // double offset of the 16-byte chunk `c` (0..7) of row `r` inside a swizzled 32x16 box
 __device__ __forceinline__ int swz(int r, int c) { return r * 16 + ((c ^ (r & 7)) << 1); }
 
+// LDS.128 is serviced per quarter-warp (8 lanes = fragment rows g = 2q, 2q+1):
+// mapping fragment index g to perm(g) = (g&1)*4 + g/2 makes the two rows of a
+// quarter-warp XOR-swizzle into disjoint chunk halves -> conflict-free.  The
+// permutation is undone when results are written.
+__device__ __forceinline__ int qperm(int g) { return ((g & 1) << 2) | (g >> 1); }
+
 struct TmaSmem {
     static __host__ __device__ int strips(int J) { return (J + 15) / 16; }
     static __host__ __device__ int vtp(int J) { return strips(J) * 16 + 8; }  // Vt pitch (== 8 mod 16)
@@ -126,11 +132,11 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_xv3(const __grid_constant_
     }
     const int mb = w & 3, nb = w >> 2;  // 8-row block, 8-column block of the 32 x 16 output tile
     const double *vrow = vt + (8 * nb + g) * VTP + 2 * t;
+    const int row = 8 * mb + qperm(g);  // tile row of this lane's A fragment and output
     for (int64_t i = 0; i < mine; ++i) {
         const int st = (int)(i % kStages);
         mbar_wait(&full[st], (uint32_t)((i / kStages) & 1));
         const double *xt = xs + st * SD;
-        const int row = 8 * mb + g;
         double acc[2] = {0.0, 0.0}, acc2[2] = {0.0, 0.0};
         for (int s = 0; s < JS; ++s) {
 #pragma unroll
@@ -197,6 +203,7 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_fgemm3(const __grid_consta
         }
         return;
     }
+    const int pg = qperm(g);  // j pair (A) and r pair (B) of this lane: 2 pg, 2 pg + 1
     double acc[MAXS][4][2];
 #pragma unroll
     for (int q = 0; q < MAXS; ++q)
@@ -210,12 +217,12 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_fgemm3(const __grid_consta
 #pragma unroll
         for (int kk = 0; kk < kTR / 4; ++kk) {
             const int row = 4 * kk + t;
-            const double2 b = *reinterpret_cast<const double2 *>(ut + swz(row, g));  // US[row][2g], [2g+1]
+            const double2 b = *reinterpret_cast<const double2 *>(ut + swz(row, pg));  // US[row][2pg], [2pg+1]
 #pragma unroll
             for (int q = 0; q < MAXS; ++q) {
                 const int s = w + kCW * q;
                 if (s < JS) {
-                    const double2 a = *reinterpret_cast<const double2 *>(xt + s * 512 + swz(row, g));
+                    const double2 a = *reinterpret_cast<const double2 *>(xt + s * 512 + swz(row, pg));
                     dmma884(acc[q][0], a.x, b.x);  // even j, even r
                     dmma884(acc[q][1], a.x, b.y);  // even j, odd r
                     dmma884(acc[q][2], a.y, b.x);  // odd j, even r
@@ -233,10 +240,10 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_fgemm3(const __grid_consta
         if (s < JS) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                const int j = 16 * s + 2 * g + (k >> 1);
+                const int j = 16 * s + 2 * pg + (k >> 1);
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
-                    const int r = 2 * (2 * t + e) + (k & 1);
+                    const int r = 2 * qperm(2 * t + e) + (k & 1);
                     if (j < J && r < R) slot[j * R + r] = acc[q][k][e];
                 }
             }
