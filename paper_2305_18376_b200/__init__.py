@@ -8,7 +8,8 @@ __version__ = "0.1.0"
 
 from .als import ALSInfo, FactorSet, FactorizationError, parafac2_als, reconstruct, relative_error
 from .linalg import RIDGE_EPS, SolveError
-from .tensor import DatasetError, IrregularTensor, NewSlice, SliceMatrix, UpdateBatch
+from .tensor import (CAUSAL, GLOBAL, ColumnStats, DatasetError, IrregularTensor, NewSlice, SliceMatrix, UpdateBatch,
+                     global_stats, normalize_batch, normalize_tensor)
 
 
 def __getattr__(name):
@@ -19,6 +20,9 @@ def __getattr__(name):
     if name == "local_error":
         from .evaluate import local_error
         return local_error
+    if name in ("save_state", "load_state"):
+        from . import checkpoint
+        return getattr(checkpoint, name)
     if name == "ShardedStream":
         from .distributed import ShardedStream
         return ShardedStream
@@ -26,6 +30,8 @@ def __getattr__(name):
 
 
 __all__ = [
+    "CAUSAL", "ColumnStats", "GLOBAL", "global_stats", "load_state", "normalize_batch", "normalize_tensor",
+    "save_state",
     "ALSInfo", "DatasetError", "FactorSet", "FactorizationError", "HelperState", "HostPipeline",
     "IrregularTensor",
     "NewSlice", "RIDGE_EPS", "ShardedStream", "SliceMatrix", "SolveError", "StreamState",

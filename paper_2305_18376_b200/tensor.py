@@ -10,7 +10,7 @@ unchanged.  The engine packs them into a CSR row table (``pack_batch`` in
 """
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -138,3 +138,96 @@ class UpdateBatch:
             yield sid, mat, False
         for ns in self.new_slices:
             yield ns.slice_id, ns.rows, True
+
+
+# ---------------------------------------------------------------------------
+# Ingest normalisation (reference tensor.py:252-360): each (slice, column) is
+# mapped to [0, 1] by a running min-max.  Host-side, like the reference: it
+# touches every batch row once before packing, O(N J) next to the upload of
+# the same bytes.  Policies: CAUSAL (stats from strictly earlier data, then
+# extended by what was seen) and GLOBAL (fixed stats).
+# ---------------------------------------------------------------------------
+CAUSAL = "causal"
+GLOBAL = "global"
+
+
+@dataclass
+class ColumnStats:
+    """Per-slice column minima / maxima (reference tensor.py:252-275)."""
+
+    minimum: dict = field(default_factory=dict)
+    maximum: dict = field(default_factory=dict)
+
+    def has(self, slice_id: str) -> bool:
+        return slice_id in self.minimum
+
+    def observe(self, slice_id: str, rows: np.ndarray) -> None:
+        lo, hi = rows.min(axis=0), rows.max(axis=0)
+        if self.has(slice_id):
+            lo = np.minimum(self.minimum[slice_id], lo)
+            hi = np.maximum(self.maximum[slice_id], hi)
+        self.minimum[slice_id], self.maximum[slice_id] = lo.copy(), hi.copy()
+
+    def copy(self) -> "ColumnStats":
+        dup = ColumnStats()
+        for sid in self.minimum:
+            dup.minimum[sid] = self.minimum[sid].copy()
+            dup.maximum[sid] = self.maximum[sid].copy()
+        return dup
+
+
+def _minmax_scale(rows: np.ndarray, lo: np.ndarray, hi: np.ndarray) -> np.ndarray:
+    """(x - lo) / (hi - lo) column-wise; zero-width columns become 0."""
+    width = hi - lo
+    return np.divide(rows - lo, width, out=np.zeros(rows.shape, dtype=float), where=width > 0)
+
+
+def _policy(policy: str) -> bool:
+    """True when the policy extends the stats (causal)."""
+    if policy not in (CAUSAL, GLOBAL):
+        raise ValueError(f"unknown stats policy {policy!r}; expected one of {(CAUSAL, GLOBAL)}")
+    return policy == CAUSAL
+
+
+def _normalise_slice(stats: ColumnStats, sid: str, rows: np.ndarray, extend: bool, need_stats: bool):
+    if stats.has(sid):
+        lo, hi = stats.minimum[sid], stats.maximum[sid]
+    elif need_stats:
+        raise DatasetError(f"no normalization stats for existing slice {sid!r}")
+    else:  # first sight of a slice: its own data sets the range
+        lo, hi = rows.min(axis=0), rows.max(axis=0)
+    scaled = _minmax_scale(rows, lo, hi)
+    if extend:
+        stats.observe(sid, rows)
+    return scaled
+
+
+def global_stats(tensor: IrregularTensor) -> ColumnStats:
+    """Stats over a whole recorded tensor (reference tensor.py:292-297)."""
+    stats = ColumnStats()
+    for sl in tensor.slices:
+        stats.observe(sl.slice_id, sl.rows)
+    return stats
+
+
+def normalize_tensor(tensor: IrregularTensor, stats: ColumnStats | None = None,
+                     policy: str = CAUSAL) -> tuple:
+    """Normalise every slice (reference tensor.py:300-323) -> (tensor, stats)."""
+    extend = _policy(policy)
+    stats = ColumnStats() if stats is None else stats.copy()
+    out = [SliceMatrix(sl.slice_id, _normalise_slice(stats, sl.slice_id, sl.rows, extend, False),
+                       sl.first_time_step) for sl in tensor.slices]
+    return IrregularTensor(out), stats
+
+
+def normalize_batch(batch: UpdateBatch, stats: ColumnStats, policy: str = CAUSAL) -> tuple:
+    """Normalise one update batch (reference tensor.py:326-360) -> (batch,
+    stats).  Existing slices must already have stats; a new slice without
+    stats is scaled by its own rows."""
+    extend = _policy(policy)
+    stats = stats.copy()
+    existing = {sid: _normalise_slice(stats, sid, rows, extend, True)
+                for sid, rows in batch.existing_rows.items()}
+    fresh = [NewSlice(ns.slice_id, _normalise_slice(stats, ns.slice_id, ns.rows, extend, False),
+                      ns.first_time_step) for ns in batch.new_slices]
+    return UpdateBatch(batch.update_index, existing, fresh, batch.cycle_span), stats

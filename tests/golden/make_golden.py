@@ -20,6 +20,10 @@ regenerating), and records what the reference returns:
                     only new / only existing slices, R=32 wide-ish state.
   kernel.npz        direct ``group_update`` calls (numba kernel) on random
                     inputs, for the bit-level check of oracle/group_update.c.
+  ckpt_ref.json     reference ``save_state`` checkpoints (JSON and npz) of a
+  ckpt_ref.npz      planted tiny state after 3 updates, with column stats;
+  ckpt.npz          the 2 updates that follow (resume trajectory) and a causal
+                    ``normalize_batch`` chain (normalised rows + final stats).
 """
 from __future__ import annotations
 
@@ -206,7 +210,39 @@ def make_kernel():
     np.savez_compressed(HERE / "kernel.npz", **out)
 
 
+def make_checkpoint():
+    from p2stream.tensor import global_stats, normalize_batch
+    stream = wl.make_stream("tiny")
+    state, ps = planted_ref_state(stream)
+    batches = list(stream.batches())
+    out = {}
+    save_planted(out, "", ps)
+    # causal normalisation chain, seeded by the initial tensor's global stats
+    init = stream.initial_tensor()
+    stats = global_stats(p2stream.IrregularTensor(
+        p2stream.SliceMatrix(s.slice_id, s.rows) for s in init.slices))
+    for t, batch in enumerate(batches[:4]):
+        X, ids, counts, new = pack_batch(batch)
+        out[f"nb{t}_X"], out[f"nb{t}_ids"], out[f"nb{t}_counts"], out[f"nb{t}_new"] = X, ids, counts, new
+        nb, stats = normalize_batch(to_ref_batch(batch), stats)
+        out[f"nb{t}_Xn"] = np.concatenate(
+            [nb.existing_rows[sid] for sid in nb.existing_rows] + [ns.rows for ns in nb.new_slices])
+    sids = sorted(stats.minimum)
+    out["nstats_ids"] = np.array(sids)
+    out["nstats_min"] = np.stack([stats.minimum[s] for s in sids])
+    out["nstats_max"] = np.stack([stats.maximum[s] for s in sids])
+    out["n_norm"] = np.array(4)
+    # checkpoint after 3 updates (with the stats), then the resume trajectory
+    for batch in batches[:3]:
+        state.update(to_ref_batch(batch))
+    ref_stream.save_state(state, HERE / "ckpt_ref.json", column_stats=stats)
+    ref_stream.save_state(state, HERE / "ckpt_ref.npz", column_stats=stats)
+    record_updates(state, batches[3:5], out, "r")
+    np.savez_compressed(HERE / "ckpt.npz", **out)
+
+
 if __name__ == "__main__":
+    make_checkpoint()
     make_kernel()
     make_edge()
     make_multipass()
