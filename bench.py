@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=2)
+    ap.add_argument("--no-fp32", dest="fp32", action="store_false",
+                    help="skip the FP32 data-mode measurement")
     return ap.parse_args()
 
 
@@ -336,6 +338,13 @@ def run_gpu(args):
     value = elems / (t_max / 1e3)
     ms_per_step = t_max / len(timed)
 
+    # FP32 data mode (north_star: optional, reported separately): a second
+    # state fed the same batches rounded to FP32; device-resident timing of the
+    # same K steps, then the same e2e protocol with FP32 host buffers.
+    fp32 = None
+    if args.fp32:
+        fp32 = run_fp32_arm(args, arrays, batches, dev, stream, world, J, R, prof_steps, barrier)
+
     # e2e through the public API with host buffers: HostPipeline uploads batch
     # t+1 (pinned host -> HBM) and reads back batch t-1's U / v_used while
     # batch t is updated; every step's H2D and D2H lie inside the timed region.
@@ -436,12 +445,116 @@ def run_gpu(args):
                     "ms_per_step": e2e_ms / max(len(e2e_b), 1), "steps": len(e2e_b)},
             "gpu_launches": launches,
             "lu_fallbacks": fallbacks,
+            "fp32": fp32,
             "clocks": clocks,
         }
     del batches
     if world > 1:
         dist.barrier()
     return out, cfg
+
+
+def run_fp32_arm(args, arrays, batches, dev, stream, world, J, R, prof_steps, barrier):
+    """FP32 data mode: X in / U_new out in FP32 (dash_update_f32); state and
+    arithmetic FP64.  Same batches (rounded), same step protocol as the FP64
+    arm: W warm-ups, K device-timed steps, the profiled steps untimed (the
+    stream must see every batch), then the e2e steps through HostPipeline."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2305_18376_b200.distributed import ShardedStream
+    from paper_2305_18376_b200.stream import HostPipeline, StreamState
+    st32 = StreamState.from_arrays(arrays, device=dev, dtype=torch.float32)
+    eng = ShardedStream(st32, rank=int(os.environ.get("RANK", "0")), world=world) if world > 1 else st32
+    X32 = [b["X"].float() for b in batches]
+
+    def step(k):
+        b = batches[k]
+        return eng.update_packed(X32[k], b["counts"], b["ex_rows"], b["new"])
+
+    W, K = args.warmup, args.steps
+    for k in range(W):
+        step(k)
+    torch.cuda.synchronize()
+    st32.check()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for k in range(W, W + K):
+        step(k)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t_ms = e0.elapsed_time(e1)
+    import ctypes
+    from paper_2305_18376_b200 import _native as nat
+    L = nat.lib()
+    L.dash_ctx_set_profiling(st32._ctx, 1)
+    for k in range(W + K, W + K + prof_steps):
+        step(k)
+    torch.cuda.synchronize()
+    nph = len(nat.PHASES)
+    ms_arr = (ctypes.c_double * nph)()
+    cnt_arr = (ctypes.c_int32 * nph)()
+    L.dash_ctx_phase_ms(st32._ctx, ms_arr, cnt_arr, nph)
+    L.dash_ctx_set_profiling(st32._ctx, 0)
+    phase = {nat.PHASES[i]: ms_arr[i] / prof_steps for i in range(nph) if cnt_arr[i]}
+    e2e_ks = list(range(W + K + prof_steps, len(batches)))
+    pins = []
+    for k in e2e_ks:
+        pins.append(X32[k].cpu().pin_memory())
+    maxN = max((batches[k]["N"] for k in e2e_ks), default=1)
+    Uh = [torch.empty((maxN, R), dtype=torch.float32).pin_memory() for _ in range(2)]
+    vh = [torch.empty((J, R), dtype=torch.float64).pin_memory() for _ in range(2)]
+    pipe = HostPipeline(eng, maxN, J, device=dev)
+    torch.cuda.synchronize()
+    st32.check()
+    barrier()
+    h2d = d2h = 0
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    pipe.start()
+    staged = pipe.put(pins[0]) if e2e_ks else None
+    for i, k in enumerate(e2e_ks):
+        b = batches[k]
+        nxt = pipe.put(pins[i + 1]) if i + 1 < len(e2e_ks) else None
+        pipe.update(staged, b["counts"], b["ex_rows"], b["new"], U_host=Uh[i % 2], v_host=vh[i % 2])
+        staged = nxt
+        h2d += b["N"] * J * 4 + (b["M_old"] + b["L"]) * (8 + 4 + 1) + 8
+        d2h += b["N"] * R * 4 + J * R * 8
+    pipe.finish()
+    e3.record(stream)
+    torch.cuda.synchronize()
+    st32.check()
+    e2e_ms = e2.elapsed_time(e3)
+    elems = sum(batches[k]["N"] for k in range(W, W + K)) * J
+    e2e_elems = sum(batches[k]["N"] for k in e2e_ks) * J
+    vals = torch.tensor([t_ms, e2e_ms, elems, e2e_elems], device=dev, dtype=torch.float64)
+    if world > 1:
+        mx = vals[:2].clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = vals[2:].clone()
+        dist.all_reduce(sm)
+        vals = torch.cat([mx, sm])
+    t_ms, e2e_ms, elems, e2e_elems = (float(v) for v in vals.tolist())
+    del X32, pins
+    N_avg = sum(batches[k]["N"] for k in range(W, W + K)) / K
+    M_old = sum(batches[k]["M_old"] for k in range(W, W + K)) / K
+    L_avg = sum(batches[k]["L"] for k in range(W, W + K)) / K
+    # algorithmic bytes with FP32 X and U_new (state terms stay FP64)
+    by = 4 * (N_avg * J + N_avg * R) + 8 * (2 * M_old * (R * R + 2 * R) + L_avg * (R * R + 2 * R)
+                                             + 3 * J * R + 2 * R * R)
+    peak, _ = peaks()
+    ms = t_ms / K
+    return {"dtype": "f32 data (X in, U_new out); f64 state and arithmetic",
+            "value": elems / (t_ms / 1e3), "unit": "elements/s", "ms_per_step": ms, "steps": K,
+            "step_roofline": {"alg_bytes": by, "achieved_gbs": by / (ms / 1e3) / 1e9,
+                              "frac": by / (ms / 1e3) / 1e9 / peak},
+            "phase_ms_per_step": phase,
+            "e2e": {"value": e2e_elems / (e2e_ms / 1e3) if e2e_ks else None, "unit": "elements/s",
+                    "h2d_bytes_per_step": h2d / max(len(e2e_ks), 1),
+                    "d2h_bytes_per_step": d2h / max(len(e2e_ks), 1),
+                    "ms_per_step": e2e_ms / max(len(e2e_ks), 1), "steps": len(e2e_ks)},
+            "parity": "tests/test_gpu_fp32.py: <= 1e-3 vs the FP64 oracle, <= 1e-5 vs the oracle on FP32-rounded X"}
 
 
 # ---------------------------------------------------------------------------

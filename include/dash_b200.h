@@ -22,6 +22,10 @@
  *   dash_local_error_f64    local_error / slice_error         evaluate.py:93-118,
  *                                                             anomaly.py:23-42
  *   dash_als_sweep_f64      parafac2_als sweep (initialize)    als.py:102-201
+ *   dash_update_f32 / dash_update_pass_begin_f32 / dash_local_error_f32
+ *                           the same update / fitness with the streamed data
+ *                           in FP32 (north_star's optional FP32 mode; the
+ *                           reference has FP64 only)
  */
 #ifndef DASH_B200_H
 #define DASH_B200_H
@@ -78,6 +82,21 @@ typedef struct {
     const uint8_t *is_new;       /* M: 1 = registered by this batch             */
 } dash_batch_f64;
 
+/* FP32 data mode: the same batch with X in single precision (ldx % 4 == 0
+ * and a 16-byte aligned X enable the TMA path).  Only the streamed data (X in,
+ * U_new out) are FP32; the per-slice state and the factors stay FP64 on the
+ * device, and every product / sum inside the kernels is formed in FP64. */
+typedef struct {
+    const float *X;              /* N x ldx                                    */
+    int64_t ldx;
+    int64_t N;
+    int32_t M;
+    const int64_t *row_ptr;
+    const int64_t *row_ptr_host;
+    const int32_t *state_row;
+    const uint8_t *is_new;
+} dash_batch_f32;
+
 /* Stream state (StreamState fields, stream.py:196-206).  W/C/D have at least
  * max(state_row)+1 rows.  F, G, V are updated in place. */
 typedef struct {
@@ -115,6 +134,15 @@ int dash_update_pass_begin_f64(dash_ctx *ctx, void *stream, const dash_batch_f64
 int dash_update_pass_finish_f64(dash_ctx *ctx, void *stream, dash_state_f64 *state,
                                 const double *fg, double eps);
 
+/* FP32 data mode of dash_update_f64 / pass_begin: X (batch) and U_out in
+ * FP32; state, v_used, fg and all arithmetic FP64.  Results equal the FP64
+ * update of the FP32-rounded X up to the final rounding of U_out. */
+int dash_update_f32(dash_ctx *ctx, void *stream, const dash_batch_f32 *batch,
+                    dash_state_f64 *state, float *U_out, double *v_used_out, double eps);
+int dash_update_pass_begin_f32(dash_ctx *ctx, void *stream, const dash_batch_f32 *batch,
+                               dash_state_f64 *state, float *U_out, double *v_used_out,
+                               double eps, int32_t pass, double *fg_out);
+
 /* Phase timing for benchmarks: when enabled, CUDA events bracket every
  * launch; dash_ctx_phase_ms syncs and returns the summed milliseconds (and
  * launch counts) per phase id since the last call:
@@ -132,6 +160,11 @@ int dash_group_update_f64(dash_ctx *ctx, void *stream, int32_t G, int32_t I, int
                           const double *c_old, const double *d_old, double lam, double eps,
                           double *u, double *us, double *c_new, double *d_new, double *w,
                           double *g_fresh, int32_t *ok_host);
+
+/* local_error on an FP32 batch with FP32 U (the FP32 data mode's fitness). */
+int dash_local_error_f32(dash_ctx *ctx, void *stream, const dash_batch_f32 *batch,
+                         const float *U, const double *W, const double *V, int32_t J,
+                         int32_t R, double *slice_err, double *tensor_err);
 
 /* ridge_solve for a batch of systems: x_b = (lhs_b + eps*mean(diag lhs_b) I)^-1 rhs_b,
  * lhs (B,n,n), rhs (B,n,m), x (B,n,m).  n <= DASH_MAX_RANK_ALS. */

@@ -28,6 +28,7 @@ _c_dp = ctypes.c_void_p  # device pointers travel as integers
 
 
 class DashBatch(ctypes.Structure):
+    """dash_batch_f64 / dash_batch_f32 (same layout; X is a device pointer)."""
     _fields_ = [
         ("X", _c_dp), ("ldx", ctypes.c_int64), ("N", ctypes.c_int64), ("M", ctypes.c_int32),
         ("row_ptr", _c_dp), ("row_ptr_host", _c_dp), ("state_row", _c_dp), ("is_new", _c_dp),
@@ -55,6 +56,14 @@ SIGNATURES = {
                                                   ctypes.c_int32, _c_dp]),
     "dash_update_pass_finish_f64": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(DashState),
                                                    _c_dp, ctypes.c_double]),
+    "dash_update_f32": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(DashBatch),
+                                       ctypes.POINTER(DashState), _c_dp, _c_dp, ctypes.c_double]),
+    "dash_update_pass_begin_f32": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(DashBatch),
+                                                  ctypes.POINTER(DashState), _c_dp, _c_dp, ctypes.c_double,
+                                                  ctypes.c_int32, _c_dp]),
+    "dash_local_error_f32": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(DashBatch),
+                                            _c_dp, _c_dp, _c_dp, ctypes.c_int32, ctypes.c_int32,
+                                            _c_dp, _c_dp]),
     "dash_ctx_fallbacks": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32]),
     "dash_ctx_set_profiling": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "dash_ctx_phase_ms": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),

@@ -95,10 +95,11 @@ __global__ void __launch_bounds__(NW * 32) k_helpers(const int64_t *__restrict__
 
 // Per-slice mean |X - (U o w) V^T| with post-update W, V; one warp per slice,
 // lanes over columns.  V is read through L1 (J x R may exceed shared memory).
-__global__ void __launch_bounds__(256) k_local_error(const double *__restrict__ X, int64_t ldx,
+template <typename TX>
+__global__ void __launch_bounds__(256) k_local_error(const TX *__restrict__ X, int64_t ldx,
                                                      const int64_t *__restrict__ row_ptr,
                                                      const int32_t *__restrict__ state_row, int M,
-                                                     const double *__restrict__ U, const double *__restrict__ W,
+                                                     const TX *__restrict__ U, const double *__restrict__ W,
                                                      const double *__restrict__ V, int J, int R,
                                                      double *__restrict__ slice_err) {
     const int lane = lane_id();
@@ -111,12 +112,12 @@ __global__ void __launch_bounds__(256) k_local_error(const double *__restrict__ 
         const double *w = W + (int64_t)state_row[m] * R;
         double acc = 0.0;
         for (int64_t row = r0; row < r1; ++row) {
-            if (lane < R) us[lane] = U[row * R + lane] * w[lane];
+            if (lane < R) us[lane] = (double)U[row * R + lane] * w[lane];
             __syncwarp();
             for (int j = lane; j < J; j += 32) {
                 double rec = 0.0;
                 for (int r = 0; r < R; ++r) rec = fma(us[r], __ldg(V + (int64_t)j * R + r), rec);
-                acc += fabs(X[row * ldx + j] - rec);
+                acc += fabs((double)X[row * ldx + j] - rec);
             }
             __syncwarp();
         }
@@ -271,7 +272,11 @@ int dash_init_helpers_f64(dash_ctx *ctx, void *stream, const dash_batch_f64 *t, 
     return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_E_CUDA;
 }
 
-int dash_local_error_f64(dash_ctx *ctx, void *stream, const dash_batch_f64 *b, const double *U, const double *W,
+}  // extern "C"
+
+namespace {
+template <class B, typename TX>
+int local_error_impl(dash_ctx *ctx, void *stream, const B *b, const TX *U, const double *W,
                          const double *V, int32_t J, int32_t R, double *slice_err, double *tensor_err) {
     if (!ctx || !b || R < 1 || R > DASH_MAX_RANK || J < 1) return DASH_E_ARG;
     cudaStream_t st = (cudaStream_t)stream;
@@ -282,6 +287,20 @@ int dash_local_error_f64(dash_ctx *ctx, void *stream, const dash_batch_f64 *b, c
     }
     k_mean<<<1, 32, 0, st>>>(slice_err, b->M, tensor_err);
     return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_E_CUDA;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dash_local_error_f64(dash_ctx *ctx, void *stream, const dash_batch_f64 *b, const double *U, const double *W,
+                         const double *V, int32_t J, int32_t R, double *slice_err, double *tensor_err) {
+    return local_error_impl(ctx, stream, b, U, W, V, J, R, slice_err, tensor_err);
+}
+
+int dash_local_error_f32(dash_ctx *ctx, void *stream, const dash_batch_f32 *b, const float *U, const double *W,
+                         const double *V, int32_t J, int32_t R, double *slice_err, double *tensor_err) {
+    return local_error_impl(ctx, stream, b, U, W, V, J, R, slice_err, tensor_err);
 }
 
 int dash_ridge_solve_f64(dash_ctx *ctx, void *stream, int32_t B, int32_t n, int32_t m, const double *lhs,

@@ -76,7 +76,10 @@ __global__ void __launch_bounds__(256, 2) k_big(SliceParams p, const int4 *__res
     // after their own pdl_wait -- so XV, vtv and the plan are complete here.
     // The two kernels touch disjoint slices / rows / G slots, so this one does
     // not wait for the small-slice kernel until it exits (tail overlap).
-    pdl_trigger();
+    // Its own dependent (the F GEMM) is released only once every CTA is past
+    // its row pass: a successor made resident earlier would hold shared
+    // memory the remaining big / small slices need (measured: the FP32 data
+    // mode's 83 KB F-GEMM CTAs, which fit beside k_big, cost 160 us/update).
     const int nsmall = __ldcg(plan_counts), nbig = __ldcg(plan_counts + 1);
     for (int i = tid; i < RB * LDV; i += blockDim.x) {
         const int a = i / LDV, b = i % LDV;
@@ -232,6 +235,7 @@ __global__ void __launch_bounds__(256, 2) k_big(SliceParams p, const int4 *__res
             for (int ww = 0; ww < 8; ++ww) cs += red[ww * 64 + tid];
             vec[RB + tid] = tid < R ? p.lam * cold + cs : 0.0;  // c_new
         }
+        pdl_trigger();
         __syncthreads();
         // ---- D accumulation and the S-row system by warp 0 lanes 0..15 (D row in shared dns)
         if (w == 0) {
@@ -330,5 +334,5 @@ int launch_big(cudaStream_t st, int grid, const SliceParams &sp, const int4 *met
         cudaFuncSetAttribute(k_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    return launch_k(true, k_big, grid, 256, smem, st, sp, meta, plan_counts);
+    return launch_k(pdl_site("big"), k_big, grid, 256, smem, st, sp, meta, plan_counts);
 }

@@ -436,5 +436,5 @@ int launch_slices3(cudaStream_t st, int grid, const SliceParams &sp, const int4 
         cudaFuncSetAttribute(k_slices3<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    return launch_k(true, k_slices3<RB>, grid, S3<RB>::NW * 32, smem, st, sp, meta, plan_counts);
+    return launch_k(pdl_site("sl3"), k_slices3<RB>, grid, S3<RB>::NW * 32, smem, st, sp, meta, plan_counts);
 }

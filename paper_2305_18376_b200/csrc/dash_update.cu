@@ -27,6 +27,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/dash_b200.h"
@@ -87,8 +88,8 @@ __global__ void k_row_slice(const int64_t *__restrict__ row_ptr, int M, int32_t 
 // k_xv: XV (N x R) = X (N x J, ld ldx) . V (J x R).  64-row tiles, 8 warps,
 // warp w owns rows 8w..8w+7 of the tile and all RP/8 column tiles.
 // ---------------------------------------------------------------------------
-template <int RP>
-__global__ void __launch_bounds__(256) k_xv(const double *__restrict__ X, int64_t ldx, int64_t N, int J,
+template <int RP, typename TX>
+__global__ void __launch_bounds__(256) k_xv(const TX *__restrict__ X, int64_t ldx, int64_t N, int J,
                                             const double *__restrict__ V, int R, double *__restrict__ XV) {
     constexpr int BM = 64, BK = 32, LDXS = BK + 4;
     constexpr int LDVS = (RP % 16 == 0) ? RP + 8 : RP;
@@ -110,7 +111,7 @@ __global__ void __launch_bounds__(256) k_xv(const double *__restrict__ X, int64_
                 int r = i / BK, c = i % BK;
                 int64_t row = row0 + r;
                 int col = k0 + c;
-                Xs[r * LDXS + c] = (row < N && col < J) ? __ldg(X + row * ldx + col) : 0.0;
+                Xs[r * LDXS + c] = (row < N && col < J) ? (double)__ldg(X + row * ldx + col) : 0.0;
             }
             for (int i = tid; i < BK * RP; i += 256) {
                 int r = i / RP, c = i % RP;
@@ -464,6 +465,11 @@ bool pdl_enabled() {
     static const bool on = getenv("DASH_NO_PDL") == nullptr;
     return on;
 }
+// per-launch-site switch for A/B timing: DASH_PDL_OFF=<comma list of site names>
+bool pdl_site(const char *name) {
+    static const char *off = getenv("DASH_PDL_OFF");
+    return !(off && strstr(off, name));
+}
 
 template <typename... KArgs, typename... Args>
 int launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
@@ -483,6 +489,7 @@ int launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 #include "dash_slices.cuh"
 #include "dash_stream.cuh"
 #include "dash_tma.cuh"
+#include "dash_tma32.cuh"
 #include "dash_slices_cta.cuh"
 #include "dash_slices3.cuh"
 #include "dash_big.cuh"
@@ -490,8 +497,8 @@ int launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 // ---------------------------------------------------------------------------
 // k_fgemm: F partial slot s = X[rows_s]^T (U o w)[rows_s], J-block of 64.
 // ---------------------------------------------------------------------------
-template <int RP>
-__global__ void __launch_bounds__(256) k_fgemm(const double *__restrict__ X, int64_t ldx, int64_t N, int J,
+template <int RP, typename TX>
+__global__ void __launch_bounds__(256) k_fgemm(const TX *__restrict__ X, int64_t ldx, int64_t N, int J,
                                                const double *__restrict__ U, const int32_t *__restrict__ row_slice,
                                                const int32_t *__restrict__ state_row, const double *__restrict__ W,
                                                int R, int64_t rows_per_split, double *__restrict__ F_slots) {
@@ -515,7 +522,7 @@ __global__ void __launch_bounds__(256) k_fgemm(const double *__restrict__ X, int
             int r = i / BJ, c = i % BJ;
             int64_t row = k0 + r;
             int col = j0 + c;
-            Xs[r * LDXS + c] = (row < rend && col < J) ? __ldg(X + row * ldx + col) : 0.0;
+            Xs[r * LDXS + c] = (row < rend && col < J) ? (double)__ldg(X + row * ldx + col) : 0.0;
         }
         for (int i = tid; i < BK * RP; i += 256) {
             int r = i / RP, c = i % RP;
@@ -769,7 +776,7 @@ struct dash_ctx {
         void *p = nullptr;
         size_t cap = 0;
     };
-    Buf xv, row_slice, items, gslots, fslots, vtv, fsnap, gsnap, fg, part, us, scratch, smeta, plan_hist;
+    Buf xv, row_slice, items, gslots, fslots, vtv, fsnap, gsnap, fg, part, us, scratch, smeta, plan_hist, u64;
     unsigned long long *err = nullptr;
     unsigned int *fallbacks = nullptr;
     int4 *items_host[2] = {nullptr, nullptr};
@@ -966,7 +973,8 @@ SlicePlan make_plan(const int64_t *row_ptr, int M, int RB, int R, int num_sms) {
 SlicePlan &plan_of(dash_ctx *ctx) { return *reinterpret_cast<SlicePlan *>(ctx->plan_p); }
 
 // device plan (R <= 16): meta[M] in plan order + plan_counts {nsmall, nbig}
-int device_plan(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b) {
+template <class B>
+int device_plan(dash_ctx *ctx, cudaStream_t st, const B *b) {
     const int M = b->M;
     const int nch = std::max(1, (M + kPlanChunk - 1) / kPlanChunk);
     // hist[B][nch] | off[B][nch] | tot[B] | counts[2]
@@ -1020,9 +1028,8 @@ int launch_plan(dash_ctx *ctx, cudaStream_t st, int RB, const SlicePlan &pl, Sli
     return 0;
 }
 
-template <int RP>
-void launch_xv_t(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, const double *V, int R,
-                 double *XV) {
+template <int RP, class B>
+void launch_xv_t(dash_ctx *ctx, cudaStream_t st, const B *b, int J, const double *V, int R, double *XV) {
     int64_t ntiles = (b->N + 63) / 64;
     int grid = (int)std::min<int64_t>(ntiles, (int64_t)ctx->num_sms * 8);
     if (grid < 1) grid = 1;
@@ -1030,8 +1037,8 @@ void launch_xv_t(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J,
     k_xv<RP><<<grid, 256, 0, st>>>(b->X, b->ldx, b->N, J, V, R, XV);
 }
 
-void launch_xv(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, const double *V, int R,
-               double *XV) {
+template <class B>
+void launch_xv(dash_ctx *ctx, cudaStream_t st, const B *b, int J, const double *V, int R, double *XV) {
     switch (rank_bucket(R) < 8 ? 8 : rank_bucket(R)) {
         case 8: launch_xv_t<8>(ctx, st, b, J, V, R, XV); break;
         case 16: launch_xv_t<16>(ctx, st, b, J, V, R, XV); break;
@@ -1040,15 +1047,16 @@ void launch_xv(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, c
     }
 }
 
-template <int RP>
-void launch_fgemm_t(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, const double *U,
+template <int RP, class B>
+void launch_fgemm_t(dash_ctx *ctx, cudaStream_t st, const B *b, int J, const double *U,
                     const int32_t *row_slice, const double *W, int R, int64_t rps, int nsplit, double *F_slots) {
     dim3 grid((J + 63) / 64, nsplit);
     PhaseScope ps(ctx, st, PH_FGEMM);
     k_fgemm<RP><<<grid, 256, 0, st>>>(b->X, b->ldx, b->N, J, U, row_slice, b->state_row, W, R, rps, F_slots);
 }
 
-void launch_fgemm(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, const double *U,
+template <class B>
+void launch_fgemm(dash_ctx *ctx, cudaStream_t st, const B *b, int J, const double *U,
                   const int32_t *row_slice, const double *W, int R, int64_t rps, int nsplit, double *F_slots) {
     switch (rank_bucket(R) < 8 ? 8 : rank_bucket(R)) {
         case 8: launch_fgemm_t<8>(ctx, st, b, J, U, row_slice, W, R, rps, nsplit, F_slots); break;
@@ -1141,6 +1149,59 @@ bool make_box_map(CUtensorMap *map, const double *base, int64_t cols, int64_t ro
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+bool make_box_map(CUtensorMap *map, const float *base, int64_t cols, int64_t rows, int64_t ld) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(float)};
+    cuuint32_t box[2] = {32, (cuuint32_t)kTR};
+    cuuint32_t es[2] = {1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool tma_ok(const dash_batch_f32 *b, int J, int R) {
+    const size_t lim = 220 * 1024;
+    return rank_bucket(R) == 16 && !(R & 1) && !(b->ldx & 3) && (reinterpret_cast<uintptr_t>(b->X) & 15) == 0 &&
+           b->N < (int64_t)1 << 31 && TmaSmem32::strips(J) <= 8 && TmaSmem32::xv_bytes(J) <= lim &&
+           TmaSmem32::f_bytes(J) <= lim && encode_fn() != nullptr;
+}
+
+int launch_xv3(dash_ctx *ctx, cudaStream_t st, const dash_batch_f32 *b, int J, const double *V, int R, double *XV,
+               const FusedPrologue &pro, bool pdl) {
+    CUtensorMap mx;
+    if (!make_box_map(&mx, b->X, J, b->N, b->ldx)) return DASH_E_CUDA;
+    const size_t smem = TmaSmem32::xv_bytes(J);
+    static size_t attr = 0;
+    if (attr < smem) {
+        cudaFuncSetAttribute(k_xv3f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = smem;
+    }
+    PhaseScope ps(ctx, st, PH_XV);
+    return launch_k(pdl && pdl_site("xv3f"), k_xv3f, ctx->num_sms, kCW * 32 + 32, smem, st, mx, b->N, J, V, R, XV, pro);
+}
+
+int launch_f3(dash_ctx *ctx, cudaStream_t st, const dash_batch_f32 *b, int J, const double *US, int R,
+              double *F_slots) {
+    CUtensorMap mx, mu;
+    if (!make_box_map(&mx, b->X, J, b->N, b->ldx) || !make_box_map(&mu, US, R, b->N, R)) return DASH_E_CUDA;
+    const size_t smem = TmaSmem32::f_bytes(J);
+    static size_t attr = 0;
+    if (attr < smem) {
+        cudaFuncSetAttribute(k_fgemm3f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = smem;
+    }
+    PhaseScope ps(ctx, st, PH_FGEMM);
+    return launch_k(pdl_site("f3f"), k_fgemm3f, ctx->num_sms, kCW * 32 + 32, smem, st, mx, mu, b->N, J, R, F_slots);
+}
+
+// U_new of the FP32 data mode: FP64 working copy -> caller's FP32 array
+__global__ void k_u_to_f32(const double *__restrict__ U, int64_t n, float *__restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (float)U[i];
+}
+
 bool tma_ok(const dash_batch_f64 *b, int J, int R) {
     const size_t lim = 220 * 1024;
     return rank_bucket(R) == 16 && !(R & 1) && !(b->ldx & 1) && (reinterpret_cast<uintptr_t>(b->X) & 15) == 0 &&
@@ -1218,6 +1279,135 @@ bool valid_state(const dash_state_f64 *s) {
 
 }  // namespace
 
+// One pass of the update (U / c / D / W for the batch's slices, F and G fresh
+// sums into fg_out).  B = dash_batch_f64 or dash_batch_f32 (the FP32 data
+// mode: X and U_out in FP32; the slice kernels then write an FP64 working U
+// that is rounded into U_out after the final pass).
+template <class B, typename TU>
+int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, TU *U_out, double *v_used_out,
+                    double eps, int32_t pass, double *fg_out) {
+    constexpr bool f32 = std::is_same<B, dash_batch_f32>::value;
+    static_assert(std::is_same<TU, typename std::conditional<f32, float, double>::type>::value, "U type");
+    if (!ctx || !b || !valid_state(s) || !U_out || !v_used_out || !fg_out) return DASH_E_ARG;
+    if (b->M < 0 || b->N < 0 || b->N > DASH_MAX_BATCH_ROWS || (b->N > 0 && b->ldx < s->J) || pass < 0 ||
+        pass >= s->passes)
+        return DASH_E_ARG;
+    const int J = s->J, R = s->R;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int RB = rank_bucket(R);
+    const int64_t N = b->N;
+    const int M = b->M;
+    const int last = pass == s->passes - 1;
+    static const bool host_timing = getenv("DASH_HOST_TIMING") != nullptr;
+    auto tnow = [] { return std::chrono::steady_clock::now(); };
+    auto t0 = tnow();
+    if (pass == 0) {
+        ctx->last_launches = 0;
+        if (!ctx->plan_p) ctx->plan_p = new SlicePlan();
+        plan_of(ctx) = make_plan(b->row_ptr_host, M, RB, R, ctx->num_sms);
+        if (host_timing) fprintf(stderr, "[dash host] plan %.1f us\n", std::chrono::duration<double, std::micro>(tnow() - t0).count());
+        ctx->nitems = plan_of(ctx).nslots;
+        const std::vector<int4> &items = plan_of(ctx).items;
+        if constexpr (f32) {  // FP32 X: tensor-map path, else the generic GEMMs (no row-copy ring)
+            ctx->tma = N > 0 && tma_ok(b, J, R);
+            ctx->stream = ctx->tma;
+        } else {
+            ctx->stream = stream_ok(J, b->ldx, R) && N > 0;
+        }
+        plan_fsplit(ctx, N, J, ctx->nsplit, ctx->rps);
+        if (ctx->stream) ctx->nsplit = ctx->num_sms * (f32 ? TmaSmem32::row_groups(J) : 1);
+        if constexpr (!f32) ctx->tma = ctx->stream && tma_ok(b, J, R);
+        if (ensure(ctx->xv, sizeof(double) * std::max<int64_t>(N, 1) * R) ||
+            ensure(ctx->row_slice, sizeof(int32_t) * std::max<int64_t>(N, 1)) ||
+            ensure(ctx->gslots, sizeof(double) * std::max(ctx->nitems, 1) * R * R) ||
+            ensure(ctx->fslots, sizeof(double) * ctx->nsplit * J * R) || ensure(ctx->vtv, sizeof(double) * R * R) ||
+            ensure(ctx->fsnap, sizeof(double) * J * R) || ensure(ctx->gsnap, sizeof(double) * R * R) ||
+            (ctx->stream && ensure(ctx->us, sizeof(double) * std::max<int64_t>(N, 1) * R)) ||
+            (f32 && ensure(ctx->u64, sizeof(double) * std::max<int64_t>(N, 1) * R)))
+            return DASH_E_CUDA;
+        if (!items.empty() && stage_items(ctx, st, items)) return DASH_E_CUDA;
+        if (plan_of(ctx).split && M > 0 && N > 0 && device_plan(ctx, st, b)) return DASH_E_CUDA;
+        if (M > 0 && !ctx->stream) {  // row -> slice map: only the generic F GEMM needs it
+            PhaseScope ps(ctx, st, PH_ROWSLICE);
+            k_row_slice<<<std::min(ctx->num_sms * 4, (M + 7) / 8 + 1), 256, 0, st>>>(b->row_ptr, M,
+                                                                                    (int32_t *)ctx->row_slice.p);
+        }
+    }
+    double *XV = (double *)ctx->xv.p;
+    double *Ud = f32 ? (double *)ctx->u64.p : (double *)(void *)U_out;  // U written by the slice kernels
+    double *Fsl = (double *)ctx->fslots.p, *Gsl = (double *)ctx->gslots.p;
+    const bool fused_pro = ctx->tma && N > 0;  // k_xv3 runs the prologue itself
+    if (!fused_pro) {
+        PhaseScope ps(ctx, st, PH_PROLOGUE);
+        k_prologue<<<1 + std::max(1, std::min(16, (J * R + 255) / 256)), 256, 0, st>>>(
+            s->V, J, R, (double *)ctx->vtv.p, s->F, s->G, (double *)ctx->fsnap.p,
+                                      (double *)ctx->gsnap.p, v_used_out, pass == 0, last);
+    }
+    if (N > 0) {
+        if (ctx->tma) {
+            const FusedPrologue pro{(double *)ctx->vtv.p, s->F, s->G, (double *)ctx->fsnap.p, (double *)ctx->gsnap.p,
+                                    v_used_out, pass == 0, last};
+            // PDL only behind the plan kernels (pass 0); a later pass follows the V solve
+            if (launch_xv3(ctx, st, b, J, s->V, R, XV, pro, pass == 0)) return DASH_E_CUDA;
+        } else if (ctx->stream) {
+            if constexpr (!f32) {
+                if (rank_bucket(R) <= 8) launch_xv2_t<8>(ctx, st, b, J, s->V, R, XV);
+                else launch_xv2_t<16>(ctx, st, b, J, s->V, R, XV);
+            }
+        } else {
+            launch_xv(ctx, st, b, J, s->V, R, XV);
+        }
+        SliceParams sp;
+        sp.items = (const int4 *)ctx->items.p;
+        sp.row_ptr = b->row_ptr;
+        sp.state_row = b->state_row;
+        sp.is_new = b->is_new;
+        sp.XV = XV;
+        sp.U = Ud;
+        sp.US = ctx->stream ? (double *)ctx->us.p : nullptr;
+        sp.W = s->W;
+        sp.C = s->C;
+        sp.D = s->D;
+        sp.vtv = (const double *)ctx->vtv.p;
+        sp.G_slots = Gsl;
+        sp.err = ctx->err;
+        sp.fallbacks = ctx->fallbacks;
+        sp.R = R;
+        sp.lam = s->forgetting;
+        sp.eps = eps;
+        sp.pass = pass;
+        sp.final_pass = last;
+        if (launch_plan(ctx, st, RB, plan_of(ctx), sp, M)) return DASH_E_CUDA;
+        if (ctx->tma) {
+            if (launch_f3(ctx, st, b, J, (const double *)ctx->us.p, R, Fsl)) return DASH_E_CUDA;
+        } else if (ctx->stream) {
+            if constexpr (!f32) {
+                if (rank_bucket(R) <= 8) launch_f2_t<8>(ctx, st, b, J, (const double *)ctx->us.p, R, Fsl);
+                else launch_f2_t<16>(ctx, st, b, J, (const double *)ctx->us.p, R, Fsl);
+            }
+        } else {
+            launch_fgemm(ctx, st, b, J, Ud, (const int32_t *)ctx->row_slice.p, s->W, R, ctx->rps,
+                         (int)ctx->nsplit, Fsl);
+        }
+    }
+    if constexpr (f32) {
+        if (last && N > 0) {
+            const int64_t n = N * R;
+            k_u_to_f32<<<(int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->num_sms * 8), 256, 0, st>>>(
+                Ud, n, (float *)U_out);
+            ctx->last_launches++;
+        }
+    }
+    if (host_timing) fprintf(stderr, "[dash host] pass_begin total %.1f us\n", std::chrono::duration<double, std::micro>(tnow() - t0).count());
+    {
+        PhaseScope ps(ctx, st, PH_SUMFG);
+        if (colsum2(ctx, st, Fsl, N > 0 ? (int)ctx->nsplit : 0, (int64_t)J * R, fg_out, Gsl,
+                    N > 0 ? ctx->nitems : 0, (int64_t)R * R, fg_out + (int64_t)J * R))
+            return DASH_E_CUDA;
+    }
+    return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_E_CUDA;
+}
+
 extern "C" {
 
 int dash_ctx_create(dash_ctx **out) {
@@ -1244,7 +1434,7 @@ void dash_ctx_destroy(dash_ctx *ctx) {
     cudaDeviceSynchronize();
     dash_ctx::Buf *bufs[] = {&ctx->xv,  &ctx->row_slice, &ctx->items, &ctx->gslots, &ctx->fslots,
                              &ctx->vtv, &ctx->fsnap,     &ctx->gsnap, &ctx->fg,     &ctx->part, &ctx->us, &ctx->scratch,
-                             &ctx->smeta, &ctx->plan_hist};
+                             &ctx->smeta, &ctx->plan_hist, &ctx->u64};
     for (auto *b : bufs)
         if (b->p) cudaFree(b->p);
     cudaFree(ctx->err);
@@ -1325,105 +1515,12 @@ int dash_ctx_phase_ms(dash_ctx *ctx, double *ms_out, int32_t *count_out, int32_t
 
 int dash_update_pass_begin_f64(dash_ctx *ctx, void *stream, const dash_batch_f64 *b, dash_state_f64 *s,
                                double *U_out, double *v_used_out, double eps, int32_t pass, double *fg_out) {
-    if (!ctx || !b || !valid_state(s) || !U_out || !v_used_out || !fg_out) return DASH_E_ARG;
-    if (b->M < 0 || b->N < 0 || b->N > DASH_MAX_BATCH_ROWS || (b->N > 0 && b->ldx < s->J) || pass < 0 ||
-        pass >= s->passes)
-        return DASH_E_ARG;
-    const int J = s->J, R = s->R;
-    cudaStream_t st = (cudaStream_t)stream;
-    const int RB = rank_bucket(R);
-    const int64_t N = b->N;
-    const int M = b->M;
-    const int last = pass == s->passes - 1;
-    static const bool host_timing = getenv("DASH_HOST_TIMING") != nullptr;
-    auto tnow = [] { return std::chrono::steady_clock::now(); };
-    auto t0 = tnow();
-    if (pass == 0) {
-        ctx->last_launches = 0;
-        if (!ctx->plan_p) ctx->plan_p = new SlicePlan();
-        plan_of(ctx) = make_plan(b->row_ptr_host, M, RB, R, ctx->num_sms);
-        if (host_timing) fprintf(stderr, "[dash host] plan %.1f us\n", std::chrono::duration<double, std::micro>(tnow() - t0).count());
-        ctx->nitems = plan_of(ctx).nslots;
-        const std::vector<int4> &items = plan_of(ctx).items;
-        ctx->stream = stream_ok(J, b->ldx, R) && N > 0;
-        plan_fsplit(ctx, N, J, ctx->nsplit, ctx->rps);
-        if (ctx->stream) ctx->nsplit = ctx->num_sms;
-        ctx->tma = ctx->stream && tma_ok(b, J, R);
-        if (ensure(ctx->xv, sizeof(double) * std::max<int64_t>(N, 1) * R) ||
-            ensure(ctx->row_slice, sizeof(int32_t) * std::max<int64_t>(N, 1)) ||
-            ensure(ctx->gslots, sizeof(double) * std::max(ctx->nitems, 1) * R * R) ||
-            ensure(ctx->fslots, sizeof(double) * ctx->nsplit * J * R) || ensure(ctx->vtv, sizeof(double) * R * R) ||
-            ensure(ctx->fsnap, sizeof(double) * J * R) || ensure(ctx->gsnap, sizeof(double) * R * R) ||
-            (ctx->stream && ensure(ctx->us, sizeof(double) * std::max<int64_t>(N, 1) * R)))
-            return DASH_E_CUDA;
-        if (!items.empty() && stage_items(ctx, st, items)) return DASH_E_CUDA;
-        if (plan_of(ctx).split && M > 0 && N > 0 && device_plan(ctx, st, b)) return DASH_E_CUDA;
-        if (M > 0 && !ctx->stream) {  // row -> slice map: only the generic F GEMM needs it
-            PhaseScope ps(ctx, st, PH_ROWSLICE);
-            k_row_slice<<<std::min(ctx->num_sms * 4, (M + 7) / 8 + 1), 256, 0, st>>>(b->row_ptr, M,
-                                                                                    (int32_t *)ctx->row_slice.p);
-        }
-    }
-    double *XV = (double *)ctx->xv.p;
-    double *Fsl = (double *)ctx->fslots.p, *Gsl = (double *)ctx->gslots.p;
-    const bool fused_pro = ctx->tma && N > 0;  // k_xv3 runs the prologue itself
-    if (!fused_pro) {
-        PhaseScope ps(ctx, st, PH_PROLOGUE);
-        k_prologue<<<1 + std::max(1, std::min(16, (J * R + 255) / 256)), 256, 0, st>>>(
-            s->V, J, R, (double *)ctx->vtv.p, s->F, s->G, (double *)ctx->fsnap.p,
-                                      (double *)ctx->gsnap.p, v_used_out, pass == 0, last);
-    }
-    if (N > 0) {
-        if (ctx->tma) {
-            const FusedPrologue pro{(double *)ctx->vtv.p, s->F, s->G, (double *)ctx->fsnap.p, (double *)ctx->gsnap.p,
-                                    v_used_out, pass == 0, last};
-            // PDL only behind the plan kernels (pass 0); a later pass follows the V solve
-            if (launch_xv3(ctx, st, b, J, s->V, R, XV, pro, pass == 0)) return DASH_E_CUDA;
-        } else if (ctx->stream) {
-            if (rank_bucket(R) <= 8) launch_xv2_t<8>(ctx, st, b, J, s->V, R, XV);
-            else launch_xv2_t<16>(ctx, st, b, J, s->V, R, XV);
-        } else {
-            launch_xv(ctx, st, b, J, s->V, R, XV);
-        }
-        SliceParams sp;
-        sp.items = (const int4 *)ctx->items.p;
-        sp.row_ptr = b->row_ptr;
-        sp.state_row = b->state_row;
-        sp.is_new = b->is_new;
-        sp.XV = XV;
-        sp.U = U_out;
-        sp.US = ctx->stream ? (double *)ctx->us.p : nullptr;
-        sp.W = s->W;
-        sp.C = s->C;
-        sp.D = s->D;
-        sp.vtv = (const double *)ctx->vtv.p;
-        sp.G_slots = Gsl;
-        sp.err = ctx->err;
-        sp.fallbacks = ctx->fallbacks;
-        sp.R = R;
-        sp.lam = s->forgetting;
-        sp.eps = eps;
-        sp.pass = pass;
-        sp.final_pass = last;
-        if (launch_plan(ctx, st, RB, plan_of(ctx), sp, M)) return DASH_E_CUDA;
-        if (ctx->tma) {
-            if (launch_f3(ctx, st, b, J, (const double *)ctx->us.p, R, Fsl)) return DASH_E_CUDA;
-        } else if (ctx->stream) {
-            if (rank_bucket(R) <= 8) launch_f2_t<8>(ctx, st, b, J, (const double *)ctx->us.p, R, Fsl);
-            else launch_f2_t<16>(ctx, st, b, J, (const double *)ctx->us.p, R, Fsl);
-        } else {
-            launch_fgemm(ctx, st, b, J, U_out, (const int32_t *)ctx->row_slice.p, s->W, R, ctx->rps,
-                         (int)ctx->nsplit, Fsl);
-        }
-    }
-    if (host_timing) fprintf(stderr, "[dash host] pass_begin total %.1f us\n", std::chrono::duration<double, std::micro>(tnow() - t0).count());
-    {
-        PhaseScope ps(ctx, st, PH_SUMFG);
-        if (colsum2(ctx, st, Fsl, N > 0 ? (int)ctx->nsplit : 0, (int64_t)J * R, fg_out, Gsl,
-                    N > 0 ? ctx->nitems : 0, (int64_t)R * R, fg_out + (int64_t)J * R))
-            return DASH_E_CUDA;
-    }
-    return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_E_CUDA;
+    return pass_begin_impl(ctx, stream, b, s, U_out, v_used_out, eps, pass, fg_out);
+}
+
+int dash_update_pass_begin_f32(dash_ctx *ctx, void *stream, const dash_batch_f32 *b, dash_state_f64 *s,
+                               float *U_out, double *v_used_out, double eps, int32_t pass, double *fg_out) {
+    return pass_begin_impl(ctx, stream, b, s, U_out, v_used_out, eps, pass, fg_out);
 }
 
 int dash_update_pass_finish_f64(dash_ctx *ctx, void *stream, dash_state_f64 *s, const double *fg, double eps) {
@@ -1455,6 +1552,20 @@ int dash_update_f64(dash_ctx *ctx, void *stream, const dash_batch_f64 *b, dash_s
     double *fg = (double *)ctx->fg.p;
     for (int pass = 0; pass < s->passes; ++pass) {
         int rc = dash_update_pass_begin_f64(ctx, stream, b, s, U_out, v_used_out, eps, pass, fg);
+        if (rc) return rc;
+        rc = dash_update_pass_finish_f64(ctx, stream, s, fg, eps);
+        if (rc) return rc;
+    }
+    return DASH_OK;
+}
+
+int dash_update_f32(dash_ctx *ctx, void *stream, const dash_batch_f32 *b, dash_state_f64 *s, float *U_out,
+                    double *v_used_out, double eps) {
+    if (!ctx || !valid_state(s)) return DASH_E_ARG;
+    if (ensure(ctx->fg, sizeof(double) * ((size_t)s->J * s->R + s->R * s->R))) return DASH_E_CUDA;
+    double *fg = (double *)ctx->fg.p;
+    for (int pass = 0; pass < s->passes; ++pass) {
+        int rc = dash_update_pass_begin_f32(ctx, stream, b, s, U_out, v_used_out, eps, pass, fg);
         if (rc) return rc;
         rc = dash_update_pass_finish_f64(ctx, stream, s, fg, eps);
         if (rc) return rc;

@@ -24,10 +24,11 @@ def local_error(batch_items, u_new, state):
         counts = np.array([np.asarray(r).shape[0] for _, r in batch_items], dtype=np.int64)
         row_ptr = np.zeros(len(ids) + 1, dtype=np.int64)
         np.cumsum(counts, out=row_ptr[1:])
+        dt = getattr(state, "dtype", torch.float64)
         X = torch.as_tensor(np.concatenate([np.asarray(r, dtype=float) for _, r in batch_items]),
-                            device=dev)
+                            device=dev).to(dt)
         U = torch.as_tensor(np.concatenate([np.asarray(u_new[s], dtype=float) for s in ids]),
-                            device=dev)
+                            device=dev).to(dt)
         state_row = np.array([state.row_of(s) for s in ids], dtype=np.int32)
         N = int(row_ptr[-1])
     slice_err, te = local_error_device(X, N, row_ptr, state_row, U, state)
@@ -47,9 +48,12 @@ def local_error_device(X, N, row_ptr, state_row, U, state):
                       row_ptr_host=np.asarray(row_ptr, dtype=np.int64).ctypes.data,
                       state_row=int(sr.data_ptr()), is_new=0)
     W = state.device_tensors["W"]
-    nat.check(nat.lib().dash_local_error_f64(state._ctx, nat.stream_ptr(), ctypes.byref(b),
-                                             int(U.data_ptr()), int(W.data_ptr()),
-                                             int(state._V.data_ptr()), state.J, state.rank,
-                                             int(slice_err.data_ptr()), int(te.data_ptr())),
-              "dash_local_error_f64")
+    if X.dtype != U.dtype or X.dtype not in (torch.float32, torch.float64):
+        raise TypeError("local_error: X and U must both be float64 or both float32")
+    fn = nat.lib().dash_local_error_f32 if X.dtype == torch.float32 else nat.lib().dash_local_error_f64
+    nat.check(fn(state._ctx, nat.stream_ptr(), ctypes.byref(b),
+                 int(U.data_ptr()), int(W.data_ptr()),
+                 int(state._V.data_ptr()), state.J, state.rank,
+                 int(slice_err.data_ptr()), int(te.data_ptr())),
+              "dash_local_error")
     return slice_err[:M], te

@@ -16,6 +16,12 @@ Layout in HBM (torch owns every buffer; the C ABI only sees pointers):
                                              every update, fed from a pinned
                                              host buffer
 
+FP32 data mode (``dtype=torch.float32``, north_star's optional FP32 mode):
+the streamed data -- the staged batch X and the returned U_new blocks -- are
+single precision (half the PCIe and HBM bytes); the per-slice state, the
+factors and every product / sum inside the kernels stay FP64
+(``dash_update_f32``).
+
 ``update(batch)`` validates ids on the host, registers new slices, packs the
 batch into CSR (rows in ``batch.items()`` order), and launches the whole pass
 loop through ``dash_update_f64``.  It then synchronises once to turn a device
@@ -146,12 +152,13 @@ class StreamState:
     (stream.py:184-247).  Exclusively owned during an update."""
 
     def __init__(self, slice_ids, u_blocks, W, V, C, D, F, G, forgetting,
-                 update_index: int = 0, passes: int = 1, device=None):
+                 update_index: int = 0, passes: int = 1, device=None, dtype=F64):
         if not 0.0 < forgetting <= 1.0:
             raise ValueError("forgetting factor must lie in (0, 1]")
         if passes < 1:
             raise ValueError("passes must be at least 1")
         self.device = _dev(device)
+        self.dtype = torch.float32 if dtype in (torch.float32, np.float32, "float32", "fp32") else F64
         self.forgetting = float(forgetting)
         self.update_index = int(update_index)
         self.passes = int(passes)
@@ -207,7 +214,7 @@ class StreamState:
                 self._ublk[sid].append((bi, lo, hi))
 
     @classmethod
-    def from_arrays(cls, arrays: dict, device=None, u_blocks=None) -> "StreamState":
+    def from_arrays(cls, arrays: dict, device=None, u_blocks=None, dtype=F64) -> "StreamState":
         """Build from a dict with slice_ids, W, V, C, D, F, G, forgetting
         (e.g. ``workloads.planted_state``); U history starts empty unless
         ``u_blocks`` is given."""
@@ -216,7 +223,7 @@ class StreamState:
             u_blocks = {sid: [np.zeros((0, R))] for sid in arrays["slice_ids"]}
         return cls(arrays["slice_ids"], u_blocks, arrays["W"], arrays["V"], arrays["C"],
                    arrays["D"], arrays["F"], arrays["G"], arrays["forgetting"],
-                   passes=arrays.get("passes", 1), device=device)
+                   passes=arrays.get("passes", 1), device=device, dtype=dtype)
 
     # -- reference attribute API --------------------------------------------
     @property
@@ -342,10 +349,10 @@ class StreamState:
         J = self.J
         if self._X is None or self._X.shape[0] < N:
             cap = max(N, 1024, int(N * 1.25))
-            self._X = torch.empty((cap, J), dtype=F64, device=self.device)
+            self._X = torch.empty((cap, J), dtype=self.dtype, device=self.device)
         if self._Xpin is None or self._Xpin.shape[0] < N:
             cap = max(N, 1024, int(N * 1.25))
-            self._Xpin = torch.empty((cap, J), dtype=F64, pin_memory=True)
+            self._Xpin = torch.empty((cap, J), dtype=self.dtype, pin_memory=True)
             self._pin_event = None
         if self._pin_event is not None:
             self._pin_event.synchronize()  # previous H2D from the staging buffer is done
@@ -417,8 +424,8 @@ class StreamState:
 
     def update_packed(self, X: torch.Tensor, counts: np.ndarray, existing_rows: np.ndarray,
                       new_ids: list, check: bool = False, allreduce=None):
-        """Device-resident fast path: ``X`` (N, J) already on this GPU in
-        batch order -- existing slices (state rows ``existing_rows``) then the
+        """Device-resident fast path: ``X`` (N, J) already on this GPU (in the
+        state's dtype) in batch order -- existing slices (state rows ``existing_rows``) then the
         ``len(new_ids)`` new slices; ``counts`` their row counts.  No host sync
         unless ``check``.  Returns (U_new (N, R), v_used (J, R)) device tensors."""
         M_old = len(existing_rows)
@@ -447,8 +454,11 @@ class StreamState:
     def _run(self, X, N, row_ptr, state_row, is_new, check, ids, allreduce=None):
         dev = self.device
         M = len(state_row)
+        if N and X.dtype != self.dtype:
+            raise TypeError(f"batch X is {X.dtype}, the stream state runs in {self.dtype}")
+        f32 = self.dtype == torch.float32
         rp_d, sr_d, nw_d = self._stage_meta(row_ptr, state_row, is_new)
-        U = torch.empty((max(N, 0), self._R), dtype=F64, device=dev)
+        U = torch.empty((max(N, 0), self._R), dtype=self.dtype, device=dev)
         v_used = torch.empty((self.J, self._R), dtype=F64, device=dev)
         b = nat.DashBatch(X=_ptr(X), ldx=int(X.stride(0)) if N else self.J, N=N, M=M,
                           row_ptr=_ptr(rp_d), row_ptr_host=row_ptr.ctypes.data,
@@ -458,16 +468,17 @@ class StreamState:
                           forgetting=self.forgetting, passes=self.passes)
         L = nat.lib()
         st = nat.stream_ptr()
+        upd = L.dash_update_f32 if f32 else L.dash_update_f64
+        begin = L.dash_update_pass_begin_f32 if f32 else L.dash_update_pass_begin_f64
         if allreduce is None:
-            nat.check(L.dash_update_f64(self._ctx, st, ctypes.byref(b), ctypes.byref(s), _ptr(U),
-                                        _ptr(v_used), RIDGE_EPS), "dash_update_f64")
+            nat.check(upd(self._ctx, st, ctypes.byref(b), ctypes.byref(s), _ptr(U), _ptr(v_used), RIDGE_EPS),
+                      "dash_update_f32" if f32 else "dash_update_f64")
         else:
             # sharded: per pass, local fresh sums -> all-reduce -> replicated finish
             fg = torch.empty(self.J * self._R + self._R * self._R, dtype=F64, device=dev)
             for p in range(self.passes):
-                nat.check(L.dash_update_pass_begin_f64(self._ctx, st, ctypes.byref(b), ctypes.byref(s),
-                                                       _ptr(U), _ptr(v_used), RIDGE_EPS, p, _ptr(fg)),
-                          "dash_update_pass_begin_f64")
+                nat.check(begin(self._ctx, st, ctypes.byref(b), ctypes.byref(s),
+                                _ptr(U), _ptr(v_used), RIDGE_EPS, p, _ptr(fg)), "dash_update_pass_begin")
                 allreduce(fg)
                 nat.check(L.dash_update_pass_finish_f64(self._ctx, st, ctypes.byref(s), _ptr(fg),
                                                         RIDGE_EPS), "dash_update_pass_finish_f64")
@@ -552,7 +563,8 @@ class HostPipeline:
         dev = _dev(device)
         self.device = dev
         self.depth = depth
-        self.bufs = [torch.empty((max(int(max_rows), 1), J), dtype=F64, device=dev) for _ in range(depth)]
+        dt = getattr(engine, "dtype", F64)
+        self.bufs = [torch.empty((max(int(max_rows), 1), J), dtype=dt, device=dev) for _ in range(depth)]
         self.h2d = torch.cuda.Stream(dev)
         self.d2h = torch.cuda.Stream(dev)
         self._free = [None] * depth
@@ -652,8 +664,10 @@ def init_helpers_packed(X, row_ptr, U, W, V):
 
 
 def initialize(tensor: IrregularTensor, rank: int, iters: int = 10, seed: int = 0,
-               forgetting: float = 0.7, passes: int = 1, device=None):
-    """stream.py:383-407: parafac2_als fit, init_helpers, wrap as stream state."""
+               forgetting: float = 0.7, passes: int = 1, device=None, dtype=F64):
+    """stream.py:383-407: parafac2_als fit, init_helpers, wrap as stream state.
+    ``dtype=torch.float32`` selects the FP32 data mode for the updates (the
+    initial fit itself is FP64)."""
     from .als import parafac2_als
     dev = _dev(device)
     factors, info = parafac2_als(tensor, rank, iters=iters, seed=seed, return_info=True, device=dev)
@@ -662,5 +676,5 @@ def initialize(tensor: IrregularTensor, rank: int, iters: int = 10, seed: int = 
         slice_ids=list(factors.slice_ids),
         u_blocks={sid: [factors.U[sid]] for sid in factors.slice_ids},
         W=factors.W, V=factors.V, C=C, D=D, F=F, G=G,
-        forgetting=forgetting, update_index=0, passes=passes, device=dev,
+        forgetting=forgetting, update_index=0, passes=passes, device=dev, dtype=dtype,
     ), info
