@@ -1,0 +1,518 @@
+// Fused big-slice path (R bucket 16, FP64, TMA): the rows of BIG slices
+// (> kSmallRows rows) are read from HBM ONCE.  The old path read them three
+// times (X in the XV GEMM, XV in k_big, X again in the F GEMM) plus wrote and
+// re-read XV / U o w.  Here, per 32-row tile of a big slice:
+//
+//   XV   = X V                   (DMMA, X as swizzled TMA boxes)
+//   U    = XV Ms^T               (DMMA; Ms = A^{-1} diag(s) of the slice)  -> U_out
+//   c   += diag(XV^T U)          (fragment FMAs)
+//   gram+= U^T U                 (DMMA)
+//   P   += X^T XV                (DMMA, J x R, X still in shared memory)
+//
+// and the slice's F contribution X^T (U o w) = P Ms^T diag(w) is formed once
+// w is known (stream.py:321 with the row sum reassociated; differences are
+// rounding-level).  Three kernels:
+//
+//   k_bigx_pre   one warp per big slice: the A system by the symmetric sweep
+//                (LU fallback) -> Ms (global); zeroes U o w on the slice's
+//                partial boundary tiles (the small-row F GEMM may read those
+//                tiles); block 0 scans the slices' tile counts -> toff[].
+//   k_bigx       persistent, one CTA per SM, warp-specialised (producer warp +
+//                8 DMMA warps, mbarrier ring): the big slices' tiles, in plan
+//                order, are split EVENLY over the CTAs (a slice may span CTAs);
+//                each (slice, CTA) segment writes its partial P, gram, c to
+//                parts[slice + CTA] (unique: slices and CTAs are both ordered).
+//   k_bigx_post  one CTA per big slice: segment partials summed in CTA order
+//                (deterministic), D = lam D + gram, the S-row system (Gauss-
+//                Jordan, LU fallback) -> w; W / C / D rows; G slot gram o w w^T;
+//                F slot P Ms^T diag(w).
+//
+// (included inside dash_update.cu's anonymous namespace, after dash_big.cuh)
+#pragma once
+
+constexpr int kBxRB = 16;           // rank bucket
+constexpr int kBxMP = kBxRB + 4;    // Ms pitch (B-frag reads)
+constexpr int kBxUP = kBxRB + 8;    // U tile pitch (gram frags conflict-free)
+
+struct BigxSmem {
+    static __host__ __device__ int strips(int J) { return (J + 15) / 16; }
+    static __host__ __device__ int stages(int J) { return strips(J) <= 8 ? 3 : 2; }
+    static __host__ __device__ int vtp(int J) { return strips(J) * 16 + 8; }
+    static __host__ __device__ size_t stage_doubles(int J) { return (size_t)strips(J) * 512; }
+    // [stages x JS boxes] | vt[16 x VTP] | xvs[32 x 16 swz] | us[32 x UP] | ms[16 x MP] | red[8 x 16] | bars
+    static __host__ __device__ size_t bytes(int J) {
+        return 1024 + sizeof(double) * (stages(J) * stage_doubles(J) + 16 * (size_t)vtp(J) + 512 + 32 * kBxUP +
+                                         16 * kBxMP + 128) +
+               16 * 4;
+    }
+    // partial slot of one (slice, CTA) segment: P[J x 16] | gram[2][16 x 16] | c[4][16]
+    static __host__ __device__ int64_t part_doubles(int J) { return (int64_t)J * 16 + 512 + 64; }
+};
+
+// element (row, col) of a 32 x 16 swizzled double tile (16-byte chunk c at c ^ (row & 7))
+__device__ __forceinline__ int swz_e(int row, int col) { return swz(row, col >> 1) + (col & 1); }
+
+// CTA c of G owns tiles [tile_start(c), tile_start(c + 1)) of the T big-slice tiles
+__host__ __device__ __forceinline__ int64_t tile_start(int64_t c, int64_t T, int64_t G) {
+    const int64_t base = T / G, rem = T % G;
+    return c * base + (c < rem ? c : rem);
+}
+__device__ __forceinline__ int64_t cta_of_tile(int64_t tau, int64_t T, int64_t G) {
+    const int64_t base = T / G, rem = T % G;
+    const int64_t split = rem * (base + 1);
+    return tau < split ? tau / (base + 1) : rem + (tau - split) / base;
+}
+
+struct BigxParams {
+    const int4 *meta;         // device plan: big slice bi at meta[nsmall + bi]
+    const int *plan_counts;   // {nsmall, nbig}
+    const double *V;          // J x R
+    const double *vtv;        // R x R (written by the XV kernel)
+    const double *W, *C;      // state (read)
+    double *Wo, *Co, *D;      // state (written by post)
+    double *U, *US;           // U_out; U o w workspace (boundary rows zeroed)
+    double *ms;               // nbig x 16 x kBxMP: Ms per big slice
+    int *toff;                // nbig + 1: tile offsets in plan order
+    double *parts;            // (nbig + G) x part_doubles
+    double *F_slots;          // post: one J x R slot per big slice
+    double *G_slots;          // post: one R x R slot per big slice
+    unsigned long long *err;
+    unsigned int *fallbacks;
+    int64_t N, T;             // rows in the batch; big-slice tiles
+    int J, R, G;              // G = k_bigx grid
+    double lam, eps;
+    int pass, final_pass;
+};
+
+// ---------------------------------------------------------------------------
+// k_bigx_pre: block 0 = tile scan; blocks >= 1: one warp per big slice (A system)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_bigx_pre(BigxParams p) {
+    constexpr int RB = kBxRB, LDV = RB + 2, LDL = RB + 1;
+    __shared__ double vtv_s[RB * LDV];
+    __shared__ __align__(16) double wbuf[8][2 * RB + RB * LDL + RB];  // gather bufs (2) | lu | s
+    __shared__ int wpiv[8][RB];
+    // launched behind the small-slice kernel, which triggered only after its
+    // own pdl_wait: the XV kernel's vtv and the plan are complete and visible.
+    pdl_trigger();
+    const int lane = lane_id(), w = warp_id();
+    const int nsmall = __ldcg(p.plan_counts), nbig = __ldcg(p.plan_counts + 1);
+    const int R = p.R;
+    if (blockIdx.x == 0) {
+        if (w == 0) {  // toff = exclusive scan of ceil(n / 32) in plan order
+            int run = 0;
+            for (int b0 = 0; b0 < nbig; b0 += 32) {
+                const int bi = b0 + lane;
+                const int nt = bi < nbig ? (int)((__ldcg(&p.meta[nsmall + bi].y) + kTR - 1) / kTR) : 0;
+                int inc = nt;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int u = __shfl_up_sync(FULL_MASK, inc, d);
+                    if (lane >= d) inc += u;
+                }
+                if (bi < nbig) p.toff[bi] = run + inc - nt;
+                run += __shfl_sync(FULL_MASK, inc, 31);
+            }
+            if (lane == 0) p.toff[nbig] = run;
+        }
+        pdl_wait();
+        return;
+    }
+    for (int i = threadIdx.x; i < RB * LDV; i += blockDim.x) {
+        const int a = i / LDV, b = i % LDV;
+        vtv_s[i] = (a < R && b < R) ? __ldcg(p.vtv + a * R + b) : 0.0;
+    }
+    __syncthreads();
+    const int bi = (blockIdx.x - 1) * 8 + w;
+    if (bi < nbig) {
+        const int4 mt = __ldcg(p.meta + nsmall + bi);
+        const int m = mt.w;
+        const int64_t r0 = mt.x, n = mt.y;
+        const int wrow = mt.z & 0x7fffffff;
+        const bool fresh = mt.z < 0;
+        double *buf = wbuf[w];
+        double *lu = buf + 2 * RB;
+        double *svec = lu + RB * LDL;
+        const int r = lane % RB;
+        const bool real = lane < RB && r < R;
+        if (lane < RB) svec[lane] = real ? ((fresh && p.pass == 0) ? 1.0 : __ldcg(p.W + (int64_t)wrow * R + r)) : 0.0;
+        __syncwarp();
+        const double s_r = real ? svec[r] : 0.0;
+        double sh = 0.0;
+#pragma unroll
+        for (int z = 0; z < RB; ++z)
+            if (z < R) sh += vtv_s[z * LDV + z] * svec[z] * svec[z];
+        sh = p.eps * sh / R;
+        const double dg = real ? sh : 1.0;
+        const double *vrow = vtv_s + r * LDV;
+        double a2[RB];
+#pragma unroll
+        for (int z = 0; z < RB; ++z) a2[z] = (lane < RB ? vrow[z] * s_r * svec[z] : 0.0) + ((z == r) ? dg : 0.0);
+        // lanes 0..15 sweep A; lanes 16..31 sweep a harmless identity (own gather buffer)
+        const bool okA = sweep_inverse<RB>(a2, lane < RB ? buf : buf + RB, r);
+        const unsigned badA = __ballot_sync(FULL_MASK, !okA) & 0xffffu;
+        if (badA) {
+            const bool need = lane < RB;
+#pragma unroll
+            for (int z = 0; z < RB; ++z)
+                if (need) a2[z] = vrow[z] * s_r * svec[z] + ((z == r) ? dg : 0.0);
+            if (lane == 0) atomicAdd(p.fallbacks, 1u);
+            const bool okLU = lu_fallback<RB>(a2, lu, wpiv[w], r, R, need);
+            if (lane == 0 && !okLU) report_error(p.err, m, DASH_E_SINGULAR);
+        }
+        // Ms[n][k] = A^{-1}[n][k] s_k  (a2 holds -A^{-1}), so U = XV Ms^T
+        if (lane < RB) {
+            double *msr = p.ms + (int64_t)bi * RB * kBxMP + r * kBxMP;
+#pragma unroll
+            for (int z = 0; z < RB; ++z) msr[z] = (r < R && z < R) ? -a2[z] * svec[z] : 0.0;
+        }
+        // U o w rows of the partial boundary tiles (the small-row F GEMM may read them)
+        if (p.US != nullptr) {
+            const int64_t e0 = min(r0 + n, (r0 + kTR - 1) / kTR * kTR);  // end of the first partial tile
+            const int64_t s1 = max(e0, (r0 + n) / kTR * kTR);            // start of the last partial tile
+            for (int64_t row = r0 + lane / R; row < e0; row += 32 / R)
+                if (lane < (32 / R) * R) p.US[row * R + lane % R] = 0.0;
+            for (int64_t row = s1 + lane / R; row < r0 + n; row += 32 / R)
+                if (lane < (32 / R) * R) p.US[row * R + lane % R] = 0.0;
+        }
+    }
+    pdl_wait();  // completion of this grid implies completion of the small-slice kernel
+}
+
+// ---------------------------------------------------------------------------
+// k_bigx: the streaming fused kernel (see the file comment)
+// ---------------------------------------------------------------------------
+template <int MAXS>
+__global__ void __launch_bounds__(kCW * 32 + 32, 1) k_bigx(const __grid_constant__ CUtensorMap tmX, BigxParams p) {
+    extern __shared__ __align__(16) double sm_raw[];
+    double *sm = align1k(sm_raw);
+    const int J = p.J, R = p.R;
+    const int JS = BigxSmem::strips(J), VTP = BigxSmem::vtp(J), NST = BigxSmem::stages(J);
+    const size_t SD = BigxSmem::stage_doubles(J);
+    double *xs = sm;
+    double *vt = xs + NST * SD;         // vt[n][k] = V[k][n]
+    double *xvs = vt + 16 * VTP;        // 32 x 16, swizzled (1024-aligned: NST*SD and 16*VTP are multiples of 128)
+    double *us = xvs + 512;             // 32 x UP
+    double *ms = us + 32 * kBxUP;       // 16 x MP
+    double *red = ms + 16 * kBxMP;      // 8 x 16 (unused slack)
+    uint64_t *full = reinterpret_cast<uint64_t *>(red + 128);
+    uint64_t *empty = full + 3;
+    const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
+    const int g = lane >> 2, t = lane & 3;
+    pdl_wait();  // Ms, toff from k_bigx_pre (and, transitively, XV / plan / small slices)
+    pdl_trigger();
+    for (int i = tid; i < 16 * VTP; i += blockDim.x) {
+        const int nn = i / VTP, k = i % VTP;
+        vt[i] = (nn < R && k < J) ? p.V[k * R + nn] : 0.0;
+    }
+    if (tid == 0) {
+        prefetch_map(&tmX);
+        for (int s2 = 0; s2 < NST; ++s2) {
+            mbar_init(&full[s2], 1);
+            mbar_init(&empty[s2], kCW);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int nsmall = __ldcg(p.plan_counts);
+    const int64_t T = p.T, G = p.G;
+    const int64_t tau0 = tile_start(blockIdx.x, T, G), tau1 = tile_start(blockIdx.x + 1, T, G);
+    if (tau0 >= tau1) return;
+    // first big slice of this CTA's range: last bi with toff[bi] <= tau0
+    int bi0 = 0;
+    {
+        const int nbig = __ldcg(p.plan_counts + 1);
+        int lo = 0, hi = nbig - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (__ldcg(p.toff + mid) <= tau0) lo = mid;
+            else hi = mid - 1;
+        }
+        bi0 = lo;
+    }
+    if (w == kCW) {  // producer
+        if (lane == 0) {
+            int bi = bi0;
+            int64_t tb = __ldcg(p.toff + bi), te = __ldcg(p.toff + bi + 1);
+            int64_t r0 = __ldcg(&p.meta[nsmall + bi].x);
+            for (int64_t tau = tau0, i = 0; tau < tau1; ++tau, ++i) {
+                while (tau >= te) {
+                    ++bi;
+                    tb = te;
+                    te = __ldcg(p.toff + bi + 1);
+                    r0 = __ldcg(&p.meta[nsmall + bi].x);
+                }
+                const int st = (int)(i % NST);
+                if (i >= NST) mbar_wait(&empty[st], (uint32_t)(((i / NST) - 1) & 1));
+                const int row0 = (int)(r0 + (tau - tb) * kTR);
+                mbar_arrive_expect_tx(&full[st], (uint32_t)JS * 4096u);
+                for (int s = 0; s < JS; ++s) tma_load_2d(xs + st * SD + s * 512, &tmX, 16 * s, row0, &full[st]);
+            }
+        }
+        return;
+    }
+    const int mb = w & 3, nb = w >> 2;
+    const double *vrow = vt + (8 * nb + g) * VTP + 2 * t;
+    const int xrow = 8 * mb + qperm(g);  // XV A-fragment row (conflict-free X reads)
+    const int pg = qperm(g);
+    double pacc[MAXS][4][2];
+    double gacc[2] = {0.0, 0.0};
+    double cacc[2] = {0.0, 0.0};
+#pragma unroll
+    for (int q = 0; q < MAXS; ++q)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) pacc[q][k][0] = pacc[q][k][1] = 0.0;
+    int bi = bi0 - 1;
+    int64_t tb = 0, te = 0, r0 = 0, n = 0;
+    for (int64_t tau = tau0, i = 0; tau < tau1; ++tau, ++i) {
+        if (tau >= te) {  // next slice: load its Ms (the previous tile's barrier protects ms)
+            do {
+                ++bi;
+                tb = __ldcg(p.toff + bi);
+                te = __ldcg(p.toff + bi + 1);
+            } while (tau >= te);
+            const int4 mt = __ldcg(p.meta + nsmall + bi);
+            r0 = mt.x;
+            n = mt.y;
+            for (int e = tid; e < 16 * kBxMP; e += kCW * 32) ms[e] = __ldcg(p.ms + (int64_t)bi * 16 * kBxMP + e);
+        }
+        const int64_t row0 = r0 + (tau - tb) * kTR;
+        const int nvalid = (int)min((int64_t)kTR, r0 + n - row0);
+        const int st = (int)(i % NST);
+        mbar_wait(&full[st], (uint32_t)((i / NST) & 1));
+        const double *xt = xs + st * SD;
+        // ---- XV = X V (warp: rows 8mb.., cols 8nb..)
+        {
+            double acc[2] = {0.0, 0.0}, acc2[2] = {0.0, 0.0};
+            for (int s = 0; s < JS; ++s) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const double2 a = *reinterpret_cast<const double2 *>(xt + s * 512 + swz(xrow, 4 * h + t));
+                    const double2 b = *reinterpret_cast<const double2 *>(vrow + 16 * s + 8 * h);
+                    dmma884(acc, a.x, b.x);
+                    dmma884(acc2, a.y, b.y);
+                }
+            }
+            const bool ok = xrow < nvalid;
+            *reinterpret_cast<double2 *>(xvs + swz_e(xrow, 8 * nb + 2 * t)) =
+                make_double2(ok ? acc[0] + acc2[0] : 0.0, ok ? acc[1] + acc2[1] : 0.0);
+        }
+        compute_bar();  // xvs complete; also: ms of a new slice is visible
+        // ---- U = XV Ms^T (warp: rows 8mb + g, cols 8nb..), c partial; U -> global and us
+        {
+            const int row = 8 * mb + g;
+            double ua[2] = {0.0, 0.0};
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                const double a = xvs[swz_e(row, 4 * kk + t)];
+                dmma884(ua, a, ms[(8 * nb + g) * kBxMP + 4 * kk + t]);
+            }
+            const int col = 8 * nb + 2 * t;
+            const double2 xv2 = *reinterpret_cast<const double2 *>(xvs + swz_e(row, col));
+            const bool ok = row < nvalid;
+            const double u0 = ok ? ua[0] : 0.0, u1 = ok ? ua[1] : 0.0;
+            cacc[0] = fma(xv2.x, u0, cacc[0]);
+            cacc[1] = fma(xv2.y, u1, cacc[1]);
+            *reinterpret_cast<double2 *>(us + row * kBxUP + col) = make_double2(u0, u1);
+            if (ok && col < R) *reinterpret_cast<double2 *>(p.U + (row0 + row) * R + col) = make_double2(u0, u1);
+        }
+        // ---- P += X^T XV (warp: strip(s) w, w + 8; 2x2 DMMA block per LDS pair)
+#pragma unroll
+        for (int kk = 0; kk < kTR / 4; ++kk) {
+            const int row = 4 * kk + t;
+            const double2 b = *reinterpret_cast<const double2 *>(xvs + swz(row, pg));  // XV[row][2pg, 2pg+1]
+#pragma unroll
+            for (int q = 0; q < MAXS; ++q) {
+                const int s = w + kCW * q;
+                if (s < JS) {
+                    const double2 a = *reinterpret_cast<const double2 *>(xt + s * 512 + swz(row, pg));
+                    dmma884(pacc[q][0], a.x, b.x);
+                    dmma884(pacc[q][1], a.x, b.y);
+                    dmma884(pacc[q][2], a.y, b.x);
+                    dmma884(pacc[q][3], a.y, b.y);
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+        compute_bar();  // us complete; xvs / us free for the next tile after the gram step
+        // ---- gram += U^T U: 8 warps = 4 tiles x 2 K-halves
+        {
+            const int mi = (w & 3) >> 1, ni = w & 1, kh = w >> 2;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                const int row = 4 * (kk + 4 * kh) + t;
+                dmma884(gacc, us[row * kBxUP + 8 * mi + g], us[row * kBxUP + 8 * ni + g]);
+            }
+        }
+        // ---- segment end: flush the partials of (slice bi, this CTA)
+        if (tau == te - 1 || tau == tau1 - 1) {
+            double *part = p.parts + (int64_t)(bi + blockIdx.x) * BigxSmem::part_doubles(J);
+#pragma unroll
+            for (int q = 0; q < MAXS; ++q) {
+                const int s = w + kCW * q;
+                if (s < JS) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int j = 16 * s + 2 * pg + (k >> 1);
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int r = 2 * qperm(2 * t + e) + (k & 1);
+                            if (j < J) part[j * 16 + r] = pacc[q][k][e];
+                            pacc[q][k][e] = 0.0;
+                        }
+                    }
+                }
+            }
+            {
+                const int mi = (w & 3) >> 1, ni = w & 1, kh = w >> 2;
+                double *gp = part + (int64_t)J * 16 + kh * 256;
+#pragma unroll
+                for (int e = 0; e < 2; ++e) gp[(8 * mi + g) * 16 + 8 * ni + 2 * t + e] = gacc[e];
+                gacc[0] = gacc[1] = 0.0;
+            }
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                double v = cacc[e];
+                v += __shfl_xor_sync(FULL_MASK, v, 4);
+                v += __shfl_xor_sync(FULL_MASK, v, 8);
+                v += __shfl_xor_sync(FULL_MASK, v, 16);
+                if (g == 0) part[(int64_t)J * 16 + 512 + mb * 16 + 8 * nb + 2 * t + e] = v;
+                cacc[e] = 0.0;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k_bigx_post: one CTA (256 threads) per big slice
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_bigx_post(BigxParams p) {
+    constexpr int RB = kBxRB, LDV = RB + 2, LDL = RB + 1;
+    extern __shared__ __align__(16) double smp[];
+    const int J = p.J, R = p.R;
+    double *psum = smp;                   // J x 16
+    double *vtv_s = psum + J * 16;        // RB x LDV
+    double *gram_s = vtv_s + RB * LDV;    // RB x LDL
+    double *dns = gram_s + RB * LDL;      // RB x LDL
+    double *lu = dns + RB * LDL;          // RB x LDL
+    double *vec = lu + RB * LDL;          // c | w | buf(RB+2) | spare
+    double *ms = vec + 4 * RB + 8;        // 16 x MP
+    int *piv = reinterpret_cast<int *>(ms + 16 * kBxMP);
+    pdl_wait();
+    pdl_trigger();
+    const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
+    const int nsmall = __ldcg(p.plan_counts), nbig = __ldcg(p.plan_counts + 1);
+    const int bi = blockIdx.x;
+    if (bi >= nbig) return;
+    const int4 mt = __ldcg(p.meta + nsmall + bi);
+    const int m = mt.w;
+    const int wrow = mt.z & 0x7fffffff;
+    const bool fresh = mt.z < 0;
+    const int64_t T = p.T, G = p.G;
+    const int64_t c0 = cta_of_tile(__ldcg(p.toff + bi), T, G);
+    const int64_t c1 = cta_of_tile(__ldcg(p.toff + bi + 1) - 1, T, G);
+    const int64_t PD = BigxSmem::part_doubles(J);
+    // segment sums in CTA order
+    for (int e = tid; e < J * 16; e += blockDim.x) {
+        double acc = 0.0;
+        for (int64_t c = c0; c <= c1; ++c) acc += __ldcg(p.parts + (bi + c) * PD + e);
+        psum[e] = acc;
+    }
+    if (tid < 256) {
+        double acc = 0.0;
+        for (int64_t c = c0; c <= c1; ++c) {
+            const double *gp = p.parts + (bi + c) * PD + (int64_t)J * 16;
+            acc += __ldcg(gp + tid) + __ldcg(gp + 256 + tid);
+        }
+        gram_s[(tid / 16) * LDL + tid % 16] = acc;
+    }
+    if (tid < 16) {
+        double acc = 0.0;
+        for (int64_t c = c0; c <= c1; ++c) {
+            const double *cp = p.parts + (bi + c) * PD + (int64_t)J * 16 + 512;
+            acc += ((__ldcg(cp + tid) + __ldcg(cp + 16 + tid)) + (__ldcg(cp + 32 + tid) + __ldcg(cp + 48 + tid)));
+        }
+        vec[tid] = tid < R ? p.lam * (fresh ? 0.0 : __ldcg(p.C + (int64_t)wrow * R + tid)) + acc : 0.0;  // c_new
+    }
+    for (int i = tid; i < RB * LDV; i += blockDim.x) {
+        const int a = i / LDV, b = i % LDV;
+        vtv_s[i] = (a < R && b < R) ? __ldcg(p.vtv + a * R + b) : 0.0;
+    }
+    for (int e = tid; e < 16 * kBxMP; e += blockDim.x) ms[e] = __ldcg(p.ms + (int64_t)bi * 16 * kBxMP + e);
+    if (tid < RB && !fresh)
+        for (int z = 0; z < R; ++z)
+            dns[tid * LDL + z] = tid < R ? __ldcg(p.D + (int64_t)wrow * R * R + (int64_t)z * R + tid) : 0.0;
+    __syncthreads();
+    // ---- D accumulation and the S-row system by warp 0 lanes 0..15 (as k_big)
+    if (w == 0) {
+        const int r = lane % RB;
+        const bool lreal = lane < RB && r < R;
+        double *dn = dns + r * LDL;
+        if (lane < RB) {
+#pragma unroll
+            for (int z = 0; z < RB; ++z)
+                dn[z] = (lreal && z < R) ? p.lam * (fresh ? 0.0 : dn[z]) + gram_s[r * LDL + z] : 0.0;
+        }
+        __syncwarp();
+        double dsum = 0.0;
+#pragma unroll
+        for (int z = 0; z < RB; ++z)
+            if (z < R) dsum += vtv_s[z * LDV + z] * dns[z * LDL + z];
+        const double sh2 = p.eps * dsum / R;
+        const double dg2 = lreal ? sh2 : 1.0;
+        double a[RB];
+#pragma unroll
+        for (int z = 0; z < RB; ++z) a[z] = (lane < RB ? vtv_s[r * LDV + z] * dn[z] : 0.0) + ((z == r) ? dg2 : 0.0);
+        double wv;
+        double *gbuf = vec + 2 * RB;  // RB + 2 scratch, 16-byte aligned
+        bool okB = gj_solve<RB>(a, lreal ? vec[r] : 0.0, lane < RB ? gbuf : lu, r, wv);
+        if (!lreal) wv = 0.0;
+        const bool good = __all_sync(FULL_MASK, (okB && isfinite(wv)) || lane >= RB);
+        if (!good) {
+            const bool need = lane < RB;
+#pragma unroll
+            for (int z = 0; z < RB; ++z) a[z] = (lane < RB ? vtv_s[r * LDV + z] * dn[z] : 0.0) + ((z == r) ? dg2 : 0.0);
+            if (lane == 0) atomicAdd(p.fallbacks, 1u);
+            const bool okLU = lu_fallback<RB>(a, lu, piv, r, R, need);
+            if (lane == 0 && !okLU) report_error(p.err, m, DASH_E_SINGULAR);
+            wv = 0.0;
+#pragma unroll
+            for (int z = 0; z < RB; ++z) wv = fma(-a[z], vec[z], wv);
+            if (!lreal) wv = 0.0;
+            if (lreal && !isfinite(wv)) report_error(p.err, m, DASH_E_NONFINITE);
+        }
+        __syncwarp();
+        if (lreal) {
+            p.Wo[(int64_t)wrow * R + r] = wv;
+            if (p.final_pass) {
+                p.Co[(int64_t)wrow * R + r] = vec[r];
+#pragma unroll
+                for (int z = 0; z < RB; ++z)
+                    if (z < R) p.D[(int64_t)wrow * R * R + (int64_t)z * R + r] = dn[z];
+            }
+        }
+        if (lane < RB) vec[RB + lane] = lreal ? wv : 0.0;
+    }
+    __syncthreads();
+    const double *wv = vec + RB;
+    // ---- G slot: gram o w w^T;  F slot: P Ms^T diag(w)
+    if (tid < R * R) {
+        const int a = tid / R, b = tid % R;
+        p.G_slots[(int64_t)bi * R * R + tid] = gram_s[a * LDL + b] * wv[a] * wv[b];
+    }
+    double *fs = p.F_slots + (int64_t)bi * J * R;
+    for (int e = tid; e < J * R; e += blockDim.x) {
+        const int j = e / R, r = e % R;
+        const double *pr = psum + j * 16;
+        const double *mr = ms + r * kBxMP;
+        double acc = 0.0;
+#pragma unroll
+        for (int z = 0; z < 16; ++z) acc = fma(pr[z], mr[z], acc);
+        fs[e] = acc * wv[r];
+    }
+}
+
+size_t bigx_post_smem(int J) {
+    return sizeof(double) * ((size_t)J * 16 + 18 * 18 + 3 * 16 * 17 + 4 * 16 + 8 + 16 * kBxMP) + 16 * sizeof(int) + 64;
+}

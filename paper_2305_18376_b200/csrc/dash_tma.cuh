@@ -68,9 +68,12 @@ struct FusedPrologue {
     int snap, last;
 };
 
+// tflag (optional): visit only tiles with tflag[tile] != 0 (the small-slice
+// tiles when big slices take the fused path); producer and consumers skip the
+// same tiles, the ring advances only on visited ones.
 __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_xv3(const __grid_constant__ CUtensorMap tmX, int64_t N, int J,
                                                           const double *__restrict__ V, int R, double *__restrict__ XV,
-                                                          FusedPrologue pro) {
+                                                          FusedPrologue pro, const uint8_t *__restrict__ tflag) {
     extern __shared__ __align__(16) double sm_raw[];
     double *sm = align1k(sm_raw);
     const int JS = TmaSmem::strips(J), VTP = TmaSmem::vtp(J);
@@ -119,10 +122,13 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_xv3(const __grid_constant_
     const int64_t mine = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     if (w == kCW) {
         if (lane == 0) {
-            for (int64_t i = 0; i < mine; ++i) {
-                const int st = (int)(i % kStages);
-                if (i >= kStages) mbar_wait(&empty[st], (uint32_t)(((i / kStages) - 1) & 1));
-                const int r0 = (int)((blockIdx.x + i * gridDim.x) * kTR);
+            for (int64_t i = 0, k = 0; i < mine; ++i) {
+                const int64_t tile = blockIdx.x + i * gridDim.x;
+                if (tflag != nullptr && !tflag[tile]) continue;
+                const int st = (int)(k % kStages);
+                if (k >= kStages) mbar_wait(&empty[st], (uint32_t)(((k / kStages) - 1) & 1));
+                ++k;
+                const int r0 = (int)(tile * kTR);
                 mbar_arrive_expect_tx(&full[st], (uint32_t)JS * 4096u);
                 for (int s = 0; s < JS; ++s) tma_load_2d(xs + st * SD + s * 512, &tmX, 16 * s, r0, &full[st]);
             }
@@ -133,9 +139,11 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_xv3(const __grid_constant_
     const int mb = w & 3, nb = w >> 2;  // 8-row block, 8-column block of the 32 x 16 output tile
     const double *vrow = vt + (8 * nb + g) * VTP + 2 * t;
     const int row = 8 * mb + qperm(g);  // tile row of this lane's A fragment and output
-    for (int64_t i = 0; i < mine; ++i) {
-        const int st = (int)(i % kStages);
-        mbar_wait(&full[st], (uint32_t)((i / kStages) & 1));
+    for (int64_t i = 0, k = -1; i < mine; ++i) {
+        if (tflag != nullptr && !tflag[blockIdx.x + i * gridDim.x]) continue;
+        ++k;
+        const int st = (int)(k % kStages);
+        mbar_wait(&full[st], (uint32_t)((k / kStages) & 1));
         const double *xt = xs + st * SD;
         double acc[2] = {0.0, 0.0}, acc2[2] = {0.0, 0.0};
         for (int s = 0; s < JS; ++s) {
@@ -166,7 +174,8 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_xv3(const __grid_constant_
 template <int MAXS>
 __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_fgemm3(const __grid_constant__ CUtensorMap tmX,
                                                              const __grid_constant__ CUtensorMap tmU, int64_t N, int J,
-                                                             int R, double *__restrict__ F_slots) {
+                                                             int R, double *__restrict__ F_slots,
+                                                             const uint8_t *__restrict__ tflag) {
     extern __shared__ __align__(16) double sm_raw[];
     double *sm = align1k(sm_raw);
     const int JS = TmaSmem::strips(J);
@@ -192,10 +201,13 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_fgemm3(const __grid_consta
     const int64_t mine = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     if (w == kCW) {
         if (lane == 0) {
-            for (int64_t i = 0; i < mine; ++i) {
-                const int st = (int)(i % kStages);
-                if (i >= kStages) mbar_wait(&empty[st], (uint32_t)(((i / kStages) - 1) & 1));
-                const int r0 = (int)((blockIdx.x + i * gridDim.x) * kTR);
+            for (int64_t i = 0, k = 0; i < mine; ++i) {
+                const int64_t tile = blockIdx.x + i * gridDim.x;
+                if (tflag != nullptr && !tflag[tile]) continue;
+                const int st = (int)(k % kStages);
+                if (k >= kStages) mbar_wait(&empty[st], (uint32_t)(((k / kStages) - 1) & 1));
+                ++k;
+                const int r0 = (int)(tile * kTR);
                 mbar_arrive_expect_tx(&full[st], (uint32_t)(JS + 1) * 4096u);
                 for (int s = 0; s < JS; ++s) tma_load_2d(xs + st * SD + s * 512, &tmX, 16 * s, r0, &full[st]);
                 tma_load_2d(xs + st * SD + JS * 512, &tmU, 0, r0, &full[st]);
@@ -209,9 +221,11 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_fgemm3(const __grid_consta
     for (int q = 0; q < MAXS; ++q)
 #pragma unroll
         for (int k = 0; k < 4; ++k) acc[q][k][0] = acc[q][k][1] = 0.0;
-    for (int64_t i = 0; i < mine; ++i) {
-        const int st = (int)(i % kStages);
-        mbar_wait(&full[st], (uint32_t)((i / kStages) & 1));
+    for (int64_t i = 0, k = -1; i < mine; ++i) {
+        if (tflag != nullptr && !tflag[blockIdx.x + i * gridDim.x]) continue;
+        ++k;
+        const int st = (int)(k % kStages);
+        mbar_wait(&full[st], (uint32_t)((k / kStages) & 1));
         const double *xt = xs + st * SD;
         const double *ut = xt + JS * 512;
 #pragma unroll

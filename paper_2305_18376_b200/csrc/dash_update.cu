@@ -493,6 +493,7 @@ int launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 #include "dash_slices_cta.cuh"
 #include "dash_slices3.cuh"
 #include "dash_big.cuh"
+#include "dash_bigx.cuh"
 
 // ---------------------------------------------------------------------------
 // k_fgemm: F partial slot s = X[rows_s]^T (U o w)[rows_s], J-block of 64.
@@ -777,6 +778,7 @@ struct dash_ctx {
         size_t cap = 0;
     };
     Buf xv, row_slice, items, gslots, fslots, vtv, fsnap, gsnap, fg, part, us, scratch, smeta, plan_hist, u64;
+    Buf tflag, bx_ms, bx_toff, bx_parts;  // fused big-slice path
     unsigned long long *err = nullptr;
     unsigned int *fallbacks = nullptr;
     int4 *items_host[2] = {nullptr, nullptr};
@@ -790,6 +792,8 @@ struct dash_ctx {
     int64_t nsplit = 1, rps = 32;
     bool stream = false;  // TMA-ring GEMM path for this update
     bool tma = false;     // ... with tensor-map (swizzled box) copies: k_xv3 / k_fgemm3
+    bool bigx = false;    // big slices on the fused single-read path (dash_bigx.cuh)
+    int bigx_nbig = 0, bigx_grid = 0;
     void *plan_p = nullptr;  // SlicePlan of the update in flight
     // phase timing (bench): events around every launch when enabled
     int prof = 0;
@@ -939,6 +943,7 @@ int dispatch_slices(dash_ctx *ctx, cudaStream_t st, int RB, int nitems, const Sl
 struct SlicePlan {
     std::vector<int4> items;  // host-planned items (k_slices2 big items, or all items for RB > 16)
     int nbig = 0, g3 = 0, gbig = 0, nslots = 0;
+    int64_t big_tiles = 0;  // 32-row tiles of the big slices (fused path grid split)
     bool split = false, big_dev = false;
 };
 
@@ -954,8 +959,16 @@ SlicePlan make_plan(const int64_t *row_ptr, int M, int RB, int R, int num_sms) {
     if (RB == 16 && (R % 2) == 0) {  // order on device; the host only counts big slices (grid size)
         pl.big_dev = true;
         int nbig = 0;
-        for (int m = 0; m < M; ++m) nbig += (row_ptr[m + 1] - row_ptr[m]) > kSmallRows;
+        int64_t tiles = 0;
+        for (int m = 0; m < M; ++m) {
+            const int64_t n = row_ptr[m + 1] - row_ptr[m];
+            if (n > kSmallRows) {
+                ++nbig;
+                tiles += (n + kTR - 1) / kTR;
+            }
+        }
         pl.gbig = nbig;  // one CTA (and G slot) per big slice
+        pl.big_tiles = tiles;
         pl.nslots = pl.g3 + pl.gbig;
         return pl;
     }
@@ -974,7 +987,7 @@ SlicePlan &plan_of(dash_ctx *ctx) { return *reinterpret_cast<SlicePlan *>(ctx->p
 
 // device plan (R <= 16): meta[M] in plan order + plan_counts {nsmall, nbig}
 template <class B>
-int device_plan(dash_ctx *ctx, cudaStream_t st, const B *b) {
+int device_plan(dash_ctx *ctx, cudaStream_t st, const B *b, uint8_t *tflag) {
     const int M = b->M;
     const int nch = std::max(1, (M + kPlanChunk - 1) / kPlanChunk);
     // hist[B][nch] | off[B][nch] | tot[B] | counts[2]
@@ -987,7 +1000,8 @@ int device_plan(dash_ctx *ctx, cudaStream_t st, const B *b) {
     int *counts = tot + kPlanBuckets;
     PhaseScope ps(ctx, st, PH_ROWSLICE);
     // first kernel of the update: a normal launch (fully ordered after the previous update)
-    k_plan_count<<<nch, kPlanChunk, 0, st>>>(b->row_ptr, M, hist);
+    if (tflag) cudaMemsetAsync(tflag, 0, (size_t)((b->N + kTR - 1) / kTR), st);
+    k_plan_count<<<nch, kPlanChunk, 0, st>>>(b->row_ptr, M, hist, tflag);
     ctx->last_launches += 2;  // three kernels under one phase
     return launch_k(true, k_plan_scan, kPlanBuckets, kScanThreads, 0, st, (const int *)hist, nch, off, tot) ||
            launch_k(true, k_plan_scatter, (nch + 3) / 4, 128, 0, st, (const int64_t *)b->row_ptr, b->state_row,
@@ -999,7 +1013,8 @@ const int *plan_counts_of(dash_ctx *ctx, int M) {
     return (const int *)ctx->plan_hist.p + 2 * (size_t)nch * kPlanBuckets + kPlanBuckets;
 }
 
-int launch_plan(dash_ctx *ctx, cudaStream_t st, int RB, const SlicePlan &pl, SliceParams sp, int M) {
+int launch_plan(dash_ctx *ctx, cudaStream_t st, int RB, const SlicePlan &pl, SliceParams sp, int M,
+                bool skip_big = false) {
     if (!pl.split) return dispatch_slices(ctx, st, RB, (int)pl.items.size(), sp);
     const int4 *meta = (const int4 *)ctx->smeta.p;
     const int *counts = plan_counts_of(ctx, M);
@@ -1013,7 +1028,7 @@ int launch_plan(dash_ctx *ctx, cudaStream_t st, int RB, const SlicePlan &pl, Sli
     SliceParams sb = sp;
     sb.G_slots = sp.G_slots + (int64_t)pl.g3 * sp.R * sp.R;
     if (pl.big_dev) {
-        if (pl.gbig == 0) return 0;
+        if (pl.gbig == 0 || skip_big) return 0;
         PhaseScope ps(ctx, st, PH_BIG);
         return launch_big(st, pl.gbig, sb, meta, counts);  // DMMA big-slice kernel, plan order
     }
@@ -1210,7 +1225,7 @@ bool tma_ok(const dash_batch_f64 *b, int J, int R) {
 }
 
 int launch_xv3(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, const double *V, int R, double *XV,
-               const FusedPrologue &pro, bool pdl) {
+               const FusedPrologue &pro, bool pdl, const uint8_t *tflag = nullptr) {
     CUtensorMap mx;
     if (!make_box_map(&mx, b->X, J, b->N, b->ldx)) return DASH_E_CUDA;
     const size_t smem = TmaSmem::xv_bytes(J);
@@ -1220,12 +1235,12 @@ int launch_xv3(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, c
         attr = smem;
     }
     PhaseScope ps(ctx, st, PH_XV);
-    return launch_k(pdl, k_xv3, ctx->num_sms, kCW * 32 + 32, smem, st, mx, b->N, J, V, R, XV, pro);
+    return launch_k(pdl, k_xv3, ctx->num_sms, kCW * 32 + 32, smem, st, mx, b->N, J, V, R, XV, pro, tflag);
 }
 
 template <int MAXS>
 void launch_f3_t(dash_ctx *ctx, cudaStream_t st, const CUtensorMap &mx, const CUtensorMap &mu, int64_t N, int J,
-                 int R, double *F_slots) {
+                 int R, double *F_slots, const uint8_t *tflag) {
     const size_t smem = TmaSmem::f_bytes(J);
     static size_t attr = 0;
     if (attr < smem) {
@@ -1233,16 +1248,52 @@ void launch_f3_t(dash_ctx *ctx, cudaStream_t st, const CUtensorMap &mx, const CU
         attr = smem;
     }
     PhaseScope ps(ctx, st, PH_FGEMM);
-    launch_k(true, k_fgemm3<MAXS>, ctx->num_sms, kCW * 32 + 32, smem, st, mx, mu, N, J, R, F_slots);
+    launch_k(true, k_fgemm3<MAXS>, ctx->num_sms, kCW * 32 + 32, smem, st, mx, mu, N, J, R, F_slots, tflag);
 }
 
 int launch_f3(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, const double *US, int R,
-              double *F_slots) {
+              double *F_slots, const uint8_t *tflag = nullptr) {
     CUtensorMap mx, mu;
     if (!make_box_map(&mx, b->X, J, b->N, b->ldx) || !make_box_map(&mu, US, R, b->N, R)) return DASH_E_CUDA;
-    if (TmaSmem::strips(J) <= kCW) launch_f3_t<1>(ctx, st, mx, mu, b->N, J, R, F_slots);
-    else launch_f3_t<2>(ctx, st, mx, mu, b->N, J, R, F_slots);
+    if (TmaSmem::strips(J) <= kCW) launch_f3_t<1>(ctx, st, mx, mu, b->N, J, R, F_slots, tflag);
+    else launch_f3_t<2>(ctx, st, mx, mu, b->N, J, R, F_slots, tflag);
     return 0;
+}
+
+// fused big-slice chain (dash_bigx.cuh): pre (A systems, toff), the streaming kernel, post
+int launch_bigx(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, const BigxParams &bp) {
+    if (bp.T == 0) return 0;
+    const int nbig = ctx->bigx_nbig;
+    PhaseScope ps(ctx, st, PH_BIG);
+    ctx->last_launches += 2;  // three kernels under one phase
+    if (launch_k(true, k_bigx_pre, 1 + (nbig + 7) / 8, 256, 0, st, bp)) return DASH_E_CUDA;
+    CUtensorMap mx;
+    if (!make_box_map(&mx, b->X, bp.J, b->N, b->ldx)) return DASH_E_CUDA;
+    const size_t smem = BigxSmem::bytes(bp.J);
+    int rc;
+    if (BigxSmem::strips(bp.J) <= kCW) {
+        static size_t attr = 0;
+        if (attr < smem) {
+            cudaFuncSetAttribute(k_bigx<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            attr = smem;
+        }
+        rc = launch_k(true, k_bigx<1>, bp.G, kCW * 32 + 32, smem, st, mx, bp);
+    } else {
+        static size_t attr = 0;
+        if (attr < smem) {
+            cudaFuncSetAttribute(k_bigx<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            attr = smem;
+        }
+        rc = launch_k(true, k_bigx<2>, bp.G, kCW * 32 + 32, smem, st, mx, bp);
+    }
+    if (rc) return rc;
+    const size_t ps_smem = bigx_post_smem(bp.J);
+    static size_t pattr = 0;
+    if (pattr < ps_smem) {
+        cudaFuncSetAttribute(k_bigx_post, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps_smem);
+        pattr = ps_smem;
+    }
+    return launch_k(true, k_bigx_post, nbig, 256, ps_smem, st, bp);
 }
 
 template <int RP>
@@ -1317,16 +1368,33 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
         plan_fsplit(ctx, N, J, ctx->nsplit, ctx->rps);
         if (ctx->stream) ctx->nsplit = ctx->num_sms * (f32 ? TmaSmem32::row_groups(J) : 1);
         if constexpr (!f32) ctx->tma = ctx->stream && tma_ok(b, J, R);
+        {
+            static const bool no_bigx = getenv("DASH_BIGX") == nullptr;  // opt-in while being tuned
+            const SlicePlan &pl = plan_of(ctx);
+            ctx->bigx = !f32 && !no_bigx && ctx->tma && pl.big_dev && pl.gbig > 0 && BigxSmem::strips(J) <= 16 &&
+                        BigxSmem::bytes(J) <= 227 * 1024;
+            ctx->bigx_nbig = ctx->bigx ? pl.gbig : 0;
+            ctx->bigx_grid = ctx->bigx ? (int)std::min<int64_t>(ctx->num_sms, pl.big_tiles) : 0;
+            if (ctx->bigx && (ensure(ctx->tflag, (size_t)((N + kTR - 1) / kTR) + 16) ||
+                              ensure(ctx->bx_ms, sizeof(double) * (size_t)pl.gbig * 16 * kBxMP) ||
+                              ensure(ctx->bx_toff, sizeof(int) * ((size_t)pl.gbig + 1)) ||
+                              ensure(ctx->bx_parts, sizeof(double) * (size_t)(pl.gbig + ctx->bigx_grid) *
+                                                        BigxSmem::part_doubles(J))))
+                return DASH_E_CUDA;
+        }
         if (ensure(ctx->xv, sizeof(double) * std::max<int64_t>(N, 1) * R) ||
             ensure(ctx->row_slice, sizeof(int32_t) * std::max<int64_t>(N, 1)) ||
             ensure(ctx->gslots, sizeof(double) * std::max(ctx->nitems, 1) * R * R) ||
-            ensure(ctx->fslots, sizeof(double) * ctx->nsplit * J * R) || ensure(ctx->vtv, sizeof(double) * R * R) ||
+            ensure(ctx->fslots, sizeof(double) * (ctx->nsplit + ctx->bigx_nbig) * J * R) ||
+            ensure(ctx->vtv, sizeof(double) * R * R) ||
             ensure(ctx->fsnap, sizeof(double) * J * R) || ensure(ctx->gsnap, sizeof(double) * R * R) ||
             (ctx->stream && ensure(ctx->us, sizeof(double) * std::max<int64_t>(N, 1) * R)) ||
             (f32 && ensure(ctx->u64, sizeof(double) * std::max<int64_t>(N, 1) * R)))
             return DASH_E_CUDA;
         if (!items.empty() && stage_items(ctx, st, items)) return DASH_E_CUDA;
-        if (plan_of(ctx).split && M > 0 && N > 0 && device_plan(ctx, st, b)) return DASH_E_CUDA;
+        if (plan_of(ctx).split && M > 0 && N > 0 &&
+            device_plan(ctx, st, b, ctx->bigx ? (uint8_t *)ctx->tflag.p : nullptr))
+            return DASH_E_CUDA;
         if (M > 0 && !ctx->stream) {  // row -> slice map: only the generic F GEMM needs it
             PhaseScope ps(ctx, st, PH_ROWSLICE);
             k_row_slice<<<std::min(ctx->num_sms * 4, (M + 7) / 8 + 1), 256, 0, st>>>(b->row_ptr, M,
@@ -1348,7 +1416,13 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
             const FusedPrologue pro{(double *)ctx->vtv.p, s->F, s->G, (double *)ctx->fsnap.p, (double *)ctx->gsnap.p,
                                     v_used_out, pass == 0, last};
             // PDL only behind the plan kernels (pass 0); a later pass follows the V solve
-            if (launch_xv3(ctx, st, b, J, s->V, R, XV, pro, pass == 0)) return DASH_E_CUDA;
+            if constexpr (f32) {
+                if (launch_xv3(ctx, st, b, J, s->V, R, XV, pro, pass == 0)) return DASH_E_CUDA;
+            } else {
+                if (launch_xv3(ctx, st, b, J, s->V, R, XV, pro, pass == 0,
+                               ctx->bigx ? (const uint8_t *)ctx->tflag.p : nullptr))
+                    return DASH_E_CUDA;
+            }
         } else if (ctx->stream) {
             if constexpr (!f32) {
                 if (rank_bucket(R) <= 8) launch_xv2_t<8>(ctx, st, b, J, s->V, R, XV);
@@ -1377,9 +1451,48 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
         sp.eps = eps;
         sp.pass = pass;
         sp.final_pass = last;
-        if (launch_plan(ctx, st, RB, plan_of(ctx), sp, M)) return DASH_E_CUDA;
+        if (launch_plan(ctx, st, RB, plan_of(ctx), sp, M, ctx->bigx)) return DASH_E_CUDA;
+        if constexpr (!f32) {
+            if (ctx->bigx) {
+                BigxParams bp;
+                bp.meta = (const int4 *)ctx->smeta.p;
+                bp.plan_counts = plan_counts_of(ctx, M);
+                bp.V = s->V;
+                bp.vtv = (const double *)ctx->vtv.p;
+                bp.W = s->W;
+                bp.C = s->C;
+                bp.Wo = s->W;
+                bp.Co = s->C;
+                bp.D = s->D;
+                bp.U = Ud;
+                bp.US = (double *)ctx->us.p;
+                bp.ms = (double *)ctx->bx_ms.p;
+                bp.toff = (int *)ctx->bx_toff.p;
+                bp.parts = (double *)ctx->bx_parts.p;
+                bp.F_slots = Fsl + (int64_t)ctx->nsplit * J * R;
+                bp.G_slots = Gsl + (int64_t)plan_of(ctx).g3 * R * R;
+                bp.err = ctx->err;
+                bp.fallbacks = ctx->fallbacks;
+                bp.N = N;
+                bp.T = plan_of(ctx).big_tiles;
+                bp.J = J;
+                bp.R = R;
+                bp.G = ctx->bigx_grid;
+                bp.lam = s->forgetting;
+                bp.eps = eps;
+                bp.pass = pass;
+                bp.final_pass = last;
+                if (launch_bigx(ctx, st, b, bp)) return DASH_E_CUDA;
+            }
+        }
         if (ctx->tma) {
-            if (launch_f3(ctx, st, b, J, (const double *)ctx->us.p, R, Fsl)) return DASH_E_CUDA;
+            if constexpr (f32) {
+                if (launch_f3(ctx, st, b, J, (const double *)ctx->us.p, R, Fsl)) return DASH_E_CUDA;
+            } else {
+                if (launch_f3(ctx, st, b, J, (const double *)ctx->us.p, R, Fsl,
+                              ctx->bigx ? (const uint8_t *)ctx->tflag.p : nullptr))
+                    return DASH_E_CUDA;
+            }
         } else if (ctx->stream) {
             if constexpr (!f32) {
                 if (rank_bucket(R) <= 8) launch_f2_t<8>(ctx, st, b, J, (const double *)ctx->us.p, R, Fsl);
@@ -1401,7 +1514,7 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
     if (host_timing) fprintf(stderr, "[dash host] pass_begin total %.1f us\n", std::chrono::duration<double, std::micro>(tnow() - t0).count());
     {
         PhaseScope ps(ctx, st, PH_SUMFG);
-        if (colsum2(ctx, st, Fsl, N > 0 ? (int)ctx->nsplit : 0, (int64_t)J * R, fg_out, Gsl,
+        if (colsum2(ctx, st, Fsl, N > 0 ? (int)ctx->nsplit + ctx->bigx_nbig : 0, (int64_t)J * R, fg_out, Gsl,
                     N > 0 ? ctx->nitems : 0, (int64_t)R * R, fg_out + (int64_t)J * R))
             return DASH_E_CUDA;
     }
@@ -1434,7 +1547,8 @@ void dash_ctx_destroy(dash_ctx *ctx) {
     cudaDeviceSynchronize();
     dash_ctx::Buf *bufs[] = {&ctx->xv,  &ctx->row_slice, &ctx->items, &ctx->gslots, &ctx->fslots,
                              &ctx->vtv, &ctx->fsnap,     &ctx->gsnap, &ctx->fg,     &ctx->part, &ctx->us, &ctx->scratch,
-                             &ctx->smeta, &ctx->plan_hist, &ctx->u64};
+                             &ctx->smeta, &ctx->plan_hist, &ctx->u64,
+                             &ctx->tflag, &ctx->bx_ms, &ctx->bx_toff, &ctx->bx_parts};
     for (auto *b : bufs)
         if (b->p) cudaFree(b->p);
     cudaFree(ctx->err);
