@@ -112,17 +112,32 @@ def batch_stats(batches):
     return {k: v / max(len(batches), 1) for k, v in acc.items()}
 
 
-def kernel_bytes(phase, st, J, R, nsplit, b=8):
-    """Algorithmic bytes per launch of each kernel (DESIGN.md table)."""
-    N = st["N"]
+def kernel_bytes(phase, st, J, R, nsplit, b=8, bigx=False):
+    """Algorithmic bytes per launch of each kernel (DESIGN.md table).  With the
+    fused big-slice path (bigx) the XV / F GEMMs stream only the small slices'
+    rows and "big" reads the big slices' rows once (X in, U out, state)."""
+    N = st["Ns"] if bigx else st["N"]
     if phase == "xv":        # read X, V; write XV
         return b * (N * J + N * R + J * R)
     if phase == "fgemm":     # read X, US; write one J x R slot per CTA
         return b * (N * J + N * R + nsplit * J * R)
+    if phase == "big" and bigx:  # read X once; write U; per-slice W/C/D r/w (new: write only)
+        return b * (st["Nb"] * J + st["Nb"] * R + st["Mob"] * (2 * R * R + 4 * R) + st["Lb"] * (R * R + 2 * R))
     if phase in ("slices", "big"):  # read XV; write U, US; per-slice W/C/D r/w (new: write only)
         k = "s" if phase == "slices" else "b"
         return b * (3 * st["N" + k] * R + st["Mo" + k] * (2 * R * R + 4 * R) + st["L" + k] * (R * R + 2 * R))
     return 0
+
+
+def kernel_flops(phase, st, J, R, bigx=False):
+    """FP64 flops per launch of the DMMA-bound fused big-slice kernel: XV = X V,
+    P = X^T U (2 N J R each), U = XV Ms^T and U^T U (2 N R^2 each)."""
+    if phase == "big" and bigx:
+        return 4 * st["Nb"] * J * R + 4 * st["Nb"] * R * R
+    return 0
+
+
+FP64_TENSOR_PEAK = 37.1  # TFLOP/s, DMMA, measured on this pool's B200 (profiles/r01_fp64_peak.md)
 
 
 class ClockSampler:
@@ -195,6 +210,23 @@ def ncu_traffic(phase):
         return None
     d = json.loads(p.read_text())
     return d.get(phase)
+
+
+def roofline_of(dom, per_kernel, achieved, peak, peak_kind, per_launch_ms, kb):
+    """Roofline of the dominant kernel: its binding roof (HBM bytes, or FP64
+    tensor flops for the DMMA-bound fused big-slice kernel, whichever fraction
+    is higher), with the other roof alongside."""
+    pk = per_kernel.get(dom, {})
+    hbm = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+           "frac": achieved / peak, "traffic": ncu_traffic(dom), "peak_source": peak_kind,
+           "per_launch_ms": per_launch_ms, "alg_bytes_per_launch": kb}
+    if pk.get("tflops") and pk["frac_fp64_tensor"] > hbm["frac"]:
+        return {"bound": "tensor", "kernel": dom, "achieved": pk["tflops"], "peak": FP64_TENSOR_PEAK,
+                "unit": "TFLOP/s", "frac": pk["frac_fp64_tensor"], "traffic": ncu_traffic(dom),
+                "peak_source": "measured FP64 DMMA peak (profiles/r01_fp64_peak.md)",
+                "per_launch_ms": per_launch_ms, "alg_flops_per_launch": pk["alg_flops"],
+                "hbm": {"achieved": achieved, "peak": peak, "frac": achieved / peak, "alg_bytes_per_launch": kb}}
+    return hbm
 
 
 # ---------------------------------------------------------------------------
@@ -404,15 +436,20 @@ def run_gpu(args):
     peak, peak_kind = peaks()
     per_launch_ms = phase_ms[dom] / max(phase_n[dom], 1)
     stt = batch_stats(profiled)
-    kb = kernel_bytes(dom, stt, J, R, nsplit)
+    bigx = bool(L.dash_ctx_path_flags(state._ctx) & nat.PATH_BIGX)
+    kb = kernel_bytes(dom, stt, J, R, nsplit, bigx=bigx)
     per_kernel = {}
     for ph in phase_ms:
         if phase_n[ph]:
             ms1 = phase_ms[ph] / phase_n[ph]
-            kb1 = kernel_bytes(ph, stt, J, R, nsplit)
+            kb1 = kernel_bytes(ph, stt, J, R, nsplit, bigx=bigx)
+            kf1 = kernel_flops(ph, stt, J, R, bigx=bigx)
             per_kernel[ph] = {"ms_per_launch": ms1, "alg_bytes": kb1,
                               "gbs": kb1 / (ms1 / 1e3) / 1e9 if kb1 else None,
                               "frac_hbm": kb1 / (ms1 / 1e3) / 1e9 / peak if kb1 else None}
+            if kf1:
+                per_kernel[ph].update({"alg_flops": kf1, "tflops": kf1 / (ms1 / 1e3) / 1e12,
+                                       "frac_fp64_tensor": kf1 / (ms1 / 1e3) / 1e12 / FP64_TENSOR_PEAK})
     achieved = kb / (per_launch_ms / 1e3) / 1e9
     step_bytes = algorithmic_bytes(N_avg, J, R, M_old_avg, L_avg)
     step_achieved = step_bytes / (ms_per_step / 1e3) / 1e9
@@ -430,10 +467,7 @@ def run_gpu(args):
                        "rows_per_update": N_avg, "slices_per_update": M_old_avg + L_avg,
                        "passes": cfg.passes, "l2": "inputs larger than L2 (0.8 GB per step)",
                        "parallelism": f"slice-sharded x{world}"},
-            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
-                         "unit": "GB/s", "frac": achieved / peak, "traffic": ncu_traffic(dom),
-                         "peak_source": peak_kind, "per_launch_ms": per_launch_ms,
-                         "alg_bytes_per_launch": kb},
+            "roofline": roofline_of(dom, per_kernel, achieved, peak, peak_kind, per_launch_ms, kb),
             "step_roofline": {"alg_bytes": step_bytes, "achieved_gbs": step_achieved,
                               "frac": step_achieved / peak,
                               "alg_flops": algorithmic_flops(N_avg, J, R, M_old_avg + L_avg),

@@ -61,6 +61,19 @@ int dash_ctx_status(dash_ctx *ctx, void *stream, int64_t *fail_slice_host);
  * gpu_launches figure). */
 int dash_ctx_last_launches(const dash_ctx *ctx);
 
+/* Host helper (no device work): row_ptr[0] = 0, row_ptr[m+1] = row_ptr[m] +
+ * counts[m] for m < M (row_ptr may be pinned memory that is then copied to
+ * the device), *N_out = total rows.  DASH_E_ARG on a negative count. */
+int dash_host_row_ptr(const int64_t *counts, int64_t M, int64_t *row_ptr, int64_t *N_out);
+
+/* Kernel path chosen for the last update (for benchmarks): bit 0 = streaming
+ * (TMA-ring) GEMMs, bit 1 = tensor-map boxes (k_xv3 / k_fgemm3 or the FP32
+ * variants), bit 2 = fused big-slice path (k_bigx: big-slice rows read once). */
+#define DASH_PATH_STREAM 1
+#define DASH_PATH_TMA 2
+#define DASH_PATH_BIGX 4
+int dash_ctx_path_flags(const dash_ctx *ctx);
+
 /* Number of ridge systems that needed the LU fallback (Cholesky failed or a
  * non-finite solution) since the last reset; syncs `stream`. */
 int dash_ctx_fallbacks(dash_ctx *ctx, void *stream, int32_t reset);

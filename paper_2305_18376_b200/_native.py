@@ -23,6 +23,7 @@ DASH_E_NONFINITE = 4
 MAX_RANK = 64       # update path
 MAX_RANK_ALS = 32   # parafac2_als / init_helpers / ridge_solve
 PHASES = ("row_slice", "prologue", "xv", "slices", "fgemm", "sum_fg", "vsolve", "big")
+PATH_STREAM, PATH_TMA, PATH_BIGX = 1, 2, 4
 
 _c_dp = ctypes.c_void_p  # device pointers travel as integers
 
@@ -49,6 +50,8 @@ SIGNATURES = {
     "dash_ctx_destroy": (None, [ctypes.c_void_p]),
     "dash_ctx_status": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]),
     "dash_ctx_last_launches": (ctypes.c_int, [ctypes.c_void_p]),
+    "dash_ctx_path_flags": (ctypes.c_int, [ctypes.c_void_p]),
+    "dash_host_row_ptr": (ctypes.c_int, [_c_dp, ctypes.c_int64, _c_dp, ctypes.POINTER(ctypes.c_int64)]),
     "dash_update_f64": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(DashBatch),
                                        ctypes.POINTER(DashState), _c_dp, _c_dp, ctypes.c_double]),
     "dash_update_pass_begin_f64": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(DashBatch),

@@ -7,25 +7,25 @@
 //   U    = XV Ms^T               (DMMA; Ms = A^{-1} diag(s) of the slice)  -> U_out
 //   c   += diag(XV^T U)          (fragment FMAs)
 //   gram+= U^T U                 (DMMA)
-//   P   += X^T XV                (DMMA, J x R, X still in shared memory)
+//   P   += X^T U                 (DMMA, J x R, X still in shared memory)
 //
-// and the slice's F contribution X^T (U o w) = P Ms^T diag(w) is formed once
-// w is known (stream.py:321 with the row sum reassociated; differences are
-// rounding-level).  Three kernels:
+// and the slice's F contribution X^T (U o w) = P diag(w) is formed once w is
+// known (stream.py:321; only the row-sum order differs).  Three kernels:
 //
 //   k_bigx_pre   one warp per big slice: the A system by the symmetric sweep
 //                (LU fallback) -> Ms (global); zeroes U o w on the slice's
 //                partial boundary tiles (the small-row F GEMM may read those
 //                tiles); block 0 scans the slices' tile counts -> toff[].
-//   k_bigx       persistent, one CTA per SM, warp-specialised (producer warp +
-//                8 DMMA warps, mbarrier ring): the big slices' tiles, in plan
+//   k_bigx       persistent, one CTA per SM, warp-specialised (producer warp,
+//                4 XV / U warps, 4 X^T U / gram warps, mbarrier handoffs, no
+//                CTA barriers in the loop): the big slices' tiles, in plan
 //                order, are split EVENLY over the CTAs (a slice may span CTAs);
 //                each (slice, CTA) segment writes its partial P, gram, c to
 //                parts[slice + CTA] (unique: slices and CTAs are both ordered).
 //   k_bigx_post  one CTA per big slice: segment partials summed in CTA order
 //                (deterministic), D = lam D + gram, the S-row system (Gauss-
 //                Jordan, LU fallback) -> w; W / C / D rows; G slot gram o w w^T;
-//                F slot P Ms^T diag(w).
+//                F slot P diag(w).
 //
 // (included inside dash_update.cu's anonymous namespace, after dash_big.cuh)
 #pragma once
@@ -34,19 +34,19 @@ constexpr int kBxRB = 16;           // rank bucket
 constexpr int kBxMP = kBxRB + 4;    // Ms pitch (B-frag reads)
 constexpr int kBxUP = kBxRB + 8;    // U tile pitch (gram frags conflict-free)
 
+constexpr int kBxMaxStages = 4;
 struct BigxSmem {
     static __host__ __device__ int strips(int J) { return (J + 15) / 16; }
-    static __host__ __device__ int stages(int J) { return strips(J) <= 8 ? 3 : 2; }
+    static __host__ __device__ int stages(int J) { return strips(J) <= 8 ? 4 : 2; }
     static __host__ __device__ int vtp(int J) { return strips(J) * 16 + 8; }
     static __host__ __device__ size_t stage_doubles(int J) { return (size_t)strips(J) * 512; }
-    // [stages x JS boxes] | vt[16 x VTP] | xvs[32 x 16 swz] | us[32 x UP] | ms[16 x MP] | red[8 x 16] | bars
+    // [stages x JS boxes] | vt[16 x VTP] | ubuf[2][32 x 16 swz] | barriers
     static __host__ __device__ size_t bytes(int J) {
-        return 1024 + sizeof(double) * (stages(J) * stage_doubles(J) + 16 * (size_t)vtp(J) + 512 + 32 * kBxUP +
-                                         16 * kBxMP + 128) +
-               16 * 4;
+        return 1024 + sizeof(double) * (stages(J) * stage_doubles(J) + 16 * (size_t)vtp(J) + 1024) +
+               8 * (2 * kBxMaxStages + 4);
     }
-    // partial slot of one (slice, CTA) segment: P[J x 16] | gram[2][16 x 16] | c[4][16]
-    static __host__ __device__ int64_t part_doubles(int J) { return (int64_t)J * 16 + 512 + 64; }
+    // partial slot of one (slice, CTA) segment: P[J x 16] | gram[16 x 16] | c[4][16]
+    static __host__ __device__ int64_t part_doubles(int J) { return (int64_t)J * 16 + 256 + 64; }
 };
 
 // element (row, col) of a 32 x 16 swizzled double tile (16-byte chunk c at c ^ (row & 7))
@@ -94,7 +94,8 @@ __global__ void __launch_bounds__(256) k_bigx_pre(BigxParams p) {
     __shared__ int wpiv[8][RB];
     // launched behind the small-slice kernel, which triggered only after its
     // own pdl_wait: the XV kernel's vtv and the plan are complete and visible.
-    pdl_trigger();
+    // No early trigger: the streaming kernel behind this one must not become
+    // resident (150 KB of shared memory per SM) while small slices still run.
     const int lane = lane_id(), w = warp_id();
     const int nsmall = __ldcg(p.plan_counts), nbig = __ldcg(p.plan_counts + 1);
     const int R = p.R;
@@ -116,6 +117,7 @@ __global__ void __launch_bounds__(256) k_bigx_pre(BigxParams p) {
             if (lane == 0) p.toff[nbig] = run;
         }
         pdl_wait();
+        pdl_trigger();
         return;
     }
     for (int i = threadIdx.x; i < RB * LDV; i += blockDim.x) {
@@ -177,26 +179,38 @@ __global__ void __launch_bounds__(256) k_bigx_pre(BigxParams p) {
         }
     }
     pdl_wait();  // completion of this grid implies completion of the small-slice kernel
+    pdl_trigger();
 }
 
 // ---------------------------------------------------------------------------
-// k_bigx: the streaming fused kernel (see the file comment)
+// k_bigx: the streaming fused kernel.  Warp-specialised, no CTA barriers in
+// the tile loop:
+//   producer warp     TMA ring of 32-row X tiles (JS swizzled 16-column boxes)
+//   group A (warps 0-3, warp = 8-row block mb of the tile):
+//                     XV = X V (DMMA, 4 chains), U = XV Ms^T straight from the
+//                     XV accumulator fragments (the K order of the U product
+//                     is permuted to the C-fragment layout: no shuffles), c
+//                     partial, U -> U_out and -> ubuf[tile & 1]
+//   group B (warps 4-7, warp b = strips s == b (mod 4) of P, gram tile b):
+//                     P += X^T U (DMMA, X still in the stage), gram += U^T U
+// A runs up to two tiles ahead of B (ubuf double-buffered, uready / ufree
+// mbarriers); a stage is released when both groups are done with it.
+// Partials of (slice, CTA): A writes c, B writes P and gram (disjoint parts).
 // ---------------------------------------------------------------------------
-template <int MAXS>
+template <int MAXS, int JSC>
 __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_bigx(const __grid_constant__ CUtensorMap tmX, BigxParams p) {
     extern __shared__ __align__(16) double sm_raw[];
     double *sm = align1k(sm_raw);
     const int J = p.J, R = p.R;
-    const int JS = BigxSmem::strips(J), VTP = BigxSmem::vtp(J), NST = BigxSmem::stages(J);
+    const int JS = JSC ? JSC : BigxSmem::strips(J), VTP = BigxSmem::vtp(J), NST = BigxSmem::stages(J);
     const size_t SD = BigxSmem::stage_doubles(J);
     double *xs = sm;
-    double *vt = xs + NST * SD;         // vt[n][k] = V[k][n]
-    double *xvs = vt + 16 * VTP;        // 32 x 16, swizzled (1024-aligned: NST*SD and 16*VTP are multiples of 128)
-    double *us = xvs + 512;             // 32 x UP
-    double *ms = us + 32 * kBxUP;       // 16 x MP
-    double *red = ms + 16 * kBxMP;      // 8 x 16 (unused slack)
-    uint64_t *full = reinterpret_cast<uint64_t *>(red + 128);
-    uint64_t *empty = full + 3;
+    double *vt = xs + NST * SD;          // vt[n][k] = V[k][n]
+    double *ubuf = vt + 16 * VTP;        // 2 x (32 x 16 swizzled)
+    uint64_t *full = reinterpret_cast<uint64_t *>(ubuf + 1024);
+    uint64_t *empty = full + kBxMaxStages;
+    uint64_t *uready = empty + kBxMaxStages;
+    uint64_t *ufree = uready + 2;
     const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
     const int g = lane >> 2, t = lane & 3;
     pdl_wait();  // Ms, toff from k_bigx_pre (and, transitively, XV / plan / small slices)
@@ -211,6 +225,10 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_bigx(const __grid_constant
             mbar_init(&full[s2], 1);
             mbar_init(&empty[s2], kCW);
         }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&uready[b], 4);
+            mbar_init(&ufree[b], 4);
+        }
         fence_mbar_init();
     }
     __syncthreads();
@@ -218,8 +236,7 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_bigx(const __grid_constant
     const int64_t T = p.T, G = p.G;
     const int64_t tau0 = tile_start(blockIdx.x, T, G), tau1 = tile_start(blockIdx.x + 1, T, G);
     if (tau0 >= tau1) return;
-    // first big slice of this CTA's range: last bi with toff[bi] <= tau0
-    int bi0 = 0;
+    int bi0 = 0;  // first big slice of this CTA's range: last bi with toff[bi] <= tau0
     {
         const int nbig = __ldcg(p.plan_counts + 1);
         int lo = 0, hi = nbig - 1;
@@ -230,18 +247,26 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_bigx(const __grid_constant
         }
         bi0 = lo;
     }
-    if (w == kCW) {  // producer
+    // slice tracking shared by every role: advance to the slice of tile tau
+    int bi = bi0 - 1;
+    int64_t tb = 0, te = 0, r0 = 0, n = 0;
+    auto advance = [&](int64_t tau) -> bool {
+        if (tau < te) return false;
+        do {
+            ++bi;
+            tb = __ldcg(p.toff + bi);
+            te = __ldcg(p.toff + bi + 1);
+        } while (tau >= te);
+        const int4 mt = __ldcg(p.meta + nsmall + bi);
+        r0 = mt.x;
+        n = mt.y;
+        return true;
+    };
+    const int64_t PD = BigxSmem::part_doubles(J);
+    if (w == kCW) {  // ---------------- producer
         if (lane == 0) {
-            int bi = bi0;
-            int64_t tb = __ldcg(p.toff + bi), te = __ldcg(p.toff + bi + 1);
-            int64_t r0 = __ldcg(&p.meta[nsmall + bi].x);
             for (int64_t tau = tau0, i = 0; tau < tau1; ++tau, ++i) {
-                while (tau >= te) {
-                    ++bi;
-                    tb = te;
-                    te = __ldcg(p.toff + bi + 1);
-                    r0 = __ldcg(&p.meta[nsmall + bi].x);
-                }
+                advance(tau);
                 const int st = (int)(i % NST);
                 if (i >= NST) mbar_wait(&empty[st], (uint32_t)(((i / NST) - 1) & 1));
                 const int row0 = (int)(r0 + (tau - tb) * kTR);
@@ -251,106 +276,134 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_bigx(const __grid_constant
         }
         return;
     }
-    const int mb = w & 3, nb = w >> 2;
-    const double *vrow = vt + (8 * nb + g) * VTP + 2 * t;
-    const int xrow = 8 * mb + qperm(g);  // XV A-fragment row (conflict-free X reads)
-    const int pg = qperm(g);
-    double pacc[MAXS][4][2];
-    double gacc[2] = {0.0, 0.0};
-    double cacc[2] = {0.0, 0.0};
+    if (w < 4) {  // ---------------- group A: XV, U, c for rows 8 mb .. 8 mb + 7
+        const int mb = w;
+        const int xrow = 8 * mb + qperm(g);  // A-fragment / output row (conflict-free X reads)
+        double msf[4][2];                    // B frags of U = XV Ms^T in the permuted K order
+        double cacc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+        for (int64_t tau = tau0, i = 0; tau < tau1; ++tau, ++i) {
+            if (advance(tau)) {
+                // K step kk feeds XV column col(kk, t) = 8 (kk >> 1) + 2 t + (kk & 1) (the C layout)
+                const double *msg = p.ms + (int64_t)bi * 16 * kBxMP;
 #pragma unroll
-    for (int q = 0; q < MAXS; ++q)
+                for (int kk = 0; kk < 4; ++kk)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) pacc[q][k][0] = pacc[q][k][1] = 0.0;
-    int bi = bi0 - 1;
-    int64_t tb = 0, te = 0, r0 = 0, n = 0;
-    for (int64_t tau = tau0, i = 0; tau < tau1; ++tau, ++i) {
-        if (tau >= te) {  // next slice: load its Ms (the previous tile's barrier protects ms)
-            do {
-                ++bi;
-                tb = __ldcg(p.toff + bi);
-                te = __ldcg(p.toff + bi + 1);
-            } while (tau >= te);
-            const int4 mt = __ldcg(p.meta + nsmall + bi);
-            r0 = mt.x;
-            n = mt.y;
-            for (int e = tid; e < 16 * kBxMP; e += kCW * 32) ms[e] = __ldcg(p.ms + (int64_t)bi * 16 * kBxMP + e);
-        }
-        const int64_t row0 = r0 + (tau - tb) * kTR;
-        const int nvalid = (int)min((int64_t)kTR, r0 + n - row0);
-        const int st = (int)(i % NST);
-        mbar_wait(&full[st], (uint32_t)((i / NST) & 1));
-        const double *xt = xs + st * SD;
-        // ---- XV = X V (warp: rows 8mb.., cols 8nb..)
-        {
-            double acc[2] = {0.0, 0.0}, acc2[2] = {0.0, 0.0};
+                    for (int nb = 0; nb < 2; ++nb)
+                        msf[kk][nb] = __ldcg(msg + (8 * nb + g) * kBxMP + 8 * (kk >> 1) + 2 * t + (kk & 1));
+            }
+            const int64_t row0 = r0 + (tau - tb) * kTR;
+            const int nvalid = (int)min((int64_t)kTR, r0 + n - row0);
+            const int st = (int)(i % NST);
+            mbar_wait(&full[st], (uint32_t)((i / NST) & 1));
+            const double *xt = xs + st * SD;
+            double xa[2][2][2];  // [nb][even/odd K chain][2]
+#pragma unroll
+            for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) xa[nb][c][0] = xa[nb][c][1] = 0.0;
+#pragma unroll
             for (int s = 0; s < JS; ++s) {
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const double2 a = *reinterpret_cast<const double2 *>(xt + s * 512 + swz(xrow, 4 * h + t));
-                    const double2 b = *reinterpret_cast<const double2 *>(vrow + 16 * s + 8 * h);
-                    dmma884(acc, a.x, b.x);
-                    dmma884(acc2, a.y, b.y);
+#pragma unroll
+                    for (int nb = 0; nb < 2; ++nb) {
+                        const double2 b = *reinterpret_cast<const double2 *>(vt + (8 * nb + g) * VTP + 16 * s + 8 * h + 2 * t);
+                        dmma884(xa[nb][0], a.x, b.x);
+                        dmma884(xa[nb][1], a.y, b.y);
+                    }
                 }
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
             const bool ok = xrow < nvalid;
-            *reinterpret_cast<double2 *>(xvs + swz_e(xrow, 8 * nb + 2 * t)) =
-                make_double2(ok ? acc[0] + acc2[0] : 0.0, ok ? acc[1] + acc2[1] : 0.0);
-        }
-        compute_bar();  // xvs complete; also: ms of a new slice is visible
-        // ---- U = XV Ms^T (warp: rows 8mb + g, cols 8nb..), c partial; U -> global and us
-        {
-            const int row = 8 * mb + g;
-            double ua[2] = {0.0, 0.0};
+            double xv[2][2];
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-                const double a = xvs[swz_e(row, 4 * kk + t)];
-                dmma884(ua, a, ms[(8 * nb + g) * kBxMP + 4 * kk + t]);
+            for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) xv[nb][e] = ok ? xa[nb][0][e] + xa[nb][1][e] : 0.0;
+            // U = XV Ms^T: A fragment of K step kk = this lane's XV value xv[kk >> 1][kk & 1]
+            double ua[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+                for (int nb = 0; nb < 2; ++nb) dmma884(ua[nb], xv[kk >> 1][kk & 1], msf[kk][nb]);
+            const int bsel = (int)(i & 1);
+            if (i >= 2) mbar_wait(&ufree[bsel], (uint32_t)(((i >> 1) - 1) & 1));
+            double *ub = ubuf + bsel * 512;
+#pragma unroll
+            for (int nb = 0; nb < 2; ++nb) {
+                const int col = 8 * nb + 2 * t;
+                cacc[nb][0] = fma(xv[nb][0], ua[nb][0], cacc[nb][0]);
+                cacc[nb][1] = fma(xv[nb][1], ua[nb][1], cacc[nb][1]);
+                *reinterpret_cast<double2 *>(ub + swz_e(xrow, col)) = make_double2(ua[nb][0], ua[nb][1]);
+                if (ok && col < R)
+                    *reinterpret_cast<double2 *>(p.U + (row0 + xrow) * R + col) = make_double2(ua[nb][0], ua[nb][1]);
             }
-            const int col = 8 * nb + 2 * t;
-            const double2 xv2 = *reinterpret_cast<const double2 *>(xvs + swz_e(row, col));
-            const bool ok = row < nvalid;
-            const double u0 = ok ? ua[0] : 0.0, u1 = ok ? ua[1] : 0.0;
-            cacc[0] = fma(xv2.x, u0, cacc[0]);
-            cacc[1] = fma(xv2.y, u1, cacc[1]);
-            *reinterpret_cast<double2 *>(us + row * kBxUP + col) = make_double2(u0, u1);
-            if (ok && col < R) *reinterpret_cast<double2 *>(p.U + (row0 + row) * R + col) = make_double2(u0, u1);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&uready[bsel]);
+            if (tau == te - 1 || tau == tau1 - 1) {  // c partial of (slice, CTA): row block mb
+                double *cp = p.parts + (int64_t)(bi + blockIdx.x) * PD + (int64_t)J * 16 + 256 + mb * 16;
+#pragma unroll
+                for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        double v = cacc[nb][e];
+                        v += __shfl_xor_sync(FULL_MASK, v, 4);
+                        v += __shfl_xor_sync(FULL_MASK, v, 8);
+                        v += __shfl_xor_sync(FULL_MASK, v, 16);
+                        if (g == 0) cp[8 * nb + 2 * t + e] = v;
+                        cacc[nb][e] = 0.0;
+                    }
+            }
         }
-        // ---- P += X^T XV (warp: strip(s) w, w + 8; 2x2 DMMA block per LDS pair)
+        return;
+    }
+    // ---------------- group B: P += X^T U (strips b, b + 4, ...), gram tile b
+    const int b = w - 4;
+    const int pg = qperm(g);
+    const int mi = b >> 1, ni = b & 1;
+    double pacc[MAXS][4][2];
+    double gacc[2] = {0.0, 0.0};
+#pragma unroll
+    for (int q = 0; q < MAXS; ++q)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) pacc[q][k][0] = pacc[q][k][1] = 0.0;
+    for (int64_t tau = tau0, i = 0; tau < tau1; ++tau, ++i) {
+        advance(tau);
+        const int st = (int)(i % NST);
+        const int bsel = (int)(i & 1);
+        mbar_wait(&uready[bsel], (uint32_t)((i >> 1) & 1));
+        mbar_wait(&full[st], (uint32_t)((i / NST) & 1));  // completed long ago (group A waited on it)
+        const double *xt = xs + st * SD;
+        const double *ub = ubuf + bsel * 512;
 #pragma unroll
         for (int kk = 0; kk < kTR / 4; ++kk) {
             const int row = 4 * kk + t;
-            const double2 b = *reinterpret_cast<const double2 *>(xvs + swz(row, pg));  // XV[row][2pg, 2pg+1]
+            const double2 bu = *reinterpret_cast<const double2 *>(ub + swz(row, pg));  // U[row][2pg, 2pg+1]
 #pragma unroll
             for (int q = 0; q < MAXS; ++q) {
-                const int s = w + kCW * q;
+                const int s = b + 4 * q;
                 if (s < JS) {
                     const double2 a = *reinterpret_cast<const double2 *>(xt + s * 512 + swz(row, pg));
-                    dmma884(pacc[q][0], a.x, b.x);
-                    dmma884(pacc[q][1], a.x, b.y);
-                    dmma884(pacc[q][2], a.y, b.x);
-                    dmma884(pacc[q][3], a.y, b.y);
+                    dmma884(pacc[q][0], a.x, bu.x);
+                    dmma884(pacc[q][1], a.x, bu.y);
+                    dmma884(pacc[q][2], a.y, bu.x);
+                    dmma884(pacc[q][3], a.y, bu.y);
                 }
             }
+            dmma884(gacc, ub[swz_e(row, 8 * mi + g)], ub[swz_e(row, 8 * ni + g)]);
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[st]);
-        compute_bar();  // us complete; xvs / us free for the next tile after the gram step
-        // ---- gram += U^T U: 8 warps = 4 tiles x 2 K-halves
-        {
-            const int mi = (w & 3) >> 1, ni = w & 1, kh = w >> 2;
-#pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-                const int row = 4 * (kk + 4 * kh) + t;
-                dmma884(gacc, us[row * kBxUP + 8 * mi + g], us[row * kBxUP + 8 * ni + g]);
-            }
+        if (lane == 0) {
+            mbar_arrive(&empty[st]);
+            mbar_arrive(&ufree[bsel]);
         }
-        // ---- segment end: flush the partials of (slice bi, this CTA)
-        if (tau == te - 1 || tau == tau1 - 1) {
-            double *part = p.parts + (int64_t)(bi + blockIdx.x) * BigxSmem::part_doubles(J);
+        if (tau == te - 1 || tau == tau1 - 1) {  // P strips and gram tile of (slice, CTA)
+            double *part = p.parts + (int64_t)(bi + blockIdx.x) * PD;
 #pragma unroll
             for (int q = 0; q < MAXS; ++q) {
-                const int s = w + kCW * q;
+                const int s = b + 4 * q;
                 if (s < JS) {
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
@@ -364,44 +417,32 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_bigx(const __grid_constant
                     }
                 }
             }
-            {
-                const int mi = (w & 3) >> 1, ni = w & 1, kh = w >> 2;
-                double *gp = part + (int64_t)J * 16 + kh * 256;
+            double *gp = part + (int64_t)J * 16;
 #pragma unroll
-                for (int e = 0; e < 2; ++e) gp[(8 * mi + g) * 16 + 8 * ni + 2 * t + e] = gacc[e];
-                gacc[0] = gacc[1] = 0.0;
-            }
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                double v = cacc[e];
-                v += __shfl_xor_sync(FULL_MASK, v, 4);
-                v += __shfl_xor_sync(FULL_MASK, v, 8);
-                v += __shfl_xor_sync(FULL_MASK, v, 16);
-                if (g == 0) part[(int64_t)J * 16 + 512 + mb * 16 + 8 * nb + 2 * t + e] = v;
-                cacc[e] = 0.0;
-            }
+            for (int e = 0; e < 2; ++e) gp[(8 * mi + g) * 16 + 8 * ni + 2 * t + e] = gacc[e];
+            gacc[0] = gacc[1] = 0.0;
         }
     }
 }
 
 // ---------------------------------------------------------------------------
-// k_bigx_post: one CTA (256 threads) per big slice
+// k_bigx_post: one CTA (256 threads) per big slice.  The P / gram / c segment
+// sums are issued first (independent of w), then warp 0 solves for w, then
+// F slot = P diag(w) and G slot = gram o w w^T are written.
 // ---------------------------------------------------------------------------
+constexpr int kPostPer = 8;  // P entries per thread: J * 16 <= 256 * kPostPer (J <= 128)
 __global__ void __launch_bounds__(256) k_bigx_post(BigxParams p) {
     constexpr int RB = kBxRB, LDV = RB + 2, LDL = RB + 1;
-    extern __shared__ __align__(16) double smp[];
-    const int J = p.J, R = p.R;
-    double *psum = smp;                   // J x 16
-    double *vtv_s = psum + J * 16;        // RB x LDV
-    double *gram_s = vtv_s + RB * LDV;    // RB x LDL
-    double *dns = gram_s + RB * LDL;      // RB x LDL
-    double *lu = dns + RB * LDL;          // RB x LDL
-    double *vec = lu + RB * LDL;          // c | w | buf(RB+2) | spare
-    double *ms = vec + 4 * RB + 8;        // 16 x MP
-    int *piv = reinterpret_cast<int *>(ms + 16 * kBxMP);
+    __shared__ double vtv_s[RB * LDV];
+    __shared__ double gram_s[RB * LDL];
+    __shared__ double dns[RB * LDL];
+    __shared__ double lu[RB * LDL];
+    __shared__ __align__(16) double vec[4 * RB + 8];  // c | w | gj scratch
+    __shared__ int piv[RB];
     pdl_wait();
     pdl_trigger();
     const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
+    const int J = p.J, R = p.R;
     const int nsmall = __ldcg(p.plan_counts), nbig = __ldcg(p.plan_counts + 1);
     const int bi = blockIdx.x;
     if (bi >= nbig) return;
@@ -413,24 +454,28 @@ __global__ void __launch_bounds__(256) k_bigx_post(BigxParams p) {
     const int64_t c0 = cta_of_tile(__ldcg(p.toff + bi), T, G);
     const int64_t c1 = cta_of_tile(__ldcg(p.toff + bi + 1) - 1, T, G);
     const int64_t PD = BigxSmem::part_doubles(J);
-    // segment sums in CTA order
-    for (int e = tid; e < J * 16; e += blockDim.x) {
-        double acc = 0.0;
-        for (int64_t c = c0; c <= c1; ++c) acc += __ldcg(p.parts + (bi + c) * PD + e);
-        psum[e] = acc;
-    }
-    if (tid < 256) {
-        double acc = 0.0;
-        for (int64_t c = c0; c <= c1; ++c) {
-            const double *gp = p.parts + (bi + c) * PD + (int64_t)J * 16;
-            acc += __ldcg(gp + tid) + __ldcg(gp + 256 + tid);
+    const double *base = p.parts + (bi + c0) * PD;
+    const int nseg = (int)(c1 - c0 + 1);
+    // P (J x 16) segment sums in CTA order: thread tid owns entries tid + 256 k
+    double pv[kPostPer];
+#pragma unroll
+    for (int k = 0; k < kPostPer; ++k) pv[k] = 0.0;
+    for (int sg = 0; sg < nseg; ++sg) {
+#pragma unroll
+        for (int k = 0; k < kPostPer; ++k) {
+            const int e = tid + 256 * k;
+            if (e < J * 16) pv[k] += __ldcg(base + sg * PD + e);
         }
+    }
+    {
+        double acc = 0.0;
+        for (int sg = 0; sg < nseg; ++sg) acc += __ldcg(base + sg * PD + (int64_t)J * 16 + tid);
         gram_s[(tid / 16) * LDL + tid % 16] = acc;
     }
     if (tid < 16) {
         double acc = 0.0;
-        for (int64_t c = c0; c <= c1; ++c) {
-            const double *cp = p.parts + (bi + c) * PD + (int64_t)J * 16 + 512;
+        for (int sg = 0; sg < nseg; ++sg) {
+            const double *cp = base + sg * PD + (int64_t)J * 16 + 256;
             acc += ((__ldcg(cp + tid) + __ldcg(cp + 16 + tid)) + (__ldcg(cp + 32 + tid) + __ldcg(cp + 48 + tid)));
         }
         vec[tid] = tid < R ? p.lam * (fresh ? 0.0 : __ldcg(p.C + (int64_t)wrow * R + tid)) + acc : 0.0;  // c_new
@@ -439,7 +484,6 @@ __global__ void __launch_bounds__(256) k_bigx_post(BigxParams p) {
         const int a = i / LDV, b = i % LDV;
         vtv_s[i] = (a < R && b < R) ? __ldcg(p.vtv + a * R + b) : 0.0;
     }
-    for (int e = tid; e < 16 * kBxMP; e += blockDim.x) ms[e] = __ldcg(p.ms + (int64_t)bi * 16 * kBxMP + e);
     if (tid < RB && !fresh)
         for (int z = 0; z < R; ++z)
             dns[tid * LDL + z] = tid < R ? __ldcg(p.D + (int64_t)wrow * R * R + (int64_t)z * R + tid) : 0.0;
@@ -496,23 +540,15 @@ __global__ void __launch_bounds__(256) k_bigx_post(BigxParams p) {
     }
     __syncthreads();
     const double *wv = vec + RB;
-    // ---- G slot: gram o w w^T;  F slot: P Ms^T diag(w)
     if (tid < R * R) {
         const int a = tid / R, b = tid % R;
         p.G_slots[(int64_t)bi * R * R + tid] = gram_s[a * LDL + b] * wv[a] * wv[b];
     }
     double *fs = p.F_slots + (int64_t)bi * J * R;
-    for (int e = tid; e < J * R; e += blockDim.x) {
-        const int j = e / R, r = e % R;
-        const double *pr = psum + j * 16;
-        const double *mr = ms + r * kBxMP;
-        double acc = 0.0;
 #pragma unroll
-        for (int z = 0; z < 16; ++z) acc = fma(pr[z], mr[z], acc);
-        fs[e] = acc * wv[r];
+    for (int k = 0; k < kPostPer; ++k) {
+        const int e = tid + 256 * k;  // P entry (j, r) = (e / 16, e % 16)
+        const int j = e >> 4, r = e & 15;
+        if (e < J * 16 && r < R) fs[j * R + r] = pv[k] * wv[r];
     }
-}
-
-size_t bigx_post_smem(int J) {
-    return sizeof(double) * ((size_t)J * 16 + 18 * 18 + 3 * 16 * 17 + 4 * 16 + 8 + 16 * kBxMP) + 16 * sizeof(int) + 64;
 }

@@ -71,11 +71,13 @@ __device__ __forceinline__ int plan_bucket(int64_t n) {
 }
 
 // hist[b][c]: bucket-b count of chunk c (bucket-major; one CTA of kPlanChunk threads per chunk)
-// tflag (optional, zeroed by the host): tflag[t] = 1 for every 32-row tile
-// holding a row of a small slice -- the tiles the small-row GEMMs must visit
-// when big slices take the fused path (dash_bigx.cuh).
+// tflag (optional): tflag[t] = tgen for every 32-row tile holding a row of a
+// small slice -- the tiles the small-row GEMMs must visit when big slices take
+// the fused path (dash_bigx.cuh).  tgen changes every update, so stale marks
+// never match and the array is never cleared (zeroed once at allocation).
 __global__ void __launch_bounds__(kPlanChunk) k_plan_count(const int64_t *__restrict__ row_ptr, int M,
-                                                           int *__restrict__ hist, uint8_t *__restrict__ tflag) {
+                                                           int *__restrict__ hist, uint32_t *__restrict__ tflag,
+                                                           uint32_t tgen) {
     pdl_trigger();
     __shared__ int h[kPlanBuckets];
     for (int i = threadIdx.x; i < kPlanBuckets; i += blockDim.x) h[i] = 0;
@@ -85,7 +87,7 @@ __global__ void __launch_bounds__(kPlanChunk) k_plan_count(const int64_t *__rest
         const int64_t r0 = row_ptr[m], n = row_ptr[m + 1] - r0;
         atomicAdd(&h[plan_bucket(n)], 1);
         if (tflag != nullptr && n > 0 && n <= kSmallRows)
-            for (int64_t t = r0 / 32; t <= (r0 + n - 1) / 32; ++t) tflag[t] = 1;
+            for (int64_t t = r0 / 32; t <= (r0 + n - 1) / 32; ++t) tflag[t] = tgen;
     }
     __syncthreads();
     for (int i = threadIdx.x; i < kPlanBuckets; i += blockDim.x) hist[(size_t)i * gridDim.x + blockIdx.x] = h[i];

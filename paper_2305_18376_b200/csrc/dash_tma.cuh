@@ -40,6 +40,15 @@ __device__ __forceinline__ int swz(int r, int c) { return r * 16 + ((c ^ (r & 7)
 // permutation is undone when results are written.
 __device__ __forceinline__ int qperm(int g) { return ((g & 1) << 2) | (g >> 1); }
 
+// Tile-visit mask for 32 consecutive local tiles i0 .. i0+31 of this CTA
+// (tile = blockIdx.x + i * gridDim.x): one coalesced flag load per lane and a
+// ballot, so the skip test costs one global round trip per 32 tiles.
+__device__ __forceinline__ unsigned visit_mask(const uint32_t *tflag, uint32_t tgen, int64_t i0, int64_t mine) {
+    const int64_t i = i0 + lane_id();
+    const bool v = i < mine && (tflag == nullptr || tflag[blockIdx.x + i * gridDim.x] == tgen);
+    return __ballot_sync(FULL_MASK, v);
+}
+
 struct TmaSmem {
     static __host__ __device__ int strips(int J) { return (J + 15) / 16; }
     static __host__ __device__ int vtp(int J) { return strips(J) * 16 + 8; }  // Vt pitch (== 8 mod 16)
@@ -68,12 +77,13 @@ struct FusedPrologue {
     int snap, last;
 };
 
-// tflag (optional): visit only tiles with tflag[tile] != 0 (the small-slice
+// tflag (optional): visit only tiles with tflag[tile] == tgen (the small-slice
 // tiles when big slices take the fused path); producer and consumers skip the
 // same tiles, the ring advances only on visited ones.
 __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_xv3(const __grid_constant__ CUtensorMap tmX, int64_t N, int J,
                                                           const double *__restrict__ V, int R, double *__restrict__ XV,
-                                                          FusedPrologue pro, const uint8_t *__restrict__ tflag) {
+                                                          FusedPrologue pro, const uint32_t *__restrict__ tflag,
+                                                          uint32_t tgen) {
     extern __shared__ __align__(16) double sm_raw[];
     double *sm = align1k(sm_raw);
     const int JS = TmaSmem::strips(J), VTP = TmaSmem::vtp(J);
@@ -121,17 +131,22 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_xv3(const __grid_constant_
     const int64_t ntiles = (N + kTR - 1) / kTR;
     const int64_t mine = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     if (w == kCW) {
-        if (lane == 0) {
-            for (int64_t i = 0, k = 0; i < mine; ++i) {
-                const int64_t tile = blockIdx.x + i * gridDim.x;
-                if (tflag != nullptr && !tflag[tile]) continue;
-                const int st = (int)(k % kStages);
-                if (k >= kStages) mbar_wait(&empty[st], (uint32_t)(((k / kStages) - 1) & 1));
-                ++k;
-                const int r0 = (int)(tile * kTR);
-                mbar_arrive_expect_tx(&full[st], (uint32_t)JS * 4096u);
-                for (int s = 0; s < JS; ++s) tma_load_2d(xs + st * SD + s * 512, &tmX, 16 * s, r0, &full[st]);
+        for (int64_t i0 = 0, k = 0; i0 < mine; i0 += 32) {
+            unsigned vm = visit_mask(tflag, tgen, i0, mine);
+            if (lane == 0) {
+                while (vm) {
+                    const int b = __ffs(vm) - 1;
+                    vm &= vm - 1;
+                    const int64_t tile = blockIdx.x + (i0 + b) * gridDim.x;
+                    const int st = (int)(k % kStages);
+                    if (k >= kStages) mbar_wait(&empty[st], (uint32_t)(((k / kStages) - 1) & 1));
+                    ++k;
+                    const int r0 = (int)(tile * kTR);
+                    mbar_arrive_expect_tx(&full[st], (uint32_t)JS * 4096u);
+                    for (int s = 0; s < JS; ++s) tma_load_2d(xs + st * SD + s * 512, &tmX, 16 * s, r0, &full[st]);
+                }
             }
+            __syncwarp();
         }
         pdl_wait();
         return;
@@ -139,8 +154,10 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_xv3(const __grid_constant_
     const int mb = w & 3, nb = w >> 2;  // 8-row block, 8-column block of the 32 x 16 output tile
     const double *vrow = vt + (8 * nb + g) * VTP + 2 * t;
     const int row = 8 * mb + qperm(g);  // tile row of this lane's A fragment and output
+    unsigned vm = 0;
     for (int64_t i = 0, k = -1; i < mine; ++i) {
-        if (tflag != nullptr && !tflag[blockIdx.x + i * gridDim.x]) continue;
+        if ((i & 31) == 0) vm = visit_mask(tflag, tgen, i, mine);
+        if (!((vm >> (i & 31)) & 1u)) continue;
         ++k;
         const int st = (int)(k % kStages);
         mbar_wait(&full[st], (uint32_t)((k / kStages) & 1));
@@ -175,7 +192,7 @@ template <int MAXS>
 __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_fgemm3(const __grid_constant__ CUtensorMap tmX,
                                                              const __grid_constant__ CUtensorMap tmU, int64_t N, int J,
                                                              int R, double *__restrict__ F_slots,
-                                                             const uint8_t *__restrict__ tflag) {
+                                                             const uint32_t *__restrict__ tflag, uint32_t tgen) {
     extern __shared__ __align__(16) double sm_raw[];
     double *sm = align1k(sm_raw);
     const int JS = TmaSmem::strips(J);
@@ -200,18 +217,23 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_fgemm3(const __grid_consta
     const int64_t ntiles = (N + kTR - 1) / kTR;
     const int64_t mine = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     if (w == kCW) {
-        if (lane == 0) {
-            for (int64_t i = 0, k = 0; i < mine; ++i) {
-                const int64_t tile = blockIdx.x + i * gridDim.x;
-                if (tflag != nullptr && !tflag[tile]) continue;
-                const int st = (int)(k % kStages);
-                if (k >= kStages) mbar_wait(&empty[st], (uint32_t)(((k / kStages) - 1) & 1));
-                ++k;
-                const int r0 = (int)(tile * kTR);
-                mbar_arrive_expect_tx(&full[st], (uint32_t)(JS + 1) * 4096u);
-                for (int s = 0; s < JS; ++s) tma_load_2d(xs + st * SD + s * 512, &tmX, 16 * s, r0, &full[st]);
-                tma_load_2d(xs + st * SD + JS * 512, &tmU, 0, r0, &full[st]);
+        for (int64_t i0 = 0, k = 0; i0 < mine; i0 += 32) {
+            unsigned vm = visit_mask(tflag, tgen, i0, mine);
+            if (lane == 0) {
+                while (vm) {
+                    const int b = __ffs(vm) - 1;
+                    vm &= vm - 1;
+                    const int64_t tile = blockIdx.x + (i0 + b) * gridDim.x;
+                    const int st = (int)(k % kStages);
+                    if (k >= kStages) mbar_wait(&empty[st], (uint32_t)(((k / kStages) - 1) & 1));
+                    ++k;
+                    const int r0 = (int)(tile * kTR);
+                    mbar_arrive_expect_tx(&full[st], (uint32_t)(JS + 1) * 4096u);
+                    for (int s = 0; s < JS; ++s) tma_load_2d(xs + st * SD + s * 512, &tmX, 16 * s, r0, &full[st]);
+                    tma_load_2d(xs + st * SD + JS * 512, &tmU, 0, r0, &full[st]);
+                }
             }
+            __syncwarp();
         }
         return;
     }
@@ -221,8 +243,10 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_fgemm3(const __grid_consta
     for (int q = 0; q < MAXS; ++q)
 #pragma unroll
         for (int k = 0; k < 4; ++k) acc[q][k][0] = acc[q][k][1] = 0.0;
+    unsigned vm = 0;
     for (int64_t i = 0, k = -1; i < mine; ++i) {
-        if (tflag != nullptr && !tflag[blockIdx.x + i * gridDim.x]) continue;
+        if ((i & 31) == 0) vm = visit_mask(tflag, tgen, i, mine);
+        if (!((vm >> (i & 31)) & 1u)) continue;
         ++k;
         const int st = (int)(k % kStages);
         mbar_wait(&full[st], (uint32_t)((k / kStages) & 1));

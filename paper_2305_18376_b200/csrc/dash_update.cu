@@ -794,6 +794,7 @@ struct dash_ctx {
     bool tma = false;     // ... with tensor-map (swizzled box) copies: k_xv3 / k_fgemm3
     bool bigx = false;    // big slices on the fused single-read path (dash_bigx.cuh)
     int bigx_nbig = 0, bigx_grid = 0;
+    uint32_t tgen = 0;  // generation of the small-tile marks
     void *plan_p = nullptr;  // SlicePlan of the update in flight
     // phase timing (bench): events around every launch when enabled
     int prof = 0;
@@ -987,7 +988,7 @@ SlicePlan &plan_of(dash_ctx *ctx) { return *reinterpret_cast<SlicePlan *>(ctx->p
 
 // device plan (R <= 16): meta[M] in plan order + plan_counts {nsmall, nbig}
 template <class B>
-int device_plan(dash_ctx *ctx, cudaStream_t st, const B *b, uint8_t *tflag) {
+int device_plan(dash_ctx *ctx, cudaStream_t st, const B *b, uint32_t *tflag) {
     const int M = b->M;
     const int nch = std::max(1, (M + kPlanChunk - 1) / kPlanChunk);
     // hist[B][nch] | off[B][nch] | tot[B] | counts[2]
@@ -1000,8 +1001,7 @@ int device_plan(dash_ctx *ctx, cudaStream_t st, const B *b, uint8_t *tflag) {
     int *counts = tot + kPlanBuckets;
     PhaseScope ps(ctx, st, PH_ROWSLICE);
     // first kernel of the update: a normal launch (fully ordered after the previous update)
-    if (tflag) cudaMemsetAsync(tflag, 0, (size_t)((b->N + kTR - 1) / kTR), st);
-    k_plan_count<<<nch, kPlanChunk, 0, st>>>(b->row_ptr, M, hist, tflag);
+    k_plan_count<<<nch, kPlanChunk, 0, st>>>(b->row_ptr, M, hist, tflag, ctx->tgen);
     ctx->last_launches += 2;  // three kernels under one phase
     return launch_k(true, k_plan_scan, kPlanBuckets, kScanThreads, 0, st, (const int *)hist, nch, off, tot) ||
            launch_k(true, k_plan_scatter, (nch + 3) / 4, 128, 0, st, (const int64_t *)b->row_ptr, b->state_row,
@@ -1225,7 +1225,7 @@ bool tma_ok(const dash_batch_f64 *b, int J, int R) {
 }
 
 int launch_xv3(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, const double *V, int R, double *XV,
-               const FusedPrologue &pro, bool pdl, const uint8_t *tflag = nullptr) {
+               const FusedPrologue &pro, bool pdl, const uint32_t *tflag = nullptr) {
     CUtensorMap mx;
     if (!make_box_map(&mx, b->X, J, b->N, b->ldx)) return DASH_E_CUDA;
     const size_t smem = TmaSmem::xv_bytes(J);
@@ -1235,12 +1235,12 @@ int launch_xv3(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, c
         attr = smem;
     }
     PhaseScope ps(ctx, st, PH_XV);
-    return launch_k(pdl, k_xv3, ctx->num_sms, kCW * 32 + 32, smem, st, mx, b->N, J, V, R, XV, pro, tflag);
+    return launch_k(pdl, k_xv3, ctx->num_sms, kCW * 32 + 32, smem, st, mx, b->N, J, V, R, XV, pro, tflag, ctx->tgen);
 }
 
 template <int MAXS>
 void launch_f3_t(dash_ctx *ctx, cudaStream_t st, const CUtensorMap &mx, const CUtensorMap &mu, int64_t N, int J,
-                 int R, double *F_slots, const uint8_t *tflag) {
+                 int R, double *F_slots, const uint32_t *tflag) {
     const size_t smem = TmaSmem::f_bytes(J);
     static size_t attr = 0;
     if (attr < smem) {
@@ -1248,11 +1248,12 @@ void launch_f3_t(dash_ctx *ctx, cudaStream_t st, const CUtensorMap &mx, const CU
         attr = smem;
     }
     PhaseScope ps(ctx, st, PH_FGEMM);
-    launch_k(true, k_fgemm3<MAXS>, ctx->num_sms, kCW * 32 + 32, smem, st, mx, mu, N, J, R, F_slots, tflag);
+    launch_k(true, k_fgemm3<MAXS>, ctx->num_sms, kCW * 32 + 32, smem, st, mx, mu, N, J, R, F_slots, tflag,
+             ctx->tgen);
 }
 
 int launch_f3(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, const double *US, int R,
-              double *F_slots, const uint8_t *tflag = nullptr) {
+              double *F_slots, const uint32_t *tflag = nullptr) {
     CUtensorMap mx, mu;
     if (!make_box_map(&mx, b->X, J, b->N, b->ldx) || !make_box_map(&mu, US, R, b->N, R)) return DASH_E_CUDA;
     if (TmaSmem::strips(J) <= kCW) launch_f3_t<1>(ctx, st, mx, mu, b->N, J, R, F_slots, tflag);
@@ -1270,30 +1271,14 @@ int launch_bigx(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, const B
     CUtensorMap mx;
     if (!make_box_map(&mx, b->X, bp.J, b->N, b->ldx)) return DASH_E_CUDA;
     const size_t smem = BigxSmem::bytes(bp.J);
-    int rc;
-    if (BigxSmem::strips(bp.J) <= kCW) {
-        static size_t attr = 0;
-        if (attr < smem) {
-            cudaFuncSetAttribute(k_bigx<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attr = smem;
-        }
-        rc = launch_k(true, k_bigx<1>, bp.G, kCW * 32 + 32, smem, st, mx, bp);
-    } else {
-        static size_t attr = 0;
-        if (attr < smem) {
-            cudaFuncSetAttribute(k_bigx<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attr = smem;
-        }
-        rc = launch_k(true, k_bigx<2>, bp.G, kCW * 32 + 32, smem, st, mx, bp);
-    }
+    const int js = BigxSmem::strips(bp.J);
+    auto go = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        return launch_k(true, kern, bp.G, kCW * 32 + 32, smem, st, mx, bp);
+    };
+    const int rc = js == 8 ? go(k_bigx<2, 8>) : js <= 4 ? go(k_bigx<1, 0>) : js <= 8 ? go(k_bigx<2, 0>) : go(k_bigx<4, 0>);
     if (rc) return rc;
-    const size_t ps_smem = bigx_post_smem(bp.J);
-    static size_t pattr = 0;
-    if (pattr < ps_smem) {
-        cudaFuncSetAttribute(k_bigx_post, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ps_smem);
-        pattr = ps_smem;
-    }
-    return launch_k(true, k_bigx_post, nbig, 256, ps_smem, st, bp);
+    return launch_k(true, k_bigx_post, nbig, 256, 0, st, bp);
 }
 
 template <int RP>
@@ -1369,14 +1354,24 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
         if (ctx->stream) ctx->nsplit = ctx->num_sms * (f32 ? TmaSmem32::row_groups(J) : 1);
         if constexpr (!f32) ctx->tma = ctx->stream && tma_ok(b, J, R);
         {
-            static const bool no_bigx = getenv("DASH_BIGX") == nullptr;  // opt-in while being tuned
+            static const bool no_bigx = getenv("DASH_NO_BIGX") != nullptr;  // A/B switch: the k_big path
             const SlicePlan &pl = plan_of(ctx);
-            ctx->bigx = !f32 && !no_bigx && ctx->tma && pl.big_dev && pl.gbig > 0 && BigxSmem::strips(J) <= 16 &&
+            ctx->bigx = !f32 && !no_bigx && ctx->tma && pl.big_dev && pl.gbig > 0 && J * 16 <= kPostPer * 256 &&
                         BigxSmem::bytes(J) <= 227 * 1024;
             ctx->bigx_nbig = ctx->bigx ? pl.gbig : 0;
             ctx->bigx_grid = ctx->bigx ? (int)std::min<int64_t>(ctx->num_sms, pl.big_tiles) : 0;
-            if (ctx->bigx && (ensure(ctx->tflag, (size_t)((N + kTR - 1) / kTR) + 16) ||
-                              ensure(ctx->bx_ms, sizeof(double) * (size_t)pl.gbig * 16 * kBxMP) ||
+            if (ctx->bigx) {
+                const size_t tb = sizeof(uint32_t) * (size_t)((N + kTR - 1) / kTR + 16);
+                if (ctx->tflag.cap < tb) {  // zeroed once: marks are generation-tagged
+                    if (ensure(ctx->tflag, tb)) return DASH_E_CUDA;
+                    cudaMemsetAsync(ctx->tflag.p, 0, ctx->tflag.cap, st);
+                }
+                if (++ctx->tgen == 0) {  // generation wrapped: clear, restart at 1
+                    cudaMemsetAsync(ctx->tflag.p, 0, ctx->tflag.cap, st);
+                    ctx->tgen = 1;
+                }
+            }
+            if (ctx->bigx && (ensure(ctx->bx_ms, sizeof(double) * (size_t)pl.gbig * 16 * kBxMP) ||
                               ensure(ctx->bx_toff, sizeof(int) * ((size_t)pl.gbig + 1)) ||
                               ensure(ctx->bx_parts, sizeof(double) * (size_t)(pl.gbig + ctx->bigx_grid) *
                                                         BigxSmem::part_doubles(J))))
@@ -1393,7 +1388,7 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
             return DASH_E_CUDA;
         if (!items.empty() && stage_items(ctx, st, items)) return DASH_E_CUDA;
         if (plan_of(ctx).split && M > 0 && N > 0 &&
-            device_plan(ctx, st, b, ctx->bigx ? (uint8_t *)ctx->tflag.p : nullptr))
+            device_plan(ctx, st, b, ctx->bigx ? (uint32_t *)ctx->tflag.p : nullptr))
             return DASH_E_CUDA;
         if (M > 0 && !ctx->stream) {  // row -> slice map: only the generic F GEMM needs it
             PhaseScope ps(ctx, st, PH_ROWSLICE);
@@ -1420,7 +1415,7 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
                 if (launch_xv3(ctx, st, b, J, s->V, R, XV, pro, pass == 0)) return DASH_E_CUDA;
             } else {
                 if (launch_xv3(ctx, st, b, J, s->V, R, XV, pro, pass == 0,
-                               ctx->bigx ? (const uint8_t *)ctx->tflag.p : nullptr))
+                               ctx->bigx ? (const uint32_t *)ctx->tflag.p : nullptr))
                     return DASH_E_CUDA;
             }
         } else if (ctx->stream) {
@@ -1490,7 +1485,7 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
                 if (launch_f3(ctx, st, b, J, (const double *)ctx->us.p, R, Fsl)) return DASH_E_CUDA;
             } else {
                 if (launch_f3(ctx, st, b, J, (const double *)ctx->us.p, R, Fsl,
-                              ctx->bigx ? (const uint8_t *)ctx->tflag.p : nullptr))
+                              ctx->bigx ? (const uint32_t *)ctx->tflag.p : nullptr))
                     return DASH_E_CUDA;
             }
         } else if (ctx->stream) {
@@ -1581,6 +1576,25 @@ int dash_ctx_status(dash_ctx *ctx, void *stream, int64_t *fail_slice_host) {
 }
 
 int dash_ctx_last_launches(const dash_ctx *ctx) { return ctx ? ctx->last_launches : 0; }
+
+int dash_host_row_ptr(const int64_t *counts, int64_t M, int64_t *row_ptr, int64_t *N_out) {
+    if (M < 0 || (M > 0 && (!counts || !row_ptr))) return DASH_E_ARG;
+    int64_t acc = 0;
+    if (row_ptr) row_ptr[0] = 0;
+    for (int64_t m = 0; m < M; ++m) {
+        const int64_t c = counts[m];
+        if (c < 0) return DASH_E_ARG;
+        acc += c;
+        row_ptr[m + 1] = acc;
+    }
+    if (N_out) *N_out = acc;
+    return DASH_OK;
+}
+
+int dash_ctx_path_flags(const dash_ctx *ctx) {
+    if (!ctx) return 0;
+    return (ctx->stream ? 1 : 0) | (ctx->tma ? 2 : 0) | (ctx->bigx ? 4 : 0);
+}
 
 #ifdef DASH_DEBUG_TIMING
 int dash_debug_timing(long long *host, int n) {

@@ -19,7 +19,8 @@ def local_error(batch_items, u_new, state):
     dev = state.device
     if (last is not None and last[0] == ids and hasattr(u_new, "device_tensor")
             and u_new.device_tensor is last[5]):
-        _, row_ptr, state_row, X, N, U = last
+        _, row_ptr, meta, X, N, U = last
+        state_row = meta[1][:len(row_ptr) - 1]  # device copy staged by the update
     else:
         counts = np.array([np.asarray(r).shape[0] for _, r in batch_items], dtype=np.int64)
         row_ptr = np.zeros(len(ids) + 1, dtype=np.int64)
@@ -41,7 +42,8 @@ def local_error_device(X, N, row_ptr, state_row, U, state):
     dev = state.device
     M = len(row_ptr) - 1
     rp = torch.as_tensor(np.asarray(row_ptr, dtype=np.int64), device=dev)
-    sr = torch.as_tensor(np.asarray(state_row, dtype=np.int32), device=dev)
+    sr = (state_row if isinstance(state_row, torch.Tensor)
+          else torch.as_tensor(np.asarray(state_row, dtype=np.int32), device=dev))
     slice_err = torch.empty(max(M, 1), dtype=torch.float64, device=dev)
     te = torch.empty((), dtype=torch.float64, device=dev)
     b = nat.DashBatch(X=int(X.data_ptr()), ldx=int(X.stride(0)), N=N, M=M, row_ptr=int(rp.data_ptr()),

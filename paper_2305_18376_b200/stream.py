@@ -379,17 +379,12 @@ class StreamState:
         new_ids = [sid for sid, _, is_new in entries if is_new]
         M = len(entries)
         counts = np.fromiter((r.shape[0] for _, r, _ in entries), dtype=np.int64, count=M)
-        row_ptr = np.zeros(M + 1, dtype=np.int64)
-        np.cumsum(counts, out=row_ptr[1:])
-        N = int(row_ptr[-1])
+        # items() order: existing slices, then new ones (tensor.py:166-171)
+        existing_rows = np.fromiter((self._row_of[sid] for sid, _, n in entries if not n), dtype=np.int32)
+        N, row_ptr, meta = self._stage_meta(counts, existing_rows, len(new_ids))
+        row_ptr = row_ptr.copy()  # kept by UpdateResult / local_error beyond the ring's lifetime
         # registration (stream.py:270-280): new rows appended in batch order
-        self._reserve(self._K + len(new_ids))
-        for sid in new_ids:
-            self._row_of[sid] = len(self.slice_ids)
-            self.slice_ids.append(sid)
-        state_row = np.fromiter((self._row_of[sid] for sid, _, _ in entries), dtype=np.int32, count=M)
-        is_new = np.fromiter((1 if n else 0 for _, _, n in entries), dtype=np.uint8, count=M)
-        self._K += len(new_ids)
+        self._register(new_ids)
 
         pin, X = self._stage_x(N)
         if N:
@@ -398,7 +393,7 @@ class StreamState:
             ev = torch.cuda.Event()
             ev.record()
             self._pin_event = ev
-        res = self._run(X, N, row_ptr, state_row, is_new, check=True,
+        res = self._run(X, N, row_ptr, meta, check=True,
                         ids=[sid for sid, _, _ in entries], allreduce=allreduce)
         U_dev, v_used = res
         # U history
@@ -412,7 +407,7 @@ class StreamState:
                 self._ublk[sid].append(ref)
         self.update_index += 1
         ids = [sid for sid, _, _ in entries]
-        self._last = (ids, row_ptr, state_row, X, N, U_dev)
+        self._last = (ids, row_ptr, meta, X, N, U_dev)
         return UpdateResult(
             update_index=self.update_index,
             u_new=_UNew(ids, row_ptr, U_dev),
@@ -428,36 +423,30 @@ class StreamState:
         state's dtype) in batch order -- existing slices (state rows ``existing_rows``) then the
         ``len(new_ids)`` new slices; ``counts`` their row counts.  No host sync
         unless ``check``.  Returns (U_new (N, R), v_used (J, R)) device tensors."""
-        M_old = len(existing_rows)
-        L = len(new_ids)
-        M = M_old + L
-        counts = np.asarray(counts, dtype=np.int64)
-        row_ptr = np.zeros(M + 1, dtype=np.int64)
-        np.cumsum(counts, out=row_ptr[1:])
-        N = int(row_ptr[-1])
-        self._reserve(self._K + L)
-        state_row = np.empty(M, dtype=np.int32)
-        state_row[:M_old] = existing_rows
-        state_row[M_old:] = np.arange(self._K, self._K + L, dtype=np.int32)
-        for sid in new_ids:
-            self._row_of[sid] = len(self.slice_ids)
-            self.slice_ids.append(sid)
-        self._K += L
-        is_new = np.zeros(M, dtype=np.uint8)
-        is_new[M_old:] = 1
-        U_dev, v_used = self._run(X, N, row_ptr, state_row, is_new, check=check, ids=None,
-                                  allreduce=allreduce)
+        N, row_ptr, meta = self._stage_meta(counts, existing_rows, len(new_ids))
+        self._register(new_ids)
+        U_dev, v_used = self._run(X, N, row_ptr, meta, check=check, ids=None, allreduce=allreduce)
         self.update_index += 1
-        self._last = (None, row_ptr, state_row, X, N, U_dev)
+        self._last = (None, row_ptr, meta, X, N, U_dev)
         return U_dev, v_used
 
-    def _run(self, X, N, row_ptr, state_row, is_new, check, ids, allreduce=None):
+    def _register(self, new_ids):
+        """stream.py:270-280: new slices take the next state rows, in batch order."""
+        L = len(new_ids)
+        self._reserve(self._K + L)
+        self._row_of.update(zip(new_ids, range(len(self.slice_ids), len(self.slice_ids) + L)))
+        self.slice_ids.extend(new_ids)
+        self._K += L
+
+    def _run(self, X, N, row_ptr, meta, check, ids, allreduce=None):
         dev = self.device
-        M = len(state_row)
+        M = len(row_ptr) - 1
         if N and X.dtype != self.dtype:
             raise TypeError(f"batch X is {X.dtype}, the stream state runs in {self.dtype}")
+        if N and X.shape[0] < N:
+            raise ValueError(f"batch X has {X.shape[0]} rows, the counts sum to {N}")
         f32 = self.dtype == torch.float32
-        rp_d, sr_d, nw_d = self._stage_meta(row_ptr, state_row, is_new)
+        rp_d, sr_d, nw_d = meta
         U = torch.empty((max(N, 0), self._R), dtype=self.dtype, device=dev)
         v_used = torch.empty((self.J, self._R), dtype=F64, device=dev)
         b = nat.DashBatch(X=_ptr(X), ldx=int(X.stride(0)) if N else self.J, N=N, M=M,
@@ -490,38 +479,53 @@ class StreamState:
             self.check()
         return U, v_used
 
-    def _stage_meta(self, row_ptr, state_row, is_new):
-        """Copy the CSR index arrays through a double-buffered pinned ring, so
-        the host never blocks on the previous update."""
-        M = len(state_row)
+    _META_RING = 3  # updates whose index arrays stay valid (local_error reads the last one)
+
+    def _stage_meta(self, counts, existing_rows, L):
+        """Pack the batch's CSR index arrays -- row_ptr (M+1) i64 | state_row
+        (M) i32 | is_new (M) u8 -- into one pinned ring slot (the prefix sum is
+        written there by the library's host helper) and copy them to the
+        device in ONE transfer; the host never waits for the GPU unless the
+        ring wraps onto a copy still in flight.  Returns (N, row_ptr host view,
+        (row_ptr, state_row, is_new) device views)."""
+        counts = np.ascontiguousarray(counts, dtype=np.int64)
+        M_old = len(existing_rows)
+        M = M_old + L
+        if counts.shape[0] != M:
+            raise ValueError(f"{counts.shape[0]} counts for {M_old} existing + {L} new slices")
+        o_sr = 8 * (M + 1)
+        o_nw = o_sr + ((4 * M + 7) // 8) * 8
+        nbytes = o_nw + M
         ring = getattr(self, "_meta_ring", None)
-        if ring is None or ring[0][1].shape[0] < M:
-            cap = max(256, int(M * 1.25) + 2)
-            ring = []
-            for _ in range(2):
-                ring.append([torch.empty(cap + 1, dtype=torch.int64, pin_memory=True),
-                             torch.empty(cap, dtype=torch.int32, pin_memory=True),
-                             torch.empty(cap, dtype=torch.uint8, pin_memory=True),
-                             torch.empty(cap + 1, dtype=torch.int64, device=self.device),
-                             torch.empty(cap, dtype=torch.int32, device=self.device),
-                             torch.empty(cap, dtype=torch.uint8, device=self.device),
-                             None])
+        if ring is None or ring[0][0].shape[0] < nbytes:
+            cap = max(4096, int(nbytes * 1.25) + 64)
+            ring = [[torch.empty(cap, dtype=torch.uint8, pin_memory=True),
+                     torch.empty(cap, dtype=torch.uint8, device=self.device), None]
+                    for _ in range(self._META_RING)]
             self._meta_ring = ring
             self._meta_i = 0
         slot = ring[self._meta_i]
-        self._meta_i ^= 1
-        if slot[6] is not None:
-            slot[6].synchronize()
-        slot[0][:M + 1].numpy()[:] = row_ptr
-        slot[1][:M].numpy()[:] = state_row
-        slot[2][:M].numpy()[:] = is_new
-        slot[3][:M + 1].copy_(slot[0][:M + 1], non_blocking=True)
-        slot[4][:M].copy_(slot[1][:M], non_blocking=True)
-        slot[5][:M].copy_(slot[2][:M], non_blocking=True)
+        self._meta_i = (self._meta_i + 1) % self._META_RING
+        if slot[2] is not None:
+            slot[2].synchronize()
+        hb = slot[0].numpy()
+        row_ptr = hb[:o_sr].view(np.int64)
+        Nout = ctypes.c_int64(0)
+        nat.check(nat.load_library().dash_host_row_ptr(counts.ctypes.data, M, row_ptr.ctypes.data,
+                                                       ctypes.byref(Nout)), "dash_host_row_ptr")
+        sr = hb[o_sr:o_sr + 4 * M].view(np.int32)
+        sr[:M_old] = existing_rows
+        sr[M_old:] = np.arange(self._K, self._K + L, dtype=np.int32)
+        nw = hb[o_nw:o_nw + M]
+        nw[:M_old] = 0
+        nw[M_old:] = 1
+        db = slot[1]
+        db[:nbytes].copy_(slot[0][:nbytes], non_blocking=True)
         ev = torch.cuda.Event()
         ev.record()
-        slot[6] = ev
-        return slot[3], slot[4], slot[5]
+        slot[2] = ev
+        meta = (db[:o_sr].view(torch.int64), db[o_sr:o_sr + 4 * M].view(torch.int32), db[o_nw:o_nw + M])
+        return int(Nout.value), row_ptr, meta
 
     def check(self):
         """Synchronise and raise SolveError for a device-side solver failure."""
