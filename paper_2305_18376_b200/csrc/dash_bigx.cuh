@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(256) k_bigx_pre(BigxParams p) {
 // Partials of (slice, CTA): A writes c, B writes P and gram (disjoint parts).
 // ---------------------------------------------------------------------------
 template <int MAXS, int JSC>
-__global__ void __launch_bounds__(kCW * 32 + 32, 1) k_bigx(const __grid_constant__ CUtensorMap tmX, BigxParams p) {
+__global__ void __maxnreg__(128) k_bigx(const __grid_constant__ CUtensorMap tmX, BigxParams p) {
     extern __shared__ __align__(16) double sm_raw[];
     double *sm = align1k(sm_raw);
     const int J = p.J, R = p.R;
