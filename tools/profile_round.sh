@@ -11,12 +11,12 @@ if [ "$MODE" = list ]; then
   echo "bench rc=$?"
   ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_" -c 200 --csv \
       --log-file $OUT/${TAG}_launches.csv \
-      python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > $OUT/${TAG}_ncu_list.log 2>&1
+      python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-fp32 --e2e-steps 1 > $OUT/${TAG}_ncu_list.log 2>&1
   echo "launch list rc=$?"
 else
   for k in "$@"; do
     ncu --set full --clock-control none --import-source on -k regex:"$k" --launch-skip 3 --launch-count 1 \
-        -o $OUT/${TAG}_full_$k -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 1 \
+        -o $OUT/${TAG}_full_$k -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-fp32 --e2e-steps 1 \
         > $OUT/${TAG}_ncu_full_$k.log 2>&1
     echo "full $k rc=$?"
   done
