@@ -34,11 +34,18 @@ constexpr int kBxRB = 16;           // rank bucket
 constexpr int kBxMP = kBxRB + 4;    // Ms pitch (B-frag reads)
 constexpr int kBxUP = kBxRB + 8;    // U tile pitch (gram frags conflict-free)
 
-constexpr int kBxMaxStages = 4;
-struct BigxSmem {
-    static __host__ __device__ int strips(int J) { return (J + 15) / 16; }
-    static __host__ __device__ int stages(int J) { return strips(J) <= 8 ? 4 : 2; }
-    static __host__ __device__ int vtp(int J) { return strips(J) * 16 + 8; }
+constexpr int kBxMaxStages = 6;
+// Shared-memory plan of k_bigx for X in FP64 (boxes of 16 doubles x 32 rows)
+// or FP32 (the FP32 data mode: boxes of 32 floats x 32 rows).  A box is 4 KB
+// either way (32 rows of one 128-byte swizzled line).
+template <typename TX>
+struct BigxSmemT {
+    static constexpr bool F32 = sizeof(TX) == 4;
+    static constexpr int CW = F32 ? 32 : 16;  // X columns per box
+    static __host__ __device__ int strips(int J) { return (J + CW - 1) / CW; }
+    static __host__ __device__ int stages(int J) { return F32 ? (strips(J) <= 4 ? 6 : 3) : (strips(J) <= 8 ? 4 : 2); }
+    // V^T pitch: == 8 (mod 16) doubles for the FP64 fragment pairs, == 2 (mod 16) for the FP32 quads
+    static __host__ __device__ int vtp(int J) { return strips(J) * CW + (F32 ? 2 : 8); }
     static __host__ __device__ size_t stage_doubles(int J) { return (size_t)strips(J) * 512; }
     // [stages x JS boxes] | vt[16 x VTP] | ubuf[2][32 x 16 swz] | barriers
     static __host__ __device__ size_t bytes(int J) {
@@ -48,6 +55,7 @@ struct BigxSmem {
     // partial slot of one (slice, CTA) segment: P[J x 16] | gram[16 x 16] | c[4][16]
     static __host__ __device__ int64_t part_doubles(int J) { return (int64_t)J * 16 + 256 + 64; }
 };
+using BigxSmem = BigxSmemT<double>;
 
 // element (row, col) of a 32 x 16 swizzled double tile (16-byte chunk c at c ^ (row & 7))
 __device__ __forceinline__ int swz_e(int row, int col) { return swz(row, col >> 1) + (col & 1); }
@@ -197,13 +205,15 @@ __global__ void __launch_bounds__(256) k_bigx_pre(BigxParams p) {
 // mbarriers); a stage is released when both groups are done with it.
 // Partials of (slice, CTA): A writes c, B writes P and gram (disjoint parts).
 // ---------------------------------------------------------------------------
-template <int MAXS, int JSC>
+template <int MAXS, int JSC, typename TX>
 __global__ void __maxnreg__(128) k_bigx(const __grid_constant__ CUtensorMap tmX, BigxParams p) {
+    using SM = BigxSmemT<TX>;
+    constexpr bool F32 = SM::F32;
     extern __shared__ __align__(16) double sm_raw[];
     double *sm = align1k(sm_raw);
     const int J = p.J, R = p.R;
-    const int JS = JSC ? JSC : BigxSmem::strips(J), VTP = BigxSmem::vtp(J), NST = BigxSmem::stages(J);
-    const size_t SD = BigxSmem::stage_doubles(J);
+    const int JS = JSC ? JSC : SM::strips(J), VTP = SM::vtp(J), NST = SM::stages(J);
+    const size_t SD = SM::stage_doubles(J);
     double *xs = sm;
     double *vt = xs + NST * SD;          // vt[n][k] = V[k][n]
     double *ubuf = vt + 16 * VTP;        // 2 x (32 x 16 swizzled)
@@ -271,7 +281,7 @@ __global__ void __maxnreg__(128) k_bigx(const __grid_constant__ CUtensorMap tmX,
                 if (i >= NST) mbar_wait(&empty[st], (uint32_t)(((i / NST) - 1) & 1));
                 const int row0 = (int)(r0 + (tau - tb) * kTR);
                 mbar_arrive_expect_tx(&full[st], (uint32_t)JS * 4096u);
-                for (int s = 0; s < JS; ++s) tma_load_2d(xs + st * SD + s * 512, &tmX, 16 * s, row0, &full[st]);
+                for (int s = 0; s < JS; ++s) tma_load_2d(xs + st * SD + s * 512, &tmX, SM::CW * s, row0, &full[st]);
             }
         }
         return;
@@ -296,21 +306,43 @@ __global__ void __maxnreg__(128) k_bigx(const __grid_constant__ CUtensorMap tmX,
             const int st = (int)(i % NST);
             mbar_wait(&full[st], (uint32_t)((i / NST) & 1));
             const double *xt = xs + st * SD;
-            double xa[2][2][2];  // [nb][even/odd K chain][2]
+            double xa[2][4][2];  // [nb][K chain][2]
 #pragma unroll
             for (int nb = 0; nb < 2; ++nb)
 #pragma unroll
-                for (int c = 0; c < 2; ++c) xa[nb][c][0] = xa[nb][c][1] = 0.0;
+                for (int c = 0; c < 4; ++c) xa[nb][c][0] = xa[nb][c][1] = 0.0;
+            if constexpr (!F32) {
 #pragma unroll
-            for (int s = 0; s < JS; ++s) {
+                for (int s = 0; s < JS; ++s) {
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const double2 a = *reinterpret_cast<const double2 *>(xt + s * 512 + swz(xrow, 4 * h + t));
+                    for (int h = 0; h < 2; ++h) {
+                        const double2 a = *reinterpret_cast<const double2 *>(xt + s * 512 + swz(xrow, 4 * h + t));
 #pragma unroll
-                    for (int nb = 0; nb < 2; ++nb) {
-                        const double2 b = *reinterpret_cast<const double2 *>(vt + (8 * nb + g) * VTP + 16 * s + 8 * h + 2 * t);
-                        dmma884(xa[nb][0], a.x, b.x);
-                        dmma884(xa[nb][1], a.y, b.y);
+                        for (int nb = 0; nb < 2; ++nb) {
+                            const double2 b =
+                                *reinterpret_cast<const double2 *>(vt + (8 * nb + g) * VTP + 16 * s + 8 * h + 2 * t);
+                            dmma884(xa[nb][2 * h], a.x, b.x);
+                            dmma884(xa[nb][2 * h + 1], a.y, b.y);
+                        }
+                    }
+                }
+            } else {  // FP32 boxes: one float4 = 4 consecutive columns 32 s + 16 h + 4 t + {0..3}
+                const float *xf = reinterpret_cast<const float *>(xt);
+#pragma unroll
+                for (int s = 0; s < JS; ++s) {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const float4 a = *reinterpret_cast<const float4 *>(xf + s * 1024 + swzf(xrow, 4 * h + t));
+#pragma unroll
+                        for (int nb = 0; nb < 2; ++nb) {
+                            const double *vb = vt + (8 * nb + g) * VTP + 32 * s + 16 * h + 4 * t;
+                            const double2 b0 = *reinterpret_cast<const double2 *>(vb);
+                            const double2 b1 = *reinterpret_cast<const double2 *>(vb + 2);
+                            dmma884(xa[nb][0], (double)a.x, b0.x);
+                            dmma884(xa[nb][1], (double)a.y, b0.y);
+                            dmma884(xa[nb][2], (double)a.z, b1.x);
+                            dmma884(xa[nb][3], (double)a.w, b1.y);
+                        }
                     }
                 }
             }
@@ -321,7 +353,8 @@ __global__ void __maxnreg__(128) k_bigx(const __grid_constant__ CUtensorMap tmX,
 #pragma unroll
             for (int nb = 0; nb < 2; ++nb)
 #pragma unroll
-                for (int e = 0; e < 2; ++e) xv[nb][e] = ok ? xa[nb][0][e] + xa[nb][1][e] : 0.0;
+                for (int e = 0; e < 2; ++e)
+                    xv[nb][e] = ok ? (xa[nb][0][e] + xa[nb][1][e]) + (xa[nb][2][e] + xa[nb][3][e]) : 0.0;
             // U = XV Ms^T: A fragment of K step kk = this lane's XV value xv[kk >> 1][kk & 1]
             double ua[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
@@ -363,12 +396,15 @@ __global__ void __maxnreg__(128) k_bigx(const __grid_constant__ CUtensorMap tmX,
     const int b = w - 4;
     const int pg = qperm(g);
     const int mi = b >> 1, ni = b & 1;
-    double pacc[MAXS][4][2];
+    // FP64: pacc[q][k] = (j parity k >> 1, r parity k & 1) of strip q's 2x2 block;
+    // FP32: pacc[q][2 e + f] = (j = 4 pg + e, r parity f) of strip q's 4x2 block
+    constexpr int NPT = F32 ? 8 : 4;
+    double pacc[MAXS][NPT][2];
     double gacc[2] = {0.0, 0.0};
 #pragma unroll
     for (int q = 0; q < MAXS; ++q)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) pacc[q][k][0] = pacc[q][k][1] = 0.0;
+        for (int k = 0; k < NPT; ++k) pacc[q][k][0] = pacc[q][k][1] = 0.0;
     for (int64_t tau = tau0, i = 0; tau < tau1; ++tau, ++i) {
         advance(tau);
         const int st = (int)(i % NST);
@@ -385,11 +421,22 @@ __global__ void __maxnreg__(128) k_bigx(const __grid_constant__ CUtensorMap tmX,
             for (int q = 0; q < MAXS; ++q) {
                 const int s = b + 4 * q;
                 if (s < JS) {
-                    const double2 a = *reinterpret_cast<const double2 *>(xt + s * 512 + swz(row, pg));
-                    dmma884(pacc[q][0], a.x, bu.x);
-                    dmma884(pacc[q][1], a.x, bu.y);
-                    dmma884(pacc[q][2], a.y, bu.x);
-                    dmma884(pacc[q][3], a.y, bu.y);
+                    if constexpr (!F32) {
+                        const double2 a = *reinterpret_cast<const double2 *>(xt + s * 512 + swz(row, pg));
+                        dmma884(pacc[q][0], a.x, bu.x);
+                        dmma884(pacc[q][1], a.x, bu.y);
+                        dmma884(pacc[q][2], a.y, bu.x);
+                        dmma884(pacc[q][3], a.y, bu.y);
+                    } else {
+                        const float4 a = *reinterpret_cast<const float4 *>(reinterpret_cast<const float *>(xt) +
+                                                                           s * 1024 + swzf(row, pg));
+                        const double av[4] = {(double)a.x, (double)a.y, (double)a.z, (double)a.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            dmma884(pacc[q][2 * e], av[e], bu.x);
+                            dmma884(pacc[q][2 * e + 1], av[e], bu.y);
+                        }
+                    }
                 }
             }
             dmma884(gacc, ub[swz_e(row, 8 * mi + g)], ub[swz_e(row, 8 * ni + g)]);
@@ -406,8 +453,8 @@ __global__ void __maxnreg__(128) k_bigx(const __grid_constant__ CUtensorMap tmX,
                 const int s = b + 4 * q;
                 if (s < JS) {
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const int j = 16 * s + 2 * pg + (k >> 1);
+                    for (int k = 0; k < NPT; ++k) {
+                        const int j = F32 ? 32 * s + 4 * pg + (k >> 1) : 16 * s + 2 * pg + (k >> 1);
 #pragma unroll
                         for (int e = 0; e < 2; ++e) {
                             const int r = 2 * qperm(2 * t + e) + (k & 1);

@@ -51,7 +51,8 @@ __device__ __forceinline__ float *align1kf(float *p) {
 
 __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_xv3f(const __grid_constant__ CUtensorMap tmX, int64_t N, int J,
                                                            const double *__restrict__ V, int R, double *__restrict__ XV,
-                                                           FusedPrologue pro) {
+                                                           FusedPrologue pro, const uint32_t *__restrict__ tflag,
+                                                           uint32_t tgen) {
     extern __shared__ __align__(16) float smf_raw[];
     float *sm = align1kf(smf_raw);
     const int JS = TmaSmem32::strips(J), VTP = TmaSmem32::vtp(J);
@@ -96,14 +97,22 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_xv3f(const __grid_constant
     const int64_t ntiles = (N + kTR - 1) / kTR;
     const int64_t mine = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     if (w == kCW) {
-        if (lane == 0) {
-            for (int64_t i = 0; i < mine; ++i) {
-                const int st = (int)(i % kStages32);
-                if (i >= kStages32) mbar_wait(&empty[st], (uint32_t)(((i / kStages32) - 1) & 1));
-                const int r0 = (int)((blockIdx.x + i * gridDim.x) * kTR);
-                mbar_arrive_expect_tx(&full[st], (uint32_t)JS * 4096u);
-                for (int s = 0; s < JS; ++s) tma_load_2d(xs + st * SF + s * 1024, &tmX, 32 * s, r0, &full[st]);
+        for (int64_t i0 = 0, k = 0; i0 < mine; i0 += 32) {
+            unsigned vm = visit_mask(tflag, tgen, i0, mine);
+            if (lane == 0) {
+                while (vm) {
+                    const int b = __ffs(vm) - 1;
+                    vm &= vm - 1;
+                    const int64_t tile = blockIdx.x + (i0 + b) * gridDim.x;
+                    const int st = (int)(k % kStages32);
+                    if (k >= kStages32) mbar_wait(&empty[st], (uint32_t)(((k / kStages32) - 1) & 1));
+                    ++k;
+                    const int r0 = (int)(tile * kTR);
+                    mbar_arrive_expect_tx(&full[st], (uint32_t)JS * 4096u);
+                    for (int s = 0; s < JS; ++s) tma_load_2d(xs + st * SF + s * 1024, &tmX, 32 * s, r0, &full[st]);
+                }
             }
+            __syncwarp();
         }
         pdl_wait();
         return;
@@ -111,9 +120,13 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_xv3f(const __grid_constant
     const int mb = w & 3, nb = w >> 2;
     const double *vrow = vt + (8 * nb + g) * VTP + 4 * t;
     const int row = 8 * mb + qperm(g);
-    for (int64_t i = 0; i < mine; ++i) {
-        const int st = (int)(i % kStages32);
-        mbar_wait(&full[st], (uint32_t)((i / kStages32) & 1));
+    unsigned vm = 0;
+    for (int64_t i = 0, k = -1; i < mine; ++i) {
+        if ((i & 31) == 0) vm = visit_mask(tflag, tgen, i, mine);
+        if (!((vm >> (i & 31)) & 1u)) continue;
+        ++k;
+        const int st = (int)(k % kStages32);
+        mbar_wait(&full[st], (uint32_t)((k / kStages32) & 1));
         const float *xt = xs + st * SF;
         double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
         for (int s = 0; s < JS; ++s) {
@@ -145,7 +158,8 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_xv3f(const __grid_constant
 // F slot (CTA b, row group q) at F_slots + (b * RG + q) * J * R.
 __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_fgemm3f(const __grid_constant__ CUtensorMap tmX,
                                                               const __grid_constant__ CUtensorMap tmU, int64_t N,
-                                                              int J, int R, double *__restrict__ F_slots) {
+                                                              int J, int R, double *__restrict__ F_slots,
+                                                              const uint32_t *__restrict__ tflag, uint32_t tgen) {
     extern __shared__ __align__(16) float smf_raw[];
     float *sm = align1kf(smf_raw);
     const int JS = TmaSmem32::strips(J), RG = TmaSmem32::row_groups(J);
@@ -170,15 +184,23 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_fgemm3f(const __grid_const
     const int64_t ntiles = (N + kTR - 1) / kTR;
     const int64_t mine = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     if (w == kCW) {
-        if (lane == 0) {
-            for (int64_t i = 0; i < mine; ++i) {
-                const int st = (int)(i % kStages32);
-                if (i >= kStages32) mbar_wait(&empty[st], (uint32_t)(((i / kStages32) - 1) & 1));
-                const int r0 = (int)((blockIdx.x + i * gridDim.x) * kTR);
-                mbar_arrive_expect_tx(&full[st], (uint32_t)(JS + 1) * 4096u);
-                for (int s = 0; s < JS; ++s) tma_load_2d(xs + st * SF + s * 1024, &tmX, 32 * s, r0, &full[st]);
-                tma_load_2d(xs + st * SF + JS * 1024, &tmU, 0, r0, &full[st]);
+        for (int64_t i0 = 0, k = 0; i0 < mine; i0 += 32) {
+            unsigned vm = visit_mask(tflag, tgen, i0, mine);
+            if (lane == 0) {
+                while (vm) {
+                    const int b = __ffs(vm) - 1;
+                    vm &= vm - 1;
+                    const int64_t tile = blockIdx.x + (i0 + b) * gridDim.x;
+                    const int st = (int)(k % kStages32);
+                    if (k >= kStages32) mbar_wait(&empty[st], (uint32_t)(((k / kStages32) - 1) & 1));
+                    ++k;
+                    const int r0 = (int)(tile * kTR);
+                    mbar_arrive_expect_tx(&full[st], (uint32_t)(JS + 1) * 4096u);
+                    for (int s = 0; s < JS; ++s) tma_load_2d(xs + st * SF + s * 1024, &tmX, 32 * s, r0, &full[st]);
+                    tma_load_2d(xs + st * SF + JS * 1024, &tmU, 0, r0, &full[st]);
+                }
             }
+            __syncwarp();
         }
         return;
     }
@@ -191,9 +213,13 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_fgemm3f(const __grid_const
     for (int e = 0; e < 4; ++e)
 #pragma unroll
         for (int f = 0; f < 2; ++f) acc[e][f][0] = acc[e][f][1] = 0.0;
-    for (int64_t i = 0; i < mine; ++i) {
-        const int st = (int)(i % kStages32);
-        mbar_wait(&full[st], (uint32_t)((i / kStages32) & 1));
+    unsigned vm = 0;
+    for (int64_t i = 0, k = -1; i < mine; ++i) {
+        if ((i & 31) == 0) vm = visit_mask(tflag, tgen, i, mine);
+        if (!((vm >> (i & 31)) & 1u)) continue;
+        ++k;
+        const int st = (int)(k % kStages32);
+        mbar_wait(&full[st], (uint32_t)((k / kStages32) & 1));
         const float *xt = xs + st * SF;
         const double *ut = reinterpret_cast<const double *>(xt + JS * 1024);
         if (act) {

@@ -1184,7 +1184,7 @@ bool tma_ok(const dash_batch_f32 *b, int J, int R) {
 }
 
 int launch_xv3(dash_ctx *ctx, cudaStream_t st, const dash_batch_f32 *b, int J, const double *V, int R, double *XV,
-               const FusedPrologue &pro, bool pdl) {
+               const FusedPrologue &pro, bool pdl, const uint32_t *tflag = nullptr) {
     CUtensorMap mx;
     if (!make_box_map(&mx, b->X, J, b->N, b->ldx)) return DASH_E_CUDA;
     const size_t smem = TmaSmem32::xv_bytes(J);
@@ -1194,11 +1194,12 @@ int launch_xv3(dash_ctx *ctx, cudaStream_t st, const dash_batch_f32 *b, int J, c
         attr = smem;
     }
     PhaseScope ps(ctx, st, PH_XV);
-    return launch_k(pdl && pdl_site("xv3f"), k_xv3f, ctx->num_sms, kCW * 32 + 32, smem, st, mx, b->N, J, V, R, XV, pro);
+    return launch_k(pdl && pdl_site("xv3f"), k_xv3f, ctx->num_sms, kCW * 32 + 32, smem, st, mx, b->N, J, V, R, XV, pro,
+                    tflag, ctx->tgen);
 }
 
 int launch_f3(dash_ctx *ctx, cudaStream_t st, const dash_batch_f32 *b, int J, const double *US, int R,
-              double *F_slots) {
+              double *F_slots, const uint32_t *tflag = nullptr) {
     CUtensorMap mx, mu;
     if (!make_box_map(&mx, b->X, J, b->N, b->ldx) || !make_box_map(&mu, US, R, b->N, R)) return DASH_E_CUDA;
     const size_t smem = TmaSmem32::f_bytes(J);
@@ -1208,7 +1209,8 @@ int launch_f3(dash_ctx *ctx, cudaStream_t st, const dash_batch_f32 *b, int J, co
         attr = smem;
     }
     PhaseScope ps(ctx, st, PH_FGEMM);
-    return launch_k(pdl_site("f3f"), k_fgemm3f, ctx->num_sms, kCW * 32 + 32, smem, st, mx, mu, b->N, J, R, F_slots);
+    return launch_k(pdl_site("f3f"), k_fgemm3f, ctx->num_sms, kCW * 32 + 32, smem, st, mx, mu, b->N, J, R, F_slots,
+                    tflag, ctx->tgen);
 }
 
 // U_new of the FP32 data mode: FP64 working copy -> caller's FP32 array
@@ -1262,7 +1264,10 @@ int launch_f3(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, co
 }
 
 // fused big-slice chain (dash_bigx.cuh): pre (A systems, toff), the streaming kernel, post
-int launch_bigx(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, const BigxParams &bp) {
+template <class B>
+int launch_bigx(dash_ctx *ctx, cudaStream_t st, const B *b, const BigxParams &bp) {
+    using TX = typename std::remove_const<typename std::remove_pointer<decltype(b->X)>::type>::type;
+    using SM = BigxSmemT<TX>;
     if (bp.T == 0) return 0;
     const int nbig = ctx->bigx_nbig;
     PhaseScope ps(ctx, st, PH_BIG);
@@ -1270,13 +1275,18 @@ int launch_bigx(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, const B
     if (launch_k(true, k_bigx_pre, 1 + (nbig + 7) / 8, 256, 0, st, bp)) return DASH_E_CUDA;
     CUtensorMap mx;
     if (!make_box_map(&mx, b->X, bp.J, b->N, b->ldx)) return DASH_E_CUDA;
-    const size_t smem = BigxSmem::bytes(bp.J);
-    const int js = BigxSmem::strips(bp.J);
+    const size_t smem = SM::bytes(bp.J);
+    const int js = SM::strips(bp.J);
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         return launch_k(true, kern, bp.G, kCW * 32 + 32, smem, st, mx, bp);
     };
-    const int rc = js == 8 ? go(k_bigx<2, 8>) : js <= 4 ? go(k_bigx<1, 0>) : js <= 8 ? go(k_bigx<2, 0>) : go(k_bigx<4, 0>);
+    int rc;
+    if constexpr (SM::F32)  // float boxes: 32 columns per strip
+        rc = js == 4 ? go(k_bigx<1, 4, float>) : js <= 4 ? go(k_bigx<1, 0, float>) : go(k_bigx<2, 0, float>);
+    else
+        rc = js == 8 ? go(k_bigx<2, 8, double>) : js <= 4 ? go(k_bigx<1, 0, double>)
+             : js <= 8 ? go(k_bigx<2, 0, double>) : go(k_bigx<4, 0, double>);
     if (rc) return rc;
     return launch_k(true, k_bigx_post, nbig, 256, 0, st, bp);
 }
@@ -1356,8 +1366,8 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
         {
             static const bool no_bigx = getenv("DASH_NO_BIGX") != nullptr;  // A/B switch: the k_big path
             const SlicePlan &pl = plan_of(ctx);
-            ctx->bigx = !f32 && !no_bigx && ctx->tma && pl.big_dev && pl.gbig > 0 && J * 16 <= kPostPer * 256 &&
-                        BigxSmem::bytes(J) <= 227 * 1024;
+            ctx->bigx = !no_bigx && ctx->tma && pl.big_dev && pl.gbig > 0 && J * 16 <= kPostPer * 256 &&
+                        BigxSmemT<typename std::conditional<f32, float, double>::type>::bytes(J) <= 227 * 1024;
             ctx->bigx_nbig = ctx->bigx ? pl.gbig : 0;
             ctx->bigx_grid = ctx->bigx ? (int)std::min<int64_t>(ctx->num_sms, pl.big_tiles) : 0;
             if (ctx->bigx) {
@@ -1411,13 +1421,9 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
             const FusedPrologue pro{(double *)ctx->vtv.p, s->F, s->G, (double *)ctx->fsnap.p, (double *)ctx->gsnap.p,
                                     v_used_out, pass == 0, last};
             // PDL only behind the plan kernels (pass 0); a later pass follows the V solve
-            if constexpr (f32) {
-                if (launch_xv3(ctx, st, b, J, s->V, R, XV, pro, pass == 0)) return DASH_E_CUDA;
-            } else {
-                if (launch_xv3(ctx, st, b, J, s->V, R, XV, pro, pass == 0,
-                               ctx->bigx ? (const uint32_t *)ctx->tflag.p : nullptr))
-                    return DASH_E_CUDA;
-            }
+            if (launch_xv3(ctx, st, b, J, s->V, R, XV, pro, pass == 0,
+                           ctx->bigx ? (const uint32_t *)ctx->tflag.p : nullptr))
+                return DASH_E_CUDA;
         } else if (ctx->stream) {
             if constexpr (!f32) {
                 if (rank_bucket(R) <= 8) launch_xv2_t<8>(ctx, st, b, J, s->V, R, XV);
@@ -1447,7 +1453,7 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
         sp.pass = pass;
         sp.final_pass = last;
         if (launch_plan(ctx, st, RB, plan_of(ctx), sp, M, ctx->bigx)) return DASH_E_CUDA;
-        if constexpr (!f32) {
+        {
             if (ctx->bigx) {
                 BigxParams bp;
                 bp.meta = (const int4 *)ctx->smeta.p;
@@ -1481,13 +1487,9 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
             }
         }
         if (ctx->tma) {
-            if constexpr (f32) {
-                if (launch_f3(ctx, st, b, J, (const double *)ctx->us.p, R, Fsl)) return DASH_E_CUDA;
-            } else {
-                if (launch_f3(ctx, st, b, J, (const double *)ctx->us.p, R, Fsl,
-                              ctx->bigx ? (const uint32_t *)ctx->tflag.p : nullptr))
-                    return DASH_E_CUDA;
-            }
+            if (launch_f3(ctx, st, b, J, (const double *)ctx->us.p, R, Fsl,
+                          ctx->bigx ? (const uint32_t *)ctx->tflag.p : nullptr))
+                return DASH_E_CUDA;
         } else if (ctx->stream) {
             if constexpr (!f32) {
                 if (rank_bucket(R) <= 8) launch_f2_t<8>(ctx, st, b, J, (const double *)ctx->us.p, R, Fsl);
