@@ -7,6 +7,7 @@ raises -- the product path never silently runs anything on the CPU.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
@@ -104,7 +105,7 @@ def load_library(path: Path | None = None):
     with _lock:
         if _lib is not None and path is None:
             return _lib
-        p = Path(path) if path is not None else LIB_PATH
+        p = Path(path) if path is not None else Path(os.environ.get("DASH_LIB_PATH", LIB_PATH))
         if not p.exists():
             raise NativeUnavailable(
                 f"{p} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")

@@ -107,6 +107,36 @@ __device__ __forceinline__ bool sweep_inverse(double (&a)[RB], double *buf, int 
     return ok;
 }
 
+// The same sweep for a matrix whose pivots are all <= 1 (the caller scales A
+// by 1 / max diag: every pivot of an SPD matrix is at most its largest
+// diagonal entry).  The pivot row's scaling a_k <- a_k / d is folded into the
+// FMA every other row does, a <- a - f col, with f = 1 - 1/d on the pivot row
+// (its row equals the gathered column: A stays symmetric), so each step costs
+// RB DFMAs instead of RB DMULs + RB DFMAs.  With d <= 1, |1 - 1/d| <= 1/d and
+// the folded form keeps full relative accuracy.  Returns a <- -(scaled A)^{-1}.
+template <int RB>
+__device__ __forceinline__ bool sweep_inverse_unit(double (&a)[RB], double *buf, int r) {
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < RB; ++k) {
+        double col[RB];
+        group_gather<RB>(a[k], buf, r, col);  // col[z] = A[z][k] = A[k][z]
+        const double d = col[k];
+        ok = ok && (d > 0.0) && isfinite(d);
+        const double id = rcp_nr(d);
+        const bool piv = (r == k);
+        const double f = a[k] * id;
+        const double beta = piv ? 1.0 - id : f;
+#pragma unroll
+        for (int z = 0; z < RB; ++z) {
+            if (z == k) continue;
+            a[z] = fma(-beta, col[z], a[z]);
+        }
+        a[k] = piv ? -id : f;
+    }
+    return ok;
+}
+
 // x = B^{-1} rhs for one right-hand side (lane r holds row r of the SPD B in
 // a[] and rhs_r), by Gauss-Jordan elimination without normalising the pivot
 // row: step k subtracts (a_i[k] / d_k) x (pivot row) from every other row,

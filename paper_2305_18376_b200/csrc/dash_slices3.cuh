@@ -13,6 +13,11 @@
 // (included inside dash_update.cu's anonymous namespace)
 #pragma once
 
+#ifndef DASH_S3_CTAS
+#define DASH_S3_CTAS 4
+#endif
+constexpr int kS3CtasPerSM = DASH_S3_CTAS;  // resident CTAs per SM (register budget 65536 / (128 x this))
+
 template <int RB>
 struct S3 {
     static constexpr int NW = 4;
@@ -211,7 +216,7 @@ __global__ void __launch_bounds__(128) k_plan_scatter(const int64_t *__restrict_
 }
 
 template <int RB>
-__global__ void __launch_bounds__(S3<RB>::NW * 32, 4) k_slices3(SliceParams p, const int4 *__restrict__ meta,
+__global__ void __launch_bounds__(S3<RB>::NW * 32, kS3CtasPerSM) k_slices3(SliceParams p, const int4 *__restrict__ meta,
                                                                  const int *__restrict__ plan_counts) {
     using S = S3<RB>;
     constexpr int LDV = S::LDV, GPW = S::GPW, CAPW = S::CAPW;
@@ -292,12 +297,19 @@ __global__ void __launch_bounds__(S3<RB>::NW * 32, 4) k_slices3(SliceParams p, c
                 if (z < R) sh += vtv_s[z * LDV + z] * s_all[z] * s_all[z];
         sh = p.eps * sh / R;
         double a[RB];
+        double im;  // 1 / max diag(A): the sweep runs on A / max diag (all pivots <= 1)
         {
             const double dg = real ? sh : 1.0;
+            double mx = vrow[r] * s_r * s_r + dg;  // this lane's diagonal (padded lanes: 1)
 #pragma unroll
-            for (int z = 0; z < RB; ++z) a[z] = vrow[z] * s_r * s_all[z] + ((z == r) ? dg : 0.0);
+            for (int off = RB / 2; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL_MASK, mx, off));
+            im = (mx > 0.0 && isfinite(mx)) ? 1.0 / mx : 1.0;
+            const double sr_im = s_r * im, dg_im = dg * im;
+#pragma unroll
+            for (int z = 0; z < RB; ++z) a[z] = vrow[z] * sr_im * s_all[z] + ((z == r) ? dg_im : 0.0);
         }
-        const bool okA = sweep_inverse<RB>(a, buf, r);
+        const bool okA = sweep_inverse_unit<RB>(a, buf, r);
+        if (!okA) im = 1.0;  // LU fallback below solves the unscaled A
         if (__any_sync(FULL_MASK, !okA)) {
             const double dg = real ? sh : 1.0;
 #pragma unroll
@@ -340,6 +352,7 @@ __global__ void __launch_bounds__(S3<RB>::NW * 32, 4) k_slices3(SliceParams p, c
                     xrr = r < R ? __ldg(xr + r) : 0.0;
                 }
             }
+            u *= im;
             if (!(valid && r < R)) u = 0.0;
             if (valid && r < R) {
                 p.U[(r0 + i) * R + r] = u;

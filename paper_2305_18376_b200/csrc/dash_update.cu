@@ -956,7 +956,7 @@ SlicePlan make_plan(const int64_t *row_ptr, int M, int RB, int R, int num_sms) {
         return pl;
     }
     pl.split = true;
-    pl.g3 = 4 * num_sms;
+    pl.g3 = kS3CtasPerSM * num_sms;
     if (RB == 16 && (R % 2) == 0) {  // order on device; the host only counts big slices (grid size)
         pl.big_dev = true;
         int nbig = 0;
