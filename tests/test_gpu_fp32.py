@@ -51,6 +51,8 @@ def _oracle(ps, passes):
     ("wide32", dict(K0=40, steps=2, new_slices=2)),   # R=32: generic FP32-input GEMMs
     ("wide64", dict(K0=30, steps=2, new_slices=2)),
     ("tiny", dict(steps=3)),                          # J=20, R=5: generic path
+    ("large", dict(K0=80, steps=2, new_slices=3, add_rows=("uniform", 1, 150))),  # interleaved big / small
+    ("large", dict(K0=80, steps=2, new_slices=3, passes=2)),                      # multi-pass, fused path
 ])
 def test_fp32_mode_matches_oracle(name, kw):
     from paper_2305_18376_b200 import workloads as wl

@@ -135,6 +135,27 @@ def test_config_shaped_streams_match_oracle(name, kw):
     stream_parity(cfg)
 
 
+@pytest.mark.parametrize("name,kw", [
+    # existing slices of 1..150 rows: big and small slices interleave, so tiles on
+    # both sides of a big slice are shared with small ones (boundary U o w zeroing)
+    ("large", dict(K0=80, steps=2, new_slices=3, add_rows=("uniform", 1, 150))),
+    ("large", dict(K0=80, steps=2, new_slices=3, passes=2)),      # multi-pass on the fused path
+    ("large", dict(K0=60, steps=2, new_slices=2, R=14)),          # R < 16, even: fused path
+    ("large", dict(K0=60, steps=2, new_slices=2, R=13)),          # odd R: k_xv2 / k_slices2 path
+    ("medium", dict(K0=100, steps=2, J=120)),                     # J < 128 in 8 box strips
+])
+def test_fused_path_edges_match_oracle(name, kw):
+    from paper_2305_18376_b200 import _native as nat
+    from paper_2305_18376_b200 import workloads as wl
+    cfg = wl.scaled(wl.CONFIGS[name], **kw)
+    stream_parity(cfg)
+    if cfg.R % 2 == 0:  # the fused big-slice path ran
+        stream = wl.make_stream(cfg)
+        st = gpu_state_from_planted(wl.planted_state(stream), passes=cfg.passes)
+        st.update(next(stream.batches()))
+        assert nat.lib().dash_ctx_path_flags(st._ctx) & nat.PATH_BIGX
+
+
 def test_update_is_bit_reproducible():
     from paper_2305_18376_b200 import workloads as wl
     cfg = wl.scaled(wl.CONFIGS["large"], K0=100, steps=2, new_slices=2)
