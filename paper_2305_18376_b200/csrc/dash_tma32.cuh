@@ -169,7 +169,6 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_fgemm3f(const __grid_const
     uint64_t *empty = full + kStages32;
     const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
     const int g = lane >> 2, t = lane & 3;
-    pdl_trigger();
     if (tid == 0) {
         prefetch_map(&tmX);
         prefetch_map(&tmU);
@@ -180,7 +179,8 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_fgemm3f(const __grid_const
         fence_mbar_init();
     }
     __syncthreads();
-    pdl_wait();  // US from the slice kernels
+    pdl_wait();     // US from the slice kernels
+    pdl_trigger();  // only now: a successor may rely on everything before this kernel
     const int64_t ntiles = (N + kTR - 1) / kTR;
     const int64_t mine = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     if (w == kCW) {

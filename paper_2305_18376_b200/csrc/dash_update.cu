@@ -1271,7 +1271,7 @@ int launch_bigx(dash_ctx *ctx, cudaStream_t st, const B *b, const BigxParams &bp
     if (bp.T == 0) return 0;
     const int nbig = ctx->bigx_nbig;
     PhaseScope ps(ctx, st, PH_BIG);
-    ctx->last_launches += 2;  // three kernels under one phase
+    ctx->last_launches += 1;  // two kernels under one phase (pre, streaming); post after the F GEMM
     if (launch_k(true, k_bigx_pre, 1 + (nbig + 7) / 8, 256, 0, st, bp)) return DASH_E_CUDA;
     CUtensorMap mx;
     if (!make_box_map(&mx, b->X, bp.J, b->N, b->ldx)) return DASH_E_CUDA;
@@ -1287,8 +1287,13 @@ int launch_bigx(dash_ctx *ctx, cudaStream_t st, const B *b, const BigxParams &bp
     else
         rc = js == 8 ? go(k_bigx<2, 8, double>) : js <= 4 ? go(k_bigx<1, 0, double>)
              : js <= 8 ? go(k_bigx<2, 0, double>) : go(k_bigx<4, 0, double>);
-    if (rc) return rc;
-    return launch_k(true, k_bigx_post, nbig, 256, 0, st, bp);
+    return rc;
+}
+
+int launch_bigx_post(dash_ctx *ctx, cudaStream_t st, const BigxParams &bp) {
+    if (bp.T == 0) return 0;
+    PhaseScope ps(ctx, st, PH_BIG);
+    return launch_k(true, k_bigx_post, ctx->bigx_nbig, 256, 0, st, bp);
 }
 
 template <int RP>
@@ -1453,9 +1458,9 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
         sp.pass = pass;
         sp.final_pass = last;
         if (launch_plan(ctx, st, RB, plan_of(ctx), sp, M, ctx->bigx)) return DASH_E_CUDA;
+        BigxParams bp{};
         {
             if (ctx->bigx) {
-                BigxParams bp;
                 bp.meta = (const int4 *)ctx->smeta.p;
                 bp.plan_counts = plan_counts_of(ctx, M);
                 bp.V = s->V;
@@ -1499,6 +1504,8 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
             launch_fgemm(ctx, st, b, J, Ud, (const int32_t *)ctx->row_slice.p, s->W, R, ctx->rps,
                          (int)ctx->nsplit, Fsl);
         }
+        // big slices' S-row systems and F / G slots: beside the F GEMM (independent of it)
+        if (ctx->bigx && launch_bigx_post(ctx, st, bp)) return DASH_E_CUDA;
     }
     if constexpr (f32) {
         if (last && N > 0) {
