@@ -35,6 +35,10 @@ constexpr int kBxMP = kBxRB + 4;    // Ms pitch (B-frag reads)
 constexpr int kBxUP = kBxRB + 8;    // U tile pitch (gram frags conflict-free)
 
 constexpr int kBxMaxStages = 6;
+constexpr int kBxA = 8;                           // XV / U warps: two tiles in flight (4 row blocks each)
+constexpr int kBxB = 4;                           // X^T U / gram warps: P strips b, b + 4 (J <= 128)
+constexpr int kBxThreads = (kBxA + kBxB + 1) * 32;  // + the producer warp
+constexpr int kBxUSlots = 4;                      // U hand-off buffers
 // Shared-memory plan of k_bigx for X in FP64 (boxes of 16 doubles x 32 rows)
 // or FP32 (the FP32 data mode: boxes of 32 floats x 32 rows).  A box is 4 KB
 // either way (32 rows of one 128-byte swizzled line).
@@ -47,13 +51,13 @@ struct BigxSmemT {
     // V^T pitch: == 8 (mod 16) doubles for the FP64 fragment pairs, == 2 (mod 16) for the FP32 quads
     static __host__ __device__ int vtp(int J) { return strips(J) * CW + (F32 ? 2 : 8); }
     static __host__ __device__ size_t stage_doubles(int J) { return (size_t)strips(J) * 512; }
-    // [stages x JS boxes] | vt[16 x VTP] | ubuf[2][32 x 16 swz] | barriers
+    // [stages x JS boxes] | vt[16 x VTP] | ubuf[kBxUSlots][32 x 16 swz] | barriers
     static __host__ __device__ size_t bytes(int J) {
-        return 1024 + sizeof(double) * (stages(J) * stage_doubles(J) + 16 * (size_t)vtp(J) + 1024) +
-               8 * (2 * kBxMaxStages + 4);
+        return 1024 + sizeof(double) * (stages(J) * stage_doubles(J) + 16 * (size_t)vtp(J) + 512 * kBxUSlots) +
+               8 * (2 * kBxMaxStages + 2 * kBxUSlots);
     }
-    // partial slot of one (slice, CTA) segment: P[J x 16] | gram[16 x 16] | c[4][16]
-    static __host__ __device__ int64_t part_doubles(int J) { return (int64_t)J * 16 + 256 + 64; }
+    // partial slot of one (slice, CTA) segment: P[J x 16] | gram[16 x 16] | c[kBxA][16]
+    static __host__ __device__ int64_t part_doubles(int J) { return (int64_t)J * 16 + 256 + 16 * kBxA; }
 };
 using BigxSmem = BigxSmemT<double>;
 
@@ -216,11 +220,11 @@ __global__ void __maxnreg__(128) k_bigx(const __grid_constant__ CUtensorMap tmX,
     const size_t SD = SM::stage_doubles(J);
     double *xs = sm;
     double *vt = xs + NST * SD;          // vt[n][k] = V[k][n]
-    double *ubuf = vt + 16 * VTP;        // 2 x (32 x 16 swizzled)
-    uint64_t *full = reinterpret_cast<uint64_t *>(ubuf + 1024);
+    double *ubuf = vt + 16 * VTP;        // kBxUSlots x (32 x 16 swizzled)
+    uint64_t *full = reinterpret_cast<uint64_t *>(ubuf + 512 * kBxUSlots);
     uint64_t *empty = full + kBxMaxStages;
     uint64_t *uready = empty + kBxMaxStages;
-    uint64_t *ufree = uready + 2;
+    uint64_t *ufree = uready + kBxUSlots;
     const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
     const int g = lane >> 2, t = lane & 3;
     pdl_wait();  // Ms, toff from k_bigx_pre (and, transitively, XV / plan / small slices)
@@ -233,11 +237,11 @@ __global__ void __maxnreg__(128) k_bigx(const __grid_constant__ CUtensorMap tmX,
         prefetch_map(&tmX);
         for (int s2 = 0; s2 < NST; ++s2) {
             mbar_init(&full[s2], 1);
-            mbar_init(&empty[s2], kCW);
+            mbar_init(&empty[s2], 4 + kBxB);  // the 4 XV warps of the tile's parity + every X^T U warp
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < kBxUSlots; ++b) {
             mbar_init(&uready[b], 4);
-            mbar_init(&ufree[b], 4);
+            mbar_init(&ufree[b], kBxB);
         }
         fence_mbar_init();
     }
@@ -273,7 +277,7 @@ __global__ void __maxnreg__(128) k_bigx(const __grid_constant__ CUtensorMap tmX,
         return true;
     };
     const int64_t PD = BigxSmem::part_doubles(J);
-    if (w == kCW) {  // ---------------- producer
+    if (w == kBxA + kBxB) {  // ---------------- producer
         if (lane == 0) {
             for (int64_t tau = tau0, i = 0; tau < tau1; ++tau, ++i) {
                 advance(tau);
@@ -286,97 +290,102 @@ __global__ void __maxnreg__(128) k_bigx(const __grid_constant__ CUtensorMap tmX,
         }
         return;
     }
-    if (w < 4) {  // ---------------- group A: XV, U, c for rows 8 mb .. 8 mb + 7
-        const int mb = w;
+    if (w < kBxA) {  // ---------------- group A: XV, U, c; tiles of parity w / 4, rows 8 mb .. 8 mb + 7
+        const int par = w >> 2, mb = w & 3;
         const int xrow = 8 * mb + qperm(g);  // A-fragment / output row (conflict-free X reads)
         double msf[4][2];                    // B frags of U = XV Ms^T in the permuted K order
+        int msf_bi = -1;
         double cacc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
         for (int64_t tau = tau0, i = 0; tau < tau1; ++tau, ++i) {
-            if (advance(tau)) {
-                // K step kk feeds XV column col(kk, t) = 8 (kk >> 1) + 2 t + (kk & 1) (the C layout)
-                const double *msg = p.ms + (int64_t)bi * 16 * kBxMP;
+            advance(tau);
+            if ((int)(i & 1) == par) {
+                if (msf_bi != bi) {
+                    // K step kk feeds XV column col(kk, t) = 8 (kk >> 1) + 2 t + (kk & 1) (the C layout)
+                    const double *msg = p.ms + (int64_t)bi * 16 * kBxMP;
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+                        for (int nb = 0; nb < 2; ++nb)
+                            msf[kk][nb] = __ldcg(msg + (8 * nb + g) * kBxMP + 8 * (kk >> 1) + 2 * t + (kk & 1));
+                    msf_bi = bi;
+                }
+                const int64_t row0 = r0 + (tau - tb) * kTR;
+                const int nvalid = (int)min((int64_t)kTR, r0 + n - row0);
+                const int st = (int)(i % NST);
+                mbar_wait(&full[st], (uint32_t)((i / NST) & 1));
+                const double *xt = xs + st * SD;
+                double xa[2][4][2];  // [nb][K chain][2]
+    #pragma unroll
+                for (int nb = 0; nb < 2; ++nb)
+    #pragma unroll
+                    for (int c = 0; c < 4; ++c) xa[nb][c][0] = xa[nb][c][1] = 0.0;
+                if constexpr (!F32) {
+    #pragma unroll
+                    for (int s = 0; s < JS; ++s) {
+    #pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const double2 a = *reinterpret_cast<const double2 *>(xt + s * 512 + swz(xrow, 4 * h + t));
+    #pragma unroll
+                            for (int nb = 0; nb < 2; ++nb) {
+                                const double2 b =
+                                    *reinterpret_cast<const double2 *>(vt + (8 * nb + g) * VTP + 16 * s + 8 * h + 2 * t);
+                                dmma884(xa[nb][2 * h], a.x, b.x);
+                                dmma884(xa[nb][2 * h + 1], a.y, b.y);
+                            }
+                        }
+                    }
+                } else {  // FP32 boxes: one float4 = 4 consecutive columns 32 s + 16 h + 4 t + {0..3}
+                    const float *xf = reinterpret_cast<const float *>(xt);
+    #pragma unroll
+                    for (int s = 0; s < JS; ++s) {
+    #pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const float4 a = *reinterpret_cast<const float4 *>(xf + s * 1024 + swzf(xrow, 4 * h + t));
+    #pragma unroll
+                            for (int nb = 0; nb < 2; ++nb) {
+                                const double *vb = vt + (8 * nb + g) * VTP + 32 * s + 16 * h + 4 * t;
+                                const double2 b0 = *reinterpret_cast<const double2 *>(vb);
+                                const double2 b1 = *reinterpret_cast<const double2 *>(vb + 2);
+                                dmma884(xa[nb][0], (double)a.x, b0.x);
+                                dmma884(xa[nb][1], (double)a.y, b0.y);
+                                dmma884(xa[nb][2], (double)a.z, b1.x);
+                                dmma884(xa[nb][3], (double)a.w, b1.y);
+                            }
+                        }
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[st]);
+                const bool ok = xrow < nvalid;
+                double xv[2][2];
+#pragma unroll
+                for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e)
+                        xv[nb][e] = ok ? (xa[nb][0][e] + xa[nb][1][e]) + (xa[nb][2][e] + xa[nb][3][e]) : 0.0;
+                // U = XV Ms^T: A fragment of K step kk = this lane's XV value xv[kk >> 1][kk & 1]
+                double ua[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk)
 #pragma unroll
-                    for (int nb = 0; nb < 2; ++nb)
-                        msf[kk][nb] = __ldcg(msg + (8 * nb + g) * kBxMP + 8 * (kk >> 1) + 2 * t + (kk & 1));
-            }
-            const int64_t row0 = r0 + (tau - tb) * kTR;
-            const int nvalid = (int)min((int64_t)kTR, r0 + n - row0);
-            const int st = (int)(i % NST);
-            mbar_wait(&full[st], (uint32_t)((i / NST) & 1));
-            const double *xt = xs + st * SD;
-            double xa[2][4][2];  // [nb][K chain][2]
+                    for (int nb = 0; nb < 2; ++nb) dmma884(ua[nb], xv[kk >> 1][kk & 1], msf[kk][nb]);
+                const int bsel = (int)(i % kBxUSlots);
+                if (i >= kBxUSlots) mbar_wait(&ufree[bsel], (uint32_t)(((i / kBxUSlots) - 1) & 1));
+                double *ub = ubuf + bsel * 512;
 #pragma unroll
-            for (int nb = 0; nb < 2; ++nb)
-#pragma unroll
-                for (int c = 0; c < 4; ++c) xa[nb][c][0] = xa[nb][c][1] = 0.0;
-            if constexpr (!F32) {
-#pragma unroll
-                for (int s = 0; s < JS; ++s) {
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const double2 a = *reinterpret_cast<const double2 *>(xt + s * 512 + swz(xrow, 4 * h + t));
-#pragma unroll
-                        for (int nb = 0; nb < 2; ++nb) {
-                            const double2 b =
-                                *reinterpret_cast<const double2 *>(vt + (8 * nb + g) * VTP + 16 * s + 8 * h + 2 * t);
-                            dmma884(xa[nb][2 * h], a.x, b.x);
-                            dmma884(xa[nb][2 * h + 1], a.y, b.y);
-                        }
-                    }
+                for (int nb = 0; nb < 2; ++nb) {
+                    const int col = 8 * nb + 2 * t;
+                    cacc[nb][0] = fma(xv[nb][0], ua[nb][0], cacc[nb][0]);
+                    cacc[nb][1] = fma(xv[nb][1], ua[nb][1], cacc[nb][1]);
+                    *reinterpret_cast<double2 *>(ub + swz_e(xrow, col)) = make_double2(ua[nb][0], ua[nb][1]);
+                    if (ok && col < R)
+                        *reinterpret_cast<double2 *>(p.U + (row0 + xrow) * R + col) = make_double2(ua[nb][0], ua[nb][1]);
                 }
-            } else {  // FP32 boxes: one float4 = 4 consecutive columns 32 s + 16 h + 4 t + {0..3}
-                const float *xf = reinterpret_cast<const float *>(xt);
-#pragma unroll
-                for (int s = 0; s < JS; ++s) {
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const float4 a = *reinterpret_cast<const float4 *>(xf + s * 1024 + swzf(xrow, 4 * h + t));
-#pragma unroll
-                        for (int nb = 0; nb < 2; ++nb) {
-                            const double *vb = vt + (8 * nb + g) * VTP + 32 * s + 16 * h + 4 * t;
-                            const double2 b0 = *reinterpret_cast<const double2 *>(vb);
-                            const double2 b1 = *reinterpret_cast<const double2 *>(vb + 2);
-                            dmma884(xa[nb][0], (double)a.x, b0.x);
-                            dmma884(xa[nb][1], (double)a.y, b0.y);
-                            dmma884(xa[nb][2], (double)a.z, b1.x);
-                            dmma884(xa[nb][3], (double)a.w, b1.y);
-                        }
-                    }
-                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&uready[bsel]);
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[st]);
-            const bool ok = xrow < nvalid;
-            double xv[2][2];
-#pragma unroll
-            for (int nb = 0; nb < 2; ++nb)
-#pragma unroll
-                for (int e = 0; e < 2; ++e)
-                    xv[nb][e] = ok ? (xa[nb][0][e] + xa[nb][1][e]) + (xa[nb][2][e] + xa[nb][3][e]) : 0.0;
-            // U = XV Ms^T: A fragment of K step kk = this lane's XV value xv[kk >> 1][kk & 1]
-            double ua[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-#pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
-#pragma unroll
-                for (int nb = 0; nb < 2; ++nb) dmma884(ua[nb], xv[kk >> 1][kk & 1], msf[kk][nb]);
-            const int bsel = (int)(i & 1);
-            if (i >= 2) mbar_wait(&ufree[bsel], (uint32_t)(((i >> 1) - 1) & 1));
-            double *ub = ubuf + bsel * 512;
-#pragma unroll
-            for (int nb = 0; nb < 2; ++nb) {
-                const int col = 8 * nb + 2 * t;
-                cacc[nb][0] = fma(xv[nb][0], ua[nb][0], cacc[nb][0]);
-                cacc[nb][1] = fma(xv[nb][1], ua[nb][1], cacc[nb][1]);
-                *reinterpret_cast<double2 *>(ub + swz_e(xrow, col)) = make_double2(ua[nb][0], ua[nb][1]);
-                if (ok && col < R)
-                    *reinterpret_cast<double2 *>(p.U + (row0 + xrow) * R + col) = make_double2(ua[nb][0], ua[nb][1]);
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&uready[bsel]);
-            if (tau == te - 1 || tau == tau1 - 1) {  // c partial of (slice, CTA): row block mb
-                double *cp = p.parts + (int64_t)(bi + blockIdx.x) * PD + (int64_t)J * 16 + 256 + mb * 16;
+            if (tau == te - 1 || tau == tau1 - 1) {  // c partial of (slice, CTA): this warp's tiles
+                double *cp = p.parts + (int64_t)(bi + blockIdx.x) * PD + (int64_t)J * 16 + 256 + w * 16;
 #pragma unroll
                 for (int nb = 0; nb < 2; ++nb)
 #pragma unroll
@@ -392,10 +401,10 @@ __global__ void __maxnreg__(128) k_bigx(const __grid_constant__ CUtensorMap tmX,
         }
         return;
     }
-    // ---------------- group B: P += X^T U (strips b, b + 4, ...), gram tile b
-    const int b = w - 4;
+    // ---------------- group B: P += X^T U (strips b, b + 8, ...), gram tile b (b < 4)
+    const int b = w - kBxA;
     const int pg = qperm(g);
-    const int mi = b >> 1, ni = b & 1;
+    const int mi = (b >> 1) & 1, ni = b & 1;
     // FP64: pacc[q][k] = (j parity k >> 1, r parity k & 1) of strip q's 2x2 block;
     // FP32: pacc[q][2 e + f] = (j = 4 pg + e, r parity f) of strip q's 4x2 block
     constexpr int NPT = F32 ? 8 : 4;
@@ -408,8 +417,8 @@ __global__ void __maxnreg__(128) k_bigx(const __grid_constant__ CUtensorMap tmX,
     for (int64_t tau = tau0, i = 0; tau < tau1; ++tau, ++i) {
         advance(tau);
         const int st = (int)(i % NST);
-        const int bsel = (int)(i & 1);
-        mbar_wait(&uready[bsel], (uint32_t)((i >> 1) & 1));
+        const int bsel = (int)(i % kBxUSlots);
+        mbar_wait(&uready[bsel], (uint32_t)((i / kBxUSlots) & 1));
         mbar_wait(&full[st], (uint32_t)((i / NST) & 1));  // completed long ago (group A waited on it)
         const double *xt = xs + st * SD;
         const double *ub = ubuf + bsel * 512;
@@ -419,7 +428,7 @@ __global__ void __maxnreg__(128) k_bigx(const __grid_constant__ CUtensorMap tmX,
             const double2 bu = *reinterpret_cast<const double2 *>(ub + swz(row, pg));  // U[row][2pg, 2pg+1]
 #pragma unroll
             for (int q = 0; q < MAXS; ++q) {
-                const int s = b + 4 * q;
+                const int s = b + kBxB * q;
                 if (s < JS) {
                     if constexpr (!F32) {
                         const double2 a = *reinterpret_cast<const double2 *>(xt + s * 512 + swz(row, pg));
@@ -439,7 +448,7 @@ __global__ void __maxnreg__(128) k_bigx(const __grid_constant__ CUtensorMap tmX,
                     }
                 }
             }
-            dmma884(gacc, ub[swz_e(row, 8 * mi + g)], ub[swz_e(row, 8 * ni + g)]);
+            if (b < 4) dmma884(gacc, ub[swz_e(row, 8 * mi + g)], ub[swz_e(row, 8 * ni + g)]);
         }
         __syncwarp();
         if (lane == 0) {
@@ -450,7 +459,7 @@ __global__ void __maxnreg__(128) k_bigx(const __grid_constant__ CUtensorMap tmX,
             double *part = p.parts + (int64_t)(bi + blockIdx.x) * PD;
 #pragma unroll
             for (int q = 0; q < MAXS; ++q) {
-                const int s = b + 4 * q;
+                const int s = b + kBxB * q;
                 if (s < JS) {
 #pragma unroll
                     for (int k = 0; k < NPT; ++k) {
@@ -464,10 +473,12 @@ __global__ void __maxnreg__(128) k_bigx(const __grid_constant__ CUtensorMap tmX,
                     }
                 }
             }
-            double *gp = part + (int64_t)J * 16;
+            if (b < 4) {
+                double *gp = part + (int64_t)J * 16;
 #pragma unroll
-            for (int e = 0; e < 2; ++e) gp[(8 * mi + g) * 16 + 8 * ni + 2 * t + e] = gacc[e];
-            gacc[0] = gacc[1] = 0.0;
+                for (int e = 0; e < 2; ++e) gp[(8 * mi + g) * 16 + 8 * ni + 2 * t + e] = gacc[e];
+                gacc[0] = gacc[1] = 0.0;
+            }
         }
     }
 }
@@ -528,7 +539,8 @@ __global__ void __launch_bounds__(256) k_bigx_post(BigxParams p) {
         double acc = 0.0;
         for (int sg = 0; sg < nseg; ++sg) {
             const double *cp = base + sg * PD + (int64_t)J * 16 + 256;
-            acc += ((__ldcg(cp + tid) + __ldcg(cp + 16 + tid)) + (__ldcg(cp + 32 + tid) + __ldcg(cp + 48 + tid)));
+#pragma unroll
+            for (int a = 0; a < kBxA; ++a) acc += __ldcg(cp + 16 * a + tid);
         }
         vec[tid] = tid < R ? p.lam * (fresh ? 0.0 : __ldcg(p.C + (int64_t)wrow * R + tid)) + acc : 0.0;  // c_new
     }

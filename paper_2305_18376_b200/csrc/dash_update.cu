@@ -483,7 +483,15 @@ int launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = (pdl && pdl_enabled()) ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, kern, args...) == cudaSuccess ? 0 : DASH_E_CUDA;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, args...);
+    if (e != cudaSuccess) {
+        static const bool verbose = getenv("DASH_VERBOSE") != nullptr;
+        if (verbose)
+            fprintf(stderr, "[dash] launch failed: %s (grid %u, block %u, smem %zu)\n", cudaGetErrorString(e), grid.x,
+                    block.x, smem);
+        return DASH_E_CUDA;
+    }
+    return 0;
 }
 
 #include "dash_slices.cuh"
@@ -1279,14 +1287,15 @@ int launch_bigx(dash_ctx *ctx, cudaStream_t st, const B *b, const BigxParams &bp
     const int js = SM::strips(bp.J);
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        return launch_k(true, kern, bp.G, kCW * 32 + 32, smem, st, mx, bp);
+        return launch_k(true, kern, bp.G, kBxThreads, smem, st, mx, bp);
     };
     int rc;
+    // J <= 128 (the fused path's limit): <= 8 FP64 / 4 FP32 strips over kBxB X^T U warps
+    static_assert(kBxB == 4, "strip split below assumes 4 X^T U warps");
     if constexpr (SM::F32)  // float boxes: 32 columns per strip
-        rc = js == 4 ? go(k_bigx<1, 4, float>) : js <= 4 ? go(k_bigx<1, 0, float>) : go(k_bigx<2, 0, float>);
+        rc = js == 4 ? go(k_bigx<1, 4, float>) : go(k_bigx<1, 0, float>);
     else
-        rc = js == 8 ? go(k_bigx<2, 8, double>) : js <= 4 ? go(k_bigx<1, 0, double>)
-             : js <= 8 ? go(k_bigx<2, 0, double>) : go(k_bigx<4, 0, double>);
+        rc = js == 8 ? go(k_bigx<2, 8, double>) : js <= 4 ? go(k_bigx<1, 0, double>) : go(k_bigx<2, 0, double>);
     return rc;
 }
 
