@@ -229,10 +229,6 @@ __global__ void __maxnreg__(128) k_bigx(const __grid_constant__ CUtensorMap tmX,
     const int g = lane >> 2, t = lane & 3;
     pdl_wait();  // Ms, toff from k_bigx_pre (and, transitively, XV / plan / small slices)
     pdl_trigger();
-    for (int i = tid; i < 16 * VTP; i += blockDim.x) {
-        const int nn = i / VTP, k = i % VTP;
-        vt[i] = (nn < R && k < J) ? p.V[k * R + nn] : 0.0;
-    }
     if (tid == 0) {
         prefetch_map(&tmX);
         for (int s2 = 0; s2 < NST; ++s2) {
@@ -291,6 +287,11 @@ __global__ void __maxnreg__(128) k_bigx(const __grid_constant__ CUtensorMap tmX,
         return;
     }
     if (w < kBxA) {  // ---------------- group A: XV, U, c; tiles of parity w / 4, rows 8 mb .. 8 mb + 7
+        for (int i = tid; i < 16 * VTP; i += kBxA * 32) {  // V^T staging overlaps the producer's first loads
+            const int nn = i / VTP, k = i % VTP;
+            vt[i] = (nn < R && k < J) ? p.V[k * R + nn] : 0.0;
+        }
+        asm volatile("bar.sync 2, %0;" ::"n"(kBxA * 32) : "memory");  // the XV warps only
         const int par = w >> 2, mb = w & 3;
         const int xrow = 8 * mb + qperm(g);  // A-fragment / output row (conflict-free X reads)
         double msf[4][2];                    // B frags of U = XV Ms^T in the permuted K order

@@ -98,10 +98,6 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_xv3(const __grid_constant_
     // the update's first, normally launched kernel has started); waits only
     // at exit so that its completion implies theirs.
     pdl_trigger();
-    for (int i = tid; i < 16 * VTP; i += blockDim.x) {
-        const int nn = i / VTP, k = i % VTP;
-        vt[i] = (nn < R && k < J) ? V[k * R + nn] : 0.0;
-    }
     if (tid == 0) {
         prefetch_map(&tmX);
         for (int s2 = 0; s2 < kStages; ++s2) {
@@ -111,23 +107,6 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_xv3(const __grid_constant_
         fence_mbar_init();
     }
     __syncthreads();
-    {
-        const int gt = blockIdx.x * blockDim.x + tid, nt = gridDim.x * blockDim.x;
-        if (pro.snap) {
-            for (int i = gt; i < J * R; i += nt) pro.F_snap[i] = pro.F[i];
-            for (int i = gt; i < R * R; i += nt) pro.G_snap[i] = pro.G[i];
-        }
-        if (pro.last)
-            for (int i = gt; i < J * R; i += nt) pro.v_used[i] = V[i];
-        if (blockIdx.x == 0 && tid < R * R) {  // vtv[r][z] = sum_k V[k][r] V[k][z], 4 chains
-            const double *a = vt + (tid / R) * VTP, *b = vt + (tid % R) * VTP;
-            double acc[4] = {0.0, 0.0, 0.0, 0.0};
-            for (int k = 0; k < J; k += 4)
-#pragma unroll
-                for (int q = 0; q < 4; ++q) acc[q] = fma(a[k + q], b[k + q], acc[q]);  // vt padded to 16
-            pro.vtv[tid] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-        }
-    }
     const int64_t ntiles = (N + kTR - 1) / kTR;
     const int64_t mine = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     if (w == kCW) {
@@ -150,6 +129,29 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_xv3(const __grid_constant_
         }
         pdl_wait();
         return;
+    }
+    // consumers: V^T staging and the fused prologue overlap the producer's first loads
+    for (int i = tid; i < 16 * VTP; i += kCW * 32) {
+        const int nn = i / VTP, k = i % VTP;
+        vt[i] = (nn < R && k < J) ? V[k * R + nn] : 0.0;
+    }
+    compute_bar();
+    {
+        const int gt = blockIdx.x * (kCW * 32) + tid, nt = gridDim.x * (kCW * 32);
+        if (pro.snap) {
+            for (int i = gt; i < J * R; i += nt) pro.F_snap[i] = pro.F[i];
+            for (int i = gt; i < R * R; i += nt) pro.G_snap[i] = pro.G[i];
+        }
+        if (pro.last)
+            for (int i = gt; i < J * R; i += nt) pro.v_used[i] = V[i];
+        if (blockIdx.x == 0 && tid < R * R) {  // vtv[r][z] = sum_k V[k][r] V[k][z], 4 chains
+            const double *a = vt + (tid / R) * VTP, *b = vt + (tid % R) * VTP;
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int k = 0; k < J; k += 4)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[q] = fma(a[k + q], b[k + q], acc[q]);  // vt padded to 16
+            pro.vtv[tid] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+        }
     }
     const int mb = w & 3, nb = w >> 2;  // 8-row block, 8-column block of the 32 x 16 output tile
     const double *vrow = vt + (8 * nb + g) * VTP + 2 * t;

@@ -64,10 +64,6 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_xv3f(const __grid_constant
     const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
     const int g = lane >> 2, t = lane & 3;
     pdl_trigger();
-    for (int i = tid; i < 16 * VTP; i += blockDim.x) {
-        const int nn = i / VTP, k = i % VTP;
-        vt[i] = (nn < R && k < J) ? V[k * R + nn] : 0.0;
-    }
     if (tid == 0) {
         prefetch_map(&tmX);
         for (int s2 = 0; s2 < kStages32; ++s2) {
@@ -77,23 +73,6 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_xv3f(const __grid_constant
         fence_mbar_init();
     }
     __syncthreads();
-    {
-        const int gt = blockIdx.x * blockDim.x + tid, nt = gridDim.x * blockDim.x;
-        if (pro.snap) {
-            for (int i = gt; i < J * R; i += nt) pro.F_snap[i] = pro.F[i];
-            for (int i = gt; i < R * R; i += nt) pro.G_snap[i] = pro.G[i];
-        }
-        if (pro.last)
-            for (int i = gt; i < J * R; i += nt) pro.v_used[i] = V[i];
-        if (blockIdx.x == 0 && tid < R * R) {
-            const double *a = vt + (tid / R) * VTP, *b = vt + (tid % R) * VTP;
-            double acc[4] = {0.0, 0.0, 0.0, 0.0};
-            for (int k = 0; k < J; k += 4)
-#pragma unroll
-                for (int q = 0; q < 4; ++q) acc[q] = fma(a[k + q], b[k + q], acc[q]);  // vt padded to 32
-            pro.vtv[tid] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-        }
-    }
     const int64_t ntiles = (N + kTR - 1) / kTR;
     const int64_t mine = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     if (w == kCW) {
@@ -116,6 +95,29 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_xv3f(const __grid_constant
         }
         pdl_wait();
         return;
+    }
+    // consumers: V^T staging and the fused prologue overlap the producer's first loads
+    for (int i = tid; i < 16 * VTP; i += kCW * 32) {
+        const int nn = i / VTP, k = i % VTP;
+        vt[i] = (nn < R && k < J) ? V[k * R + nn] : 0.0;
+    }
+    compute_bar();
+    {
+        const int gt = blockIdx.x * (kCW * 32) + tid, nt = gridDim.x * (kCW * 32);
+        if (pro.snap) {
+            for (int i = gt; i < J * R; i += nt) pro.F_snap[i] = pro.F[i];
+            for (int i = gt; i < R * R; i += nt) pro.G_snap[i] = pro.G[i];
+        }
+        if (pro.last)
+            for (int i = gt; i < J * R; i += nt) pro.v_used[i] = V[i];
+        if (blockIdx.x == 0 && tid < R * R) {
+            const double *a = vt + (tid / R) * VTP, *b = vt + (tid % R) * VTP;
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int k = 0; k < J; k += 4)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[q] = fma(a[k + q], b[k + q], acc[q]);  // vt padded to 32
+            pro.vtv[tid] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+        }
     }
     const int mb = w & 3, nb = w >> 2;
     const double *vrow = vt + (8 * nb + g) * VTP + 4 * t;
