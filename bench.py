@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--impl", default="dash", choices=["dash", "reference"])
     ap.add_argument("--config", default=CONFIG_NAME)
     ap.add_argument("--K0", type=int, default=None, help="override K0 (smoke runs)")
-    ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--no-fp32", dest="fp32", action="store_false",
