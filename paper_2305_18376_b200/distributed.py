@@ -34,6 +34,11 @@ class ShardedStream:
         self._global = {sid: i for i, sid in enumerate(global_ids or [])}
         self._allreduce = allreduce or self._nccl_allreduce
 
+    @property
+    def dtype(self):
+        """Streamed-data dtype of the wrapped state (FP64, or FP32 data mode)."""
+        return self.state.dtype
+
     def _nccl_allreduce(self, t):
         import torch.distributed as dist
         dist.all_reduce(t, group=self.group)
