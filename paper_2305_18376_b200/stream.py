@@ -554,6 +554,12 @@ class HostPipeline:
     read-back run while batch t is being updated; a buffer is reused only
     after the update that read it has finished (event-ordered).  ``engine`` is
     a StreamState or a ShardedStream (anything with ``update_packed``).
+
+    ``depth`` = device staging buffers.  With 2, the upload of batch t+2 waits
+    for update t (buffer reuse), and update t itself waits for its small
+    index-array copy, which the copy engine serialises behind the large upload
+    of batch t+1 -- the engine idles for one update per step.  3 keeps the
+    host->device engine busy back to back (PCIe-bound serving).
     """
 
     class Staged:
@@ -562,7 +568,7 @@ class HostPipeline:
         def __init__(self, slot, X, ready):
             self.slot, self.X, self.ready = slot, X, ready
 
-    def __init__(self, engine, max_rows: int, J: int, device=None, depth: int = 2):
+    def __init__(self, engine, max_rows: int, J: int, device=None, depth: int = 3):
         self.engine = engine
         dev = _dev(device)
         self.device = dev
