@@ -53,6 +53,7 @@ def _oracle(ps, passes):
     ("tiny", dict(steps=3)),                          # J=20, R=5: generic path
     ("large", dict(K0=80, steps=2, new_slices=3, add_rows=("uniform", 1, 150))),  # interleaved big / small
     ("large", dict(K0=80, steps=2, new_slices=3, passes=2)),                      # multi-pass, fused path
+    ("large", dict(K0=60, steps=2, new_slices=2, J=200)),                         # J > 128: no fused path
 ])
 def test_fp32_mode_matches_oracle(name, kw):
     from paper_2305_18376_b200 import workloads as wl

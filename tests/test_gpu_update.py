@@ -143,13 +143,14 @@ def test_config_shaped_streams_match_oracle(name, kw):
     ("large", dict(K0=60, steps=2, new_slices=2, R=14)),          # R < 16, even: fused path
     ("large", dict(K0=60, steps=2, new_slices=2, R=13)),          # odd R: k_xv2 / k_slices2 path
     ("medium", dict(K0=100, steps=2, J=120)),                     # J < 128 in 8 box strips
+    ("large", dict(K0=60, steps=2, new_slices=2, J=200)),         # J > 128: TMA GEMMs + k_big (no fused path)
 ])
 def test_fused_path_edges_match_oracle(name, kw):
     from paper_2305_18376_b200 import _native as nat
     from paper_2305_18376_b200 import workloads as wl
     cfg = wl.scaled(wl.CONFIGS[name], **kw)
     stream_parity(cfg)
-    if cfg.R % 2 == 0:  # the fused big-slice path ran
+    if cfg.R % 2 == 0 and cfg.J <= 128:  # the fused big-slice path ran
         stream = wl.make_stream(cfg)
         st = gpu_state_from_planted(wl.planted_state(stream), passes=cfg.passes)
         st.update(next(stream.batches()))
