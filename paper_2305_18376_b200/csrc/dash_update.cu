@@ -734,6 +734,102 @@ __global__ void __launch_bounds__(NWV * 32) k_vsolve(const double *__restrict__ 
     }
 }
 
+// V solve for R <= 16 in ONE short chain: warp 0 forms G = sym(lam G0 + g)
+// + shift I and inverts it with the unit-pivot sweep (A / max diag, LU with
+// partial pivoting if a pivot fails -- the reference solves with LU,
+// linalg.py:25-45), then every thread forms one row F_j = lam F0_j + f_j and
+// V_j = G^{-1} F_j (16 x 16 FMAs against the broadcast inverse).  Replaces the
+// per-warp Cholesky + per-lane triangular solves of k_vsolve (latency chain
+// of 2 x 16 dependent steps per lane).
+template <int RB>
+__global__ void __launch_bounds__(128) k_vsolve2(const double *__restrict__ fg, const double *__restrict__ F_snap,
+                                                 const double *__restrict__ G_snap, double lam, int J, int R,
+                                                 double eps, double *__restrict__ F, double *__restrict__ G,
+                                                 double *__restrict__ V, unsigned long long *err,
+                                                 unsigned int *fallbacks) {
+    constexpr int LDL = RB + 1, NGR = 32 / RB;
+    __shared__ double gi[RB * LDL];                     // G^{-1}
+    __shared__ __align__(16) double gbuf[NGR][RB + 2];  // one gather buffer per lane group
+    __shared__ double lu[RB * LDL];
+    __shared__ int piv[RB];
+    pdl_wait();
+    pdl_trigger();
+    const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
+    const int64_t JR = (int64_t)J * R;
+    const double *g = fg + JR;
+    if (w == 0) {
+        const int r = lane % RB;
+        const bool real = lane < RB && r < R;  // lanes >= RB: harmless identity systems
+        double tr = 0.0;
+        for (int z = 0; z < R; ++z) tr += lam * G_snap[z * R + z] + __ldcg(g + z * R + z);
+        const double sh = eps * (tr / R);
+        double a[RB];
+#pragma unroll
+        for (int z = 0; z < RB; ++z) {
+            double v = (z == r) ? 1.0 : 0.0;
+            if (real && z < R) {
+                const double m1 = lam * G_snap[r * R + z] + __ldcg(g + r * R + z);
+                const double m2 = lam * G_snap[z * R + r] + __ldcg(g + z * R + r);
+                v = (m1 + m2) / 2.0;
+                if (blockIdx.x == 0) G[r * R + z] = v;
+                if (z == r) v += sh;
+            }
+            a[z] = v;
+        }
+        double mx = 0.0;
+#pragma unroll
+        for (int z = 0; z < RB; ++z)
+            if (z == r) mx = a[z];
+#pragma unroll
+        for (int off = RB / 2; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL_MASK, mx, off));
+        double im = (mx > 0.0 && isfinite(mx)) ? 1.0 / mx : 1.0;
+        double a0[RB];
+#pragma unroll
+        for (int z = 0; z < RB; ++z) {
+            a0[z] = a[z];
+            a[z] *= im;
+        }
+        const bool ok = __all_sync(FULL_MASK, sweep_inverse_unit<RB>(a, gbuf[lane / RB], r) || lane >= RB);
+        if (!ok) {  // LU with partial pivoting on the unscaled system (lane 0 of group 0)
+#pragma unroll
+            for (int z = 0; z < RB; ++z) a[z] = a0[z];
+            if (lane == 0 && blockIdx.x == 0) atomicAdd(fallbacks, 1u);
+            const bool okLU = lu_fallback<RB>(a, lu, piv, r, R, lane < RB);
+            if (lane == 0 && !okLU) report_error(err, -1, DASH_E_SINGULAR);
+            im = 1.0;
+        }
+        if (lane < RB) {  // a = -(scaled G)^{-1}  ->  G^{-1} = -a / max diag
+#pragma unroll
+            for (int z = 0; z < RB; ++z) gi[r * LDL + z] = -a[z] * im;
+        }
+    }
+    __syncthreads();
+    const int j = blockIdx.x * blockDim.x + tid;
+    if (j >= J) return;
+    double fj[RB];
+#pragma unroll
+    for (int z = 0; z < RB; ++z) {
+        double v = 0.0;
+        if (z < R) {
+            v = lam * F_snap[(int64_t)j * R + z] + __ldcg(fg + (int64_t)j * R + z);
+            F[(int64_t)j * R + z] = v;
+        }
+        fj[z] = v;
+    }
+    bool fin = true;
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+        if (r < R) {
+            double acc = 0.0;
+#pragma unroll
+            for (int z = 0; z < RB; ++z) acc = fma(gi[r * LDL + z], fj[z], acc);
+            V[(int64_t)j * R + r] = acc;
+            fin = fin && finite_d(acc);
+        }
+    }
+    if (!fin) report_error(err, -1, DASH_E_NONFINITE);
+}
+
 // us = u o w  (group_update seam output)
 __global__ void k_us(const double *__restrict__ u, const double *__restrict__ w, int G, int I, int R,
                      double *__restrict__ us) {
@@ -1092,9 +1188,17 @@ void launch_fgemm(dash_ctx *ctx, cudaStream_t st, const B *b, int J, const doubl
 template <int RB>
 void launch_vsolve_t(dash_ctx *ctx, cudaStream_t st, const double *fg, double lam, int J, int R, double eps,
                      double *F, double *G, double *V) {
+    PhaseScope ps(ctx, st, PH_VSOLVE);
+    static const bool old_vsolve = getenv("DASH_CHOL_VSOLVE") != nullptr;  // A/B: per-warp Cholesky variant
+    if constexpr (RB <= 16) {
+        if (!old_vsolve) {
+            launch_k(true, k_vsolve2<RB>, (J + 127) / 128, 128, 0, st, fg, (const double *)ctx->fsnap.p,
+                     (const double *)ctx->gsnap.p, lam, J, R, eps, F, G, V, ctx->err, ctx->fallbacks);
+            return;
+        }
+    }
     constexpr int NWV = RB <= 16 ? 4 : 1;
     int blocks = (J + NWV * 32 - 1) / (NWV * 32);
-    PhaseScope ps(ctx, st, PH_VSOLVE);
     launch_k(true, k_vsolve<RB, NWV>, blocks, NWV * 32, 0, st, fg, (const double *)ctx->fsnap.p,
              (const double *)ctx->gsnap.p, lam, J, R, eps, F, G, V, ctx->err, ctx->fallbacks);
 }
