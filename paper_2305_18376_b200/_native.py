@@ -119,10 +119,16 @@ def load_library(path: Path | None = None):
         return lib
 
 
+_cuda_ok = False
+
+
 def lib():
-    if not torch.cuda.is_available():
-        raise NativeUnavailable("the DASH engine needs a CUDA device (B200); none is visible")
-    return load_library()
+    global _cuda_ok
+    if not _cuda_ok:
+        if not torch.cuda.is_available():
+            raise NativeUnavailable("the DASH engine needs a CUDA device (B200); none is visible")
+        _cuda_ok = True
+    return _lib if _lib is not None else load_library()
 
 
 _ctx = {}
@@ -145,8 +151,12 @@ def context(device: int | None = None):
 
 
 def stream_ptr(stream=None) -> int:
-    s = torch.cuda.current_stream() if stream is None else stream
-    return int(s.cuda_stream)
+    if stream is None:
+        raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)  # no Stream object per call
+        if raw is not None:
+            return int(raw(torch.cuda.current_device()))
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream)
 
 
 def check(rc: int, what: str):

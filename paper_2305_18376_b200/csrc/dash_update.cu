@@ -27,6 +27,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <mutex>
 #include <type_traits>
 #include <vector>
 
@@ -461,6 +462,26 @@ __global__ void __launch_bounds__(NW * 32) k_slices(SliceParams p) {
 // Kernel launch, optionally with programmatic stream serialization (PDL):
 // only for kernels that call pdl_wait() before touching their predecessor's
 // data (dash_common.cuh).  DASH_NO_PDL=1 disables it (A/B timing).
+// Raise a kernel's dynamic shared-memory limit once (not on every update):
+// keyed by the kernel's address (kernels of one signature share a type).
+template <typename K>
+void ensure_smem_attr(K kern, size_t smem) {
+    static std::mutex mu;
+    static std::vector<std::pair<const void *, size_t>> done;
+    std::lock_guard<std::mutex> lock(mu);
+    const void *key = reinterpret_cast<const void *>(kern);
+    for (auto &e : done)
+        if (e.first == key) {
+            if (e.second < smem) {
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                e.second = smem;
+            }
+            return;
+        }
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    done.push_back({key, smem});
+}
+
 bool pdl_enabled() {
     static const bool on = getenv("DASH_NO_PDL") == nullptr;
     return on;
@@ -1390,7 +1411,7 @@ int launch_bigx(dash_ctx *ctx, cudaStream_t st, const B *b, const BigxParams &bp
     const size_t smem = SM::bytes(bp.J);
     const int js = SM::strips(bp.J);
     auto go = [&](auto kern) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        ensure_smem_attr(kern, smem);
         return launch_k(true, kern, bp.G, kBxThreads, smem, st, mx, bp);
     };
     int rc;
