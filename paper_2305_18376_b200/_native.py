@@ -150,6 +150,32 @@ def context(device: int | None = None):
     return c
 
 
+class OwnedContext:
+    """A dash_ctx owned by one StreamState: its workspace arena and plan are
+    private, so states updated concurrently on different streams (or host
+    threads) never share them.  Destroyed with the owner."""
+
+    def __init__(self, device: int):
+        L = lib()
+        with torch.cuda.device(device):
+            h = ctypes.c_void_p()
+            rc = L.dash_ctx_create(ctypes.byref(h))
+            if rc != DASH_OK:
+                raise RuntimeError(f"dash_ctx_create failed ({rc})")
+        self.handle = h
+        self._as_parameter_ = h  # pass straight to ctypes calls
+
+    def __del__(self):
+        import sys
+        h = getattr(self, "handle", None)
+        if h is not None and _lib is not None and not sys.is_finalizing():
+            try:
+                _lib.dash_ctx_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+
 def stream_ptr(stream=None) -> int:
     if stream is None:
         raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)  # no Stream object per call

@@ -191,7 +191,7 @@ class StreamState:
         self._pin_event = None
         self._cache: dict = {}
         self._last = None  # last update's device batch (for local_error)
-        self._ctx = nat.context(self.device.index)
+        self._ctx = nat.OwnedContext(self.device.index)  # private workspace: one update in flight per state
 
     # -- construction helpers ----------------------------------------------
     def _ingest_u_blocks(self, u_blocks):

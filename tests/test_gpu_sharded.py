@@ -5,7 +5,6 @@ is a host-side exchange summed in fixed rank order (what NCCL all-reduce
 provides across GPUs).  This exercises the split entry points
 dash_update_pass_begin / dash_update_pass_finish the multi-GPU bench uses.
 Compared with one unsharded GPU state and with the CPU oracle."""
-import ctypes
 import threading
 
 import numpy as np
@@ -48,15 +47,11 @@ class HostAllReduce:
 
 
 def _rank_state(ps, owned, dtype):
-    from paper_2305_18376_b200 import _native as nat
     from paper_2305_18376_b200.stream import StreamState
     idx = {s: k for k, s in enumerate(ps["slice_ids"])}
     rows = np.array([idx[s] for s in owned], dtype=np.int64)
     arr = dict(ps, slice_ids=list(owned), W=ps["W"][rows], C=ps["C"][rows], D=ps["D"][rows])
-    st = StreamState.from_arrays(arr, dtype=dtype)
-    h = ctypes.c_void_p()
-    assert nat.lib().dash_ctx_create(ctypes.byref(h)) == 0
-    st._ctx = h  # a rank owns its context (workspace, plan) like a process would
+    st = StreamState.from_arrays(arr, dtype=dtype)  # owns its context (workspace, plan), like a process
     return st
 
 
