@@ -46,3 +46,22 @@ def test_sm100a_cubin_in_library():
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", str(so)],
                          capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_host_row_ptr_helper_on_cpu():
+    """dash_host_row_ptr is host-only (no device): prefix sums and bad counts."""
+    import ctypes
+    import numpy as np
+    from paper_2305_18376_b200 import _native
+    from paper_2305_18376_b200.build import build_library
+    build_library()
+    lib = _native.load_library()
+    counts = np.array([3, 0, 5, 1, 64, 65], dtype=np.int64)
+    rp = np.full(counts.size + 1, -7, dtype=np.int64)
+    n = ctypes.c_int64(0)
+    assert lib.dash_host_row_ptr(counts.ctypes.data, counts.size, rp.ctypes.data, ctypes.byref(n)) == 0
+    assert rp.tolist() == [0, 3, 3, 8, 9, 73, 138] and n.value == 138
+    empty = np.zeros(1, dtype=np.int64)
+    assert lib.dash_host_row_ptr(0, 0, empty.ctypes.data, ctypes.byref(n)) == 0 and n.value == 0
+    bad = np.array([2, -1], dtype=np.int64)
+    assert lib.dash_host_row_ptr(bad.ctypes.data, 2, rp.ctypes.data, ctypes.byref(n)) == _native.DASH_E_ARG

@@ -294,3 +294,24 @@ def test_host_pipeline_matches_device_resident_updates():
         assert np.array_equal(vh[k].numpy(), vu), k
     for name in ("W", "C", "D", "F", "G", "V"):
         assert np.array_equal(getattr(a, name), getattr(b, name)), name
+
+
+def test_indefinite_G_takes_the_lu_path_like_the_reference():
+    """G0 = -10 I makes lam G0 + g indefinite: every pivot test of the V
+    solve's sweep fails and the LU fallback (the reference's np.linalg.solve,
+    linalg.py:25-45) must give the reference's V."""
+    from paper_2305_18376_b200 import _native as nat
+    from paper_2305_18376_b200 import workloads as wl
+    cfg = wl.scaled(wl.CONFIGS["large"], K0=40, steps=1, new_slices=2)
+    stream = wl.make_stream(cfg)
+    ps = wl.planted_state(stream)
+    ps["G"] = -10.0 * np.eye(cfg.R) * np.abs(ps["G"]).max()
+    gpu = gpu_state_from_planted(ps)
+    cpu = oracle_from_planted(ps)
+    nat.lib().dash_ctx_fallbacks(gpu._ctx, nat.stream_ptr(), 1)
+    batch = next(stream.batches())
+    gpu.update(batch)
+    cpu.update(batch)
+    for name in ("V", "F", "G", "W"):
+        assert rel(getattr(gpu, name), getattr(cpu, name)) < TOL, name
+    assert nat.lib().dash_ctx_fallbacks(gpu._ctx, nat.stream_ptr(), 1) >= 1
