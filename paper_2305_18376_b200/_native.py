@@ -8,6 +8,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import sys as _sys
 import threading
 from pathlib import Path
 
@@ -166,9 +167,8 @@ class OwnedContext:
         self._as_parameter_ = h  # pass straight to ctypes calls
 
     def __del__(self):
-        import sys
         h = getattr(self, "handle", None)
-        if h is not None and _lib is not None and not sys.is_finalizing():
+        if h is not None and _lib is not None and not _sys.is_finalizing():
             try:
                 _lib.dash_ctx_destroy(h)
             except Exception:

@@ -471,6 +471,9 @@ class StreamState:
                 allreduce(fg)
                 nat.check(L.dash_update_pass_finish_f64(self._ctx, st, ctypes.byref(s), _ptr(fg),
                                                         RIDGE_EPS), "dash_update_pass_finish_f64")
+        done = torch.cuda.Event()  # this update no longer reads its meta slot after this point
+        done.record()
+        self._meta_slot[3] = done
         self._cache.clear()
         self.last_launches = L.dash_ctx_last_launches(self._ctx)
         if ids is not None:
@@ -485,9 +488,13 @@ class StreamState:
         """Pack the batch's CSR index arrays -- row_ptr (M+1) i64 | state_row
         (M) i32 | is_new (M) u8 -- into one pinned ring slot (the prefix sum is
         written there by the library's host helper) and copy them to the
-        device in ONE transfer; the host never waits for the GPU unless the
-        ring wraps onto a copy still in flight.  Returns (N, row_ptr host view,
-        (row_ptr, state_row, is_new) device views)."""
+        device in ONE transfer on a side stream, so the copy runs while the
+        previous update's kernels still execute and the update's first kernel
+        follows the previous one with only an event wait between them.  The
+        host never waits for the GPU unless the ring wraps onto a copy still
+        in flight; a device slot is rewritten only after the update that read
+        it has finished.  Returns (N, row_ptr host view, (row_ptr, state_row,
+        is_new) device views)."""
         counts = np.ascontiguousarray(counts, dtype=np.int64)
         M_old = len(existing_rows)
         M = M_old + L
@@ -499,11 +506,15 @@ class StreamState:
         ring = getattr(self, "_meta_ring", None)
         if ring is None or ring[0][0].shape[0] < nbytes:
             cap = max(4096, int(nbytes * 1.25) + 64)
+            if ring is not None:
+                torch.cuda.current_stream(self.device).synchronize()  # old slots may still be read
             ring = [[torch.empty(cap, dtype=torch.uint8, pin_memory=True),
-                     torch.empty(cap, dtype=torch.uint8, device=self.device), None]
+                     torch.empty(cap, dtype=torch.uint8, device=self.device), None, None]
                     for _ in range(self._META_RING)]
             self._meta_ring = ring
             self._meta_i = 0
+            if getattr(self, "_meta_stream", None) is None:
+                self._meta_stream = torch.cuda.Stream(self.device)
         slot = ring[self._meta_i]
         self._meta_i = (self._meta_i + 1) % self._META_RING
         if slot[2] is not None:
@@ -520,10 +531,16 @@ class StreamState:
         nw[:M_old] = 0
         nw[M_old:] = 1
         db = slot[1]
-        db[:nbytes].copy_(slot[0][:nbytes], non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record()
+        cs = self._meta_stream
+        with torch.cuda.stream(cs):
+            if slot[3] is not None:
+                cs.wait_event(slot[3])  # the update that last read this device slot is done
+            db[:nbytes].copy_(slot[0][:nbytes], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cs)
         slot[2] = ev
+        torch.cuda.current_stream(self.device).wait_event(ev)
+        self._meta_slot = slot
         meta = (db[:o_sr].view(torch.int64), db[o_sr:o_sr + 4 * M].view(torch.int32), db[o_nw:o_nw + M])
         return int(Nout.value), row_ptr, meta
 
