@@ -1073,6 +1073,15 @@ struct SlicePlan {
     bool split = false, big_dev = false;
 };
 
+// Big-slice statistics of the last row_ptr built by dash_host_row_ptr on this
+// thread: the planner reuses them instead of re-scanning row_ptr (M entries).
+struct RowPtrStats {
+    const int64_t *row_ptr = nullptr;
+    int64_t M = -1, N = -1, tiles = 0;
+    int nbig = 0;
+};
+thread_local RowPtrStats g_rp_stats;
+
 SlicePlan make_plan(const int64_t *row_ptr, int M, int RB, int R, int num_sms) {
     SlicePlan pl;
     if (RB > 16) {
@@ -1086,11 +1095,17 @@ SlicePlan make_plan(const int64_t *row_ptr, int M, int RB, int R, int num_sms) {
         pl.big_dev = true;
         int nbig = 0;
         int64_t tiles = 0;
-        for (int m = 0; m < M; ++m) {
-            const int64_t n = row_ptr[m + 1] - row_ptr[m];
-            if (n > kSmallRows) {
-                ++nbig;
-                tiles += (n + kTR - 1) / kTR;
+        const RowPtrStats &c = g_rp_stats;
+        if (c.row_ptr == row_ptr && c.M == M && c.N == row_ptr[M]) {
+            nbig = c.nbig;
+            tiles = c.tiles;
+        } else {
+            for (int m = 0; m < M; ++m) {
+                const int64_t n = row_ptr[m + 1] - row_ptr[m];
+                if (n > kSmallRows) {
+                    ++nbig;
+                    tiles += (n + kTR - 1) / kTR;
+                }
             }
         }
         pl.gbig = nbig;  // one CTA (and G slot) per big slice
@@ -1722,15 +1737,25 @@ int dash_ctx_last_launches(const dash_ctx *ctx) { return ctx ? ctx->last_launche
 
 int dash_host_row_ptr(const int64_t *counts, int64_t M, int64_t *row_ptr, int64_t *N_out) {
     if (M < 0 || (M > 0 && (!counts || !row_ptr))) return DASH_E_ARG;
-    int64_t acc = 0;
+    int64_t acc = 0, tiles = 0;
+    int nbig = 0;
     if (row_ptr) row_ptr[0] = 0;
     for (int64_t m = 0; m < M; ++m) {
         const int64_t c = counts[m];
         if (c < 0) return DASH_E_ARG;
         acc += c;
         row_ptr[m + 1] = acc;
+        if (c > kSmallRows) {  // the planner's big-slice count, gathered in the same pass
+            ++nbig;
+            tiles += (c + kTR - 1) / kTR;
+        }
     }
     if (N_out) *N_out = acc;
+    g_rp_stats.row_ptr = row_ptr;
+    g_rp_stats.M = M;
+    g_rp_stats.N = acc;
+    g_rp_stats.nbig = nbig;
+    g_rp_stats.tiles = tiles;
     return DASH_OK;
 }
 

@@ -163,7 +163,8 @@ class StreamState:
         self.update_index = int(update_index)
         self.passes = int(passes)
         self.slice_ids = list(slice_ids)
-        self._row_of = {sid: k for k, sid in enumerate(self.slice_ids)}
+        self._rowmap = {sid: k for k, sid in enumerate(self.slice_ids)}
+        self._rowmap_n = len(self.slice_ids)  # slice_ids[:n] are in _rowmap (the rest register lazily)
         V = _to_dev(V, self.device)
         self.J, R = V.shape
         if R > nat.MAX_RANK:
@@ -224,6 +225,17 @@ class StreamState:
         return cls(arrays["slice_ids"], u_blocks, arrays["W"], arrays["V"], arrays["C"],
                    arrays["D"], arrays["F"], arrays["G"], arrays["forgetting"],
                    passes=arrays.get("passes", 1), device=device, dtype=dtype)
+
+    @property
+    def _row_of(self) -> dict:
+        """slice id -> state row.  Registration appends to ``slice_ids`` only;
+        the map catches up here, on first use (the device fast path never
+        needs it, and 500 dict inserts cost ~100 us of host time per update)."""
+        ids, d = self.slice_ids, self._rowmap
+        if self._rowmap_n < len(ids):
+            d.update(zip(ids[self._rowmap_n:], range(self._rowmap_n, len(ids))))
+            self._rowmap_n = len(ids)
+        return d
 
     # -- reference attribute API --------------------------------------------
     @property
@@ -434,8 +446,7 @@ class StreamState:
         """stream.py:270-280: new slices take the next state rows, in batch order."""
         L = len(new_ids)
         self._reserve(self._K + L)
-        self._row_of.update(zip(new_ids, range(len(self.slice_ids), len(self.slice_ids) + L)))
-        self.slice_ids.extend(new_ids)
+        self.slice_ids.extend(new_ids)  # _row_of catches up lazily
         self._K += L
 
     def _run(self, X, N, row_ptr, meta, check, ids, allreduce=None):
@@ -471,9 +482,8 @@ class StreamState:
                 allreduce(fg)
                 nat.check(L.dash_update_pass_finish_f64(self._ctx, st, ctypes.byref(s), _ptr(fg),
                                                         RIDGE_EPS), "dash_update_pass_finish_f64")
-        done = torch.cuda.Event()  # this update no longer reads its meta slot after this point
-        done.record()
-        self._meta_slot[3] = done
+        self._meta_slot[3].record()  # this update no longer reads its meta slot after this point
+        self._meta_slot[4][1] = True
         self._cache.clear()
         self.last_launches = L.dash_ctx_last_launches(self._ctx)
         if ids is not None:
@@ -508,8 +518,10 @@ class StreamState:
             cap = max(4096, int(nbytes * 1.25) + 64)
             if ring is not None:
                 torch.cuda.current_stream(self.device).synchronize()  # old slots may still be read
+            # slot: pinned bytes, device bytes, copy-done event, update-done event, [copy issued, update issued]
             ring = [[torch.empty(cap, dtype=torch.uint8, pin_memory=True),
-                     torch.empty(cap, dtype=torch.uint8, device=self.device), None, None]
+                     torch.empty(cap, dtype=torch.uint8, device=self.device),
+                     torch.cuda.Event(), torch.cuda.Event(), [False, False]]
                     for _ in range(self._META_RING)]
             self._meta_ring = ring
             self._meta_i = 0
@@ -517,8 +529,8 @@ class StreamState:
                 self._meta_stream = torch.cuda.Stream(self.device)
         slot = ring[self._meta_i]
         self._meta_i = (self._meta_i + 1) % self._META_RING
-        if slot[2] is not None:
-            slot[2].synchronize()
+        if slot[4][0]:
+            slot[2].synchronize()  # the pinned bytes' previous upload is done
         hb = slot[0].numpy()
         row_ptr = hb[:o_sr].view(np.int64)
         Nout = ctypes.c_int64(0)
@@ -533,13 +545,12 @@ class StreamState:
         db = slot[1]
         cs = self._meta_stream
         with torch.cuda.stream(cs):
-            if slot[3] is not None:
+            if slot[4][1]:
                 cs.wait_event(slot[3])  # the update that last read this device slot is done
             db[:nbytes].copy_(slot[0][:nbytes], non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(cs)
-        slot[2] = ev
-        torch.cuda.current_stream(self.device).wait_event(ev)
+            slot[2].record(cs)
+        slot[4][0] = True
+        torch.cuda.current_stream(self.device).wait_event(slot[2])
         self._meta_slot = slot
         meta = (db[:o_sr].view(torch.int64), db[o_sr:o_sr + 4 * M].view(torch.int32), db[o_nw:o_nw + M])
         return int(Nout.value), row_ptr, meta
