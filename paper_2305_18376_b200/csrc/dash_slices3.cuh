@@ -257,11 +257,18 @@ __global__ void __launch_bounds__(S3<RB>::NW * 32, kS3CtasPerSM) k_slices3(Slice
         const int j = unit * GPW + lane / RB;
         return (unit < nunits && j < nsmall) ? __ldg(meta + j) : none;
     };
+    // raw (predicated) loads of the next unit's W / C entries: nothing consumes
+    // them until that unit starts, so their latency hides behind this unit
+    // (the bootstrap / dormant selects are applied at the consumer)
     auto sw_of = [&](const int4 &mt, bool act, double &sw, double &cw) {
         const int wr = mt.z & 0x7fffffff;
-        const bool fr = mt.z < 0;
-        sw = (act && r < R) ? ((fr && p.pass == 0) ? 1.0 : p.W[(int64_t)wr * R + r]) : 0.0;
-        cw = (act && r < R && !fr) ? p.C[(int64_t)wr * R + r] : 0.0;
+        const int64_t idx = (int64_t)wr * R + r;
+        sw = 0.0;
+        cw = 0.0;
+        if (act && r < R) {
+            sw = p.W[idx];
+            cw = p.C[idx];
+        }
     };
     int unit = blockIdx.x * S::NW + w;
     int4 nmeta = meta_of(unit);
@@ -278,7 +285,8 @@ __global__ void __launch_bounds__(S3<RB>::NW * 32, kS3CtasPerSM) k_slices3(Slice
         const bool fresh = mt.z < 0;
         const bool real = active && r < R;
         const bool staged = n <= CAPW;
-        const double s_r = nsw, cold = ncw;
+        const double s_r = real ? ((fresh && p.pass == 0) ? 1.0 : nsw) : 0.0;  // new slice: W bootstrap 1
+        const double cold = (real && !fresh) ? ncw : 0.0;
         const int nxt = unit + nwarps;
         nmeta = meta_of(nxt);
         // ---- async prefetch: D column r (D symmetric; coalesced) and the XV rows
