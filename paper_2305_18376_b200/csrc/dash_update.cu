@@ -781,8 +781,17 @@ __global__ void __launch_bounds__(128) k_vsolve2(const double *__restrict__ fg, 
     if (w == 0) {
         const int r = lane % RB;
         const bool real = lane < RB && r < R;  // lanes >= RB: harmless identity systems
+        // trace of sym(lam G0 + g): lane r holds entry (r, r); fixed-order reduction over lanes 0..R-1
         double tr = 0.0;
-        for (int z = 0; z < R; ++z) tr += lam * G_snap[z * R + z] + __ldcg(g + z * R + z);
+        {
+            const double dr = (lane < R) ? lam * G_snap[lane * R + lane] + __ldcg(g + lane * R + lane) : 0.0;
+            if (lane == 0) tr = dr;
+            for (int z = 1; z < R; ++z) {  // same order as the serial sum (bit-identical)
+                const double v = __shfl_sync(FULL_MASK, dr, z);
+                if (lane == 0) tr += v;
+            }
+            tr = __shfl_sync(FULL_MASK, tr, 0);
+        }
         const double sh = eps * (tr / R);
         double a[RB];
 #pragma unroll
