@@ -244,10 +244,19 @@ def run_gpu(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # Validation knobs for the multi-rank code path on a single-GPU box (not
+    # for measurement): DASH_BENCH_DEVICE pins every rank to one device,
+    # DASH_BENCH_BACKEND=gloo exchanges the F/G sums on the host.
+    if "DASH_BENCH_DEVICE" in os.environ:
+        local = int(os.environ["DASH_BENCH_DEVICE"])
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("DASH_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     cfg = wl.CONFIGS[args.config]
     if args.K0:
         cfg = wl.scaled(cfg, K0=args.K0)
