@@ -159,7 +159,8 @@ int dash_update_pass_begin_f32(dash_ctx *ctx, void *stream, const dash_batch_f32
 /* Phase timing for benchmarks: when enabled, CUDA events bracket every
  * launch; dash_ctx_phase_ms syncs and returns the summed milliseconds (and
  * launch counts) per phase id since the last call:
- * 0 row_slice, 1 prologue, 2 xv, 3 slices, 4 fgemm, 5 sum_fg, 6 vsolve, 7 fused. */
+ * 0 row_slice (plan), 1 prologue, 2 xv, 3 slices, 4 fgemm, 5 sum_fg, 6 vsolve,
+ * 7 big (big-slice kernels: k_big, or k_bigx_pre + k_bigx), 8 big_post (k_bigx_post). */
 int dash_ctx_set_profiling(dash_ctx *ctx, int enable);
 int dash_ctx_phase_ms(dash_ctx *ctx, double *ms_out, int32_t *count_out, int32_t nphases);
 

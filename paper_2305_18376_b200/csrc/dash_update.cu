@@ -904,7 +904,7 @@ __global__ void k_finish_fg(const double *__restrict__ fg, const double *__restr
 }
 }  // namespace
 
-enum Phase { PH_ROWSLICE = 0, PH_PROLOGUE, PH_XV, PH_SLICES, PH_FGEMM, PH_SUMFG, PH_VSOLVE, PH_BIG, PH_COUNT };
+enum Phase { PH_ROWSLICE = 0, PH_PROLOGUE, PH_XV, PH_SLICES, PH_FGEMM, PH_SUMFG, PH_VSOLVE, PH_BIG, PH_BIGPOST, PH_COUNT };
 
 struct dash_ctx {
     struct Buf {
@@ -1450,7 +1450,7 @@ int launch_bigx(dash_ctx *ctx, cudaStream_t st, const B *b, const BigxParams &bp
 
 int launch_bigx_post(dash_ctx *ctx, cudaStream_t st, const BigxParams &bp) {
     if (bp.T == 0) return 0;
-    PhaseScope ps(ctx, st, PH_BIG);
+    PhaseScope ps(ctx, st, PH_BIGPOST);
     return launch_k(true, k_bigx_post, ctx->bigx_nbig, 256, 0, st, bp);
 }
 
