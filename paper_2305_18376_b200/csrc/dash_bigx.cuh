@@ -35,8 +35,14 @@ constexpr int kBxMP = kBxRB + 4;    // Ms pitch (B-frag reads)
 constexpr int kBxUP = kBxRB + 8;    // U tile pitch (gram frags conflict-free)
 
 constexpr int kBxMaxStages = 6;
-constexpr int kBxA = 8;                           // XV / U warps: two tiles in flight (4 row blocks each)
-constexpr int kBxB = 4;                           // X^T U / gram warps: P strips b, b + 4 (J <= 128)
+#ifndef DASH_BXA
+#define DASH_BXA 8
+#endif
+#ifndef DASH_BXB
+#define DASH_BXB 4
+#endif
+constexpr int kBxA = DASH_BXA;                    // XV / U warps: kBxA / 4 tiles in flight (4 row blocks each)
+constexpr int kBxB = DASH_BXB;                    // X^T U / gram warps: P strips b, b + kBxB, ... (J <= 128)
 constexpr int kBxThreads = (kBxA + kBxB + 1) * 32;  // + the producer warp
 constexpr int kBxUSlots = 4;                      // U hand-off buffers
 // Shared-memory plan of k_bigx for X in FP64 (boxes of 16 doubles x 32 rows)
@@ -293,13 +299,14 @@ __global__ void __maxnreg__(128) k_bigx(const __grid_constant__ CUtensorMap tmX,
         }
         asm volatile("bar.sync 2, %0;" ::"n"(kBxA * 32) : "memory");  // the XV warps only
         const int par = w >> 2, mb = w & 3;
+        constexpr int NPAR = kBxA / 4;  // tiles in flight on the XV side
         const int xrow = 8 * mb + qperm(g);  // A-fragment / output row (conflict-free X reads)
         double msf[4][2];                    // B frags of U = XV Ms^T in the permuted K order
         int msf_bi = -1;
         double cacc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
         for (int64_t tau = tau0, i = 0; tau < tau1; ++tau, ++i) {
             advance(tau);
-            if ((int)(i & 1) == par) {
+            if ((int)(i % NPAR) == par) {
                 if (msf_bi != bi) {
                     // K step kk feeds XV column col(kk, t) = 8 (kk >> 1) + 2 t + (kk & 1) (the C layout)
                     const double *msg = p.ms + (int64_t)bi * 16 * kBxMP;

@@ -1440,11 +1440,11 @@ int launch_bigx(dash_ctx *ctx, cudaStream_t st, const B *b, const BigxParams &bp
     };
     int rc;
     // J <= 128 (the fused path's limit): <= 8 FP64 / 4 FP32 strips over kBxB X^T U warps
-    static_assert(kBxB == 4, "strip split below assumes 4 X^T U warps");
-    if constexpr (SM::F32)  // float boxes: 32 columns per strip
+    constexpr int MS = kBxB >= 8 ? 1 : 2;  // P strips per X^T U warp for up to 8 strips
+    if constexpr (SM::F32)  // float boxes: 32 columns per strip (<= 4)
         rc = js == 4 ? go(k_bigx<1, 4, float>) : go(k_bigx<1, 0, float>);
     else
-        rc = js == 8 ? go(k_bigx<2, 8, double>) : js <= 4 ? go(k_bigx<1, 0, double>) : go(k_bigx<2, 0, double>);
+        rc = js == 8 ? go(k_bigx<MS, 8, double>) : js <= kBxB ? go(k_bigx<1, 0, double>) : go(k_bigx<MS, 0, double>);
     return rc;
 }
 
