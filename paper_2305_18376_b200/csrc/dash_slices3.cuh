@@ -17,6 +17,7 @@
 #define DASH_S3_CTAS 4
 #endif
 constexpr int kS3CtasPerSM = DASH_S3_CTAS;  // resident CTAs per SM (register budget 65536 / (128 x this))
+constexpr double kS3Neumann = 1e-4;         // Neumann fast path bound on ||P d||: truncation O(rho^3) <= 1e-12
 
 template <int RB>
 struct S3 {
@@ -25,16 +26,18 @@ struct S3 {
     static constexpr int NG = NW * GPW;
     static constexpr int LDV = RB + 2;
     static constexpr int LDL = RB + 1;
-    static constexpr int CAPW = 16;  // XV rows staged per group (longer slices read XV directly)
+    static constexpr int CAPW = 14;  // XV rows staged per group (longer slices read XV directly)
     // per group: buf[RB+2] (gathers; gj_solve scratch) | dn[RB*LDL] | xs[CAPW*RB]
     // per warp : gacc[RB*LDL] (the warp's groups accumulate in turn) | lu[RB*LDL] | piv[RB]
     //            (LU fallback scratch, used by one group at a time)
     // Per-lane rows use the odd pitch LDL = RB+1 (lane r's row r hits distinct banks).
+    // per CTA after the warps: P = vtv^{-1} (RB x RB, symmetric, read by column) | ||P||_inf | ok
     // ~55 KB for RB = 16: four CTAs (16 warps) per SM.
     static constexpr int per_group = (RB + 2) + RB * LDL + CAPW * RB;
     static constexpr int per_warp = GPW * per_group + 2 * RB * LDL + RB;
     static constexpr int shared = RB * LDV;
-    __host__ __device__ static constexpr size_t bytes() { return sizeof(double) * (shared + NW * per_warp); }
+    static constexpr int pinv = RB * RB + 2;
+    __host__ __device__ static constexpr size_t bytes() { return sizeof(double) * (shared + NW * per_warp + pinv); }
     static_assert(shared % 2 == 0 && per_group % 2 == 0 && per_warp % 2 == 0 && (RB * LDL) % 2 == 0,
                   "group scratch must stay 16-byte aligned");
 };
@@ -245,6 +248,39 @@ __global__ void __launch_bounds__(S3<RB>::NW * 32, kS3CtasPerSM) k_slices3(Slice
     }
     __syncthreads();
     const double *vrow = vtv_s + r * LDV;
+    // ---- P = vtv^{-1} once per CTA (warp 0; both groups compute, group 0 writes):
+    // the A system of every slice is S (vtv + sh S^-2) S, solved below by a
+    // Neumann series around P when the ridge term is small (see the unit loop)
+    double *P_s = sm + S::shared + S::NW * S::per_warp;
+    if (w == 0) {
+        double a[RB];
+        double mx = r < R ? vrow[r] : 0.0;
+#pragma unroll
+        for (int off = RB / 2; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL_MASK, mx, off));
+        const double im = (mx > 0.0 && isfinite(mx)) ? 1.0 / mx : 1.0;
+#pragma unroll
+        for (int z = 0; z < RB; ++z) a[z] = (r < R) ? ((z < R) ? vrow[z] * im : 0.0) : ((z == r) ? 1.0 : 0.0);
+        const bool ok = sweep_inverse_unit<RB>(a, buf, r);
+        double rs = 0.0;
+#pragma unroll
+        for (int z = 0; z < RB; ++z) {
+            a[z] = (r < R && z < R) ? -a[z] * im : 0.0;  // P[r][z]
+            rs += fabs(a[z]);
+        }
+#pragma unroll
+        for (int off = RB / 2; off > 0; off >>= 1) rs = fmax(rs, __shfl_xor_sync(FULL_MASK, rs, off));
+        if (gl == 0) {
+#pragma unroll
+            for (int z = 0; z < RB; ++z) P_s[z * RB + r] = a[z];  // column-major = row-major (symmetric)
+            if (r == 0) {
+                P_s[RB * RB] = rs;
+                P_s[RB * RB + 1] = (ok && isfinite(rs) && !p.sweep_only) ? 1.0 : 0.0;
+            }
+        }
+    }
+    __syncthreads();
+    const double pnorm = P_s[RB * RB];
+    const bool pok = P_s[RB * RB + 1] != 0.0;
 
     const int nsmall = plan_counts[0];
     const int nunits = (nsmall + GPW - 1) / GPW;
@@ -297,40 +333,71 @@ __global__ void __launch_bounds__(S3<RB>::NW * 32, kS3CtasPerSM) k_slices3(Slice
         if (real && staged)
             for (int i = 0; i < (int)n; ++i) cp_async8(xs + i * RB + r, p.XV + (r0 + i) * R + r);
 
-        // ---- A = vtv o s s^T + shift I, a <- -A^{-1} diag(s)  (_kernels.py:86-97)
+        // ---- A = vtv o s s^T + shift I  (_kernels.py:86-97)
         double s_all[RB];
         group_gather<RB>(s_r, buf, r, s_all);
         double sh = 0.0;
         _Pragma("unroll") for (int z = 0; z < RB; ++z)  // compile-time bound: s_all stays in registers
                 if (z < R) sh += vtv_s[z * LDV + z] * s_all[z] * s_all[z];
         sh = p.eps * sh / R;
+        // Fast path: A = S M S with M = vtv + diag(d), d_r = sh / s_r^2, so
+        // u = A^{-1} (s o xv) = S^{-1} M^{-1} xv and M^{-1} = P - P d P + P d P d P - ...
+        // Taken (warp-uniform) when rho = max_r d_r * ||P||_inf <= kS3Neumann
+        // for every active slice of the warp: the dropped terms are O(rho^3)
+        // relative (<= 1e-12).  Otherwise the exact sweep below.
         double a[RB];
-        double im;  // 1 / max diag(A): the sweep runs on A / max diag (all pivots <= 1)
+        double im;       // sweep: 1 / max diag(A); fast path: 1 / s_r
+        double dl = 0.0; // fast path: d_r
+        bool fast;
         {
-            const double dg = real ? sh : 1.0;
-            double mx = vrow[r] * s_r * s_r + dg;  // this lane's diagonal (padded lanes: 1)
+            double q = 0.0, isr = 0.0;
+            bool bad = false;
+            if (real) {
+                isr = rcp_nr(s_r);
+                q = isr * isr;
+                bad = !(s_r != 0.0) || !isfinite(q);
+            }
+            double qm = bad ? INFINITY : q;
 #pragma unroll
-            for (int off = RB / 2; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL_MASK, mx, off));
-            im = (mx > 0.0 && isfinite(mx)) ? 1.0 / mx : 1.0;
-            const double sr_im = s_r * im, dg_im = dg * im;
-#pragma unroll
-            for (int z = 0; z < RB; ++z) a[z] = vrow[z] * sr_im * s_all[z] + ((z == r) ? dg_im : 0.0);
+            for (int off = RB / 2; off > 0; off >>= 1) qm = fmax(qm, __shfl_xor_sync(FULL_MASK, qm, off));
+            const double rho = sh * qm * pnorm;
+            const bool fg = !active || (pok && rho <= kS3Neumann);  // rho NaN / inf -> sweep
+            fast = __all_sync(FULL_MASK, fg);
+            im = isr;
+            dl = real ? sh * q : 0.0;
         }
-        const bool okA = sweep_inverse_unit<RB>(a, buf, r);
-        if (!okA) im = 1.0;  // LU fallback below solves the unscaled A
-        if (__any_sync(FULL_MASK, !okA)) {
-            const double dg = real ? sh : 1.0;
+        if (fast) {
 #pragma unroll
-            for (int z = 0; z < RB; ++z)
-                if (!okA) a[z] = vrow[z] * s_r * s_all[z] + ((z == r) ? dg : 0.0);
-            if (!okA && r == 0) atomicAdd(p.fallbacks, 1u);
-            const bool okLU = lu_fallback_seq<RB>(a, lu, piv, r, R, !okA);
-            if (!okA && r == 0 && !okLU) report_error(p.err, m, DASH_E_SINGULAR);
+            for (int z = 0; z < RB; ++z) a[z] = -P_s[z * RB + r];  // -P[r][z]
+            sw_of(nmeta, nxt < nunits && nxt * GPW + lane / RB < nsmall, nsw, ncw);  // next unit's s, c_old
+        } else {
+            // a <- -A^{-1} diag(s) by the sweep (LU fallback)
+            {
+                const double dg = real ? sh : 1.0;
+                double mx = vrow[r] * s_r * s_r + dg;  // this lane's diagonal (padded lanes: 1)
+#pragma unroll
+                for (int off = RB / 2; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL_MASK, mx, off));
+                im = (mx > 0.0 && isfinite(mx)) ? 1.0 / mx : 1.0;
+                const double sr_im = s_r * im, dg_im = dg * im;
+#pragma unroll
+                for (int z = 0; z < RB; ++z) a[z] = vrow[z] * sr_im * s_all[z] + ((z == r) ? dg_im : 0.0);
+            }
+            const bool okA = sweep_inverse_unit<RB>(a, buf, r);
+            if (!okA) im = 1.0;  // LU fallback below solves the unscaled A
+            if (__any_sync(FULL_MASK, !okA)) {
+                const double dg = real ? sh : 1.0;
+#pragma unroll
+                for (int z = 0; z < RB; ++z)
+                    if (!okA) a[z] = vrow[z] * s_r * s_all[z] + ((z == r) ? dg : 0.0);
+                if (!okA && r == 0) atomicAdd(p.fallbacks, 1u);
+                const bool okLU = lu_fallback_seq<RB>(a, lu, piv, r, R, !okA);
+                if (!okA && r == 0 && !okLU) report_error(p.err, m, DASH_E_SINGULAR);
+            }
+            sw_of(nmeta, nxt < nunits && nxt * GPW + lane / RB < nsmall, nsw, ncw);  // next unit's s, c_old
+            group_gather<RB>(s_r, buf, r, s_all);
+#pragma unroll
+            for (int z = 0; z < RB; ++z) a[z] *= s_all[z];
         }
-        sw_of(nmeta, nxt < nunits && nxt * GPW + lane / RB < nsmall, nsw, ncw);  // next unit's s, c_old
-        group_gather<RB>(s_r, buf, r, s_all);
-#pragma unroll
-        for (int z = 0; z < RB; ++z) a[z] *= s_all[z];
         cp_async_wait();
         __syncwarp();
 
@@ -359,6 +426,18 @@ __global__ void __launch_bounds__(S3<RB>::NW * 32, kS3CtasPerSM) k_slices3(Slice
                         if (z < R) u = fma(-a[z], __ldg(xr + z), u);
                     xrr = r < R ? __ldg(xr + r) : 0.0;
                 }
+            }
+            if (fast) {  // u = S^{-1} (y - P d y + P d P d y), y = P xv (warp-uniform branch)
+                double t[RB];
+                group_gather<RB>(valid ? dl * u : 0.0, buf, r, t);
+                double c1 = 0.0;
+#pragma unroll
+                for (int z = 0; z < RB; ++z) c1 = fma(-a[z], t[z], c1);  // (P d y)_r
+                group_gather<RB>(valid ? dl * c1 : 0.0, buf, r, t);
+                double c2 = 0.0;
+#pragma unroll
+                for (int z = 0; z < RB; ++z) c2 = fma(-a[z], t[z], c2);  // (P d P d y)_r
+                u = (u - c1) + c2;
             }
             u *= im;
             if (!(valid && r < R)) u = 0.0;
@@ -467,5 +546,8 @@ int launch_slices3(cudaStream_t st, int grid, const SliceParams &sp, const int4 
         cudaFuncSetAttribute(k_slices3<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    return launch_k(pdl_site("sl3"), k_slices3<RB>, grid, S3<RB>::NW * 32, smem, st, sp, meta, plan_counts);
+    static const bool sweep_only = getenv("DASH_S3_SWEEP") != nullptr;  // A/B: exact sweep for every slice
+    SliceParams q = sp;
+    q.sweep_only = sweep_only ? 1 : 0;
+    return launch_k(pdl_site("sl3"), k_slices3<RB>, grid, S3<RB>::NW * 32, smem, st, q, meta, plan_counts);
 }

@@ -163,6 +163,7 @@ struct SliceParams {
     int R;
     double lam, eps;
     int pass, final_pass;
+    int sweep_only = 0;         // k_slices3: exact sweep for every A system (no Neumann fast path)
 };
 
 template <int RB>

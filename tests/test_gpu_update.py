@@ -157,6 +157,42 @@ def test_fused_path_edges_match_oracle(name, kw):
         assert nat.lib().dash_ctx_path_flags(st._ctx) & nat.PATH_BIGX
 
 
+def _spread_weights(ps):
+    """W rows with entries over many magnitudes (and signs, and exact zeros):
+    the small-slice kernel's A system S (vtv + sh S^-2) S takes its Neumann
+    fast path for most slices, the second-order term matters for the 1e-3 ..
+    1e-2 entries, and the exact sweep runs for the tiny / zero ones."""
+    W = ps["W"].copy()
+    K, R = W.shape
+    rng = np.random.default_rng(7)
+    scales = np.array([1.0, 1e-2, 3e-3, -2e-3, 1e-4, 1e-6, 0.0])
+    for k in range(K):
+        if k % 3 == 0:
+            cols = rng.choice(R, size=2, replace=False)
+            W[k, cols] *= scales[rng.integers(len(scales), size=2)]
+    return dict(ps, W=W)
+
+
+@pytest.mark.parametrize("R", [16, 10])
+def test_small_slice_neumann_and_sweep_paths_match_oracle(R):
+    from paper_2305_18376_b200 import workloads as wl
+    cfg = wl.scaled(wl.CONFIGS["large"], K0=150, steps=2, new_slices=2, R=R)
+    stream = wl.make_stream(cfg)
+    ps = _spread_weights(wl.planted_state(stream))
+    gpu = gpu_state_from_planted(ps)
+    cpu = oracle_from_planted(ps)
+    for batch in stream.batches():
+        res = gpu.update(batch)
+        ref = cpu.update(batch)
+        ids = [sid for sid, _, _ in batch.items()]
+        errs = {"U": rel(np.concatenate([res.u_new[s] for s in ids]),
+                         np.concatenate([ref["u_new"][s] for s in ids]))}
+        for name in ("W", "C", "D", "F", "G", "V"):
+            errs[name] = rel(getattr(gpu, name), getattr(cpu, name))
+        bad = {k: v for k, v in errs.items() if not v < TOL}
+        assert not bad, errs
+
+
 def test_update_is_bit_reproducible():
     from paper_2305_18376_b200 import workloads as wl
     cfg = wl.scaled(wl.CONFIGS["large"], K0=100, steps=2, new_slices=2)
