@@ -19,6 +19,16 @@
 constexpr int kS3CtasPerSM = DASH_S3_CTAS;  // resident CTAs per SM (register budget 65536 / (128 x this))
 constexpr double kS3Neumann = 1e-4;         // Neumann fast path bound on ||P d||: truncation O(rho^3) <= 1e-12
 
+// -sum_{z < n} a[z] x[z] in four interleaved chains combined in fixed order
+template <int RB, typename X>
+__device__ __forceinline__ double neg_dot4(const double (&a)[RB], const X &x, int n) {
+    double q[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int z = 0; z < RB; ++z)
+        if (z < n) q[z & 3] = fma(-a[z], x[z], q[z & 3]);
+    return (q[0] + q[1]) + (q[2] + q[3]);
+}
+
 template <int RB>
 struct S3 {
     static constexpr int NW = 4;
@@ -412,31 +422,23 @@ __global__ void __launch_bounds__(S3<RB>::NW * 32, kS3CtasPerSM) k_slices3(Slice
         for (int64_t i = 0; i < nmax; ++i) {
             const bool valid = i < n;
             double u = 0.0, xrr = 0.0;
-            if (valid) {
+            if (valid) {  // y_r = -sum_z a[z] xv_z in 4 independent chains (DFMA latency, not a 16-deep chain)
                 if (staged) {
                     const double *xr = xs + i * RB;
-#pragma unroll
-                    for (int z = 0; z < RB; ++z)
-                        if (z < R) u = fma(-a[z], xr[z], u);
+                    u = neg_dot4<RB>(a, xr, R);
                     xrr = r < R ? xr[r] : 0.0;
                 } else {
-                    const double *xr = p.XV + (r0 + i) * R;
-#pragma unroll
-                    for (int z = 0; z < RB; ++z)
-                        if (z < R) u = fma(-a[z], __ldg(xr + z), u);
+                    const double *__restrict__ xr = p.XV + (r0 + i) * R;
+                    u = neg_dot4<RB>(a, xr, R);
                     xrr = r < R ? __ldg(xr + r) : 0.0;
                 }
             }
             if (fast) {  // u = S^{-1} (y - P d y + P d P d y), y = P xv (warp-uniform branch)
                 double t[RB];
                 group_gather<RB>(valid ? dl * u : 0.0, buf, r, t);
-                double c1 = 0.0;
-#pragma unroll
-                for (int z = 0; z < RB; ++z) c1 = fma(-a[z], t[z], c1);  // (P d y)_r
+                const double c1 = neg_dot4<RB>(a, t, RB);  // (P d y)_r
                 group_gather<RB>(valid ? dl * c1 : 0.0, buf, r, t);
-                double c2 = 0.0;
-#pragma unroll
-                for (int z = 0; z < RB; ++z) c2 = fma(-a[z], t[z], c2);  // (P d P d y)_r
+                const double c2 = neg_dot4<RB>(a, t, RB);  // (P d P d y)_r
                 u = (u - c1) + c2;
             }
             u *= im;
