@@ -18,6 +18,7 @@
 #endif
 constexpr int kS3CtasPerSM = DASH_S3_CTAS;  // resident CTAs per SM (register budget 65536 / (128 x this))
 constexpr double kS3Neumann = 1e-4;         // Neumann fast path bound on ||P d||: truncation O(rho^3) <= 1e-12
+constexpr double kS3Neumann1 = 1e-6;        // below this the first-order term suffices: O(rho^2) <= 1e-12
 
 // -sum_{z < n} a[z] x[z] in four interleaved chains combined in fixed order
 template <int RB, typename X>
@@ -346,10 +347,14 @@ __global__ void __launch_bounds__(S3<RB>::NW * 32, kS3CtasPerSM) k_slices3(Slice
         // ---- A = vtv o s s^T + shift I  (_kernels.py:86-97)
         double s_all[RB];
         group_gather<RB>(s_r, buf, r, s_all);
-        double sh = 0.0;
-        _Pragma("unroll") for (int z = 0; z < RB; ++z)  // compile-time bound: s_all stays in registers
-                if (z < R) sh += vtv_s[z * LDV + z] * s_all[z] * s_all[z];
-        sh = p.eps * sh / R;
+        double sh;
+        {
+            double q4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int z = 0; z < RB; ++z)  // compile-time bound: s_all stays in registers
+                if (z < R) q4[z & 3] = fma(vtv_s[z * LDV + z] * s_all[z], s_all[z], q4[z & 3]);
+            sh = p.eps * ((q4[0] + q4[1]) + (q4[2] + q4[3])) / R;
+        }
         // Fast path: A = S M S with M = vtv + diag(d), d_r = sh / s_r^2, so
         // u = A^{-1} (s o xv) = S^{-1} M^{-1} xv and M^{-1} = P - P d P + P d P d P - ...
         // Taken (warp-uniform) when rho = max_r d_r * ||P||_inf <= kS3Neumann
@@ -358,7 +363,7 @@ __global__ void __launch_bounds__(S3<RB>::NW * 32, kS3CtasPerSM) k_slices3(Slice
         double a[RB];
         double im;       // sweep: 1 / max diag(A); fast path: 1 / s_r
         double dl = 0.0; // fast path: d_r
-        bool fast;
+        bool fast, fast2;  // fast2: the second-order term is needed (rho > kS3Neumann1)
         {
             double q = 0.0, isr = 0.0;
             bool bad = false;
@@ -373,6 +378,7 @@ __global__ void __launch_bounds__(S3<RB>::NW * 32, kS3CtasPerSM) k_slices3(Slice
             const double rho = sh * qm * pnorm;
             const bool fg = !active || (pok && rho <= kS3Neumann);  // rho NaN / inf -> sweep
             fast = __all_sync(FULL_MASK, fg);
+            fast2 = __any_sync(FULL_MASK, active && !(rho <= kS3Neumann1));
             im = isr;
             dl = real ? sh * q : 0.0;
         }
@@ -437,8 +443,11 @@ __global__ void __launch_bounds__(S3<RB>::NW * 32, kS3CtasPerSM) k_slices3(Slice
                 double t[RB];
                 group_gather<RB>(valid ? dl * u : 0.0, buf, r, t);
                 const double c1 = neg_dot4<RB>(a, t, RB);  // (P d y)_r
-                group_gather<RB>(valid ? dl * c1 : 0.0, buf, r, t);
-                const double c2 = neg_dot4<RB>(a, t, RB);  // (P d P d y)_r
+                double c2 = 0.0;
+                if (fast2) {
+                    group_gather<RB>(valid ? dl * c1 : 0.0, buf, r, t);
+                    c2 = neg_dot4<RB>(a, t, RB);  // (P d P d y)_r
+                }
                 u = (u - c1) + c2;
             }
             u *= im;
