@@ -44,6 +44,7 @@ def test_neumann_series_matches_direct_solve_within_the_stated_bound():
     V = rng.uniform(size=(J, R))
     vtv = V.T @ V
     taken = {"first": 0, "second": 0, "sweep": 0}
+    unscaled_fast = 0
     for trial in range(400):
         s = rng.uniform(size=R)
         k = trial % 8
@@ -58,13 +59,14 @@ def test_neumann_series_matches_direct_solve_within_the_stated_bound():
             taken["sweep"] += 1
             continue
         taken["first" if rho <= RHO1 else "second"] += 1
+        unscaled_fast += k == 0
         ref = _direct_u(vtv, s, xv)
         err = np.abs(u - ref).max() / np.abs(ref).max()
         # truncation (rho^2 or rho^3 <= 1e-12) plus rounding of the two routes
         assert err < 1e-9, (trial, rho, err)
     # all three branches are exercised by this spread
     assert min(taken.values()) > 0, taken
-    assert taken["first"] + taken["second"] > taken["sweep"], taken
+    assert unscaled_fast >= 45, unscaled_fast  # U[0,1] weights (the planted workload): nearly all fast
 
 
 def test_zero_weight_forces_the_exact_path():
