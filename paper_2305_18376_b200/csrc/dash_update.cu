@@ -47,26 +47,33 @@ __host__ __device__ inline int rank_bucket(int R) {
 }
 
 // ---------------------------------------------------------------------------
-// k_prologue: vtv, snapshots.  One CTA.
+// k_prologue: vtv, snapshots.  Blocks [0, nvb): vtv, one warp per (r, z)
+// entry (lanes stride J in two interleaved chains, fixed-order shuffle tree:
+// deterministic, and vtv[r][z] == vtv[z][r] bitwise since the products
+// commute); the remaining blocks copy the snapshots.
 // ---------------------------------------------------------------------------
+constexpr int kVtvWarps = 8;  // vtv entries per block
 __global__ void k_prologue(const double *__restrict__ V, int J, int R, double *__restrict__ vtv,
                            const double *__restrict__ F, const double *__restrict__ G,
                            double *__restrict__ F_snap, double *__restrict__ G_snap,
-                           double *__restrict__ v_used, int snap, int last) {
-    if (blockIdx.x == 0) {
-        // vtv: 4 threads per (r, z) split J, combined in fixed order (unrolled: loads in flight)
-        for (int p = threadIdx.x >> 2; p < R * R; p += blockDim.x >> 2) {
-            const int r = p / R, z = p % R, q = threadIdx.x & 3;
-            double acc = 0.0;
-#pragma unroll 8
-            for (int j = q; j < J; j += 4) acc = fma(V[j * R + r], V[j * R + z], acc);
-            acc += __shfl_xor_sync(FULL_MASK, acc, 1);
-            acc += __shfl_xor_sync(FULL_MASK, acc, 2);
-            if (q == 0) vtv[p] = acc;
+                           double *__restrict__ v_used, int snap, int last, int nvb) {
+    if (blockIdx.x < nvb) {
+        const int p = blockIdx.x * kVtvWarps + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+        if (p < R * R) {
+            const int r = p / R, z = p % R;
+            double a0 = 0.0, a1 = 0.0;
+            for (int j = lane; j < J; j += 64) {
+                a0 = fma(V[(int64_t)j * R + r], V[(int64_t)j * R + z], a0);
+                if (j + 32 < J) a1 = fma(V[(int64_t)(j + 32) * R + r], V[(int64_t)(j + 32) * R + z], a1);
+            }
+            double acc = a0 + a1;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(FULL_MASK, acc, off);
+            if (lane == 0) vtv[p] = acc;
         }
         return;
     }
-    const int tid = (blockIdx.x - 1) * blockDim.x + threadIdx.x, nt = (gridDim.x - 1) * blockDim.x;
+    const int tid = (blockIdx.x - nvb) * blockDim.x + threadIdx.x, nt = (gridDim.x - nvb) * blockDim.x;
     if (snap) {
         for (int i = tid; i < J * R; i += nt) F_snap[i] = F[i];
         for (int i = tid; i < R * R; i += nt) G_snap[i] = G[i];
@@ -1576,9 +1583,10 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
     const bool fused_pro = ctx->tma && N > 0;  // k_xv3 runs the prologue itself
     if (!fused_pro) {
         PhaseScope ps(ctx, st, PH_PROLOGUE);
-        k_prologue<<<1 + std::max(1, std::min(16, (J * R + 255) / 256)), 256, 0, st>>>(
+        const int nvb = (R * R + kVtvWarps - 1) / kVtvWarps;
+        k_prologue<<<nvb + std::max(1, std::min(16, (J * R + 255) / 256)), kVtvWarps * 32, 0, st>>>(
             s->V, J, R, (double *)ctx->vtv.p, s->F, s->G, (double *)ctx->fsnap.p,
-                                      (double *)ctx->gsnap.p, v_used_out, pass == 0, last);
+                                      (double *)ctx->gsnap.p, v_used_out, pass == 0, last, nvb);
     }
     if (N > 0) {
         if (ctx->tma) {
