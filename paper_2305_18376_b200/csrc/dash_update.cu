@@ -316,6 +316,10 @@ __global__ void __launch_bounds__(NW * 32) k_slices(SliceParams p) {
             for (int r = 0; r < RB; ++r)
                 if (valid && r < R) p.U[row * R + r] = b[r];
             __syncwarp();
+            // rows of this chunk that exist (the rest of Us / Xs is zero): short slices
+            // skip the empty rows of the chunk instead of 32 FMAs per pair
+            const int64_t left = r1 - (r0 + (int64_t)ch * 32);
+            const int nv = left < 32 ? (int)left : 32;
 #pragma unroll
             for (int q = 0; q < NPL; ++q) {
                 const int pp = lane + 32 * q;
@@ -323,8 +327,8 @@ __global__ void __launch_bounds__(NW * 32) k_slices(SliceParams p) {
                     const int a = pr_s[pp], c = pz_s[pp];
                     const double *A = (pp < NP) ? Us : Xs;
                     double acc = gp[q];
-#pragma unroll 8
-                    for (int i = 0; i < 32; ++i) acc = fma(A[i * LD + a], Us[i * LD + c], acc);
+#pragma unroll 4
+                    for (int i = 0; i < nv; ++i) acc = fma(A[i * LD + a], Us[i * LD + c], acc);
                     gp[q] = acc;
                 }
             }
