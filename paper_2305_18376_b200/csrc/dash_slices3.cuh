@@ -39,7 +39,10 @@ struct S3 {
     static constexpr int LDL = RB + 1;
     static constexpr int CAPW = 14;  // XV rows staged per group (longer slices read XV directly)
     // per group: buf[RB+2] (gathers; gj_solve scratch) | dn[RB*LDL] | xs[CAPW*RB]
-    // per warp : gacc[RB*LDL] (the warp's groups accumulate in turn) | lu[RB*LDL] | piv[RB]
+    // per warp : gacc[RB*LDL] | lu[RB*LDL] | piv[RB].  RB = 16 (two groups): group 0
+    // accumulates G into gacc, group 1 into lu (no turn-taking); the rare LU
+    // fallback first folds lu into gacc and re-zeroes it afterwards.  RB < 16:
+    // the warp's groups add into gacc in turn.
     //            (LU fallback scratch, used by one group at a time)
     // Per-lane rows use the odd pitch LDL = RB+1 (lane r's row r hits distinct banks).
     // per CTA after the warps: P = vtv^{-1} (RB x RB, symmetric, read by column) | ||P||_inf | ok
@@ -247,10 +250,32 @@ __global__ void __launch_bounds__(S3<RB>::NW * 32, kS3CtasPerSM) k_slices3(Slice
     double *lu = gacc + RB * S::LDL;
     int *piv = reinterpret_cast<int *>(lu + RB * S::LDL);
     const int R = p.R;
-    if (gl == 0) {
+    constexpr bool kSplitG = (GPW == 2);
+    double *gmine = (kSplitG && gl == 1) ? lu : gacc;  // this group's G accumulator
+    if (gl == 0 || kSplitG) {
 #pragma unroll
-        for (int z = 0; z < RB; ++z) gacc[r * S::LDL + z] = 0.0;
+        for (int z = 0; z < RB; ++z) gmine[r * S::LDL + z] = 0.0;
     }
+    // before an LU fallback borrows lu: fold group 1's G into gacc (fixed order)
+    auto lu_borrow = [&]() {
+        if (kSplitG) {
+            if (gl == 1) {
+#pragma unroll
+                for (int z = 0; z < RB; ++z) gacc[r * S::LDL + z] += lu[r * S::LDL + z];
+            }
+            __syncwarp();
+        }
+    };
+    auto lu_return = [&]() {
+        if (kSplitG) {
+            __syncwarp();
+            if (gl == 1) {
+#pragma unroll
+                for (int z = 0; z < RB; ++z) lu[r * S::LDL + z] = 0.0;
+            }
+            __syncwarp();
+        }
+    };
     pdl_wait();     // XV, vtv (XV kernel) and the plan must be complete
     pdl_trigger();  // only now: the big-slice kernel relies on the same inputs without waiting
     for (int i = threadIdx.x; i < RB * LDV; i += blockDim.x) {
@@ -406,7 +431,9 @@ __global__ void __launch_bounds__(S3<RB>::NW * 32, kS3CtasPerSM) k_slices3(Slice
                 for (int z = 0; z < RB; ++z)
                     if (!okA) a[z] = vrow[z] * s_r * s_all[z] + ((z == r) ? dg : 0.0);
                 if (!okA && r == 0) atomicAdd(p.fallbacks, 1u);
+                lu_borrow();
                 const bool okLU = lu_fallback_seq<RB>(a, lu, piv, r, R, !okA);
+                lu_return();
                 if (!okA && r == 0 && !okLU) report_error(p.err, m, DASH_E_SINGULAR);
             }
             sw_of(nmeta, nxt < nunits && nxt * GPW + lane / RB < nsmall, nsw, ncw);  // next unit's s, c_old
@@ -505,7 +532,9 @@ __global__ void __launch_bounds__(S3<RB>::NW * 32, kS3CtasPerSM) k_slices3(Slice
             for (int z = 0; z < RB; ++z)
                 if (need) a[z] = vrow[z] * dn[z] + ((z == r) ? dg2 : 0.0);
             if (need && r == 0) atomicAdd(p.fallbacks, 1u);
+            lu_borrow();
             const bool okLU = lu_fallback_seq<RB>(a, lu, piv, r, R, need);
+            lu_return();
             if (need && r == 0 && !okLU) report_error(p.err, m, DASH_E_SINGULAR);
             double call[RB];
             group_gather<RB>(cn, buf, r, call);
@@ -529,13 +558,20 @@ __global__ void __launch_bounds__(S3<RB>::NW * 32, kS3CtasPerSM) k_slices3(Slice
         }
         double wa[RB];
         group_gather<RB>(wv, buf, r, wa);
+        if (kSplitG) {  // each group its own accumulator (lane r owns row r of it)
+            if (active) {
 #pragma unroll
-        for (int gi = 0; gi < GPW; ++gi) {  // the warp's groups add into gacc in turn (fixed order)
-            if (active && gl == gi) {
-#pragma unroll
-                for (int z = 0; z < RB; ++z) gacc[r * S::LDL + z] = fma(gram[z] * wv, wa[z], gacc[r * S::LDL + z]);
+                for (int z = 0; z < RB; ++z) gmine[r * S::LDL + z] = fma(gram[z] * wv, wa[z], gmine[r * S::LDL + z]);
             }
-            __syncwarp();
+        } else {
+#pragma unroll
+            for (int gi = 0; gi < GPW; ++gi) {  // the warp's groups add into gacc in turn (fixed order)
+                if (active && gl == gi) {
+#pragma unroll
+                    for (int z = 0; z < RB; ++z) gacc[r * S::LDL + z] = fma(gram[z] * wv, wa[z], gacc[r * S::LDL + z]);
+                }
+                __syncwarp();
+            }
         }
     }
     // ---- per-CTA G slot, groups in order
@@ -544,7 +580,11 @@ __global__ void __launch_bounds__(S3<RB>::NW * 32, kS3CtasPerSM) k_slices3(Slice
     for (int i = threadIdx.x; i < R * R; i += blockDim.x) {
         const int a = i / R, b = i % R;
         double acc = 0.0;
-        for (int w2 = 0; w2 < S::NW; ++w2) acc += sm[S::shared + w2 * S::per_warp + GPW * S::per_group + a * S::LDL + b];
+        for (int w2 = 0; w2 < S::NW; ++w2) {
+            const double *g0 = sm + S::shared + w2 * S::per_warp + GPW * S::per_group;
+            acc += g0[a * S::LDL + b];
+            if (kSplitG) acc += g0[RB * S::LDL + a * S::LDL + b];  // the warp's lu region (group 1)
+        }
         slot[i] = acc;
     }
 }
