@@ -1036,7 +1036,7 @@ void plan_items(const int64_t *row_ptr, int M, std::vector<int4> &items, int per
 
 void plan_fsplit(dash_ctx *ctx, int64_t N, int J, int64_t &nsplit, int64_t &rps) {
     nsplit = std::max<int64_t>(1, std::min<int64_t>((N + kFSplitRows - 1) / kFSplitRows,
-                                                    (int64_t)ctx->num_sms * 4 / ((J + 63) / 64) + 1));
+                                                    (int64_t)ctx->num_sms * 8 / ((J + 63) / 64) + 1));
     rps = (N + nsplit - 1) / nsplit;
     rps = std::max<int64_t>(32, (rps + 31) / 32 * 32);
     nsplit = N > 0 ? (N + rps - 1) / rps : 1;
