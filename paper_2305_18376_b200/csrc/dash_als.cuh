@@ -463,11 +463,7 @@ int launch_als_polar(dash_ctx *ctx, cudaStream_t st, const int64_t *row_ptr, int
                      const double *W, const double *H, int R, double *T, double *Q, double *yv) {
     constexpr int NW = RB <= 16 ? 4 : 2;
     const size_t smem = AlsSmem<RB>::bytes(NW);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_als_polar<RB, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
+    ensure_smem_attr(k_als_polar<RB, NW>, smem);
     const int blocks = std::max(1, std::min((K + NW - 1) / NW, ctx->num_sms * 8));
     k_als_polar<RB, NW><<<blocks, NW * 32, smem, st>>>(row_ptr, K, XV, W, H, R, T, Q, yv, ctx->err);
     return 0;

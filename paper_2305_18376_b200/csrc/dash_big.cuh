@@ -329,10 +329,6 @@ __global__ void __launch_bounds__(256, 2) k_big(SliceParams p, const int4 *__res
 
 int launch_big(cudaStream_t st, int grid, const SliceParams &sp, const int4 *meta, const int *plan_counts) {
     const size_t smem = BigSmem::bytes();
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
+    ensure_smem_attr(k_big, smem);
     return launch_k(pdl_site("big"), k_big, grid, 256, smem, st, sp, meta, plan_counts);
 }

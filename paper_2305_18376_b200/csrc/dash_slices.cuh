@@ -556,11 +556,7 @@ __global__ void __launch_bounds__(S2<RB>::NW * 32, 3) k_slices2(SliceParams p) {
 template <int RB>
 int launch_slices2(cudaStream_t st, int nitems, const SliceParams &sp) {
     const size_t smem = S2<RB>::bytes();
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_slices2<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
+    ensure_smem_attr(k_slices2<RB>, smem);
     k_slices2<RB><<<nitems, S2<RB>::NW * 32, smem, st>>>(sp);
     return cudaGetLastError() == cudaSuccess ? 0 : DASH_E_CUDA;
 }

@@ -592,11 +592,7 @@ __global__ void __launch_bounds__(S3<RB>::NW * 32, kS3CtasPerSM) k_slices3(Slice
 template <int RB>
 int launch_slices3(cudaStream_t st, int grid, const SliceParams &sp, const int4 *meta, const int *plan_counts) {
     const size_t smem = S3<RB>::bytes();
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_slices3<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
+    ensure_smem_attr(k_slices3<RB>, smem);
     static const bool sweep_only = getenv("DASH_S3_SWEEP") != nullptr;  // A/B: exact sweep for every slice
     SliceParams q = sp;
     q.sweep_only = sweep_only ? 1 : 0;

@@ -475,23 +475,31 @@ __global__ void __launch_bounds__(NW * 32) k_slices(SliceParams p) {
 // only for kernels that call pdl_wait() before touching their predecessor's
 // data (dash_common.cuh).  DASH_NO_PDL=1 disables it (A/B timing).
 // Raise a kernel's dynamic shared-memory limit once (not on every update):
-// keyed by the kernel's address (kernels of one signature share a type).
+// keyed by (kernel address, current device): the attribute is per device, so
+// a second GPU in the same process gets its own opt-in.  Thread-safe.
+struct SmemAttrKey {
+    const void *kern;
+    int dev;
+    size_t smem;
+};
 template <typename K>
 void ensure_smem_attr(K kern, size_t smem) {
     static std::mutex mu;
-    static std::vector<std::pair<const void *, size_t>> done;
+    static std::vector<SmemAttrKey> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lock(mu);
     const void *key = reinterpret_cast<const void *>(kern);
     for (auto &e : done)
-        if (e.first == key) {
-            if (e.second < smem) {
+        if (e.kern == key && e.dev == dev) {
+            if (e.smem < smem) {
                 cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                e.second = smem;
+                e.smem = smem;
             }
             return;
         }
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    done.push_back({key, smem});
+    done.push_back({key, dev, smem});
 }
 
 bool pdl_enabled() {
@@ -1046,11 +1054,7 @@ template <int RB>
 int launch_slices(dash_ctx *ctx, cudaStream_t st, int nitems, const SliceParams &sp) {
     constexpr int NW = (RB <= 16) ? 8 : 4;
     size_t smem = SliceSmem<RB>::bytes(NW);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_slices<RB, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
+    ensure_smem_attr(k_slices<RB, NW>, smem);
     PhaseScope ps(ctx, st, PH_SLICES);
     k_slices<RB, NW><<<nitems, NW * 32, smem, st>>>(sp);
     return cudaGetLastError() == cudaSuccess ? 0 : DASH_E_CUDA;
@@ -1069,11 +1073,7 @@ int dispatch_slices(dash_ctx *ctx, cudaStream_t st, int RB, int nitems, const Sl
     }
     if (RB == 64) {
         const size_t smem = SC<64>::bytes();
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_slices_cta<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attr = true;
-        }
+        ensure_smem_attr(k_slices_cta<64>, smem);
         PhaseScope ps(ctx, st, PH_SLICES);
         k_slices_cta<64><<<nitems, 256, smem, st>>>(sp);
         return cudaGetLastError() == cudaSuccess ? 0 : DASH_E_CUDA;
@@ -1306,18 +1306,15 @@ bool stream_ok(int J, int64_t ldx, int R) {
 
 // ---- tensor-map path (R bucket 16): box 16 doubles x 32 rows, 128B swizzle, OOB rows zero-filled
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    static bool tried = false;
-    if (!tried) {
-        tried = true;
+    static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {  // thread-safe one-time init
         cudaDriverEntryPointQueryResult q;
         void *f = nullptr;
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
-        else
-            cudaGetLastError();
-    }
+            return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+        cudaGetLastError();
+        return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+    }();
     return fn;
 }
 
@@ -1357,11 +1354,7 @@ int launch_xv3(dash_ctx *ctx, cudaStream_t st, const dash_batch_f32 *b, int J, c
     CUtensorMap mx;
     if (!make_box_map(&mx, b->X, J, b->N, b->ldx)) return DASH_E_CUDA;
     const size_t smem = TmaSmem32::xv_bytes(J);
-    static size_t attr = 0;
-    if (attr < smem) {
-        cudaFuncSetAttribute(k_xv3f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = smem;
-    }
+    ensure_smem_attr(k_xv3f, smem);
     PhaseScope ps(ctx, st, PH_XV);
     return launch_k(pdl && pdl_site("xv3f"), k_xv3f, ctx->num_sms, kCW * 32 + 32, smem, st, mx, b->N, J, V, R, XV, pro,
                     tflag, ctx->tgen);
@@ -1372,11 +1365,7 @@ int launch_f3(dash_ctx *ctx, cudaStream_t st, const dash_batch_f32 *b, int J, co
     CUtensorMap mx, mu;
     if (!make_box_map(&mx, b->X, J, b->N, b->ldx) || !make_box_map(&mu, US, R, b->N, R)) return DASH_E_CUDA;
     const size_t smem = TmaSmem32::f_bytes(J);
-    static size_t attr = 0;
-    if (attr < smem) {
-        cudaFuncSetAttribute(k_fgemm3f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = smem;
-    }
+    ensure_smem_attr(k_fgemm3f, smem);
     PhaseScope ps(ctx, st, PH_FGEMM);
     return launch_k(pdl_site("f3f"), k_fgemm3f, ctx->num_sms, kCW * 32 + 32, smem, st, mx, mu, b->N, J, R, F_slots,
                     tflag, ctx->tgen);
@@ -1400,11 +1389,7 @@ int launch_xv3(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, c
     CUtensorMap mx;
     if (!make_box_map(&mx, b->X, J, b->N, b->ldx)) return DASH_E_CUDA;
     const size_t smem = TmaSmem::xv_bytes(J);
-    static size_t attr = 0;
-    if (attr < smem) {
-        cudaFuncSetAttribute(k_xv3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = smem;
-    }
+    ensure_smem_attr(k_xv3, smem);
     PhaseScope ps(ctx, st, PH_XV);
     return launch_k(pdl, k_xv3, ctx->num_sms, kCW * 32 + 32, smem, st, mx, b->N, J, V, R, XV, pro, tflag, ctx->tgen);
 }
@@ -1413,11 +1398,7 @@ template <int MAXS>
 void launch_f3_t(dash_ctx *ctx, cudaStream_t st, const CUtensorMap &mx, const CUtensorMap &mu, int64_t N, int J,
                  int R, double *F_slots, const uint32_t *tflag) {
     const size_t smem = TmaSmem::f_bytes(J);
-    static size_t attr = 0;
-    if (attr < smem) {
-        cudaFuncSetAttribute(k_fgemm3<MAXS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = smem;
-    }
+    ensure_smem_attr(k_fgemm3<MAXS>, smem);
     PhaseScope ps(ctx, st, PH_FGEMM);
     launch_k(true, k_fgemm3<MAXS>, ctx->num_sms, kCW * 32 + 32, smem, st, mx, mu, N, J, R, F_slots, tflag,
              ctx->tgen);
@@ -1469,7 +1450,7 @@ int launch_bigx_post(dash_ctx *ctx, cudaStream_t st, const BigxParams &bp) {
 template <int RP>
 void launch_xv2_t(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, const double *V, int R, double *XV) {
     const size_t smem = StreamSmem<RP>::xv_bytes(J);
-    cudaFuncSetAttribute(k_xv2<RP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ensure_smem_attr(k_xv2<RP>, smem);
     PhaseScope ps(ctx, st, PH_XV);
     k_xv2<RP><<<ctx->num_sms, kCW * 32 + 32, smem, st>>>(b->X, b->ldx, b->N, J, V, R, XV);
 }
@@ -1478,7 +1459,7 @@ template <int RP, int MAXT>
 void launch_f2_tt(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, const double *US, int R,
                   double *F_slots) {
     const size_t smem = StreamSmem<RP>::f_bytes(J);
-    cudaFuncSetAttribute(k_fgemm2<RP, MAXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ensure_smem_attr(k_fgemm2<RP, MAXT>, smem);
     PhaseScope ps(ctx, st, PH_FGEMM);
     k_fgemm2<RP, MAXT><<<ctx->num_sms, kCW * 32 + 32, smem, st>>>(b->X, b->ldx, b->N, J, US, R, F_slots);
 }
@@ -1852,7 +1833,7 @@ int dash_update_pass_finish_f64(dash_ctx *ctx, void *stream, dash_state_f64 *s, 
         case 32: launch_vsolve_t<32>(ctx, st, fg, s->forgetting, J, R, eps, s->F, s->G, s->V); break;
         default: {
             const size_t smem = sizeof(double) * (64 * SC<64>::LDM + SC<64>::NT + 64);
-            cudaFuncSetAttribute(k_vsolve_cta<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            ensure_smem_attr(k_vsolve_cta<64>, smem);
             PhaseScope ps(ctx, st, PH_VSOLVE);
             k_vsolve_cta<64><<<(J + 31) / 32, 256, smem, st>>>(fg, (const double *)ctx->fsnap.p,
                                                                (const double *)ctx->gsnap.p, s->forgetting, J, R, eps,

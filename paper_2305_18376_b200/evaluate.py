@@ -53,9 +53,11 @@ def local_error_device(X, N, row_ptr, state_row, U, state):
     if X.dtype != U.dtype or X.dtype not in (torch.float32, torch.float64):
         raise TypeError("local_error: X and U must both be float64 or both float32")
     fn = nat.lib().dash_local_error_f32 if X.dtype == torch.float32 else nat.lib().dash_local_error_f64
-    nat.check(fn(state._ctx, nat.stream_ptr(), ctypes.byref(b),
-                 int(U.data_ptr()), int(W.data_ptr()),
-                 int(state._V.data_ptr()), state.J, state.rank,
-                 int(slice_err.data_ptr()), int(te.data_ptr())),
-              "dash_local_error")
+    from .stream import _on
+    with _on(dev):
+        nat.check(fn(state._ctx, nat.stream_ptr(), ctypes.byref(b),
+                     int(U.data_ptr()), int(W.data_ptr()),
+                     int(state._V.data_ptr()), state.J, state.rank,
+                     int(slice_err.data_ptr()), int(te.data_ptr())),
+                  "dash_local_error")
     return slice_err[:M], te

@@ -70,6 +70,23 @@ def _ptr(t) -> int:
     return int(t.data_ptr()) if t is not None else 0
 
 
+class _NoGuard:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *exc):
+        return False
+
+
+_NO_GUARD = _NoGuard()
+
+
+def _on(device: torch.device):
+    """Make ``device`` current for the library calls (their stream, workspace
+    and allocations follow the current device); free when it already is."""
+    return _NO_GUARD if torch.cuda.current_device() == device.index else torch.cuda.device(device)
+
+
 @dataclass
 class HelperState:
     """Helper summaries in per-slice map form (stream.py:36-53)."""
@@ -133,6 +150,7 @@ class _UBlocks(Mapping):
 
     def __init__(self, state):
         self._s = state
+        state._flush_ulog()
 
     def __getitem__(self, sid):
         return [self._s._block_host(ref) for ref in self._s._ublk[sid]]
@@ -152,7 +170,8 @@ class StreamState:
     (stream.py:184-247).  Exclusively owned during an update."""
 
     def __init__(self, slice_ids, u_blocks, W, V, C, D, F, G, forgetting,
-                 update_index: int = 0, passes: int = 1, device=None, dtype=F64):
+                 update_index: int = 0, passes: int = 1, device=None, dtype=F64,
+                 keep_u_history: bool = True):
         if not 0.0 < forgetting <= 1.0:
             raise ValueError("forgetting factor must lie in (0, 1]")
         if passes < 1:
@@ -162,6 +181,9 @@ class StreamState:
         self.forgetting = float(forgetting)
         self.update_index = int(update_index)
         self.passes = int(passes)
+        # the reference keeps every U block (stream.py:352-360); a serving loop
+        # that never reads u_blocks can drop them (u_blocks then raises)
+        self.keep_u_history = bool(keep_u_history)
         self.slice_ids = list(slice_ids)
         self._rowmap = {sid: k for k, sid in enumerate(self.slice_ids)}
         self._rowmap_n = len(self.slice_ids)  # slice_ids[:n] are in _rowmap (the rest register lazily)
@@ -185,6 +207,11 @@ class StreamState:
         self._ustore: list = []
         self._uhost: dict = {}
         self._ublk: dict = {}
+        # per update, (U block index, device copy of the batch's index arrays, M):
+        # resolved into _ublk only when the U history is read, so an update
+        # costs no per-slice host work (stream.py:352-360 appends per slice)
+        self._ulog: list = []
+        self._unchecked = False  # an update_packed(check=False) may have latched a device error
         if u_blocks is not None:
             self._ingest_u_blocks(u_blocks)
         self._X = None
@@ -374,7 +401,10 @@ class StreamState:
     def update(self, batch: UpdateBatch) -> UpdateResult:
         """Consume one batch (stream.py:251-370): same validation, same
         registration order, same results within FP64 rounding."""
-        return self._update_items(batch.items())
+        with _on(self.device):
+            if self._unchecked:  # report a failure latched by an earlier unchecked update first
+                self.check()
+            return self._update_items(batch.items())
 
     def _update_items(self, items, allreduce=None) -> UpdateResult:
         started = time.perf_counter()
@@ -405,20 +435,9 @@ class StreamState:
             ev = torch.cuda.Event()
             ev.record()
             self._pin_event = ev
-        res = self._run(X, N, row_ptr, meta, check=True,
-                        ids=[sid for sid, _, _ in entries], allreduce=allreduce)
-        U_dev, v_used = res
-        # U history
-        self._ustore.append(U_dev)
-        bi = len(self._ustore) - 1
-        for k, (sid, _, n) in enumerate(entries):
-            ref = (bi, int(row_ptr[k]), int(row_ptr[k + 1]))
-            if n:
-                self._ublk[sid] = [ref]
-            else:
-                self._ublk[sid].append(ref)
-        self.update_index += 1
         ids = [sid for sid, _, _ in entries]
+        U_dev, v_used = self._run(X, N, row_ptr, meta, check=True, ids=ids, allreduce=allreduce)
+        self.update_index += 1
         self._last = (ids, row_ptr, meta, X, N, U_dev)
         return UpdateResult(
             update_index=self.update_index,
@@ -435,9 +454,10 @@ class StreamState:
         state's dtype) in batch order -- existing slices (state rows ``existing_rows``) then the
         ``len(new_ids)`` new slices; ``counts`` their row counts.  No host sync
         unless ``check``.  Returns (U_new (N, R), v_used (J, R)) device tensors."""
-        N, row_ptr, meta = self._stage_meta(counts, existing_rows, len(new_ids))
-        self._register(new_ids)
-        U_dev, v_used = self._run(X, N, row_ptr, meta, check=check, ids=None, allreduce=allreduce)
+        with _on(self.device):
+            N, row_ptr, meta = self._stage_meta(counts, existing_rows, len(new_ids))
+            self._register(new_ids)
+            U_dev, v_used = self._run(X, N, row_ptr, meta, check=check, ids=None, allreduce=allreduce)
         self.update_index += 1
         self._last = (None, row_ptr, meta, X, N, U_dev)
         return U_dev, v_used
@@ -482,15 +502,35 @@ class StreamState:
                 allreduce(fg)
                 nat.check(L.dash_update_pass_finish_f64(self._ctx, st, ctypes.byref(s), _ptr(fg),
                                                         RIDGE_EPS), "dash_update_pass_finish_f64")
+        # U history (stream.py:352-360): keep U and a device copy of this
+        # batch's index arrays; the per-slice refs are built on first read
+        if self.keep_u_history:
+            self._ustore.append(U)
+            self._ulog.append((len(self._ustore) - 1, self._meta_bytes.clone(), M))
         self._meta_slot[3].record()  # this update no longer reads its meta slot after this point
         self._meta_slot[4][1] = True
         self._cache.clear()
         self.last_launches = L.dash_ctx_last_launches(self._ctx)
-        if ids is not None:
-            self._err_ids = ids
+        self._err_ids = ids
         if check:
             self.check()
+        else:
+            self._unchecked = True
         return U, v_used
+
+    def _flush_ulog(self):
+        """Resolve the pending per-update U records into slice -> [(block, lo, hi)]."""
+        if not self._ulog:
+            return
+        pending, self._ulog = self._ulog, []
+        ids = self.slice_ids
+        for bi, mb, M in pending:
+            hb = mb.cpu().numpy()
+            o_sr = 8 * (M + 1)
+            rp = hb[:o_sr].view(np.int64)
+            sr = hb[o_sr:o_sr + 4 * M].view(np.int32)
+            for m in range(M):
+                self._ublk.setdefault(ids[int(sr[m])], []).append((bi, int(rp[m]), int(rp[m + 1])))
 
     _META_RING = 3  # updates whose index arrays stay valid (local_error reads the last one)
 
@@ -552,13 +592,16 @@ class StreamState:
         slot[4][0] = True
         torch.cuda.current_stream(self.device).wait_event(slot[2])
         self._meta_slot = slot
+        self._meta_bytes = db[:nbytes]
         meta = (db[:o_sr].view(torch.int64), db[o_sr:o_sr + 4 * M].view(torch.int32), db[o_nw:o_nw + M])
         return int(Nout.value), row_ptr, meta
 
     def check(self):
         """Synchronise and raise SolveError for a device-side solver failure."""
         pos = ctypes.c_int64(0)
-        rc = nat.lib().dash_ctx_status(self._ctx, nat.stream_ptr(), ctypes.byref(pos))
+        with _on(self.device):
+            rc = nat.lib().dash_ctx_status(self._ctx, nat.stream_ptr(), ctypes.byref(pos))
+        self._unchecked = False
         if rc == nat.DASH_OK:
             return
         if rc == nat.DASH_E_CUDA:
@@ -568,6 +611,8 @@ class StreamState:
         sid = None if p < 0 or ids is None or p >= len(ids) else ids[p]
         msg = ("singular normal equations" if rc == nat.DASH_E_SINGULAR
                else "non-finite solution from normal equations")
+        if ids is None and p >= 0:
+            msg += f" (batch position {p} of an unchecked update_packed batch)"
         raise SolveError(msg, sid)
 
 
@@ -639,6 +684,10 @@ class HostPipeline:
         if U_host is not None or v_host is not None:
             with torch.cuda.stream(self.d2h):
                 self.d2h.wait_event(done)
+                # the allocator must not hand U / v_used to a later update
+                # before these queued reads ran
+                U.record_stream(self.d2h)
+                v_used.record_stream(self.d2h)
                 if U_host is not None:
                     U_host[:U.shape[0]].copy_(U, non_blocking=True)
                 if v_host is not None:

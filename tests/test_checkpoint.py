@@ -138,3 +138,62 @@ def test_resume_from_reference_checkpoint_on_gpu(suffix, tmp_path):
         for name in ("W", "C", "D", "F", "G", "V"):
             assert rel(getattr(state, name), g[f"ru{t}_{name}"]) < TOL, (t, name)
     assert state.update_index == doc["update_index"] + int(g["rn_updates"])
+
+
+@pytest.mark.gpu
+def test_host_pipeline_updates_keep_u_history_for_save_state(tmp_path):
+    """update_packed / HostPipeline record the U history like update()
+    (reference stream.py:352-360): after serving the reference checkpoint's
+    follow-up batches through HostPipeline, save_state writes the same bytes
+    as the dict-path StreamState.update run, and every slice's U history is
+    its checkpointed block plus the reference's u_new rows."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2305_18376_b200.stream import HostPipeline
+    g = load("ckpt.npz")
+    a, stats = load_state(GOLDEN / "ckpt_ref.json")
+    b, _ = load_state(GOLDEN / "ckpt_ref.json")
+    u0 = {sid: a.u_matrix(sid) for sid in a.slice_ids}
+    batches = list(batches_from(g, "r"))
+    for bt in batches:
+        a.update(bt)
+    Xs, metas = [], []
+    for bt in batches:
+        ex = list(bt.existing_rows.items())
+        Xs.append(np.concatenate([r for _, r in ex] + [ns.rows for ns in bt.new_slices]))
+        metas.append((np.array([r.shape[0] for _, r in ex] + [ns.rows.shape[0] for ns in bt.new_slices]),
+                      [sid for sid, _ in ex], [ns.slice_id for ns in bt.new_slices]))
+    pins = [torch.as_tensor(X).pin_memory() for X in Xs]
+    pipe = HostPipeline(b, max(X.shape[0] for X in Xs), b.J)
+    pipe.start()
+    for k, (counts, ex_ids, new) in enumerate(metas):
+        staged = pipe.put(pins[k])
+        rows = np.array([b.row_of(s) for s in ex_ids], dtype=np.int32)
+        pipe.update(staged, counts, rows, new)
+    pipe.finish()
+    torch.cuda.synchronize()
+    b.check()
+    pa, pb = tmp_path / "a.json", tmp_path / "b.json"
+    save_state(a, pa, column_stats=stats)
+    save_state(b, pb, column_stats=stats)
+    assert pa.read_text() == pb.read_text()
+    # U history = checkpointed block + the reference's u_new per update
+    for sid in b.slice_ids:
+        want = [u0[sid]] if sid in u0 else []
+        for t, bt in enumerate(batches):
+            ids = [s for s, _, _ in bt.items()]
+            if sid in ids:
+                k = ids.index(sid)
+                offs = np.concatenate([[0], np.cumsum([r.shape[0] for _, r, _ in bt.items()])])
+                want.append(g[f"ru{t}_U"][offs[k]:offs[k + 1]])
+        got = b.u_matrix(sid)
+        want = np.vstack(want)
+        assert got.shape == want.shape, sid
+        assert rel(got, want) < TOL, sid
+    # npz round trip of the served state resumes with identical factors
+    pz = tmp_path / "b.npz"
+    save_state(b, pz, column_stats=stats)
+    c, _ = load_state(pz)
+    for name in ("W", "C", "D", "F", "G", "V"):
+        assert np.array_equal(getattr(c, name), getattr(b, name)), name

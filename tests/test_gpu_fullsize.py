@@ -1,0 +1,144 @@
+"""Full-size GPU parity: every BASELINE.json config at its FULL slice count
+(K0), through the drop-in ``StreamState.update(UpdateBatch)``, against the CPU
+oracle (the restatement of the reference's StreamState.update, stream.py:251-370,
+pinned to the reference's golden vectors in test_oracle.py) after EVERY update.
+
+Protocol: identical planted initial state and identical host
+batches for both sides; compare u_new, W, C, D, F, G, V, v_used and the
+per-update fitness local_error (evaluate.py:93-118) with the normwise metric
+max|a-b| / max|b| <= 1e-8 (north_star FP64 tolerance).
+
+Run lengths: large K0=50,000 x 3 updates (500 new
+slices each), daily K0=4,700 x 10, medium all 20, wide10/32/64 K0=20,000 x 2.
+The streams use the planted generator with i.i.d. N(0, 1/I_k) slice bases
+(``exact=False``): same shapes, laws and noise as BASELINE's generator, without
+materialising the per-slice QR of the 56 GB initial tensor.
+
+Also here: ill-conditioned V (cond(V^T V) from 1e4 to 1e7, nearly collinear
+columns) with W spread over many magnitudes, so the small-slice kernel's
+Neumann fast path, its threshold and the exact-sweep fallback are all checked
+against the oracle on data where the ridge term and P = (V^T V)^-1 rounding
+matter.
+"""
+import numpy as np
+import pytest
+import torch
+
+from golden_io import rel
+from oracle import dash_oracle as orc
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+TOL = 1e-8
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2305_18376_b200.build import build_library
+    build_library()
+
+
+def _states(ps, passes=1):
+    from paper_2305_18376_b200.stream import StreamState
+    R = ps["V"].shape[1]
+    gpu = StreamState.from_arrays(dict(ps, passes=passes))
+    cpu = orc.OracleStreamState(ps["slice_ids"], {s: [np.zeros((0, R))] for s in ps["slice_ids"]},
+                                ps["W"], ps["V"], ps["C"], ps["D"], ps["F"], ps["G"],
+                                ps["forgetting"], passes=passes)
+    return gpu, cpu
+
+
+def run_parity(stream, ps, updates, check_error=True):
+    """Drive both engines over the first ``updates`` batches; return the worst
+    normwise error per compared array."""
+    from paper_2305_18376_b200.evaluate import local_error
+    gpu, cpu = _states(ps, passes=stream.cfg.passes)
+    worst = {}
+    for t, batch in enumerate(stream.batches()):
+        if t >= updates:
+            break
+        res = gpu.update(batch)
+        ref = cpu.update(batch)
+        ids = [sid for sid, _, _ in batch.items()]
+        pairs = {"U": (np.concatenate([res.u_new[s] for s in ids]),
+                       np.concatenate([ref["u_new"][s] for s in ids])),
+                 "v_used": (res.v_used, ref["v_used"])}
+        for name in ("W", "C", "D", "F", "G", "V"):
+            pairs[name] = (getattr(gpu, name), getattr(cpu, name))
+        if check_error:
+            items = [(sid, rows) for sid, rows, _ in batch.items()]
+            te, per = local_error(items, res.u_new, gpu)
+            W_rows = {sid: cpu.W[cpu.row_of(sid)] for sid in ids}
+            te_o, per_o = orc.local_error(items, ref["u_new"], W_rows, cpu.V)
+            pairs["local_error"] = (np.array([te]), np.array([te_o]))
+            pairs["slice_error"] = (np.array([per[s] for s in ids]), np.array([per_o[s] for s in ids]))
+        for k, (a, b) in pairs.items():
+            worst[k] = max(worst.get(k, 0.0), rel(a, b))
+        assert gpu.slice_ids == cpu.slice_ids
+    return worst
+
+
+FULL = [
+    ("large", 3),
+    ("daily", 10),
+    ("medium", 20),
+    ("wide10", 2),
+    ("wide32", 2),
+    ("wide64", 2),
+]
+
+
+@pytest.mark.parametrize("name,updates", FULL, ids=[n for n, _ in FULL])
+def test_full_size_config_matches_oracle_every_update(name, updates):
+    from paper_2305_18376_b200 import workloads as wl
+    cfg = wl.scaled(wl.CONFIGS[name], steps=updates)
+    stream = wl.make_stream(cfg, exact=False)
+    ps = wl.planted_state(stream)
+    worst = run_parity(stream, ps, updates)
+    print(f"{name}: K0={cfg.K0} J={cfg.J} R={cfg.R} updates={updates} worst={worst}")
+    bad = {k: v for k, v in worst.items() if not v < TOL}
+    assert not bad, (name, worst)
+
+
+def ill_conditioned(ps, cond, seed=5):
+    """Replace V by a matrix whose Gram V^T V has condition number ~``cond``:
+    V = Q diag(sigma) Z^T with sigma log-spaced over sqrt(cond), so two or more
+    columns are nearly collinear.  W is spread over 1 .. 1e-6 (and exact
+    zeros) so the ridge term d_r = sh / s_r^2 of the small-slice A system
+    ranges from negligible to dominant.  C, F, G are re-planted for the new V."""
+    V0 = ps["V"]
+    J, R = V0.shape
+    rng = np.random.default_rng(seed)
+    Q, _ = np.linalg.qr(rng.standard_normal((J, R)))
+    Z, _ = np.linalg.qr(rng.standard_normal((R, R)))
+    sig = np.logspace(0, -0.5 * np.log10(cond), R) * np.sqrt(J / 3.0)
+    V = Q @ np.diag(sig) @ Z.T
+    W = ps["W"].copy()
+    K = W.shape[0]
+    scales = np.array([1.0, 1e-2, 3e-3, -2e-3, 1e-4, 1e-6, 0.0])
+    for k in range(K):
+        if k % 3 == 0:
+            cols = rng.choice(R, size=2, replace=False)
+            W[k, cols] *= scales[rng.integers(len(scales), size=2)]
+    D = ps["D"]
+    vtv = V.T @ V
+    C = np.einsum("krz,kz,zr->kr", D, W, vtv)
+    G = np.einsum("kr,krz,kz->rz", W, D, W)
+    G = (G + G.T) / 2.0
+    return dict(ps, V=V, W=W, C=C, F=V @ G, G=G)
+
+
+@pytest.mark.parametrize("cond", [1e4, 1e6, 1e7])
+@pytest.mark.parametrize("R", [16, 10])
+def test_ill_conditioned_V_matches_oracle(cond, R):
+    from paper_2305_18376_b200 import workloads as wl
+    cfg = wl.scaled(wl.CONFIGS["large"], K0=3000, steps=2, new_slices=4, R=R)
+    stream = wl.make_stream(cfg, exact=False)
+    ps = ill_conditioned(wl.planted_state(stream), cond)
+    vtv = ps["V"].T @ ps["V"]
+    assert np.linalg.cond(vtv) > 0.1 * cond
+    worst = run_parity(stream, ps, 2, check_error=False)
+    bad = {k: v for k, v in worst.items() if not v < TOL}
+    assert not bad, (cond, R, worst)
