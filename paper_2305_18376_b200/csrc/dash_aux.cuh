@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(256) k_local_error(const TX *__restrict__ X, i
         const double *w = W + (int64_t)state_row[m] * R;
         double acc = 0.0;
         for (int64_t row = r0; row < r1; ++row) {
-            if (lane < R) us[lane] = (double)U[row * R + lane] * w[lane];
+            for (int r = lane; r < R; r += 32) us[r] = (double)U[row * R + r] * w[r];  // R <= 64
             __syncwarp();
             for (int j = lane; j < J; j += 32) {
                 double rec = 0.0;

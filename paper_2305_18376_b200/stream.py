@@ -212,6 +212,7 @@ class StreamState:
         # costs no per-slice host work (stream.py:352-360 appends per slice)
         self._ulog: list = []
         self._unchecked = False  # an update_packed(check=False) may have latched a device error
+        self._uarena = None  # [chunk (rows, R), rows used]: U blocks are views of chunks
         if u_blocks is not None:
             self._ingest_u_blocks(u_blocks)
         self._X = None
@@ -478,7 +479,7 @@ class StreamState:
             raise ValueError(f"batch X has {X.shape[0]} rows, the counts sum to {N}")
         f32 = self.dtype == torch.float32
         rp_d, sr_d, nw_d = meta
-        U = torch.empty((max(N, 0), self._R), dtype=self.dtype, device=dev)
+        U = self._alloc_u(N)
         v_used = torch.empty((self.J, self._R), dtype=F64, device=dev)
         b = nat.DashBatch(X=_ptr(X), ldx=int(X.stride(0)) if N else self.J, N=N, M=M,
                           row_ptr=_ptr(rp_d), row_ptr_host=row_ptr.ctypes.data,
@@ -517,6 +518,37 @@ class StreamState:
         else:
             self._unchecked = True
         return U, v_used
+
+    _U_ALIGN = 32  # rows: every U block starts 256-byte aligned
+
+    def _alloc_u(self, N: int) -> torch.Tensor:
+        """U_new block of this update.  With the U history kept, blocks are
+        carved from large device chunks (one allocation per several updates
+        instead of one per update: a fresh cudaMalloc of ~100 MB inside the
+        update costs more than the update's own kernels)."""
+        R = self._R
+        if not self.keep_u_history:
+            return torch.empty((max(N, 0), R), dtype=self.dtype, device=self.device)
+        a = self._uarena
+        need = max(N, 0)
+        if a is None or a[1] + need > a[0].shape[0]:
+            self._new_u_chunk(max(need, 4 * need, 1 << 14))
+            a = self._uarena
+        lo = a[1]
+        a[1] = lo + (need + self._U_ALIGN - 1) // self._U_ALIGN * self._U_ALIGN
+        return a[0][lo:lo + need]
+
+    def _new_u_chunk(self, rows: int):
+        self._uarena = [torch.empty((rows, self._R), dtype=self.dtype, device=self.device), 0]
+
+    def reserve_u_history(self, rows: int):
+        """Pre-allocate device room for ``rows`` more U-history rows (plus
+        alignment padding), so the following updates allocate nothing."""
+        a = self._uarena
+        free = 0 if a is None else a[0].shape[0] - a[1]
+        if rows > free:
+            with _on(self.device):
+                self._new_u_chunk(int(rows * 1.02) + 64 * self._U_ALIGN)
 
     def _flush_ulog(self):
         """Resolve the pending per-update U records into slice -> [(block, lo, hi)]."""

@@ -133,12 +133,30 @@ def ill_conditioned(ps, cond, seed=5):
 @pytest.mark.parametrize("cond", [1e4, 1e6, 1e7])
 @pytest.mark.parametrize("R", [16, 10])
 def test_ill_conditioned_V_matches_oracle(cond, R):
+    """On ill-conditioned data the S-row system B = vtv o D (a Hadamard product
+    with an ill-conditioned Gram) amplifies rounding, so the reference itself
+    is not reproducible to 1e-8 here: its numba-Cholesky path and its numpy-LU
+    path (stream.py:312-339) already differ by up to ~1e-6 in W.  The bar is
+    therefore per update and per array: GPU vs the oracle's numba path within
+    max(1e-8, 10 x the reference's own numba-vs-numpy spread)."""
     from paper_2305_18376_b200 import workloads as wl
     cfg = wl.scaled(wl.CONFIGS["large"], K0=3000, steps=2, new_slices=4, R=R)
     stream = wl.make_stream(cfg, exact=False)
     ps = ill_conditioned(wl.planted_state(stream), cond)
     vtv = ps["V"].T @ ps["V"]
     assert np.linalg.cond(vtv) > 0.1 * cond
-    worst = run_parity(stream, ps, 2, check_error=False)
-    bad = {k: v for k, v in worst.items() if not v < TOL}
-    assert not bad, (cond, R, worst)
+    gpu, cpu = _states(ps)
+    _, cpu_np = _states(ps)
+    cpu_np.use_kernel = False  # the reference's numpy / LAPACK path
+    for t, batch in enumerate(stream.batches()):
+        res = gpu.update(batch)
+        ref = cpu.update(batch)
+        ref_np = cpu_np.update(batch)
+        ids = [sid for sid, _, _ in batch.items()]
+        trip = {"U": [np.concatenate([d[s] for s in ids]) for d in (res.u_new, ref["u_new"], ref_np["u_new"])],
+                "v_used": [res.v_used, ref["v_used"], ref_np["v_used"]]}
+        for name in ("W", "C", "D", "F", "G", "V"):
+            trip[name] = [getattr(e, name) for e in (gpu, cpu, cpu_np)]
+        for k, (a, b, c) in trip.items():
+            err, floor = rel(a, b), rel(c, b)
+            assert err < max(TOL, 10.0 * floor), (t, k, err, floor)
