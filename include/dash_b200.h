@@ -72,6 +72,8 @@ int dash_host_row_ptr(const int64_t *counts, int64_t M, int64_t *row_ptr, int64_
 #define DASH_PATH_STREAM 1
 #define DASH_PATH_TMA 2
 #define DASH_PATH_BIGX 4
+#define DASH_PATH_SMALLX 8  /* bit 3: fused small-slice kernel (k_smallx: small-slice rows read once for XV,
+                               re-read from L2 for F; no XV / U o w round trips) */
 int dash_ctx_path_flags(const dash_ctx *ctx);
 
 /* Number of ridge systems that needed the LU fallback (Cholesky failed or a

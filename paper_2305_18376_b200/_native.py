@@ -25,7 +25,7 @@ DASH_E_NONFINITE = 4
 MAX_RANK = 64       # update path
 MAX_RANK_ALS = 32   # parafac2_als / init_helpers / ridge_solve
 PHASES = ("row_slice", "prologue", "xv", "slices", "fgemm", "sum_fg", "vsolve", "big", "big_post")
-PATH_STREAM, PATH_TMA, PATH_BIGX = 1, 2, 4
+PATH_STREAM, PATH_TMA, PATH_BIGX, PATH_SMALLX = 1, 2, 4, 8
 
 _c_dp = ctypes.c_void_p  # device pointers travel as integers
 

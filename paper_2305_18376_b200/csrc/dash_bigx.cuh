@@ -100,6 +100,7 @@ struct BigxParams {
     int J, R, G;              // G = k_bigx grid
     double lam, eps;
     int pass, final_pass;
+    int post_wait;            // k_bigx_post: wait for k_bigx up front (no F GEMM between them)
 };
 
 // ---------------------------------------------------------------------------
@@ -507,7 +508,9 @@ __global__ void __launch_bounds__(256) k_bigx_post(BigxParams p) {
     __shared__ int piv[RB];
     // Launched behind the small-row F GEMM, which triggers only after its own
     // pdl_wait: k_bigx's partials are complete.  This kernel touches nothing the
-    // F GEMM does, so it runs beside it and waits only at its end.
+    // F GEMM does, so it runs beside it and waits only at its end.  On the fused
+    // small-slice path nothing runs between k_bigx and this kernel: wait first.
+    if (p.post_wait) pdl_wait();
     pdl_trigger();
     const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
     const int J = p.J, R = p.R;

@@ -87,7 +87,7 @@ constexpr int kPlanBuckets = kSmallRows + 1 + kBigClasses;
 
 __device__ __forceinline__ int plan_bucket(int64_t n) {
     if (n <= kSmallRows) return kSmallRows - (int)n;
-    const int64_t q = (n - 1) / 64;
+    const int64_t q = (n - 1) / 64 + 1;  // n in (kSmallRows, 64] -> class 1
     const int c = q < kBigClasses ? (int)q : kBigClasses;  // 1..kBigClasses
     return kSmallRows + 1 + (kBigClasses - c);
 }

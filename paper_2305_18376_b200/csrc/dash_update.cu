@@ -38,7 +38,7 @@ using namespace dash;
 
 namespace {
 
-constexpr int kSmallRows = 64;     // slices with more rows are "big" (one CTA each)
+constexpr int kSmallRows = 32;     // slices with more rows are "big" (k_bigx / k_big)
 constexpr int kSlicesPerItem = 16; // small slices grouped per CTA
 constexpr int kFSplitRows = 1024;  // target rows per F-GEMM split
 
@@ -543,6 +543,7 @@ int launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 #include "dash_slices3.cuh"
 #include "dash_big.cuh"
 #include "dash_bigx.cuh"
+#include "dash_smallx.cuh"
 
 // ---------------------------------------------------------------------------
 // k_fgemm: F partial slot s = X[rows_s]^T (U o w)[rows_s], J-block of 64.
@@ -948,6 +949,10 @@ struct dash_ctx {
     bool tma = false;     // ... with tensor-map (swizzled box) copies: k_xv3 / k_fgemm3
     bool bigx = false;    // big slices on the fused single-read path (dash_bigx.cuh)
     int bigx_nbig = 0, bigx_grid = 0;
+    bool smallx = false;  // small slices on the fused single-kernel path (dash_smallx.cuh)
+    bool planned = false; // the device slice plan ran for this update
+    int sx_grid = 0;
+    Buf sx_tmp, sx_units, sx_meta;  // planner: per-chunk units | compacted units | counts, choff, nunits, done
     uint32_t tgen = 0;  // generation of the small-tile marks
     void *plan_p = nullptr;  // SlicePlan of the update in flight
     // phase timing (bench): events around every launch when enabled
@@ -1318,12 +1323,13 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-bool make_box_map(CUtensorMap *map, const double *base, int64_t cols, int64_t rows, int64_t ld) {
+bool make_box_map(CUtensorMap *map, const double *base, int64_t cols, int64_t rows, int64_t ld,
+                  int box_rows = kTR) {
     auto fn = encode_fn();
     if (!fn) return false;
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
-    cuuint32_t box[2] = {16, (cuuint32_t)kTR};
+    cuuint32_t box[2] = {16, (cuuint32_t)box_rows};
     cuuint32_t es[2] = {1, 1};
     return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), dims, strides, box, es,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -1524,9 +1530,25 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
             const SlicePlan &pl = plan_of(ctx);
             ctx->bigx = !no_bigx && ctx->tma && pl.big_dev && pl.gbig > 0 && J * 16 <= kPostPer * 256 &&
                         BigxSmemT<typename std::conditional<f32, float, double>::type>::bytes(J) <= 227 * 1024;
+            // fused small-slice kernel: same eligibility as the fused big path (FP64, R
+            // bucket 16 and even, J <= 128, tensor-map X); big slices then need k_bigx
+            static const bool no_smallx = getenv("DASH_NO_SMALLX") != nullptr;  // A/B switch
+            ctx->smallx = !f32 && !no_smallx && !no_bigx && ctx->tma && pl.big_dev && J <= 128 &&
+                          (ctx->bigx || pl.gbig == 0);
+            ctx->sx_grid = ctx->smallx ? ctx->num_sms : 0;
+            if (ctx->smallx) {
+                const int nch = std::max(1, (M + kSxChunk - 1) / kSxChunk);
+                if (ensure(ctx->sx_tmp, sizeof(int4) * (size_t)nch * kSxChunk) ||
+                    ensure(ctx->sx_units, sizeof(int4) * (size_t)std::max(M, 1))) return DASH_E_CUDA;
+                if (ctx->sx_meta.cap < sizeof(int) * (2 * (size_t)nch + 8)) {
+                    if (ensure(ctx->sx_meta, sizeof(int) * (2 * (size_t)nch + 8))) return DASH_E_CUDA;
+                    cudaMemsetAsync(ctx->sx_meta.p, 0, ctx->sx_meta.cap, st);  // done counter starts at 0
+                }
+            }
             ctx->bigx_nbig = ctx->bigx ? pl.gbig : 0;
             ctx->bigx_grid = ctx->bigx ? (int)std::min<int64_t>(ctx->num_sms, pl.big_tiles) : 0;
-            if (ctx->bigx) {
+            if (ctx->smallx) ctx->nitems = ctx->sx_grid + pl.gbig;  // G slots: one per small-kernel CTA + big slice
+            if (ctx->bigx && !ctx->smallx) {
                 const size_t tb = sizeof(uint32_t) * (size_t)((N + kTR - 1) / kTR + 16);
                 if (ctx->tflag.cap < tb) {  // zeroed once: marks are generation-tagged
                     if (ensure(ctx->tflag, tb)) return DASH_E_CUDA;
@@ -1553,8 +1575,9 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
             (f32 && ensure(ctx->u64, sizeof(double) * std::max<int64_t>(N, 1) * R)))
             return DASH_E_CUDA;
         if (!items.empty() && stage_items(ctx, st, items)) return DASH_E_CUDA;
-        if (plan_of(ctx).split && M > 0 && N > 0 &&
-            device_plan(ctx, st, b, ctx->bigx ? (uint32_t *)ctx->tflag.p : nullptr))
+        ctx->planned = plan_of(ctx).split && M > 0 && N > 0 && (!ctx->smallx || ctx->bigx);
+        if (ctx->planned &&
+            device_plan(ctx, st, b, (ctx->bigx && !ctx->smallx) ? (uint32_t *)ctx->tflag.p : nullptr))
             return DASH_E_CUDA;
         if (M > 0 && !ctx->stream) {  // row -> slice map: only the generic F GEMM needs it
             PhaseScope ps(ctx, st, PH_ROWSLICE);
@@ -1565,7 +1588,41 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
     double *XV = (double *)ctx->xv.p;
     double *Ud = f32 ? (double *)ctx->u64.p : (double *)(void *)U_out;  // U written by the slice kernels
     double *Fsl = (double *)ctx->fslots.p, *Gsl = (double *)ctx->gslots.p;
-    const bool fused_pro = ctx->tma && N > 0;  // k_xv3 runs the prologue itself
+    const bool fused_pro = (ctx->tma || ctx->smallx) && N > 0;  // k_xv3 / the small-path planner run the prologue
+    if constexpr (!f32) if (ctx->smallx && N > 0) {
+        // planner (pass 0) + pass prologue, then the fused small-slice kernel
+        const int nch = pass == 0 ? std::max(1, (M + kSxChunk - 1) / kSxChunk) : 0;
+        int *sxm = (int *)ctx->sx_meta.p;
+        const int nch_all = std::max(1, (M + kSxChunk - 1) / kSxChunk);
+        SxPlan pl{b->row_ptr, M, nch, (int4 *)ctx->sx_tmp.p, sxm, sxm + nch_all, (int4 *)ctx->sx_units.p,
+                  sxm + 2 * nch_all + 1, (unsigned int *)(sxm + 2 * nch_all + 2)};
+        const FusedPrologue pro{(double *)ctx->vtv.p, s->F, s->G, (double *)ctx->fsnap.p, (double *)ctx->gsnap.p,
+                                v_used_out, pass == 0, last};
+        {
+            PhaseScope ps(ctx, st, PH_XV);
+            // PDL only behind the plan kernels: otherwise the prologue reads the V / F / G
+            // the previous update (or pass) just wrote -> normal launch
+            if (launch_k(pass == 0 && ctx->planned, k_sx_walk, nch + sx_prologue_blocks(R), 256, 0, st, pl, pro, (const double *)s->V,
+                         J, R))
+                return DASH_E_CUDA;
+            if (nch > 0) {
+                ctx->last_launches++;
+                if (launch_k(true, k_sx_copy, nch, 256, 0, st, pl)) return DASH_E_CUDA;
+            }
+        }
+        CUtensorMap m8;
+        if (!make_box_map(&m8, b->X, J, b->N, b->ldx, 8)) return DASH_E_CUDA;
+        SxParams sp{(const int4 *)ctx->sx_units.p, sxm + 2 * nch_all + 1, b->row_ptr, b->state_row, b->is_new,
+                    s->V, (const double *)ctx->vtv.p, s->W, s->C, s->D, (double *)(void *)U_out,
+                    (double *)ctx->fslots.p, (double *)ctx->gslots.p, ctx->err, ctx->fallbacks, J, R,
+                    s->forgetting, eps, pass, last, 0};
+        static const bool sweep_only = getenv("DASH_S3_SWEEP") != nullptr;
+        sp.sweep_only = sweep_only ? 1 : 0;
+        {
+            PhaseScope ps(ctx, st, PH_SLICES);
+            if (launch_smallx(ctx, st, m8, sp, ctx->sx_grid)) return DASH_E_CUDA;
+        }
+    }
     if (!fused_pro) {
         PhaseScope ps(ctx, st, PH_PROLOGUE);
         const int nvb = (R * R + kVtvWarps - 1) / kVtvWarps;
@@ -1574,7 +1631,9 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
                                       (double *)ctx->gsnap.p, v_used_out, pass == 0, last, nvb);
     }
     if (N > 0) {
-        if (ctx->tma) {
+        if (ctx->smallx) {
+            // done above
+        } else if (ctx->tma) {
             const FusedPrologue pro{(double *)ctx->vtv.p, s->F, s->G, (double *)ctx->fsnap.p, (double *)ctx->gsnap.p,
                                     v_used_out, pass == 0, last};
             // PDL only behind the plan kernels (pass 0); a later pass follows the V solve
@@ -1609,7 +1668,7 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
         sp.eps = eps;
         sp.pass = pass;
         sp.final_pass = last;
-        if (launch_plan(ctx, st, RB, plan_of(ctx), sp, M, ctx->bigx)) return DASH_E_CUDA;
+        if (!ctx->smallx && launch_plan(ctx, st, RB, plan_of(ctx), sp, M, ctx->bigx)) return DASH_E_CUDA;
         BigxParams bp{};
         {
             if (ctx->bigx) {
@@ -1623,12 +1682,12 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
                 bp.Co = s->C;
                 bp.D = s->D;
                 bp.U = Ud;
-                bp.US = (double *)ctx->us.p;
+                bp.US = ctx->smallx ? nullptr : (double *)ctx->us.p;
                 bp.ms = (double *)ctx->bx_ms.p;
                 bp.toff = (int *)ctx->bx_toff.p;
                 bp.parts = (double *)ctx->bx_parts.p;
-                bp.F_slots = Fsl + (int64_t)ctx->nsplit * J * R;
-                bp.G_slots = Gsl + (int64_t)plan_of(ctx).g3 * R * R;
+                bp.F_slots = Fsl + (int64_t)(ctx->smallx ? ctx->sx_grid : ctx->nsplit) * J * R;
+                bp.G_slots = Gsl + (int64_t)(ctx->smallx ? ctx->sx_grid : plan_of(ctx).g3) * R * R;
                 bp.err = ctx->err;
                 bp.fallbacks = ctx->fallbacks;
                 bp.N = N;
@@ -1640,10 +1699,13 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
                 bp.eps = eps;
                 bp.pass = pass;
                 bp.final_pass = last;
+                bp.post_wait = ctx->smallx ? 1 : 0;
                 if (launch_bigx(ctx, st, b, bp)) return DASH_E_CUDA;
             }
         }
-        if (ctx->tma) {
+        if (ctx->smallx) {
+            // F of the small slices: k_smallx's per-CTA slots
+        } else if (ctx->tma) {
             if (launch_f3(ctx, st, b, J, (const double *)ctx->us.p, R, Fsl,
                           ctx->bigx ? (const uint32_t *)ctx->tflag.p : nullptr))
                 return DASH_E_CUDA;
@@ -1670,7 +1732,8 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
     if (host_timing) fprintf(stderr, "[dash host] pass_begin total %.1f us\n", std::chrono::duration<double, std::micro>(tnow() - t0).count());
     {
         PhaseScope ps(ctx, st, PH_SUMFG);
-        if (colsum2(ctx, st, Fsl, N > 0 ? (int)ctx->nsplit + ctx->bigx_nbig : 0, (int64_t)J * R, fg_out, Gsl,
+        if (colsum2(ctx, st, Fsl, N > 0 ? (ctx->smallx ? ctx->sx_grid : (int)ctx->nsplit) + ctx->bigx_nbig : 0,
+                    (int64_t)J * R, fg_out, Gsl,
                     N > 0 ? ctx->nitems : 0, (int64_t)R * R, fg_out + (int64_t)J * R))
             return DASH_E_CUDA;
     }
@@ -1704,7 +1767,8 @@ void dash_ctx_destroy(dash_ctx *ctx) {
     dash_ctx::Buf *bufs[] = {&ctx->xv,  &ctx->row_slice, &ctx->items, &ctx->gslots, &ctx->fslots,
                              &ctx->vtv, &ctx->fsnap,     &ctx->gsnap, &ctx->fg,     &ctx->part, &ctx->us, &ctx->scratch,
                              &ctx->smeta, &ctx->plan_hist, &ctx->u64,
-                             &ctx->tflag, &ctx->bx_ms, &ctx->bx_toff, &ctx->bx_parts};
+                             &ctx->tflag, &ctx->bx_ms, &ctx->bx_toff, &ctx->bx_parts,
+                             &ctx->sx_tmp, &ctx->sx_units, &ctx->sx_meta};
     for (auto *b : bufs)
         if (b->p) cudaFree(b->p);
     cudaFree(ctx->err);
@@ -1764,7 +1828,7 @@ int dash_host_row_ptr(const int64_t *counts, int64_t M, int64_t *row_ptr, int64_
 
 int dash_ctx_path_flags(const dash_ctx *ctx) {
     if (!ctx) return 0;
-    return (ctx->stream ? 1 : 0) | (ctx->tma ? 2 : 0) | (ctx->bigx ? 4 : 0);
+    return (ctx->stream ? 1 : 0) | (ctx->tma ? 2 : 0) | (ctx->bigx ? 4 : 0) | (ctx->smallx ? 8 : 0);
 }
 
 #ifdef DASH_DEBUG_TIMING
