@@ -54,10 +54,10 @@ constexpr int kSxSlices = 16;        // slices per unit (max)
 constexpr int kSxChunk = 256;        // batch positions per planner block
 constexpr int kSxWalkers = 8;        // sequential walkers per planner block (32 positions each)
 constexpr int kSxNST = 3;            // X ring stages
-constexpr int kSxSlots = 6;          // units in flight
+constexpr int kSxSlots = 6;          // units in flight (XV / U tiles)
 constexpr int kSxLook = kSxSlots - 1;  // the math warps' XV runs this many units ahead of F
 constexpr int kSxMW = 4;             // math warps (one 8-row block each)
-constexpr int kSxSW = kSxSlots;      // solver warps
+constexpr int kSxSW = 11;            // solver warps (slice pairs round-robin over the unit sequence); 16 warps: 128 registers (4 warps per SM sub-partition)
 constexpr int kSxThreads = (kSxMW + kSxSW + 1) * 32;
 constexpr int kSxTP = 18;            // XV / U tile pitch (doubles): conflict-free fragment stores and row reads
 
@@ -66,22 +66,37 @@ struct SxSmem {
     static constexpr int SD = JSM * 512;                 // doubles per ring stage (32 rows x 128 columns)
     static constexpr int VTP = JSM * 16 + 8;             // V^T pitch
     static constexpr int TILE = kSxRows * kSxTP;
-    static constexpr int TBL = kSxSlices * 32;           // per slice: d[16] | sinv[16]
-    static constexpr int HDR = 16;                       // int4 desc | fastmask | fast2 | rowslice[32] (bytes)
-    static constexpr int SLOT = 2 * TILE + TBL + HDR;
-    static constexpr int SWS = 2 * 18 + 16 * 17 + 8;     // per solver warp: 2 gather bufs | lu | piv
+    static constexpr int SLOT = 2 * TILE;                // XV tile | U / US tile
+    static constexpr int LUS = 16 * 17 + 8 + 4;          // shared LU fallback scratch | piv | lock
+    static constexpr int SWS = 2 * 18 + 2 * 256;         // per solver warp: 2 gather bufs | 2 D stages
     static constexpr int OFF_VT = kSxNST * SD;
     static constexpr int OFF_P = OFF_VT + 16 * VTP;      // P = vtv^{-1} (16 x 16) | ||P||_inf | ok
     static constexpr int OFF_VTV = OFF_P + 264;
     static constexpr int OFF_SLOT = OFF_VTV + 16 * 18;
-    static constexpr int OFF_SW = OFF_SLOT + kSxSlots * SLOT;
+    static constexpr int OFF_LU = OFF_SLOT + kSxSlots * SLOT;
+    static constexpr int OFF_SW = OFF_LU + LUS;
     static constexpr int OFF_BAR = OFF_SW + kSxSW * SWS;
-    static constexpr int NBAR = 2 * kSxNST + 4 * kSxSlots;
+    static constexpr int NBAR = 2 * kSxNST + 3 * kSxSlots;
     static constexpr size_t bytes() { return 1024 + sizeof(double) * OFF_BAR + 8 * NBAR; }
     static_assert(OFF_VT % 128 == 0, "ring stages stay 1 KB aligned");
-    static_assert(SLOT % 2 == 0 && SWS % 2 == 0 && OFF_SLOT % 2 == 0 && OFF_SW % 2 == 0, "16-byte alignment");
+    static_assert(SLOT % 2 == 0 && LUS % 2 == 0 && SWS % 2 == 0 && OFF_SLOT % 2 == 0 && OFF_SW % 2 == 0,
+                  "16-byte alignment");
 };
 static_assert(SxSmem::bytes() <= 227 * 1024, "k_smallx shared memory");
+static_assert(2 * kSxSlots * SxSmem::TILE >= 256, "G scratch");
+
+#ifdef DASH_SX_TRACE
+__device__ long long g_sxtrace[148 * 64 * 8];  // [cta][unit < 64][event]
+#define SX_T(u, e)                                                                                \
+    do {                                                                                          \
+        if ((u) < 64 && blockIdx.x < 148) g_sxtrace[(blockIdx.x * 64 + (u)) * 8 + (e)] = clock64(); \
+    } while (0)
+__device__ long long g_sxtrace2[64 * 8 * 8];
+#else
+#define SX_T(u, e) \
+    do {           \
+    } while (0)
+#endif
 
 struct SxParams {
     const int4 *units;         // compacted unit list: {m0, q, a, span}
@@ -257,6 +272,145 @@ __global__ void __launch_bounds__(256) k_sx_copy(SxPlan pl) {
 // ---------------------------------------------------------------------------
 // k_smallx
 // ---------------------------------------------------------------------------
+// P = vtv^{-1} (row-distributed sweep on the scaled Gram, as k_slices3), its
+// infinity norm and an ok flag -> P_s[0..255] | P_s[256] | P_s[257].  Warp-wide.
+__device__ __noinline__ void sx_inverse_vtv(const double *vtv_s, double *P_s, double *buf, int R, int sweep_only) {
+    constexpr int RB = 16, LDV = 18;
+    const int lane = lane_id(), r = lane & 15;
+    const double *vrow = vtv_s + r * LDV;
+    double a[RB];
+    double mx = r < R ? vrow[r] : 0.0;
+#pragma unroll
+    for (int off = 8; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL_MASK, mx, off));
+    const double im = (mx > 0.0 && isfinite(mx)) ? 1.0 / mx : 1.0;
+#pragma unroll
+    for (int z = 0; z < RB; ++z) a[z] = (r < R) ? ((z < R) ? vrow[z] * im : 0.0) : ((z == r) ? 1.0 : 0.0);
+    const bool ok = sweep_inverse_unit<RB>(a, buf, r);
+    double rs = 0.0;
+#pragma unroll
+    for (int z = 0; z < RB; ++z) {
+        a[z] = (r < R && z < R) ? -a[z] * im : 0.0;
+        rs += fabs(a[z]);
+    }
+#pragma unroll
+    for (int off = 8; off > 0; off >>= 1) rs = fmax(rs, __shfl_xor_sync(FULL_MASK, rs, off));
+    if (lane < 16) {
+#pragma unroll
+        for (int z = 0; z < RB; ++z) P_s[z * RB + r] = a[z];
+        if (r == 0) {
+            P_s[256] = rs;
+            P_s[257] = (ok && isfinite(rs) && !sweep_only) ? 1.0 : 0.0;
+        }
+    }
+    __syncwarp();
+}
+
+// Cold path of the solver pair loop: the slices with `ex` set failed the
+// Neumann test; their U rows are recomputed from the XV tile by the exact
+// A = vtv o s s^T + shift I solve (scaled sweep, LU fallback; k_slices3's
+// chain) and written over the math warps' tile rows.  Warp-wide (both groups).
+__device__ __noinline__ void sx_exact_rows(const double *vtv_s, double *buf, double *lu, int *piv,
+                                           const double *xvt, double *ut, int rb, int n, int nmax, double s_r,
+                                           int R, bool ex, bool real, int m, double eps,
+                                           unsigned long long *err, unsigned int *fallbacks) {
+    constexpr int RB = 16, LDV = 18;
+    const int lane = lane_id(), r = lane & 15;
+    const double *vrow = vtv_s + r * LDV;
+    double s_all[RB];
+    group_gather<RB>(s_r, buf, r, s_all);
+    double sh;
+    {
+        double q4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int z = 0; z < RB; ++z) q4[z & 3] = fma(vtv_s[z * LDV + z] * s_all[z], s_all[z], q4[z & 3]);
+        sh = eps * ((q4[0] + q4[1]) + (q4[2] + q4[3])) / R;
+    }
+    const double dg = real ? sh : 1.0;
+    double mx = vrow[r] * s_r * s_r + dg;
+#pragma unroll
+    for (int off = 8; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL_MASK, mx, off));
+    double im = (mx > 0.0 && isfinite(mx)) ? 1.0 / mx : 1.0;
+    double a[RB];
+    {
+        const double sr_im = s_r * im, dg_im = dg * im;
+#pragma unroll
+        for (int z = 0; z < RB; ++z) a[z] = vrow[z] * sr_im * s_all[z] + ((z == r) ? dg_im : 0.0);
+    }
+    const bool okA = sweep_inverse_unit<RB>(a, buf, r);
+    if (!okA) im = 1.0;
+    if (__any_sync(FULL_MASK, ex && !okA)) {
+        const bool need = ex && !okA;
+#pragma unroll
+        for (int z = 0; z < RB; ++z)
+            if (need) a[z] = vrow[z] * s_r * s_all[z] + ((z == r) ? dg : 0.0);
+        if (need && r == 0) atomicAdd(fallbacks, 1u);
+        const bool okLU = lu_fallback_seq<RB>(a, lu, piv, r, R, need);
+        if (need && r == 0 && !okLU) report_error(err, m, DASH_E_SINGULAR);
+    }
+#pragma unroll
+    for (int z = 0; z < RB; ++z) a[z] *= s_all[z];
+    for (int i = 0; i < nmax; ++i) {
+        double u = 0.0;
+        if (ex && i < n) {
+            const double *xr = xvt + (rb + i) * kSxTP;
+            double xrow_v[RB];
+#pragma unroll
+            for (int z = 0; z < RB / 2; ++z) {
+                const double2 t2 = *reinterpret_cast<const double2 *>(xr + 2 * z);
+                xrow_v[2 * z] = t2.x;
+                xrow_v[2 * z + 1] = t2.y;
+            }
+            u = neg_dot4<RB>(a, xrow_v, RB) * im;
+            if (!(r < R)) u = 0.0;
+        }
+        __syncwarp();
+        if (ex && i < n) ut[(rb + i) * kSxTP + r] = u;
+    }
+    __syncwarp();
+}
+
+// LU fallback of the S-row system for the groups with `need` (cold path):
+// returns w_r (0 for padded lanes), reports a singular / non-finite system.
+// LU fallback of the S-row system (cold path; the caller holds the CTA's LU
+// scratch).  D_new row r is rebuilt from the D stage (D_old) and the slice's
+// U rows in the tile, in the main path's order; returns w_r for the groups
+// with `need` (0 for padded lanes) and reports a singular / non-finite system.
+__device__ __noinline__ double sx_b_fallback2(const double *vtv_s, double *buf, double *lu, int *piv,
+                                              const double *dstage, const double *ut, int rb, int n, double lam,
+                                              bool fresh, double sh2, double cn, double wv, int R, bool need,
+                                              bool real, int m, unsigned long long *err, unsigned int *fallbacks) {
+    constexpr int RB = 16, LDV = 18;
+    const int lane = lane_id(), r = lane & 15;
+    const double *vrow = vtv_s + r * LDV;
+    double gram[RB];
+#pragma unroll
+    for (int z = 0; z < RB; ++z) gram[z] = 0.0;
+    for (int i = 0; i < n; ++i) {
+        const double *urw = ut + (rb + i) * kSxTP;
+        const double ur = urw[r];
+#pragma unroll
+        for (int z = 0; z < RB; ++z) gram[z] = fma(ur, urw[z], gram[z]);
+    }
+    const double dg2 = real ? sh2 : 1.0;
+    double a[RB];
+#pragma unroll
+    for (int z = 0; z < RB; ++z) {
+        const double dn = real ? lam * (fresh ? 0.0 : dstage[z * 16 + r]) + gram[z] : 0.0;
+        a[z] = vrow[z] * dn + ((z == r) ? dg2 : 0.0);
+    }
+    if (need && r == 0) atomicAdd(fallbacks, 1u);
+    const bool okLU = lu_fallback_seq<RB>(a, lu, piv, r, R, need);
+    if (need && r == 0 && !okLU) report_error(err, m, DASH_E_SINGULAR);
+    double call[RB];
+    group_gather<RB>(cn, buf, r, call);
+    double wv2 = 0.0;
+#pragma unroll
+    for (int z = 0; z < RB; ++z) wv2 = fma(-a[z], call[z], wv2);
+    if (need) wv = real ? wv2 : 0.0;
+    if (need && real && !isfinite(wv)) report_error(err, m, DASH_E_NONFINITE);
+    return wv;
+}
+
 __global__ void __launch_bounds__(kSxThreads, 1) k_smallx(const __grid_constant__ CUtensorMap tmX, SxParams p) {
     using S = SxSmem;
     constexpr int RB = 16, LDV = 18;
@@ -267,10 +421,12 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_smallx(const __grid_constant_
     double *P_s = sm + S::OFF_P;
     double *vtv_s = sm + S::OFF_VTV;
     double *slots = sm + S::OFF_SLOT;
+    double *lu = sm + S::OFF_LU;
+    int *piv = reinterpret_cast<int *>(lu + 16 * 17);
+    int *lu_lock = reinterpret_cast<int *>(lu + 16 * 17 + 8);
     uint64_t *bar = reinterpret_cast<uint64_t *>(sm + S::OFF_BAR);
     uint64_t *full = bar, *empty = bar + kSxNST;
-    uint64_t *prep = empty + kSxNST, *uready = prep + kSxSlots, *usready = uready + kSxSlots,
-             *sfree = usready + kSxSlots;
+    uint64_t *uready = empty + kSxNST, *usready = uready + kSxSlots, *sfree = usready + kSxSlots;
     const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
     const int J = p.J, R = p.R;
     const int JS = (J + 15) / 16;
@@ -285,15 +441,17 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_smallx(const __grid_constant_
             mbar_init(&empty[s], kSxMW);
         }
         for (int s = 0; s < kSxSlots; ++s) {
-            mbar_init(&prep[s], 1);
             mbar_init(&uready[s], kSxMW);
-            mbar_init(&usready[s], 1);
+            mbar_init(&usready[s], kSxSW);
             mbar_init(&sfree[s], kSxMW);
         }
+        *lu_lock = 0;
         fence_mbar_init();
     }
-    // ring zeroed once: rows past a unit's boxes are stale but always finite
+    // ring zeroed once: rows past a unit's boxes are stale but always finite; the
+    // D stages too (rows z >= R are never loaded and must read as 0)
     for (int i = tid; i < kSxNST * S::SD; i += blockDim.x) xs[i] = 0.0;
+    for (int i = tid; i < kSxSW * S::SWS; i += blockDim.x) sm[S::OFF_SW + i] = 0.0;
     for (int i = tid; i < 16 * S::VTP; i += blockDim.x) {
         const int nn = i / S::VTP, k = i % S::VTP;
         vt[i] = (nn < R && k < J) ? __ldg(p.V + k * R + nn) : 0.0;
@@ -304,44 +462,18 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_smallx(const __grid_constant_
     }
     __syncthreads();
     // P = vtv^{-1} once per CTA (warp 0, both groups; group 0 writes), as k_slices3
-    if (w == 0) {
-        const int r = lane & 15;
-        double *buf = sm + S::OFF_SW + (lane >> 4) * 18;
-        const double *vrow = vtv_s + r * LDV;
-        double a[RB];
-        double mx = r < R ? vrow[r] : 0.0;
-#pragma unroll
-        for (int off = 8; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL_MASK, mx, off));
-        const double im = (mx > 0.0 && isfinite(mx)) ? 1.0 / mx : 1.0;
-#pragma unroll
-        for (int z = 0; z < RB; ++z) a[z] = (r < R) ? ((z < R) ? vrow[z] * im : 0.0) : ((z == r) ? 1.0 : 0.0);
-        const bool ok = sweep_inverse_unit<RB>(a, buf, r);
-        double rs = 0.0;
-#pragma unroll
-        for (int z = 0; z < RB; ++z) {
-            a[z] = (r < R && z < R) ? -a[z] * im : 0.0;
-            rs += fabs(a[z]);
-        }
-#pragma unroll
-        for (int off = 8; off > 0; off >>= 1) rs = fmax(rs, __shfl_xor_sync(FULL_MASK, rs, off));
-        if (lane < 16) {
-#pragma unroll
-            for (int z = 0; z < RB; ++z) P_s[z * RB + r] = a[z];
-            if (r == 0) {
-                P_s[256] = rs;
-                P_s[257] = (ok && isfinite(rs) && !p.sweep_only) ? 1.0 : 0.0;
-            }
-        }
-    }
+    if (w == 0) sx_inverse_vtv(vtv_s, P_s, sm + S::OFF_SW, R, p.sweep_only);
     __syncthreads();
+    const double pnorm = P_s[256];
+    const bool pok = P_s[257] != 0.0;
 
     const int U = __ldcg(p.nunits);
     const int G = gridDim.x;
     const int u0 = (int)((int64_t)U * blockIdx.x / G), u1 = (int)((int64_t)U * (blockIdx.x + 1) / G);
     const int nmine = u1 - u0;
     const int4 *units = p.units + u0;
-    const int nitems = nmine > 0 ? 2 * nmine : 0;  // XV(u) and F(u) per unit, in the math warps' order
-    // item i of the sequence: for v = 0 .. nmine + kSxLook - 1: XV(v) if v < nmine, then F(v - kSxLook) if v >= kSxLook
+    // item sequence of the ring (producer and math warps alike):
+    // for v = 0 .. nmine + kSxLook - 1: XV(v) if v < nmine, then F(v - kSxLook) if v >= kSxLook
 
     if (w == kSxMW + kSxSW) {  // ---------------- producer
         if (lane == 0 && nmine > 0) {
@@ -349,7 +481,7 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_smallx(const __grid_constant_
             auto load = [&](int u) {
                 const int4 d = __ldcg(units + u);
                 const int st = (int)(item % kSxNST);
-                if (item >= kSxNST) mbar_wait(&empty[st], (uint32_t)(((item / kSxNST) - 1) & 1));
+                if (item >= kSxNST) mbar_wait_sleep(&empty[st], (uint32_t)(((item / kSxNST) - 1) & 1));
                 const int nb = (d.w + 7) >> 3;
                 mbar_arrive_expect_tx(&full[st], (uint32_t)(JS * nb) * 1024u);
                 for (int s = 0; s < JS; ++s)
@@ -358,8 +490,14 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_smallx(const __grid_constant_
                 ++item;
             };
             for (int v = 0; v < nmine + kSxLook; ++v) {
-                if (v < nmine) load(v);
-                if (v >= kSxLook) load(v - kSxLook);
+                if (v < nmine) {
+                    load(v);
+                    SX_T(v, 0);
+                }
+                if (v >= kSxLook) {
+                    load(v - kSxLook);
+                    SX_T(v - kSxLook, 1);
+                }
             }
         }
         return;
@@ -379,19 +517,40 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_smallx(const __grid_constant_
         for (int q = 0; q < 2; ++q)
 #pragma unroll
             for (int k = 0; k < 4; ++k) facc[q][k][0] = facc[q][k][1] = 0.0;
+        double gacc[2] = {0.0, 0.0};  // G = sum US^T US: block (w >> 1, w & 1)
+        const int gmi = mb >> 1, gni = mb & 1;
         int64_t item = 0;
         for (int v = 0; v < nmine + kSxLook; ++v) {
-            if (v < nmine) {  // ---- XV(v), Y, U
+            if (v < nmine) {  // ---- XV(v), Y, the Neumann U of this warp's 8 rows
                 const int u = v, slot = u % kSxSlots, use = u / kSxSlots;
+                // the row's slice, its W row and ridge terms (loads in flight during the XV MMAs)
+                const int4 d = __ldcg(units + u);
+                const int m0 = d.x, q = d.y, a0 = d.z, span = d.w;
+                const int l_rp = lane <= q ? (int)(__ldg(p.row_ptr + m0 + lane) - a0) : (1 << 30);
+                int j = 0;
+                for (int k = 1; k <= q; ++k) j += (__shfl_sync(FULL_MASK, l_rp, k) <= xrow) ? 1 : 0;
+                const bool valid = xrow < span;
+                const int m = m0 + (valid ? j : 0);
+                const int wrow = __ldg(p.state_row + m);
+                const bool boot = __ldg(p.is_new + m) != 0 && p.pass == 0;  // new slice: W bootstrap 1
+                double sv[RB];
+#pragma unroll
+                for (int z = 0; z < RB / 2; ++z) {
+                    double2 w2 = make_double2(0.0, 0.0);
+                    if (valid && 2 * z < R) w2 = boot ? make_double2(1.0, 1.0) : __ldcg(reinterpret_cast<const double2 *>(p.W + (int64_t)wrow * R) + z);
+                    sv[2 * z] = w2.x;
+                    sv[2 * z + 1] = w2.y;
+                }
                 const int st = (int)(item % kSxNST);
-                mbar_wait(&full[st], (uint32_t)((item / kSxNST) & 1));
+                mbar_wait_sleep(&full[st], (uint32_t)((item / kSxNST) & 1));
                 ++item;
+                if (mb == 0 && lane == 0) SX_T(u, 2);
                 const double *xt = xs + st * S::SD;
-                double xa[2][4][2];
+                double xa[2][2][2];
 #pragma unroll
                 for (int nb = 0; nb < 2; ++nb)
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) xa[nb][c][0] = xa[nb][c][1] = 0.0;
+                    for (int c = 0; c < 2; ++c) xa[nb][c][0] = xa[nb][c][1] = 0.0;
 #pragma unroll
                 for (int s = 0; s < S::JSM; ++s) {
                     if (s < JS) {
@@ -402,8 +561,8 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_smallx(const __grid_constant_
                             for (int nb = 0; nb < 2; ++nb) {
                                 const double2 b = *reinterpret_cast<const double2 *>(vt + (8 * nb + g) * S::VTP +
                                                                                      16 * s + 8 * h + 2 * t);
-                                dmma884(xa[nb][2 * h], a.x, b.x);
-                                dmma884(xa[nb][2 * h + 1], a.y, b.y);
+                                dmma884(xa[nb][0], a.x, b.x);
+                                dmma884(xa[nb][1], a.y, b.y);
                             }
                         }
                     }
@@ -414,36 +573,47 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_smallx(const __grid_constant_
 #pragma unroll
                 for (int nb = 0; nb < 2; ++nb)
 #pragma unroll
-                    for (int e = 0; e < 2; ++e) xv[nb][e] = (xa[nb][0][e] + xa[nb][1][e]) + (xa[nb][2][e] + xa[nb][3][e]);
+                    for (int e = 0; e < 2; ++e) xv[nb][e] = xa[nb][0][e] + xa[nb][1][e];
+                // ridge terms of the row's slice (k_slices3's Neumann test):
+                // sh = eps mean(vtv_rr s_r^2); d_r = sh / s_r^2; rho = max_r d_r * ||P||
+                double sh;
+                {
+                    double q4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                    for (int z = 0; z < RB; ++z) q4[z & 3] = fma(vtv_s[z * LDV + z] * sv[z], sv[z], q4[z & 3]);
+                    sh = p.eps * ((q4[0] + q4[1]) + (q4[2] + q4[3])) / R;
+                }
+                double qmax = 0.0;
+#pragma unroll
+                for (int z = 0; z < RB; ++z) {
+                    if (z < R) {
+                        const double is = rcp_nr(sv[z]);
+                        const double qz = is * is;
+                        qmax = (sv[z] != 0.0 && isfinite(qz)) ? fmax(qmax, qz) : INFINITY;
+                    }
+                }
+                const double rho = sh * qmax * pnorm;
+                const bool need2 = valid && pok && rho <= kS3Neumann && !(rho <= kS3Neumann1);
+                double dd[2][2], si[2][2];
+#pragma unroll
+                for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int c = 8 * nb + 2 * t + e;
+                        double sc = 0.0;
+#pragma unroll
+                        for (int z = 0; z < RB; ++z)
+                            if (z == c) sc = sv[z];
+                        const double is = (valid && c < R) ? rcp_nr(sc) : 0.0;
+                        si[nb][e] = is;
+                        dd[nb][e] = valid ? sh * is * is : 0.0;
+                    }
                 // Y = XV P: A fragment of K step kk = this lane's XV value xv[kk >> 1][kk & 1]
                 double ya[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk)
 #pragma unroll
                     for (int nb = 0; nb < 2; ++nb) dmma884(ya[nb], xv[kk >> 1][kk & 1], pf[kk][nb]);
-                double *sl = slots + slot * S::SLOT;
-                double *xvt = sl, *ut = sl + S::TILE, *tbl = sl + 2 * S::TILE;
-                const int *hdr = reinterpret_cast<const int *>(tbl + S::TBL);
-                if (use >= 1) mbar_wait(&sfree[slot], (uint32_t)((use - 1) & 1));  // F(u - kSxSlots) done
-#pragma unroll
-                for (int nb = 0; nb < 2; ++nb)
-                    *reinterpret_cast<double2 *>(xvt + xrow * kSxTP + 8 * nb + 2 * t) = make_double2(xv[nb][0], xv[nb][1]);
-                mbar_wait(&prep[slot], (uint32_t)(use & 1));
-                const int span = hdr[3];
-                const int fast2 = hdr[5];
-                const bool valid = xrow < span;
-                const int k = valid ? (int)reinterpret_cast<const uint8_t *>(hdr + 8)[xrow] : 0;
-                const double *dk = tbl + k * 32;
-                double dd[2][2], si[2][2];
-#pragma unroll
-                for (int nb = 0; nb < 2; ++nb) {
-                    const double2 a = *reinterpret_cast<const double2 *>(dk + 8 * nb + 2 * t);
-                    const double2 b = *reinterpret_cast<const double2 *>(dk + 16 + 8 * nb + 2 * t);
-                    dd[nb][0] = valid ? a.x : 0.0;
-                    dd[nb][1] = valid ? a.y : 0.0;
-                    si[nb][0] = b.x;
-                    si[nb][1] = b.y;
-                }
                 double c1[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk)
@@ -451,15 +621,19 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_smallx(const __grid_constant_
                     for (int nb = 0; nb < 2; ++nb)
                         dmma884(c1[nb], ya[kk >> 1][kk & 1] * dd[kk >> 1][kk & 1], pf[kk][nb]);  // (Y o d) P
                 double c2[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-                if (fast2) {  // unit-uniform
+                if (__any_sync(FULL_MASK, need2)) {
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk)
 #pragma unroll
                         for (int nb = 0; nb < 2; ++nb)
                             dmma884(c2[nb], c1[kk >> 1][kk & 1] * dd[kk >> 1][kk & 1], pf[kk][nb]);
                 }
+                double *sl = slots + slot * S::SLOT;
+                double *xvt = sl, *ut = sl + S::TILE;
+                if (use >= 1) mbar_wait_sleep(&sfree[slot], (uint32_t)((use - 1) & 1));  // F(u - kSxSlots) done
 #pragma unroll
                 for (int nb = 0; nb < 2; ++nb) {
+                    *reinterpret_cast<double2 *>(xvt + xrow * kSxTP + 8 * nb + 2 * t) = make_double2(xv[nb][0], xv[nb][1]);
                     double u2[2];
 #pragma unroll
                     for (int e = 0; e < 2; ++e) u2[e] = valid ? ((ya[nb][e] - c1[nb][e]) + c2[nb][e]) * si[nb][e] : 0.0;
@@ -467,13 +641,14 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_smallx(const __grid_constant_
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&uready[slot]);
+                if (mb == 0 && lane == 0) SX_T(u, 3);
             }
-            if (v >= kSxLook) {  // ---- F(v - kSxLook) += X^T US
+            if (v >= kSxLook) {  // ---- F(v - kSxLook) += X^T US;  G += US^T US
                 const int u = v - kSxLook, slot = u % kSxSlots, use = u / kSxSlots;
                 const int st = (int)(item % kSxNST);
-                mbar_wait(&full[st], (uint32_t)((item / kSxNST) & 1));
+                mbar_wait_sleep(&full[st], (uint32_t)((item / kSxNST) & 1));
                 ++item;
-                mbar_wait(&usready[slot], (uint32_t)(use & 1));
+                mbar_wait_sleep(&usready[slot], (uint32_t)(use & 1));
                 const double *xt = xs + st * S::SD;
                 const double *ub = slots + slot * S::SLOT + S::TILE;
 #pragma unroll
@@ -491,12 +666,14 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_smallx(const __grid_constant_
                             dmma884(facc[q][3], a.y, bu.y);
                         }
                     }
+                    dmma884(gacc, ub[row * kSxTP + 8 * gmi + g], ub[row * kSxTP + 8 * gni + g]);
                 }
                 __syncwarp();
                 if (lane == 0) {
                     mbar_arrive(&empty[st]);
                     mbar_arrive(&sfree[slot]);
                 }
+                if (mb == 0 && lane == 0) SX_T(u, 7);
             }
         }
         // F slot of this CTA (every entry written by exactly one lane; zeros if no units)
@@ -516,193 +693,120 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_smallx(const __grid_constant_
                 }
             }
         }
-        (void)nitems;
-        asm volatile("bar.sync 1, %0;" ::"n"((kSxMW + kSxSW) * 32) : "memory");
+        // G slot of this CTA: block (gmi, gni) of sum US^T US (= sum_k gram_k o w_k w_k^T)
+        double *gs = p.G_slots + (int64_t)blockIdx.x * R * R;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int a = 8 * gmi + g, b = 8 * gni + 2 * t + e;
+            if (a < R && b < R) gs[a * R + b] = gacc[e];
+        }
         return;
     }
-    // ---------------- solver warps
+    // ---------------- solver warps: slice pairs round-robin over the unit sequence
     const int ws = w - kSxMW;
     const int r = lane & 15, gl = lane >> 4;
     double *wsm = sm + S::OFF_SW + ws * S::SWS;
     double *buf = wsm + gl * 18;
-    double *lu = wsm + 36;
-    int *piv = reinterpret_cast<int *>(lu + 16 * 17);
+    double *dstage = wsm + 36 + gl * 256;  // this group's D block (column r at [z * 16 + r]; rows >= R stay 0)
     const double *vrow = vtv_s + r * LDV;
-    const double pnorm = P_s[256];
-    const bool pok = P_s[257] != 0.0;
-    double gacc[RB];
-#pragma unroll
-    for (int z = 0; z < RB; ++z) gacc[z] = 0.0;
-    for (int u = ws; u < nmine; u += kSxSW) {
+    int pc = 0;  // pairs of the units before this one
+    for (int u = 0; u < nmine; ++u) {
         const int slot = u % kSxSlots, use = u / kSxSlots;
         const int4 d = __ldcg(units + u);
-        const int m0 = d.x, q = d.y, a0 = d.z, span = d.w;
-        double *sl = slots + slot * S::SLOT;
-        double *xvt = sl, *ut = sl + S::TILE, *tbl = sl + 2 * S::TILE;
-        int *hdr = reinterpret_cast<int *>(tbl + S::TBL);
-        uint8_t *rowslice = reinterpret_cast<uint8_t *>(hdr + 8);
-        if (use >= 1) mbar_wait(&sfree[slot], (uint32_t)((use - 1) & 1));
-        // ---- prep: s, ridge shift, d = sh / s^2, 1/s, Neumann test (k_slices3's) -> table
-        unsigned fastmask = 0u;
-        bool any2 = false;
-        for (int pr = 0; pr < q; pr += 2) {
-            const int j = pr + gl;
+        const int m0 = d.x, q = d.y, a0 = d.z;
+        const int np = (q + 1) >> 1;
+        const int k0 = ((ws - pc) % kSxSW + kSxSW) % kSxSW;  // my first pair of this unit
+        pc += np;
+        mbar_wait_sleep(&uready[slot], (uint32_t)(use & 1));
+        if (lane == 0 && k0 < np) SX_T(u, 5);
+        double *xvt = slots + slot * S::SLOT, *ut = xvt + S::TILE;
+        for (int k = k0; k < np; k += kSxSW) {
+            const int j = 2 * k + gl;
             const bool act = j < q;
-            const int m = m0 + (act ? j : 0);
-            const int wrow = __ldg(p.state_row + m);
-            const bool fresh = __ldg(p.is_new + m) != 0;
             const bool real = act && r < R;
-            const double s_r = real ? ((fresh && p.pass == 0) ? 1.0 : __ldcg(p.W + (int64_t)wrow * R + r)) : 0.0;
-            double s_all[RB];
-            group_gather<RB>(s_r, buf, r, s_all);
-            double q4[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-            for (int z = 0; z < RB; ++z)
-                if (z < R) q4[z & 3] = fma(vtv_s[z * LDV + z] * s_all[z], s_all[z], q4[z & 3]);
-            const double sh = p.eps * ((q4[0] + q4[1]) + (q4[2] + q4[3])) / R;
-            double qv = 0.0, isr = 0.0;
-            bool bad = false;
-            if (real) {
-                isr = rcp_nr(s_r);
-                qv = isr * isr;
-                bad = !(s_r != 0.0) || !isfinite(qv);
-            }
-            double qm = bad ? INFINITY : qv;
-#pragma unroll
-            for (int off = 8; off > 0; off >>= 1) qm = fmax(qm, __shfl_xor_sync(FULL_MASK, qm, off));
-            const double rho = sh * qm * pnorm;
-            const bool fast = act && pok && rho <= kS3Neumann;  // NaN / inf -> exact path
-            const unsigned fb = __ballot_sync(FULL_MASK, fast && r == 0);
-            fastmask |= ((fb & 1u) ? 1u : 0u) << pr;
-            fastmask |= ((fb >> 16) & 1u) << (pr + 1);
-            any2 = any2 || __any_sync(FULL_MASK, fast && !(rho <= kS3Neumann1));
-            if (act) {
-                tbl[j * 32 + r] = real ? sh * qv : 0.0;
-                tbl[j * 32 + 16 + r] = real ? isr : 0.0;
-                const int64_t rb = __ldg(p.row_ptr + m) - a0, n = __ldg(p.row_ptr + m + 1) - __ldg(p.row_ptr + m);
-                for (int64_t i = r; i < n; i += 16) rowslice[rb + i] = (uint8_t)j;
-            }
-        }
-        if (lane == 0) {
-            hdr[0] = m0;
-            hdr[1] = q;
-            hdr[2] = a0;
-            hdr[3] = span;
-            hdr[4] = (int)fastmask;
-            hdr[5] = any2 ? 1 : 0;
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&prep[slot]);
-        mbar_wait(&uready[slot], (uint32_t)(use & 1));
-        // ---- per slice pair
-        for (int pr = 0; pr < q; pr += 2) {
-            const int j = pr + gl;
-            const bool act = j < q;
             const int m = m0 + (act ? j : 0);
-            const int wrow = __ldg(p.state_row + m);
-            const bool fresh = __ldg(p.is_new + m) != 0;
-            const bool real = act && r < R;
             const int64_t rg = __ldg(p.row_ptr + m);
-            const int rb = (int)(rg - a0);
             const int n = act ? (int)(__ldg(p.row_ptr + m + 1) - rg) : 0;
-            // state loads first (latency overlaps the rows loop)
+            const int rb = (int)(rg - a0);
+            const int wrow = __ldg(p.state_row + m);
+            const bool fresh = __ldg(p.is_new + m) != 0;
+            // state: D block -> dstage (async), c_old and s into registers
+            if (real && !fresh) {
+                const double *dcol = p.D + (int64_t)wrow * R * R + r;
+                for (int z = 0; z < R; ++z) cp_async8(dstage + z * 16 + r, dcol + (int64_t)z * R);
+            }
             const double cold = (real && !fresh) ? __ldcg(p.C + (int64_t)wrow * R + r) : 0.0;
-            double dold[RB];
-#pragma unroll
-            for (int z = 0; z < RB; ++z)
-                dold[z] = (real && !fresh && z < R) ? __ldcg(p.D + (int64_t)wrow * R * R + (int64_t)z * R + r) : 0.0;
             const double s_r = real ? ((fresh && p.pass == 0) ? 1.0 : __ldcg(p.W + (int64_t)wrow * R + r)) : 0.0;
-            const bool fast = act && ((fastmask >> j) & 1u);
             int nmax = n;
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) nmax = max(nmax, __shfl_xor_sync(FULL_MASK, nmax, off));
-            // ---- slices failing the Neumann test: exact A solve (sweep, LU fallback), U rows rewritten
-            if (__any_sync(FULL_MASK, act && !fast)) {
-                const bool ex = act && !fast;
+            // the Neumann test again (the math warps applied it per row): exact path otherwise
+            bool fast;
+            {
                 double s_all[RB];
                 group_gather<RB>(s_r, buf, r, s_all);
-                double sh;
-                {
-                    double q4[4] = {0.0, 0.0, 0.0, 0.0};
+                double q4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-                    for (int z = 0; z < RB; ++z)
-                        if (z < R) q4[z & 3] = fma(vtv_s[z * LDV + z] * s_all[z], s_all[z], q4[z & 3]);
-                    sh = p.eps * ((q4[0] + q4[1]) + (q4[2] + q4[3])) / R;
-                }
-                const double dg = real ? sh : 1.0;
-                double mx = vrow[r] * s_r * s_r + dg;
-#pragma unroll
-                for (int off = 8; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL_MASK, mx, off));
-                double im = (mx > 0.0 && isfinite(mx)) ? 1.0 / mx : 1.0;
-                double a[RB];
-                {
-                    const double sr_im = s_r * im, dg_im = dg * im;
-#pragma unroll
-                    for (int z = 0; z < RB; ++z) a[z] = vrow[z] * sr_im * s_all[z] + ((z == r) ? dg_im : 0.0);
-                }
-                const bool okA = sweep_inverse_unit<RB>(a, buf, r);
-                if (!okA) im = 1.0;
-                if (__any_sync(FULL_MASK, ex && !okA)) {
-                    const bool need = ex && !okA;
-#pragma unroll
-                    for (int z = 0; z < RB; ++z)
-                        if (need) a[z] = vrow[z] * s_r * s_all[z] + ((z == r) ? dg : 0.0);
-                    if (need && r == 0) atomicAdd(p.fallbacks, 1u);
-                    const bool okLU = lu_fallback_seq<RB>(a, lu, piv, r, R, need);
-                    if (need && r == 0 && !okLU) report_error(p.err, m, DASH_E_SINGULAR);
+                for (int z = 0; z < RB; ++z) q4[z & 3] = fma(vtv_s[z * LDV + z] * s_all[z], s_all[z], q4[z & 3]);
+                const double sh = p.eps * ((q4[0] + q4[1]) + (q4[2] + q4[3])) / R;
+                double qm = 0.0;
+                if (real) {
+                    const double is = rcp_nr(s_r);
+                    const double qz = is * is;
+                    qm = (s_r != 0.0 && isfinite(qz)) ? qz : INFINITY;
                 }
 #pragma unroll
-                for (int z = 0; z < RB; ++z) a[z] *= s_all[z];
-                for (int i = 0; i < nmax; ++i) {
-                    double u = 0.0;
-                    if (ex && i < n) {
-                        const double *xr = xvt + (rb + i) * kSxTP;
-                        double xrow_v[RB];
-#pragma unroll
-                        for (int z = 0; z < RB / 2; ++z) {
-                            const double2 t2 = *reinterpret_cast<const double2 *>(xr + 2 * z);
-                            xrow_v[2 * z] = t2.x;
-                            xrow_v[2 * z + 1] = t2.y;
-                        }
-                        u = neg_dot4<RB>(a, xrow_v, R) * im;
-                        if (!(r < R)) u = 0.0;
-                    }
-                    __syncwarp();
-                    if (ex && i < n) ut[(rb + i) * kSxTP + r] = u;
-                }
+                for (int off = 8; off > 0; off >>= 1) qm = fmax(qm, __shfl_xor_sync(FULL_MASK, qm, off));
+                const double rho = sh * qm * pnorm;
+                fast = act && pok && rho <= kS3Neumann;
+            }
+            if (__any_sync(FULL_MASK, act && !fast)) {  // rare: exact A solve; serialised LU scratch
+                if (lane == 0)
+                    while (atomicCAS(lu_lock, 0, 1) != 0) __nanosleep(64);
                 __syncwarp();
+                sx_exact_rows(vtv_s, buf, lu, piv, xvt, ut, rb, n, nmax, s_r, R, act && !fast, real, m, p.eps,
+                              p.err, p.fallbacks);
+                __syncwarp();
+                if (lane == 0) atomicExch(lu_lock, 0);
             }
             // ---- rows: U -> U_out, c, gram (_kernels.py:98-115)
             double c = 0.0, gram[RB];
 #pragma unroll
             for (int z = 0; z < RB; ++z) gram[z] = 0.0;
-            for (int i = 0; i < nmax; ++i) {
-                if (i < n) {
-                    const double *urw = ut + (rb + i) * kSxTP;
-                    double ua[RB];
+            for (int i = 0; i < n; ++i) {
+                const double *urw = ut + (rb + i) * kSxTP;
+                double ua[RB];
 #pragma unroll
-                    for (int z = 0; z < RB / 2; ++z) {
-                        const double2 t2 = *reinterpret_cast<const double2 *>(urw + 2 * z);
-                        ua[2 * z] = t2.x;
-                        ua[2 * z + 1] = t2.y;
-                    }
-                    const double ur = ua[r];
+                for (int z = 0; z < RB / 2; ++z) {
+                    const double2 t2 = *reinterpret_cast<const double2 *>(urw + 2 * z);
+                    ua[2 * z] = t2.x;
+                    ua[2 * z + 1] = t2.y;
+                }
+                const double ur = urw[r];
 #pragma unroll
-                    for (int z = 0; z < RB; ++z) gram[z] = fma(ur, ua[z], gram[z]);
-                    if (real) {
-                        c = fma(xvt[(rb + i) * kSxTP + r], ur, c);
-                        p.U[(rg + i) * R + r] = ur;
-                    }
+                for (int z = 0; z < RB; ++z) gram[z] = fma(ur, ua[z], gram[z]);
+                if (real) {
+                    c = fma(xvt[(rb + i) * kSxTP + r], ur, c);
+                    p.U[(rg + i) * R + r] = ur;
                 }
             }
             // ---- c, D accumulation and the S-row system (_kernels.py:103-135)
             const double cn = real ? p.lam * cold + c : 0.0;
-            double dn[RB];
+            cp_async_wait();
+            __syncwarp();
+            double a[RB];
             double drr = 0.0;
 #pragma unroll
             for (int z = 0; z < RB; ++z) {
-                dn[z] = (real && z < R) ? p.lam * dold[z] + gram[z] : 0.0;
-                if (z == r) drr = dn[z];
+                const double dn = real ? p.lam * ((fresh) ? 0.0 : dstage[z * 16 + r]) + gram[z] : 0.0;
+                a[z] = dn;  // D_new row r (rows / columns >= R are 0)
+                if (z == r) drr = dn;
+            }
+            if (real && p.final_pass) {
+                p.C[(int64_t)wrow * R + r] = cn;
+#pragma unroll
+                for (int z = 0; z < RB; ++z)
+                    if (z < R) p.D[(int64_t)wrow * R * R + (int64_t)z * R + r] = a[z];
             }
             double sh2;
             {
@@ -710,80 +814,41 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_smallx(const __grid_constant_
                 group_gather<RB>(real ? vrow[r] * drr : 0.0, buf, r, vdd);
                 double dsum = 0.0;
 #pragma unroll
-                for (int z = 0; z < RB; ++z)
-                    if (z < R) dsum += vdd[z];
+                for (int z = 0; z < RB; ++z) dsum += vdd[z];
                 sh2 = p.eps * dsum / R;
             }
-            double a[RB];
-            {
-                const double dg2 = real ? sh2 : 1.0;
+            const double dg2 = real ? sh2 : 1.0;
 #pragma unroll
-                for (int z = 0; z < RB; ++z) a[z] = vrow[z] * dn[z] + ((z == r) ? dg2 : 0.0);
-            }
+            for (int z = 0; z < RB; ++z) a[z] = vrow[z] * a[z] + ((z == r) ? dg2 : 0.0);
             double wv;
             const bool okB = gj_solve<RB>(a, cn, buf, r, wv);
             if (!real) wv = 0.0;
             bool gok = okB && isfinite(wv);
             {
                 const unsigned bal = __ballot_sync(FULL_MASK, !gok);
-                const unsigned gmask = 0xffffu << (gl * 16);
-                gok = (bal & gmask) == 0;
+                gok = (bal & (0xffffu << (gl * 16))) == 0;
             }
-            if (__any_sync(FULL_MASK, !gok && act)) {
-                const bool need = !gok && act;
-                const double dg2 = real ? sh2 : 1.0;
-#pragma unroll
-                for (int z = 0; z < RB; ++z)
-                    if (need) a[z] = vrow[z] * dn[z] + ((z == r) ? dg2 : 0.0);
-                if (need && r == 0) atomicAdd(p.fallbacks, 1u);
-                const bool okLU = lu_fallback_seq<RB>(a, lu, piv, r, R, need);
-                if (need && r == 0 && !okLU) report_error(p.err, m, DASH_E_SINGULAR);
-                double call[RB];
-                group_gather<RB>(cn, buf, r, call);
-                double wv2 = 0.0;
-#pragma unroll
-                for (int z = 0; z < RB; ++z) wv2 = fma(-a[z], call[z], wv2);
-                if (need) wv = real ? wv2 : 0.0;
-                if (need && real && !isfinite(wv)) report_error(p.err, m, DASH_E_NONFINITE);
+            if (__any_sync(FULL_MASK, !gok && act)) {  // rare: LU (the reference's numpy fallback)
+                if (lane == 0)
+                    while (atomicCAS(lu_lock, 0, 1) != 0) __nanosleep(64);
+                __syncwarp();
+                wv = sx_b_fallback2(vtv_s, buf, lu, piv, dstage, ut, rb, n, p.lam, fresh, sh2, cn, wv, R,
+                                    !gok && act, real, m, p.err, p.fallbacks);
+                __syncwarp();
+                if (lane == 0) atomicExch(lu_lock, 0);
             }
-            if (real) {
-                p.W[(int64_t)wrow * R + r] = wv;
-                if (p.final_pass) {
-                    p.C[(int64_t)wrow * R + r] = cn;
-#pragma unroll
-                    for (int z = 0; z < RB; ++z)
-                        if (z < R) p.D[(int64_t)wrow * R * R + (int64_t)z * R + r] = dn[z];
-                }
-            }
-            __syncwarp();  // every lane's gram row reads are done before US overwrites U
+            if (real) p.W[(int64_t)wrow * R + r] = wv;
+            __syncwarp();  // every lane's row reads are done before US overwrites the tile
             for (int i = 0; i < n; ++i) ut[(rb + i) * kSxTP + r] *= wv;  // padded lanes: wv = 0
-            double wa[RB];
-            group_gather<RB>(wv, buf, r, wa);
-            if (act) {
-#pragma unroll
-                for (int z = 0; z < RB; ++z) gacc[z] = fma(gram[z] * wv, wa[z], gacc[z]);
-            }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&usready[slot]);
-    }
-    // ---- per-CTA G slot: solver groups summed in fixed order (slot tiles reused as scratch)
-    asm volatile("bar.sync 1, %0;" ::"n"((kSxMW + kSxSW) * 32) : "memory");
-    double *red = slots;  // kSxSW x 2 groups x 16 x 16 <= kSxSlots x SLOT
-#pragma unroll
-    for (int z = 0; z < RB; ++z) red[((ws * 2 + gl) * 16 + r) * 16 + z] = gacc[z];
-    asm volatile("bar.sync 2, %0;" ::"n"(kSxSW * 32) : "memory");
-    double *gs = p.G_slots + (int64_t)blockIdx.x * R * R;
-    for (int i = tid - kSxMW * 32; i < R * R; i += kSxSW * 32) {
-        const int a = i / R, b = i % R;
-        double acc = 0.0;
-        for (int k = 0; k < 2 * kSxSW; ++k) acc += red[(k * 16 + a) * 16 + b];
-        gs[i] = acc;
+        if (lane == 0 && k0 < np) SX_T(u, 6);
     }
 }
 
 int launch_smallx(dash_ctx *ctx, cudaStream_t st, const CUtensorMap &map8, const SxParams &sp, int grid) {
     const size_t smem = SxSmem::bytes();
     ensure_smem_attr(k_smallx, smem);
-    return launch_k(true, k_smallx, grid, kSxThreads, smem, st, map8, sp);
+    return launch_k(pdl_site("smallx"), k_smallx, grid, kSxThreads, smem, st, map8, sp);
 }

@@ -1254,7 +1254,7 @@ void launch_vsolve_t(dash_ctx *ctx, cudaStream_t st, const double *fg, double la
     static const bool old_vsolve = getenv("DASH_CHOL_VSOLVE") != nullptr;  // A/B: per-warp Cholesky variant
     if constexpr (RB <= 16) {
         if (!old_vsolve) {
-            launch_k(true, k_vsolve2<RB>, (J + 127) / 128, 128, 0, st, fg, (const double *)ctx->fsnap.p,
+            launch_k(pdl_site("vs"), k_vsolve2<RB>, (J + 127) / 128, 128, 0, st, fg, (const double *)ctx->fsnap.p,
                      (const double *)ctx->gsnap.p, lam, J, R, eps, F, G, V, ctx->err, ctx->fallbacks);
             return;
         }
@@ -1290,8 +1290,8 @@ int colsum2(dash_ctx *ctx, cudaStream_t st, const double *sa, int na, int64_t wa
     a.part = (double *)ctx->part.p;
     b.part = a.part + a.nseg * wa;
     ctx->last_launches++;  // two kernels under one phase
-    return launch_k(true, k_colsum_part2, a.bx * a.nseg + b.bx * b.nseg, 128, 0, st, a, b) ||
-           launch_k(true, k_colsum_final2, a.bx + b.bx, 128, 0, st, a, b);
+    return launch_k(pdl_site("cs1"), k_colsum_part2, a.bx * a.nseg + b.bx * b.nseg, 128, 0, st, a, b) ||
+           launch_k(pdl_site("cs2"), k_colsum_final2, a.bx + b.bx, 128, 0, st, a, b);
 }
 
 // ---- streaming (TMA ring) GEMM path: J, ldx, R even; ring fits in shared memory
@@ -1428,14 +1428,14 @@ int launch_bigx(dash_ctx *ctx, cudaStream_t st, const B *b, const BigxParams &bp
     const int nbig = ctx->bigx_nbig;
     PhaseScope ps(ctx, st, PH_BIG);
     ctx->last_launches += 1;  // two kernels under one phase (pre, streaming); post after the F GEMM
-    if (launch_k(true, k_bigx_pre, 1 + (nbig + 7) / 8, 256, 0, st, bp)) return DASH_E_CUDA;
+    if (launch_k(pdl_site("bxpre"), k_bigx_pre, 1 + (nbig + 7) / 8, 256, 0, st, bp)) return DASH_E_CUDA;
     CUtensorMap mx;
     if (!make_box_map(&mx, b->X, bp.J, b->N, b->ldx)) return DASH_E_CUDA;
     const size_t smem = SM::bytes(bp.J);
     const int js = SM::strips(bp.J);
     auto go = [&](auto kern) {
         ensure_smem_attr(kern, smem);
-        return launch_k(true, kern, bp.G, kBxThreads, smem, st, mx, bp);
+        return launch_k(pdl_site("bigx"), kern, bp.G, kBxThreads, smem, st, mx, bp);
     };
     int rc;
     // J <= 128 (the fused path's limit): <= 8 FP64 / 4 FP32 strips over kBxB X^T U warps
@@ -1450,7 +1450,7 @@ int launch_bigx(dash_ctx *ctx, cudaStream_t st, const B *b, const BigxParams &bp
 int launch_bigx_post(dash_ctx *ctx, cudaStream_t st, const BigxParams &bp) {
     if (bp.T == 0) return 0;
     PhaseScope ps(ctx, st, PH_BIGPOST);
-    return launch_k(true, k_bigx_post, ctx->bigx_nbig, 256, 0, st, bp);
+    return launch_k(pdl_site("bxpost"), k_bigx_post, ctx->bigx_nbig, 256, 0, st, bp);
 }
 
 template <int RP>
@@ -1602,12 +1602,12 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
             PhaseScope ps(ctx, st, PH_XV);
             // PDL only behind the plan kernels: otherwise the prologue reads the V / F / G
             // the previous update (or pass) just wrote -> normal launch
-            if (launch_k(pass == 0 && ctx->planned, k_sx_walk, nch + sx_prologue_blocks(R), 256, 0, st, pl, pro, (const double *)s->V,
+            if (launch_k(pass == 0 && ctx->planned && pdl_site("sxwalk"), k_sx_walk, nch + sx_prologue_blocks(R), 256, 0, st, pl, pro, (const double *)s->V,
                          J, R))
                 return DASH_E_CUDA;
             if (nch > 0) {
                 ctx->last_launches++;
-                if (launch_k(true, k_sx_copy, nch, 256, 0, st, pl)) return DASH_E_CUDA;
+                if (launch_k(pdl_site("sxcopy"), k_sx_copy, nch, 256, 0, st, pl)) return DASH_E_CUDA;
             }
         }
         CUtensorMap m8;
@@ -1801,6 +1801,21 @@ int dash_ctx_status(dash_ctx *ctx, void *stream, int64_t *fail_slice_host) {
 }
 
 int dash_ctx_last_launches(const dash_ctx *ctx) { return ctx ? ctx->last_launches : 0; }
+
+// debug builds (-DDASH_SX_TRACE): copy k_smallx's per-unit event clocks to the host
+int dash_sx_trace(long long *out, int n) {
+#ifdef DASH_SX_TRACE
+    cudaDeviceSynchronize();
+    if (n == -1) return cudaMemcpyFromSymbol(out, g_sxtrace2, sizeof(long long) * 64 * 8 * 8) == cudaSuccess ? 0 : 2;
+    return cudaMemcpyFromSymbol(out, g_sxtrace, sizeof(long long) * (size_t)std::min(n, 148 * 64 * 8)) == cudaSuccess
+               ? 0
+               : DASH_E_CUDA;
+#else
+    (void)out;
+    (void)n;
+    return DASH_E_ARG;
+#endif
+}
 
 int dash_host_row_ptr(const int64_t *counts, int64_t M, int64_t *row_ptr, int64_t *N_out) {
     if (M < 0 || (M > 0 && (!counts || !row_ptr))) return DASH_E_ARG;

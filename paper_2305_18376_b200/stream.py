@@ -213,6 +213,7 @@ class StreamState:
         self._ulog: list = []
         self._unchecked = False  # an update_packed(check=False) may have latched a device error
         self._uarena = None  # [chunk (rows, R), rows used]: U blocks are views of chunks
+        self._marena = None  # [chunk (bytes,), bytes used]: per-update index arrays of the U history
         if u_blocks is not None:
             self._ingest_u_blocks(u_blocks)
         self._X = None
@@ -507,7 +508,7 @@ class StreamState:
         # batch's index arrays; the per-slice refs are built on first read
         if self.keep_u_history:
             self._ustore.append(U)
-            self._ulog.append((len(self._ustore) - 1, self._meta_bytes.clone(), M))
+            self._ulog.append((len(self._ustore) - 1, self._keep_meta(self._meta_bytes), M))
         self._meta_slot[3].record()  # this update no longer reads its meta slot after this point
         self._meta_slot[4][1] = True
         self._cache.clear()
@@ -537,6 +538,20 @@ class StreamState:
         lo = a[1]
         a[1] = lo + (need + self._U_ALIGN - 1) // self._U_ALIGN * self._U_ALIGN
         return a[0][lo:lo + need]
+
+    def _keep_meta(self, mb: torch.Tensor) -> torch.Tensor:
+        """Device copy of this update's index arrays for the U history, carved
+        from a byte arena (no allocation per update: a fresh cudaMalloc can
+        stall the host behind the GPU)."""
+        n = int(mb.shape[0])
+        a = self._marena
+        if a is None or a[1] + n > a[0].shape[0]:
+            self._marena = a = [torch.empty(max(16 * n, 1 << 24), dtype=torch.uint8, device=self.device), 0]
+        lo = a[1]
+        a[1] = lo + (n + 255) // 256 * 256
+        out = a[0][lo:lo + n]
+        out.copy_(mb, non_blocking=True)
+        return out
 
     def _new_u_chunk(self, rows: int):
         self._uarena = [torch.empty((rows, self._R), dtype=self.dtype, device=self.device), 0]
