@@ -53,13 +53,19 @@ constexpr int kSxRows = 32;          // rows per unit (max)
 constexpr int kSxSlices = 16;        // slices per unit (max)
 constexpr int kSxChunk = 256;        // batch positions per planner block
 constexpr int kSxWalkers = 8;        // sequential walkers per planner block (32 positions each)
-constexpr int kSxNST = 3;            // X ring stages
+constexpr int kSxNST = 2;            // X ring stages
 constexpr int kSxSlots = 6;          // units in flight (XV / U tiles)
 constexpr int kSxLook = kSxSlots - 1;  // the math warps' XV runs this many units ahead of F
 constexpr int kSxMW = 4;             // math warps (one 8-row block each)
-constexpr int kSxSW = 11;            // solver warps (slice pairs round-robin over the unit sequence); 16 warps: 128 registers (4 warps per SM sub-partition)
-constexpr int kSxThreads = (kSxMW + kSxSW + 1) * 32;
+constexpr int kSxSW = 10;            // solver warps (slice pairs round-robin over the unit sequence)
+constexpr int kSxThreads = (kSxMW + kSxSW + 2) * 32;  // + TMA warp + metadata warp: 16 warps, 128 registers
 constexpr int kSxTP = 18;            // XV / U tile pitch (doubles): conflict-free fragment stores and row reads
+
+constexpr int kSxNM = 8;              // per-unit metadata slots (staged by the metadata warp ahead of the math)
+// unit record (planner -> producer; also the layout of a metadata slot's header), ints:
+// [0..3] {m0, q, a, span} | [4..20] rp[q+1] (unit-local first rows) | [21..36] state rows |
+// [37..40] is_new bytes | [41] "second Neumann term" flag (producer) | pad
+constexpr int kSxRec = 48;
 
 struct SxSmem {
     static constexpr int JSM = 8;                        // strips (J <= 128)
@@ -67,23 +73,28 @@ struct SxSmem {
     static constexpr int VTP = JSM * 16 + 8;             // V^T pitch
     static constexpr int TILE = kSxRows * kSxTP;
     static constexpr int SLOT = 2 * TILE;                // XV tile | U / US tile
+    // per-unit metadata (producer -> math, solver): int desc[4] | rp[kSxSlices + 1] (unit-local first
+    // rows) | wrow[kSxSlices] | fresh[kSxSlices] (bytes) -> 24 doubles, then the slices' W rows (16 each)
+    static constexpr int MHDR = 24;
+    static constexpr int MSH = MHDR + kSxSlices * 16;    // per slice: ridge shift sh
+    static constexpr int META = MSH + kSxSlices;
     static constexpr int LUS = 16 * 17 + 8 + 4;          // shared LU fallback scratch | piv | lock
     static constexpr int SWS = 2 * 18 + 2 * 256;         // per solver warp: 2 gather bufs | 2 D stages
     static constexpr int OFF_VT = kSxNST * SD;
     static constexpr int OFF_P = OFF_VT + 16 * VTP;      // P = vtv^{-1} (16 x 16) | ||P||_inf | ok
     static constexpr int OFF_VTV = OFF_P + 264;
     static constexpr int OFF_SLOT = OFF_VTV + 16 * 18;
-    static constexpr int OFF_LU = OFF_SLOT + kSxSlots * SLOT;
+    static constexpr int OFF_META = OFF_SLOT + kSxSlots * SLOT;
+    static constexpr int OFF_LU = OFF_META + kSxNM * META;
     static constexpr int OFF_SW = OFF_LU + LUS;
     static constexpr int OFF_BAR = OFF_SW + kSxSW * SWS;
-    static constexpr int NBAR = 2 * kSxNST + 3 * kSxSlots;
+    static constexpr int NBAR = 2 * kSxNST + 2 * kSxSlots + 2 * kSxNM;
     static constexpr size_t bytes() { return 1024 + sizeof(double) * OFF_BAR + 8 * NBAR; }
     static_assert(OFF_VT % 128 == 0, "ring stages stay 1 KB aligned");
-    static_assert(SLOT % 2 == 0 && LUS % 2 == 0 && SWS % 2 == 0 && OFF_SLOT % 2 == 0 && OFF_SW % 2 == 0,
-                  "16-byte alignment");
+    static_assert(SLOT % 2 == 0 && META % 2 == 0 && LUS % 2 == 0 && SWS % 2 == 0 && OFF_SLOT % 2 == 0 &&
+                      OFF_META % 2 == 0 && OFF_SW % 2 == 0, "16-byte alignment");
 };
 static_assert(SxSmem::bytes() <= 227 * 1024, "k_smallx shared memory");
-static_assert(2 * kSxSlots * SxSmem::TILE >= 256, "G scratch");
 
 #ifdef DASH_SX_TRACE
 __device__ long long g_sxtrace[148 * 64 * 8];  // [cta][unit < 64][event]
@@ -92,14 +103,28 @@ __device__ long long g_sxtrace[148 * 64 * 8];  // [cta][unit < 64][event]
         if ((u) < 64 && blockIdx.x < 148) g_sxtrace[(blockIdx.x * 64 + (u)) * 8 + (e)] = clock64(); \
     } while (0)
 __device__ long long g_sxtrace2[64 * 8 * 8];
+#define SX_P(e)                                                                                 \
+    do {                                                                                        \
+        if (blockIdx.x == 0 && ws == 0 && lane == 0 && n_pairs <= 16) g_sxtrace2[1024 + (n_pairs - 1) * 16 + (e)] = clock64(); \
+    } while (0)
+#define SX_M(u, e)                                                                    \
+    do {                                                                              \
+        if (blockIdx.x == 0 && mb == 0 && lane == 0 && (u) < 64) g_sxtrace2[(u) * 8 + (e)] = clock64(); \
+    } while (0)
 #else
+#define SX_P(e) \
+    do {        \
+    } while (0)
+#define SX_M(u, e) \
+    do {           \
+    } while (0)
 #define SX_T(u, e) \
     do {           \
     } while (0)
 #endif
 
 struct SxParams {
-    const int4 *units;         // compacted unit list: {m0, q, a, span}
+    const int *units;          // unit records (kSxRec ints each, see k_sx_copy)
     const int *nunits;         // total units (device)
     const int64_t *row_ptr;
     const int32_t *state_row;
@@ -108,6 +133,7 @@ struct SxParams {
     const double *vtv;         // R x R (planner prologue)
     double *W, *C, *D;         // state rows
     double *U;                 // U_out (N x R)
+    double *US;                // U o w (N x R): operand of the F GEMM (k_fgemm3, which also forms G)
     double *F_slots;           // gridDim.x x J x R
     double *G_slots;           // gridDim.x x R x R
     unsigned long long *err;
@@ -126,9 +152,11 @@ struct SxPlan {
     int4 *tmp;                 // nch x kSxChunk: units of chunk c at c * kSxChunk
     int *counts;               // nch
     int *choff;                // nch + 1: exclusive scan of counts (last block)
-    int4 *units;               // compacted (k_sx_copy)
+    int *units;                // compacted unit records (k_sx_copy), kSxRec ints each
     int *nunits;
     unsigned int *done;        // last-block-done counter (reset by the last block)
+    const int32_t *state_row;
+    const uint8_t *is_new;
 };
 
 __device__ __forceinline__ void sx_prologue(const FusedPrologue &pro, const double *V, int J, int R, int blk,
@@ -260,18 +288,41 @@ __global__ void __launch_bounds__(256) k_sx_walk(SxPlan pl, FusedPrologue pro, c
     pdl_wait();
 }
 
-// one block per chunk: its units -> units[choff[c] ...]
+// one block per chunk, one thread per unit: the chunk's units -> records
+// units[(choff[c] + k) * kSxRec]: desc, unit-local row offsets, state rows, flags
 __global__ void __launch_bounds__(256) k_sx_copy(SxPlan pl) {
     pdl_wait();
     pdl_trigger();
     const int c = blockIdx.x;
     const int n = __ldcg(pl.counts + c), o = __ldcg(pl.choff + c);
-    for (int k = threadIdx.x; k < n; k += blockDim.x) pl.units[o + k] = __ldcg(pl.tmp + (int64_t)c * kSxChunk + k);
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        const int4 d = __ldcg(pl.tmp + (int64_t)c * kSxChunk + k);
+        int *rec = pl.units + (int64_t)(o + k) * kSxRec;
+        int v[kSxRec];
+#pragma unroll
+        for (int i = 0; i < kSxRec; ++i) v[i] = 0;
+        v[0] = d.x;
+        v[1] = d.y;
+        v[2] = d.z;
+        v[3] = d.w;
+#pragma unroll
+        for (int j = 0; j <= kSxSlices; ++j)
+            if (j <= d.y) v[4 + j] = (int)(pl.row_ptr[d.x + j] - d.z);
+        unsigned fb[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int j = 0; j < kSxSlices; ++j)
+            if (j < d.y) {
+                v[4 + kSxSlices + 1 + j] = pl.state_row[d.x + j];
+                fb[j >> 2] |= (pl.is_new[d.x + j] ? 1u : 0u) << (8 * (j & 3));
+            }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[4 + 2 * kSxSlices + 1 + i] = (int)fb[i];
+#pragma unroll
+        for (int i = 0; i < kSxRec / 4; ++i)
+            reinterpret_cast<int4 *>(rec)[i] = make_int4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    }
 }
 
-// ---------------------------------------------------------------------------
-// k_smallx
-// ---------------------------------------------------------------------------
 // P = vtv^{-1} (row-distributed sweep on the scaled Gram, as k_slices3), its
 // infinity norm and an ok flag -> P_s[0..255] | P_s[256] | P_s[257].  Warp-wide.
 __device__ __noinline__ void sx_inverse_vtv(const double *vtv_s, double *P_s, double *buf, int R, int sweep_only) {
@@ -395,7 +446,7 @@ __device__ __noinline__ double sx_b_fallback2(const double *vtv_s, double *buf, 
     double a[RB];
 #pragma unroll
     for (int z = 0; z < RB; ++z) {
-        const double dn = real ? lam * (fresh ? 0.0 : dstage[z * 16 + r]) + gram[z] : 0.0;
+        const double dn = real ? lam * ((fresh || z >= R) ? 0.0 : dstage[(int64_t)z * R + r]) + gram[z] : 0.0;
         a[z] = vrow[z] * dn + ((z == r) ? dg2 : 0.0);
     }
     if (need && r == 0) atomicAdd(fallbacks, 1u);
@@ -411,7 +462,9 @@ __device__ __noinline__ double sx_b_fallback2(const double *vtv_s, double *buf, 
     return wv;
 }
 
-__global__ void __launch_bounds__(kSxThreads, 1) k_smallx(const __grid_constant__ CUtensorMap tmX, SxParams p) {
+__global__ void __launch_bounds__(kSxThreads, 1) k_smallx(const __grid_constant__ CUtensorMap tm8,
+                                                          const __grid_constant__ CUtensorMap tm16,
+                                                          const __grid_constant__ CUtensorMap tm32, SxParams p) {
     using S = SxSmem;
     constexpr int RB = 16, LDV = 18;
     extern __shared__ __align__(16) double sm_raw[];
@@ -421,12 +474,14 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_smallx(const __grid_constant_
     double *P_s = sm + S::OFF_P;
     double *vtv_s = sm + S::OFF_VTV;
     double *slots = sm + S::OFF_SLOT;
+    double *metas = sm + S::OFF_META;
     double *lu = sm + S::OFF_LU;
     int *piv = reinterpret_cast<int *>(lu + 16 * 17);
     int *lu_lock = reinterpret_cast<int *>(lu + 16 * 17 + 8);
     uint64_t *bar = reinterpret_cast<uint64_t *>(sm + S::OFF_BAR);
     uint64_t *full = bar, *empty = bar + kSxNST;
-    uint64_t *uready = empty + kSxNST, *usready = uready + kSxSlots, *sfree = usready + kSxSlots;
+    uint64_t *uready = empty + kSxNST, *sfree = uready + kSxSlots;
+    uint64_t *mready = sfree + kSxSlots, *mfree = mready + kSxNM;
     const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
     const int J = p.J, R = p.R;
     const int JS = (J + 15) / 16;
@@ -435,23 +490,27 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_smallx(const __grid_constant_
     pdl_trigger();  // k_bigx_pre may fill SMs as this kernel's CTAs retire
 
     if (tid == 0) {
-        prefetch_map(&tmX);
+        prefetch_map(&tm8);
+        prefetch_map(&tm16);
+        prefetch_map(&tm32);
         for (int s = 0; s < kSxNST; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], kSxMW);
         }
         for (int s = 0; s < kSxSlots; ++s) {
             mbar_init(&uready[s], kSxMW);
-            mbar_init(&usready[s], kSxSW);
-            mbar_init(&sfree[s], kSxMW);
+            mbar_init(&sfree[s], kSxSW);
+        }
+        for (int s = 0; s < kSxNM; ++s) {
+            mbar_init(&mready[s], 1);
+            mbar_init(&mfree[s], kSxMW + kSxSW);
         }
         *lu_lock = 0;
         fence_mbar_init();
     }
-    // ring zeroed once: rows past a unit's boxes are stale but always finite; the
-    // D stages too (rows z >= R are never loaded and must read as 0)
+    // ring zeroed once: rows past a unit's boxes are stale but always finite
     for (int i = tid; i < kSxNST * S::SD; i += blockDim.x) xs[i] = 0.0;
-    for (int i = tid; i < kSxSW * S::SWS; i += blockDim.x) sm[S::OFF_SW + i] = 0.0;
+    for (int i = tid; i < kSxNM * S::META; i += blockDim.x) metas[i] = 0.0;
     for (int i = tid; i < 16 * S::VTP; i += blockDim.x) {
         const int nn = i / S::VTP, k = i % S::VTP;
         vt[i] = (nn < R && k < J) ? __ldg(p.V + k * R + nn) : 0.0;
@@ -471,33 +530,101 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_smallx(const __grid_constant_
     const int G = gridDim.x;
     const int u0 = (int)((int64_t)U * blockIdx.x / G), u1 = (int)((int64_t)U * (blockIdx.x + 1) / G);
     const int nmine = u1 - u0;
-    const int4 *units = p.units + u0;
+    const int *units = p.units + (int64_t)u0 * kSxRec;
     // item sequence of the ring (producer and math warps alike):
     // for v = 0 .. nmine + kSxLook - 1: XV(v) if v < nmine, then F(v - kSxLook) if v >= kSxLook
 
-    if (w == kSxMW + kSxSW) {  // ---------------- producer
+    if (w == kSxMW + kSxSW) {  // ---------------- TMA warp: X rows of each unit into the ring
         if (lane == 0 && nmine > 0) {
-            int64_t item = 0;
-            auto load = [&](int u) {
-                const int4 d = __ldcg(units + u);
-                const int st = (int)(item % kSxNST);
-                if (item >= kSxNST) mbar_wait_sleep(&empty[st], (uint32_t)(((item / kSxNST) - 1) & 1));
+            int4 dn = __ldcg(reinterpret_cast<const int4 *>(units));
+            for (int v = 0; v < nmine; ++v) {
+                const int4 d = dn;
+                if (v + 1 < nmine) dn = __ldcg(reinterpret_cast<const int4 *>(units + (int64_t)(v + 1) * kSxRec));
+                const int st = v % kSxNST;
+                if (v >= kSxNST) mbar_wait_sleep(&empty[st], (uint32_t)(((v / kSxNST) - 1) & 1));
+                // boxes of 32 / 16 / 8 rows covering ceil(span / 8) row blocks of 8
                 const int nb = (d.w + 7) >> 3;
-                mbar_arrive_expect_tx(&full[st], (uint32_t)(JS * nb) * 1024u);
-                for (int s = 0; s < JS; ++s)
-                    for (int b = 0; b < nb; ++b)
-                        tma_load_2d(xs + st * S::SD + s * 512 + b * 128, &tmX, 16 * s, d.z + 8 * b, &full[st]);
-                ++item;
-            };
-            for (int v = 0; v < nmine + kSxLook; ++v) {
-                if (v < nmine) {
-                    load(v);
-                    SX_T(v, 0);
+                const int rows = nb == 4 ? 32 : nb == 3 ? 24 : nb * 8;
+                mbar_arrive_expect_tx(&full[st], (uint32_t)(JS * rows) * 128u);
+                double *dst = xs + st * S::SD;
+                for (int s = 0; s < JS; ++s) {
+                    if (nb == 4) {
+                        tma_load_2d(dst + s * 512, &tm32, 16 * s, d.z, &full[st]);
+                    } else {
+                        if (nb >= 2) tma_load_2d(dst + s * 512, &tm16, 16 * s, d.z, &full[st]);
+                        if (nb != 2) tma_load_2d(dst + s * 512 + (nb == 3 ? 256 : 0), &tm8, 16 * s,
+                                                 d.z + (nb == 3 ? 16 : 0), &full[st]);
+                    }
                 }
-                if (v >= kSxLook) {
-                    load(v - kSxLook);
-                    SX_T(v - kSxLook, 1);
-                }
+                SX_T(v, 0);
+            }
+        }
+        return;
+    }
+    if (w == kSxMW + kSxSW + 1) {  // ---------------- metadata warp
+        // unit record u: lane l holds ints 2l, 2l+1 (one coalesced load per unit, issued a unit ahead)
+        auto load_rec = [&](int u) -> int2 {
+            return lane < kSxRec / 2 ? __ldcg(reinterpret_cast<const int2 *>(units + (int64_t)u * kSxRec) + lane)
+                                     : make_int2(0, 0);
+        };
+        auto rec_int = [&](int2 rv, int i) -> int {  // int i of the record (warp-wide)
+            const int2 x = make_int2(__shfl_sync(FULL_MASK, rv.x, i >> 1), __shfl_sync(FULL_MASK, rv.y, i >> 1));
+            return (i & 1) ? x.y : x.x;
+        };
+        // metadata of unit u -> meta slot u % kSxNM: the record, the slices' W rows (1.0
+        // for a new slice's pass-0 bootstrap) and ridge shifts sh = eps mean(vtv_rr s_r^2),
+        // lane = slice; plus the unit-wide "second Neumann term needed" flag (k_slices3's test)
+        auto stage = [&](int u, int2 rv) {
+            const int ms = u % kSxNM, use = u / kSxNM;
+            double *mt = metas + ms * S::META;
+            int *mi = reinterpret_cast<int *>(mt);
+            double *mw = mt + S::MHDR;
+            const int q = rec_int(rv, 1);
+            const bool act = lane < q;
+            const int wr = rec_int(rv, 4 + kSxSlices + 1 + (lane & 15));
+            const int fw = rec_int(rv, 4 + 2 * kSxSlices + 1 + ((lane & 15) >> 2));
+            const bool boot = act && ((fw >> (8 * (lane & 3))) & 0xff) != 0 && p.pass == 0;
+            double sv[16];
+#pragma unroll
+            for (int z = 0; z < 8; ++z) {
+                double2 w2 = make_double2(0.0, 0.0);
+                if (act && 2 * z < R) w2 = boot ? make_double2(1.0, 1.0)
+                                                : __ldcg(reinterpret_cast<const double2 *>(p.W + (int64_t)wr * R) + z);
+                sv[2 * z] = w2.x;
+                sv[2 * z + 1] = (2 * z + 1 < R) ? w2.y : 0.0;
+            }
+            double q4[4] = {0.0, 0.0, 0.0, 0.0};
+            double smin = INFINITY;
+#pragma unroll
+            for (int z = 0; z < 16; ++z) {
+                q4[z & 3] = fma(vtv_s[z * LDV + z] * sv[z], sv[z], q4[z & 3]);
+                if (z < R) smin = fmin(smin, sv[z] * sv[z]);
+            }
+            const double sh = p.eps * ((q4[0] + q4[1]) + (q4[2] + q4[3])) / R;
+            const double rho = sh * (1.0 / smin) * pnorm;  // s_r = 0 -> inf; non-finite s -> non-finite sh
+            const bool need2 = act && pok && rho <= kS3Neumann && !(rho <= kS3Neumann1);
+            const int any2 = __any_sync(FULL_MASK, need2) ? 1 : 0;
+            if (use >= 1) mbar_wait_sleep(&mfree[ms], (uint32_t)((use - 1) & 1));
+            if (lane < kSxRec / 2) {
+                int2 hv = rv;
+                if (lane == (4 + 2 * kSxSlices + 1 + 4) / 2) hv.y = any2;  // int 41
+                reinterpret_cast<int2 *>(mi)[lane] = hv;
+            }
+            if (act) {
+#pragma unroll
+                for (int z = 0; z < 8; ++z)
+                    *reinterpret_cast<double2 *>(mw + lane * 16 + 2 * z) = make_double2(sv[2 * z], sv[2 * z + 1]);
+                mt[S::MSH + lane] = sh;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&mready[ms]);
+        };
+        if (nmine > 0) {
+            int2 rnext = load_rec(0);
+            for (int v = 0; v < nmine; ++v) {
+                const int2 rcur = rnext;
+                if (v + 1 < nmine) rnext = load_rec(v + 1);
+                stage(v, rcur);
             }
         }
         return;
@@ -512,39 +639,15 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_smallx(const __grid_constant_
         for (int kk = 0; kk < 4; ++kk)
 #pragma unroll
             for (int nb = 0; nb < 2; ++nb) pf[kk][nb] = P_s[(8 * nb + g) * 16 + 8 * (kk >> 1) + 2 * t + (kk & 1)];
-        double facc[2][4][2];
-#pragma unroll
-        for (int q = 0; q < 2; ++q)
-#pragma unroll
-            for (int k = 0; k < 4; ++k) facc[q][k][0] = facc[q][k][1] = 0.0;
-        double gacc[2] = {0.0, 0.0};  // G = sum US^T US: block (w >> 1, w & 1)
-        const int gmi = mb >> 1, gni = mb & 1;
         int64_t item = 0;
-        for (int v = 0; v < nmine + kSxLook; ++v) {
-            if (v < nmine) {  // ---- XV(v), Y, the Neumann U of this warp's 8 rows
-                const int u = v, slot = u % kSxSlots, use = u / kSxSlots;
-                // the row's slice, its W row and ridge terms (loads in flight during the XV MMAs)
-                const int4 d = __ldcg(units + u);
-                const int m0 = d.x, q = d.y, a0 = d.z, span = d.w;
-                const int l_rp = lane <= q ? (int)(__ldg(p.row_ptr + m0 + lane) - a0) : (1 << 30);
-                int j = 0;
-                for (int k = 1; k <= q; ++k) j += (__shfl_sync(FULL_MASK, l_rp, k) <= xrow) ? 1 : 0;
-                const bool valid = xrow < span;
-                const int m = m0 + (valid ? j : 0);
-                const int wrow = __ldg(p.state_row + m);
-                const bool boot = __ldg(p.is_new + m) != 0 && p.pass == 0;  // new slice: W bootstrap 1
-                double sv[RB];
-#pragma unroll
-                for (int z = 0; z < RB / 2; ++z) {
-                    double2 w2 = make_double2(0.0, 0.0);
-                    if (valid && 2 * z < R) w2 = boot ? make_double2(1.0, 1.0) : __ldcg(reinterpret_cast<const double2 *>(p.W + (int64_t)wrow * R) + z);
-                    sv[2 * z] = w2.x;
-                    sv[2 * z + 1] = w2.y;
-                }
+        for (int v = 0; v < nmine; ++v) {
+            {  // ---- XV(v), Y, the Neumann U of this warp's 8 rows
+                const int u = v, slot = u % kSxSlots, use = u / kSxSlots, ms = u % kSxNM;
                 const int st = (int)(item % kSxNST);
                 mbar_wait_sleep(&full[st], (uint32_t)((item / kSxNST) & 1));
                 ++item;
                 if (mb == 0 && lane == 0) SX_T(u, 2);
+                SX_M(u, 0);
                 const double *xt = xs + st * S::SD;
                 double xa[2][2][2];
 #pragma unroll
@@ -574,40 +677,34 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_smallx(const __grid_constant_
                 for (int nb = 0; nb < 2; ++nb)
 #pragma unroll
                     for (int e = 0; e < 2; ++e) xv[nb][e] = xa[nb][0][e] + xa[nb][1][e];
-                // ridge terms of the row's slice (k_slices3's Neumann test):
-                // sh = eps mean(vtv_rr s_r^2); d_r = sh / s_r^2; rho = max_r d_r * ||P||
-                double sh;
-                {
-                    double q4[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-                    for (int z = 0; z < RB; ++z) q4[z & 3] = fma(vtv_s[z * LDV + z] * sv[z], sv[z], q4[z & 3]);
-                    sh = p.eps * ((q4[0] + q4[1]) + (q4[2] + q4[3])) / R;
-                }
-                double qmax = 0.0;
-#pragma unroll
-                for (int z = 0; z < RB; ++z) {
-                    if (z < R) {
-                        const double is = rcp_nr(sv[z]);
-                        const double qz = is * is;
-                        qmax = (sv[z] != 0.0 && isfinite(qz)) ? fmax(qmax, qz) : INFINITY;
-                    }
-                }
-                const double rho = sh * qmax * pnorm;
-                const bool need2 = valid && pok && rho <= kS3Neumann && !(rho <= kS3Neumann1);
+                SX_M(u, 1);
+                // the row's slice and its W row (staged by the producer)
+                mbar_wait_sleep(&mready[ms], (uint32_t)((u / kSxNM) & 1));
+                SX_M(u, 2);
+                const double *mt = metas + ms * S::META;
+                const int *mi = reinterpret_cast<const int *>(mt);
+                const int q = mi[1], span = mi[3];
+                int j = 0;
+                for (int k = 1; k < q; ++k) j += (mi[4 + k] <= xrow) ? 1 : 0;
+                const bool valid = xrow < span;
+                const double *sw = mt + S::MHDR + j * 16;
+                const double sh = valid ? mt[S::MSH + j] : 0.0;
+                const int any2 = mi[4 + 2 * kSxSlices + 1 + 4];
                 double dd[2][2], si[2][2];
 #pragma unroll
-                for (int nb = 0; nb < 2; ++nb)
+                for (int nb = 0; nb < 2; ++nb) {
+                    const double2 s2 = *reinterpret_cast<const double2 *>(sw + 8 * nb + 2 * t);
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
                         const int c = 8 * nb + 2 * t + e;
-                        double sc = 0.0;
-#pragma unroll
-                        for (int z = 0; z < RB; ++z)
-                            if (z == c) sc = sv[z];
-                        const double is = (valid && c < R) ? rcp_nr(sc) : 0.0;
+                        const double is = (valid && c < R) ? rcp_nr(e ? s2.y : s2.x) : 0.0;
                         si[nb][e] = is;
-                        dd[nb][e] = valid ? sh * is * is : 0.0;
+                        dd[nb][e] = sh * is * is;
                     }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&mfree[ms]);  // last read of the metadata slot
+                SX_M(u, 3);
                 // Y = XV P: A fragment of K step kk = this lane's XV value xv[kk >> 1][kk & 1]
                 double ya[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
@@ -621,16 +718,18 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_smallx(const __grid_constant_
                     for (int nb = 0; nb < 2; ++nb)
                         dmma884(c1[nb], ya[kk >> 1][kk & 1] * dd[kk >> 1][kk & 1], pf[kk][nb]);  // (Y o d) P
                 double c2[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-                if (__any_sync(FULL_MASK, need2)) {
+                if (any2) {  // unit-uniform
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk)
 #pragma unroll
                         for (int nb = 0; nb < 2; ++nb)
                             dmma884(c2[nb], c1[kk >> 1][kk & 1] * dd[kk >> 1][kk & 1], pf[kk][nb]);
                 }
+                SX_M(u, 4);
                 double *sl = slots + slot * S::SLOT;
                 double *xvt = sl, *ut = sl + S::TILE;
-                if (use >= 1) mbar_wait_sleep(&sfree[slot], (uint32_t)((use - 1) & 1));  // F(u - kSxSlots) done
+                if (use >= 1) mbar_wait_sleep(&sfree[slot], (uint32_t)((use - 1) & 1));  // solvers done with u - kSxSlots
+                SX_M(u, 5);
 #pragma unroll
                 for (int nb = 0; nb < 2; ++nb) {
                     *reinterpret_cast<double2 *>(xvt + xrow * kSxTP + 8 * nb + 2 * t) = make_double2(xv[nb][0], xv[nb][1]);
@@ -642,101 +741,64 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_smallx(const __grid_constant_
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&uready[slot]);
                 if (mb == 0 && lane == 0) SX_T(u, 3);
+                SX_M(u, 6);
             }
-            if (v >= kSxLook) {  // ---- F(v - kSxLook) += X^T US;  G += US^T US
-                const int u = v - kSxLook, slot = u % kSxSlots, use = u / kSxSlots;
-                const int st = (int)(item % kSxNST);
-                mbar_wait_sleep(&full[st], (uint32_t)((item / kSxNST) & 1));
-                ++item;
-                mbar_wait_sleep(&usready[slot], (uint32_t)(use & 1));
-                const double *xt = xs + st * S::SD;
-                const double *ub = slots + slot * S::SLOT + S::TILE;
-#pragma unroll
-                for (int kk = 0; kk < kSxRows / 4; ++kk) {
-                    const int row = 4 * kk + t;
-                    const double2 bu = *reinterpret_cast<const double2 *>(ub + row * kSxTP + 2 * pg);
-#pragma unroll
-                    for (int q = 0; q < 2; ++q) {
-                        const int s = mb + 4 * q;
-                        if (s < JS) {
-                            const double2 a = *reinterpret_cast<const double2 *>(xt + s * 512 + swz(row, pg));
-                            dmma884(facc[q][0], a.x, bu.x);
-                            dmma884(facc[q][1], a.x, bu.y);
-                            dmma884(facc[q][2], a.y, bu.x);
-                            dmma884(facc[q][3], a.y, bu.y);
-                        }
-                    }
-                    dmma884(gacc, ub[row * kSxTP + 8 * gmi + g], ub[row * kSxTP + 8 * gni + g]);
-                }
-                __syncwarp();
-                if (lane == 0) {
-                    mbar_arrive(&empty[st]);
-                    mbar_arrive(&sfree[slot]);
-                }
-                if (mb == 0 && lane == 0) SX_T(u, 7);
-            }
-        }
-        // F slot of this CTA (every entry written by exactly one lane; zeros if no units)
-        double *fs = p.F_slots + (int64_t)blockIdx.x * J * R;
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            const int s = mb + 4 * q;
-            if (s < JS) {
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int j = 16 * s + 2 * pg + (k >> 1);
-#pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        const int r = 2 * qperm(2 * t + e) + (k & 1);
-                        if (j < J && r < R) fs[(int64_t)j * R + r] = facc[q][k][e];
-                    }
-                }
-            }
-        }
-        // G slot of this CTA: block (gmi, gni) of sum US^T US (= sum_k gram_k o w_k w_k^T)
-        double *gs = p.G_slots + (int64_t)blockIdx.x * R * R;
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            const int a = 8 * gmi + g, b = 8 * gni + 2 * t + e;
-            if (a < R && b < R) gs[a * R + b] = gacc[e];
         }
         return;
     }
     // ---------------- solver warps: slice pairs round-robin over the unit sequence
     const int ws = w - kSxMW;
     const int r = lane & 15, gl = lane >> 4;
-    double *wsm = sm + S::OFF_SW + ws * S::SWS;
-    double *buf = wsm + gl * 18;
-    double *dstage = wsm + 36 + gl * 256;  // this group's D block (column r at [z * 16 + r]; rows >= R stay 0)
+    double *buf = sm + S::OFF_SW + ws * S::SWS + gl * 18;
+    double *dstage = sm + S::OFF_SW + ws * S::SWS + 36 + gl * 256;  // the pair's D block, column r at [z * 16 + r]
     const double *vrow = vtv_s + r * LDV;
     int pc = 0;  // pairs of the units before this one
+#ifdef DASH_SX_TRACE
+    long long t_busy = 0, t_wait = 0, n_pairs = 0, t_start = clock64();
+#endif
     for (int u = 0; u < nmine; ++u) {
-        const int slot = u % kSxSlots, use = u / kSxSlots;
-        const int4 d = __ldcg(units + u);
-        const int m0 = d.x, q = d.y, a0 = d.z;
+        const int slot = u % kSxSlots, use = u / kSxSlots, ms = u % kSxNM;
+        mbar_wait_sleep(&mready[ms], (uint32_t)((u / kSxNM) & 1));
+        const double *mt = metas + ms * S::META;
+        const int *mi = reinterpret_cast<const int *>(mt);
+        const uint8_t *mf = reinterpret_cast<const uint8_t *>(mi + 4 + 2 * kSxSlices + 1);
+        const int m0 = mi[0], q = mi[1], a0 = mi[2];
         const int np = (q + 1) >> 1;
         const int k0 = ((ws - pc) % kSxSW + kSxSW) % kSxSW;  // my first pair of this unit
         pc += np;
-        mbar_wait_sleep(&uready[slot], (uint32_t)(use & 1));
-        if (lane == 0 && k0 < np) SX_T(u, 5);
-        double *xvt = slots + slot * S::SLOT, *ut = xvt + S::TILE;
+        bool waited = false;
         for (int k = k0; k < np; k += kSxSW) {
+#ifdef DASH_SX_TRACE
+            const long long tp0 = clock64();
+            ++n_pairs;
+#endif
+            SX_P(0);
             const int j = 2 * k + gl;
             const bool act = j < q;
             const bool real = act && r < R;
             const int m = m0 + (act ? j : 0);
-            const int64_t rg = __ldg(p.row_ptr + m);
-            const int n = act ? (int)(__ldg(p.row_ptr + m + 1) - rg) : 0;
-            const int rb = (int)(rg - a0);
-            const int wrow = __ldg(p.state_row + m);
-            const bool fresh = __ldg(p.is_new + m) != 0;
-            // state: D block -> dstage (async), c_old and s into registers
-            if (real && !fresh) {
+            const int rb = act ? mi[4 + j] : 0;
+            const int n = act ? mi[4 + j + 1] - rb : 0;
+            const int64_t rg = (int64_t)a0 + rb;
+            const int wrow = act ? mi[4 + kSxSlices + 1 + j] : 0;
+            const bool fresh = act && mf[j] != 0;
+            const double s_r = real ? mt[S::MHDR + j * 16 + r] : 0.0;
+            // state (latency overlaps the rows loop): c_old, D column r
+            // state: D block -> dstage (cp.async, waited for after the rows loop), c_old
+            const bool ld = real && !fresh;
+            double cold = 0.0;
+            if (ld) {
                 const double *dcol = p.D + (int64_t)wrow * R * R + r;
                 for (int z = 0; z < R; ++z) cp_async8(dstage + z * 16 + r, dcol + (int64_t)z * R);
+                cold = __ldcg(p.C + (int64_t)wrow * R + r);
             }
-            const double cold = (real && !fresh) ? __ldcg(p.C + (int64_t)wrow * R + r) : 0.0;
-            const double s_r = real ? ((fresh && p.pass == 0) ? 1.0 : __ldcg(p.W + (int64_t)wrow * R + r)) : 0.0;
+            if (!waited) {
+                mbar_wait_sleep(&uready[slot], (uint32_t)(use & 1));
+                waited = true;
+                if (lane == 0) SX_T(u, 5);
+            }
+            SX_P(1);
+            double *xvt = slots + slot * S::SLOT, *ut = xvt + S::TILE;
             int nmax = n;
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) nmax = max(nmax, __shfl_xor_sync(FULL_MASK, nmax, off));
@@ -760,6 +822,7 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_smallx(const __grid_constant_
                 const double rho = sh * qm * pnorm;
                 fast = act && pok && rho <= kS3Neumann;
             }
+            SX_P(2);
             if (__any_sync(FULL_MASK, act && !fast)) {  // rare: exact A solve; serialised LU scratch
                 if (lane == 0)
                     while (atomicCAS(lu_lock, 0, 1) != 0) __nanosleep(64);
@@ -769,6 +832,7 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_smallx(const __grid_constant_
                 __syncwarp();
                 if (lane == 0) atomicExch(lu_lock, 0);
             }
+            SX_P(3);
             // ---- rows: U -> U_out, c, gram (_kernels.py:98-115)
             double c = 0.0, gram[RB];
 #pragma unroll
@@ -791,23 +855,26 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_smallx(const __grid_constant_
                 }
             }
             // ---- c, D accumulation and the S-row system (_kernels.py:103-135)
+            SX_P(4);
             const double cn = real ? p.lam * cold + c : 0.0;
-            cp_async_wait();
-            __syncwarp();
             double a[RB];
             double drr = 0.0;
+            cp_async_wait();
+            __syncwarp();
 #pragma unroll
             for (int z = 0; z < RB; ++z) {
-                const double dn = real ? p.lam * ((fresh) ? 0.0 : dstage[z * 16 + r]) + gram[z] : 0.0;
+                const double dn = real ? p.lam * ((ld && z < R) ? dstage[z * 16 + r] : 0.0) + gram[z] : 0.0;
                 a[z] = dn;  // D_new row r (rows / columns >= R are 0)
                 if (z == r) drr = dn;
             }
+            SX_P(5);
             if (real && p.final_pass) {
                 p.C[(int64_t)wrow * R + r] = cn;
 #pragma unroll
                 for (int z = 0; z < RB; ++z)
                     if (z < R) p.D[(int64_t)wrow * R * R + (int64_t)z * R + r] = a[z];
             }
+            SX_P(6);
             double sh2;
             {
                 double vdd[RB];
@@ -820,8 +887,10 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_smallx(const __grid_constant_
             const double dg2 = real ? sh2 : 1.0;
 #pragma unroll
             for (int z = 0; z < RB; ++z) a[z] = vrow[z] * a[z] + ((z == r) ? dg2 : 0.0);
+            SX_P(7);
             double wv;
             const bool okB = gj_solve<RB>(a, cn, buf, r, wv);
+            SX_P(8);
             if (!real) wv = 0.0;
             bool gok = okB && isfinite(wv);
             {
@@ -832,23 +901,41 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_smallx(const __grid_constant_
                 if (lane == 0)
                     while (atomicCAS(lu_lock, 0, 1) != 0) __nanosleep(64);
                 __syncwarp();
-                wv = sx_b_fallback2(vtv_s, buf, lu, piv, dstage, ut, rb, n, p.lam, fresh, sh2, cn, wv, R,
-                                    !gok && act, real, m, p.err, p.fallbacks);
+                wv = sx_b_fallback2(vtv_s, buf, lu, piv, p.D + (int64_t)wrow * R * R, ut, rb, n, p.lam, fresh,
+                                    sh2, cn, wv, R, !gok && act, real, m, p.err, p.fallbacks);
                 __syncwarp();
                 if (lane == 0) atomicExch(lu_lock, 0);
             }
-            if (real) p.W[(int64_t)wrow * R + r] = wv;
-            __syncwarp();  // every lane's row reads are done before US overwrites the tile
-            for (int i = 0; i < n; ++i) ut[(rb + i) * kSxTP + r] *= wv;  // padded lanes: wv = 0
+            SX_P(9);
+            if (real) {
+                p.W[(int64_t)wrow * R + r] = wv;
+                for (int i = 0; i < n; ++i) p.US[(rg + i) * R + r] = ut[(rb + i) * kSxTP + r] * wv;
+            }
+            SX_P(10);
+#ifdef DASH_SX_TRACE
+            t_busy += clock64() - tp0;
+#endif
         }
+        if (!waited) mbar_wait_sleep(&uready[slot], (uint32_t)(use & 1));
         __syncwarp();
-        if (lane == 0) mbar_arrive(&usready[slot]);
+        if (lane == 0) {
+            mbar_arrive(&mfree[ms]);
+            mbar_arrive(&sfree[slot]);
+        }
         if (lane == 0 && k0 < np) SX_T(u, 6);
     }
+#ifdef DASH_SX_TRACE
+    if (blockIdx.x == 0 && lane == 0) {
+        g_sxtrace2[512 + ws * 4 + 0] = t_busy;
+        g_sxtrace2[512 + ws * 4 + 1] = n_pairs;
+        g_sxtrace2[512 + ws * 4 + 2] = clock64() - t_start;
+    }
+#endif
 }
 
-int launch_smallx(dash_ctx *ctx, cudaStream_t st, const CUtensorMap &map8, const SxParams &sp, int grid) {
+int launch_smallx(dash_ctx *ctx, cudaStream_t st, const CUtensorMap &m8, const CUtensorMap &m16,
+                  const CUtensorMap &m32, const SxParams &sp, int grid) {
     const size_t smem = SxSmem::bytes();
     ensure_smem_attr(k_smallx, smem);
-    return launch_k(pdl_site("smallx"), k_smallx, grid, kSxThreads, smem, st, map8, sp);
+    return launch_k(pdl_site("smallx"), k_smallx, grid, kSxThreads, smem, st, m8, m16, m32, sp);
 }

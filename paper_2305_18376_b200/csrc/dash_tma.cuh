@@ -194,7 +194,8 @@ template <int MAXS>
 __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_fgemm3(const __grid_constant__ CUtensorMap tmX,
                                                              const __grid_constant__ CUtensorMap tmU, int64_t N, int J,
                                                              int R, double *__restrict__ F_slots,
-                                                             const uint32_t *__restrict__ tflag, uint32_t tgen) {
+                                                             const uint32_t *__restrict__ tflag, uint32_t tgen,
+                                                             double *__restrict__ G_slots = nullptr) {
     extern __shared__ __align__(16) double sm_raw[];
     double *sm = align1k(sm_raw);
     const int JS = TmaSmem::strips(J);
@@ -245,6 +246,11 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_fgemm3(const __grid_consta
     for (int q = 0; q < MAXS; ++q)
 #pragma unroll
         for (int k = 0; k < 4; ++k) acc[q][k][0] = acc[q][k][1] = 0.0;
+    // optional G = sum US^T US (the fused small-slice path: sum_k gram_k o w_k w_k^T
+    // over the small slices), block (w >> 1, w & 1) on warps 0..3
+    const bool gw = G_slots != nullptr && w < 4;
+    const int gmi = w >> 1, gni = w & 1;
+    double gacc[2] = {0.0, 0.0};
     unsigned vm = 0;
     for (int64_t i = 0, k = -1; i < mine; ++i) {
         if ((i & 31) == 0) vm = visit_mask(tflag, tgen, i, mine);
@@ -257,6 +263,10 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_fgemm3(const __grid_consta
 #pragma unroll
         for (int kk = 0; kk < kTR / 4; ++kk) {
             const int row = 4 * kk + t;
+            if (gw) {
+                const int ca = 8 * gmi + g, cb = 8 * gni + g;
+                dmma884(gacc, ut[swz(row, ca >> 1) + (ca & 1)], ut[swz(row, cb >> 1) + (cb & 1)]);
+            }
             const double2 b = *reinterpret_cast<const double2 *>(ut + swz(row, pg));  // US[row][2pg], [2pg+1]
 #pragma unroll
             for (int q = 0; q < MAXS; ++q) {
@@ -287,6 +297,14 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) k_fgemm3(const __grid_consta
                     if (j < J && r < R) slot[j * R + r] = acc[q][k][e];
                 }
             }
+        }
+    }
+    if (gw) {
+        double *gs = G_slots + (int64_t)blockIdx.x * R * R;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int a = 8 * gmi + g, b = 8 * gni + 2 * t + e;
+            if (a < R && b < R) gs[a * R + b] = gacc[e];
         }
     }
 }

@@ -1402,20 +1402,21 @@ int launch_xv3(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, c
 
 template <int MAXS>
 void launch_f3_t(dash_ctx *ctx, cudaStream_t st, const CUtensorMap &mx, const CUtensorMap &mu, int64_t N, int J,
-                 int R, double *F_slots, const uint32_t *tflag) {
+                 int R, double *F_slots, const uint32_t *tflag, double *G_slots) {
     const size_t smem = TmaSmem::f_bytes(J);
     ensure_smem_attr(k_fgemm3<MAXS>, smem);
     PhaseScope ps(ctx, st, PH_FGEMM);
-    launch_k(true, k_fgemm3<MAXS>, ctx->num_sms, kCW * 32 + 32, smem, st, mx, mu, N, J, R, F_slots, tflag,
-             ctx->tgen);
+    launch_k(pdl_site("f3"), k_fgemm3<MAXS>, ctx->num_sms, kCW * 32 + 32, smem, st, mx, mu, N, J, R, F_slots, tflag,
+             ctx->tgen, G_slots);
 }
 
+// F slots (and, with G_slots, the G slots of sum US^T US) over the tiles marked in tflag
 int launch_f3(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, const double *US, int R,
-              double *F_slots, const uint32_t *tflag = nullptr) {
+              double *F_slots, const uint32_t *tflag = nullptr, double *G_slots = nullptr) {
     CUtensorMap mx, mu;
     if (!make_box_map(&mx, b->X, J, b->N, b->ldx) || !make_box_map(&mu, US, R, b->N, R)) return DASH_E_CUDA;
-    if (TmaSmem::strips(J) <= kCW) launch_f3_t<1>(ctx, st, mx, mu, b->N, J, R, F_slots, tflag);
-    else launch_f3_t<2>(ctx, st, mx, mu, b->N, J, R, F_slots, tflag);
+    if (TmaSmem::strips(J) <= kCW) launch_f3_t<1>(ctx, st, mx, mu, b->N, J, R, F_slots, tflag, G_slots);
+    else launch_f3_t<2>(ctx, st, mx, mu, b->N, J, R, F_slots, tflag, G_slots);
     return 0;
 }
 
@@ -1532,14 +1533,17 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
                         BigxSmemT<typename std::conditional<f32, float, double>::type>::bytes(J) <= 227 * 1024;
             // fused small-slice kernel: same eligibility as the fused big path (FP64, R
             // bucket 16 and even, J <= 128, tensor-map X); big slices then need k_bigx
-            static const bool no_smallx = getenv("DASH_NO_SMALLX") != nullptr;  // A/B switch
-            ctx->smallx = !f32 && !no_smallx && !no_bigx && ctx->tma && pl.big_dev && J <= 128 &&
+            // opt-in (DASH_SMALLX=1): measured slower than k_xv3 -> k_slices3 -> k_fgemm3 on the
+            // large config (0.72 vs 0.58 ms / update; latency-bound solver warps and an
+            // instruction footprint beyond the 32 KB L1.5 I-cache)
+            static const bool use_smallx = getenv("DASH_SMALLX") != nullptr;
+            ctx->smallx = !f32 && use_smallx && !no_bigx && ctx->tma && pl.big_dev && J <= 128 &&
                           (ctx->bigx || pl.gbig == 0);
             ctx->sx_grid = ctx->smallx ? ctx->num_sms : 0;
             if (ctx->smallx) {
                 const int nch = std::max(1, (M + kSxChunk - 1) / kSxChunk);
                 if (ensure(ctx->sx_tmp, sizeof(int4) * (size_t)nch * kSxChunk) ||
-                    ensure(ctx->sx_units, sizeof(int4) * (size_t)std::max(M, 1))) return DASH_E_CUDA;
+                    ensure(ctx->sx_units, sizeof(int) * kSxRec * (size_t)std::max(M, 1))) return DASH_E_CUDA;
                 if (ctx->sx_meta.cap < sizeof(int) * (2 * (size_t)nch + 8)) {
                     if (ensure(ctx->sx_meta, sizeof(int) * (2 * (size_t)nch + 8))) return DASH_E_CUDA;
                     cudaMemsetAsync(ctx->sx_meta.p, 0, ctx->sx_meta.cap, st);  // done counter starts at 0
@@ -1548,7 +1552,7 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
             ctx->bigx_nbig = ctx->bigx ? pl.gbig : 0;
             ctx->bigx_grid = ctx->bigx ? (int)std::min<int64_t>(ctx->num_sms, pl.big_tiles) : 0;
             if (ctx->smallx) ctx->nitems = ctx->sx_grid + pl.gbig;  // G slots: one per small-kernel CTA + big slice
-            if (ctx->bigx && !ctx->smallx) {
+            if (ctx->bigx) {
                 const size_t tb = sizeof(uint32_t) * (size_t)((N + kTR - 1) / kTR + 16);
                 if (ctx->tflag.cap < tb) {  // zeroed once: marks are generation-tagged
                     if (ensure(ctx->tflag, tb)) return DASH_E_CUDA;
@@ -1571,13 +1575,13 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
             ensure(ctx->fslots, sizeof(double) * (ctx->nsplit + ctx->bigx_nbig) * J * R) ||
             ensure(ctx->vtv, sizeof(double) * R * R) ||
             ensure(ctx->fsnap, sizeof(double) * J * R) || ensure(ctx->gsnap, sizeof(double) * R * R) ||
-            (ctx->stream && ensure(ctx->us, sizeof(double) * std::max<int64_t>(N, 1) * R)) ||
+            ((ctx->stream || ctx->smallx) && ensure(ctx->us, sizeof(double) * std::max<int64_t>(N, 1) * R)) ||
             (f32 && ensure(ctx->u64, sizeof(double) * std::max<int64_t>(N, 1) * R)))
             return DASH_E_CUDA;
         if (!items.empty() && stage_items(ctx, st, items)) return DASH_E_CUDA;
         ctx->planned = plan_of(ctx).split && M > 0 && N > 0 && (!ctx->smallx || ctx->bigx);
         if (ctx->planned &&
-            device_plan(ctx, st, b, (ctx->bigx && !ctx->smallx) ? (uint32_t *)ctx->tflag.p : nullptr))
+            device_plan(ctx, st, b, ctx->bigx ? (uint32_t *)ctx->tflag.p : nullptr))
             return DASH_E_CUDA;
         if (M > 0 && !ctx->stream) {  // row -> slice map: only the generic F GEMM needs it
             PhaseScope ps(ctx, st, PH_ROWSLICE);
@@ -1594,8 +1598,8 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
         const int nch = pass == 0 ? std::max(1, (M + kSxChunk - 1) / kSxChunk) : 0;
         int *sxm = (int *)ctx->sx_meta.p;
         const int nch_all = std::max(1, (M + kSxChunk - 1) / kSxChunk);
-        SxPlan pl{b->row_ptr, M, nch, (int4 *)ctx->sx_tmp.p, sxm, sxm + nch_all, (int4 *)ctx->sx_units.p,
-                  sxm + 2 * nch_all + 1, (unsigned int *)(sxm + 2 * nch_all + 2)};
+        SxPlan pl{b->row_ptr, M, nch, (int4 *)ctx->sx_tmp.p, sxm, sxm + nch_all, (int *)ctx->sx_units.p,
+                  sxm + 2 * nch_all + 1, (unsigned int *)(sxm + 2 * nch_all + 2), b->state_row, b->is_new};
         const FusedPrologue pro{(double *)ctx->vtv.p, s->F, s->G, (double *)ctx->fsnap.p, (double *)ctx->gsnap.p,
                                 v_used_out, pass == 0, last};
         {
@@ -1610,17 +1614,19 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
                 if (launch_k(pdl_site("sxcopy"), k_sx_copy, nch, 256, 0, st, pl)) return DASH_E_CUDA;
             }
         }
-        CUtensorMap m8;
-        if (!make_box_map(&m8, b->X, J, b->N, b->ldx, 8)) return DASH_E_CUDA;
-        SxParams sp{(const int4 *)ctx->sx_units.p, sxm + 2 * nch_all + 1, b->row_ptr, b->state_row, b->is_new,
+        CUtensorMap m8, m16, m32;
+        if (!make_box_map(&m8, b->X, J, b->N, b->ldx, 8) || !make_box_map(&m16, b->X, J, b->N, b->ldx, 16) ||
+            !make_box_map(&m32, b->X, J, b->N, b->ldx, 32))
+            return DASH_E_CUDA;
+        SxParams sp{(const int *)ctx->sx_units.p, sxm + 2 * nch_all + 1, b->row_ptr, b->state_row, b->is_new,
                     s->V, (const double *)ctx->vtv.p, s->W, s->C, s->D, (double *)(void *)U_out,
-                    (double *)ctx->fslots.p, (double *)ctx->gslots.p, ctx->err, ctx->fallbacks, J, R,
-                    s->forgetting, eps, pass, last, 0};
+                    (double *)ctx->us.p, (double *)ctx->fslots.p, (double *)ctx->gslots.p, ctx->err,
+                    ctx->fallbacks, J, R, s->forgetting, eps, pass, last, 0};
         static const bool sweep_only = getenv("DASH_S3_SWEEP") != nullptr;
         sp.sweep_only = sweep_only ? 1 : 0;
         {
             PhaseScope ps(ctx, st, PH_SLICES);
-            if (launch_smallx(ctx, st, m8, sp, ctx->sx_grid)) return DASH_E_CUDA;
+            if (launch_smallx(ctx, st, m8, m16, m32, sp, ctx->sx_grid)) return DASH_E_CUDA;
         }
     }
     if (!fused_pro) {
@@ -1682,7 +1688,7 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
                 bp.Co = s->C;
                 bp.D = s->D;
                 bp.U = Ud;
-                bp.US = ctx->smallx ? nullptr : (double *)ctx->us.p;
+                bp.US = (double *)ctx->us.p;
                 bp.ms = (double *)ctx->bx_ms.p;
                 bp.toff = (int *)ctx->bx_toff.p;
                 bp.parts = (double *)ctx->bx_parts.p;
@@ -1699,12 +1705,16 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
                 bp.eps = eps;
                 bp.pass = pass;
                 bp.final_pass = last;
-                bp.post_wait = ctx->smallx ? 1 : 0;
+                bp.post_wait = 0;  // the F GEMM runs between k_bigx and k_bigx_post (it waits for k_bigx)
                 if (launch_bigx(ctx, st, b, bp)) return DASH_E_CUDA;
             }
         }
         if (ctx->smallx) {
-            // F of the small slices: k_smallx's per-CTA slots
+            // F and G of the small slices: X^T US and US^T US over the small-slice tiles
+            if constexpr (!f32)
+                if (launch_f3(ctx, st, b, J, (const double *)ctx->us.p, R, Fsl,
+                              ctx->bigx ? (const uint32_t *)ctx->tflag.p : nullptr, Gsl))
+                    return DASH_E_CUDA;
         } else if (ctx->tma) {
             if (launch_f3(ctx, st, b, J, (const double *)ctx->us.p, R, Fsl,
                           ctx->bigx ? (const uint32_t *)ctx->tflag.p : nullptr))
