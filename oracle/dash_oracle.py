@@ -410,3 +410,12 @@ def local_error(batch_items, u_new, W_rows, V):
         rec = (u_new[sid] * W_rows[sid]) @ V.T
         per[sid] = float(np.abs(rows - rec).mean())
     return float(np.mean([per[sid] for sid, _ in batch_items])), per
+
+
+def global_error(old_data, old_factors, new_data, new_factors, w_rows, V):
+    """evaluate.py:121-144: mean over old slices of mean|rows - (U o w) V^T|
+    with the stored old row factors, plus the same over the newest batch."""
+    def term(data, factors):
+        vals = [float(np.abs(rows - (factors[sid] * w_rows[sid]) @ V.T).mean()) for sid, rows in data.items()]
+        return float(np.mean(vals)) if vals else 0.0
+    return term(old_data, old_factors) + term(new_data, new_factors)

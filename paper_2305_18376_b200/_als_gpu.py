@@ -23,9 +23,17 @@ F64 = torch.float64
 
 def parafac2_als_gpu(tensor, rank: int, iters: int = 10, seed: int = 0, tol: float = 1e-8,
                      return_info: bool = False, device=None):
-    slices = list(tensor.slices)
-    J = tensor.column_count
-    min_rows = min(s.row_count for s in slices)
+    from .history import DeviceTensor
+    dev_tensor = isinstance(tensor, DeviceTensor)
+    if dev_tensor:  # accumulated data already in HBM (history.py): no host round trip
+        ids_all = list(tensor.slice_ids)
+        counts = np.diff(tensor.row_ptr)
+        J = tensor.column_count
+        min_rows = int(counts.min()) if len(counts) else 0
+    else:
+        slices = list(tensor.slices)
+        J = tensor.column_count
+        min_rows = min(s.row_count for s in slices)
     if rank > min(J, min_rows):
         raise ValueError(f"rank {rank} exceeds min(columns, shortest slice) = {min(J, min_rows)}")
     if iters < 1:
@@ -34,15 +42,19 @@ def parafac2_als_gpu(tensor, rank: int, iters: int = 10, seed: int = 0, tol: flo
         raise ValueError(f"rank {rank} exceeds the ALS engine's maximum {nat.MAX_RANK_ALS}")
     from .stream import _dev
     dev = _dev(device)
-    K = len(slices)
+    K = len(tensor.slice_ids) if dev_tensor else len(slices)
     rng = np.random.default_rng(seed)
     V0 = rng.uniform(size=(J, rank))
     H0 = rng.uniform(size=(rank, rank))
-    counts = np.array([s.row_count for s in slices], dtype=np.int64)
-    row_ptr = np.zeros(K + 1, dtype=np.int64)
-    np.cumsum(counts, out=row_ptr[1:])
+    if dev_tensor:
+        row_ptr = np.ascontiguousarray(tensor.row_ptr, dtype=np.int64)
+        X = tensor.X.to(device=dev, dtype=F64).contiguous()
+    else:
+        counts = np.array([s.row_count for s in slices], dtype=np.int64)
+        row_ptr = np.zeros(K + 1, dtype=np.int64)
+        np.cumsum(counts, out=row_ptr[1:])
+        X = torch.as_tensor(np.concatenate([s.rows for s in slices]), device=dev)
     N = int(row_ptr[-1])
-    X = torch.as_tensor(np.concatenate([s.rows for s in slices]), device=dev)
     rp = torch.as_tensor(row_ptr, device=dev)
     V = torch.as_tensor(V0, device=dev)
     H = torch.as_tensor(H0, device=dev)
@@ -60,7 +72,7 @@ def parafac2_als_gpu(tensor, rank: int, iters: int = 10, seed: int = 0, tol: flo
             nat.check(L.dash_als_sweep_f64(ctx, st, ctypes.byref(b), J, rank, int(V.data_ptr()),
                                            int(H.data_ptr()), int(W.data_ptr()), int(Q.data_ptr()),
                                            int(loss.data_ptr()), RIDGE_EPS), "dash_als_sweep_f64")
-            _raise_on_error(L, ctx, st, [s.slice_id for s in slices])
+            _raise_on_error(L, ctx, st, ids_all if dev_tensor else [s.slice_id for s in slices])
             cur = float(loss.item())
             losses.append(cur)
             if len(losses) >= 2:
@@ -71,7 +83,7 @@ def parafac2_als_gpu(tensor, rank: int, iters: int = 10, seed: int = 0, tol: flo
         nat.check(L.dash_als_project_f64(ctx, st, N, rank, int(Q.data_ptr()), int(H.data_ptr()),
                                          int(U.data_ptr())), "dash_als_project_f64")
         Uh, Qh = U.cpu().numpy(), Q.cpu().numpy()
-    ids = [s.slice_id for s in slices]
+    ids = ids_all if dev_tensor else [s.slice_id for s in slices]
     factors = FactorSet(
         slice_ids=ids,
         U={sid: Uh[row_ptr[k]:row_ptr[k + 1]] for k, sid in enumerate(ids)},

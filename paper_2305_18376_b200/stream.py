@@ -357,6 +357,15 @@ class StreamState:
             self._uhost[bi] = h
         return h[lo:hi]
 
+    def u_history_device(self, slice_ids) -> torch.Tensor:
+        """U histories of ``slice_ids`` concatenated in that order (one device
+        gather; the CSR companion of a DeviceTensor with the same slices)."""
+        self._flush_ulog()
+        parts = [self._ustore[bi][lo:hi] for sid in slice_ids for bi, lo, hi in self._ublk[sid]]
+        if not parts:
+            return torch.zeros((0, self._R), dtype=self.dtype, device=self.device)
+        return torch.cat(parts)
+
     def u_matrix(self, slice_id) -> np.ndarray:
         blocks = self.u_blocks[slice_id]
         return blocks[0].copy() if len(blocks) == 1 else np.vstack(blocks)

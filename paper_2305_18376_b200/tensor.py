@@ -231,3 +231,24 @@ def normalize_batch(batch: UpdateBatch, stats: ColumnStats, policy: str = CAUSAL
     fresh = [NewSlice(ns.slice_id, _normalise_slice(stats, ns.slice_id, ns.rows, extend, False),
                       ns.first_time_step) for ns in batch.new_slices]
     return UpdateBatch(batch.update_index, existing, fresh, batch.cycle_span), stats
+
+
+def apply_batch(tensor: IrregularTensor, batch: UpdateBatch) -> IrregularTensor:
+    """Append a batch to a tensor, returning the accumulated tensor
+    (tensor.py:228-244): touched slices grow by their new rows, new slices
+    go last in batch order.  The device-resident form is
+    ``history.DeviceTensor.apply_batch``."""
+    slices = []
+    for s in tensor.slices:
+        extra = batch.existing_rows.get(s.slice_id)
+        if extra is None:
+            slices.append(s)
+        else:
+            slices.append(SliceMatrix(s.slice_id, np.vstack([s.rows, extra]), s.first_time_step))
+    known = set(tensor.slice_ids)
+    for sid in batch.existing_rows:
+        if sid not in known:
+            raise DatasetError(f"batch references unknown existing slice {sid!r}")
+    for ns in batch.new_slices:
+        slices.append(SliceMatrix(ns.slice_id, ns.rows.copy(), ns.first_time_step))
+    return IrregularTensor(slices)
