@@ -203,26 +203,44 @@ def peaks():
     return 6650.0, "fallback"
 
 
-def ncu_traffic(phase):
-    """dram bytes per launch from a committed `ncu --set full` capture."""
+def ncu_traffic(phase, config=CONFIG_NAME):
+    """dram bytes per launch from a committed `ncu --set full` capture of this
+    config (profiles/ncu_traffic.json: {config: {phase: bytes}}); None if that
+    config / kernel was not captured."""
     p = ROOT / "profiles" / "ncu_traffic.json"
     if not p.exists():
         return None
     d = json.loads(p.read_text())
-    return d.get(phase)
+    return d.get(config, {}).get(phase)
 
 
-def roofline_of(dom, per_kernel, achieved, peak, peak_kind, per_launch_ms, kb):
+def workload_config(cfg, sched, t0, t1, parallelism):
+    """The workload as both arms report it (same keys, same numbers: the row
+    counts come from the shared seeded Schedule over the timed steps)."""
+    def law(x):
+        return list(x)
+    n = [int(sched.adds[t].sum() + sched.new_len[t].sum()) for t in range(t0, t1)]
+    m = [int(len(sched.adds[t]) + len(sched.new_len[t])) for t in range(t0, t1)]
+    return {"workload": cfg.name, "K0": cfg.K0, "J": cfg.J, "R": cfg.R, "lambda": cfg.forgetting,
+            "passes": cfg.passes, "init_rows": law(cfg.init_rows), "add_rows_per_slice": law(cfg.add_rows),
+            "new_slices": law(cfg.new_slices), "new_slice_rows": law(cfg.new_rows),
+            "rows_per_update": sum(n) / max(len(n), 1), "slices_per_update": sum(m) / max(len(m), 1),
+            "l2": "inputs larger than L2" if sum(n) / max(len(n), 1) * cfg.J * 8 > 126e6
+                  else "batches smaller than L2: device-resident X of every step is distinct",
+            "parallelism": parallelism}
+
+
+def roofline_of(dom, per_kernel, achieved, peak, peak_kind, per_launch_ms, kb, config=CONFIG_NAME):
     """Roofline of the dominant kernel: its binding roof (HBM bytes, or FP64
     tensor flops for the DMMA-bound fused big-slice kernel, whichever fraction
     is higher), with the other roof alongside."""
     pk = per_kernel.get(dom, {})
     hbm = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-           "frac": achieved / peak, "traffic": ncu_traffic(dom), "peak_source": peak_kind,
+           "frac": achieved / peak, "traffic": ncu_traffic(dom, config), "peak_source": peak_kind,
            "per_launch_ms": per_launch_ms, "alg_bytes_per_launch": kb}
     if pk.get("tflops") and pk["frac_fp64_tensor"] > hbm["frac"]:
         return {"bound": "tensor", "kernel": dom, "achieved": pk["tflops"], "peak": FP64_TENSOR_PEAK,
-                "unit": "TFLOP/s", "frac": pk["frac_fp64_tensor"], "traffic": ncu_traffic(dom),
+                "unit": "TFLOP/s", "frac": pk["frac_fp64_tensor"], "traffic": ncu_traffic(dom, config),
                 "peak_source": "measured FP64 DMMA peak (profiles/r01_fp64_peak.md)",
                 "per_launch_ms": per_launch_ms, "alg_flops_per_launch": pk["alg_flops"],
                 "hbm": {"achieved": achieved, "peak": peak, "frac": achieved / peak, "alg_bytes_per_launch": kb}}
@@ -367,7 +385,7 @@ def run_gpu(args):
     L.dash_ctx_phase_ms(state._ctx, ms_arr, cnt_arr, nph)
     L.dash_ctx_set_profiling(state._ctx, 0)
     state.check()
-    t_ms = e1.elapsed_time(e0) if False else e0.elapsed_time(e1)
+    t_ms = e0.elapsed_time(e1)
     t_max = t_ms
     if world > 1:
         tt = torch.tensor([t_ms], device=dev, dtype=torch.float64)
@@ -474,12 +492,8 @@ def run_gpu(args):
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (planted low-rank + N(0,0.1) noise, drawn on device; planted initial state)",
-            "config": {"workload": f"{cfg.name}: K0={cfg.K0} slices, J={J}, R={R}, lambda={cfg.forgetting}, "
-                                   f"+U[1,8] rows/slice and 500 new slices of U[200,2000] rows per update",
-                       "rows_per_update": N_avg, "slices_per_update": M_old_avg + L_avg,
-                       "passes": cfg.passes, "l2": "inputs larger than L2 (0.8 GB per step)",
-                       "parallelism": f"slice-sharded x{world}"},
-            "roofline": roofline_of(dom, per_kernel, achieved, peak, peak_kind, per_launch_ms, kb),
+            "config": workload_config(cfg, sched, args.warmup, args.warmup + args.steps, f"slice-sharded x{world}"),
+            "roofline": roofline_of(dom, per_kernel, achieved, peak, peak_kind, per_launch_ms, kb, cfg.name),
             "step_roofline": {"alg_bytes": step_bytes, "achieved_gbs": step_achieved,
                               "frac": step_achieved / peak,
                               "alg_flops": algorithmic_flops(N_avg, J, R, M_old_avg + L_avg),
@@ -707,7 +721,8 @@ def run_reference(args):
         "steps": n, "warmup": args.warmup, "ms_per_step": 1e3 * secs / n,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (planted low-rank + N(0,0.1) noise, host numpy)",
-        "config": {"workload": f"{cfg.name}: K0={cfg.K0}, J={cfg.J}, R={cfg.R}", "parallelism": "cpu"},
+        "config": workload_config(cfg, Schedule(cfg, args.warmup + args.steps, cfg.seed), args.warmup,
+                                  args.warmup + args.steps, f"slice-sharded x{int(os.environ.get('WORLD_SIZE', '1'))}"),
         "impl": "reference",
         "cpu_baseline": {"value": value, "unit": "elements/s", "cores": cores, "kind": "port",
                          "sample": f"{n} full {cfg.name} updates of the oracle port of p2stream "

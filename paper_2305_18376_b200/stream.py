@@ -32,6 +32,7 @@ are lazy copies, cached until the next mutation.
 from __future__ import annotations
 
 import ctypes
+import os
 import time
 from collections.abc import Mapping
 from dataclasses import dataclass, field
@@ -163,6 +164,39 @@ class _UBlocks(Mapping):
 
     def __len__(self):
         return len(self._s._ublk)
+
+
+_POOL = None
+
+
+def _gather_rows(arrs, row_ptr, out, on_chunk=None):
+    """Concatenate the batch's per-slice row blocks into the pinned staging
+    buffer: one np.concatenate per contiguous share of the rows, on a small
+    thread pool (numpy releases the GIL for the copies), so the host gather
+    of a large batch runs at several GB/s instead of one core's.
+    ``on_chunk(lo, hi)`` is called in row order as each share lands (the
+    caller starts that share's host->device copy behind the others' gathers)."""
+    global _POOL
+    N = out.shape[0]
+    T = min(8, os.cpu_count() or 1)
+    if T <= 1 or N * out.shape[1] < (1 << 22) or len(arrs) < 2 * T:
+        np.concatenate(arrs, axis=0, out=out)
+        if on_chunk is not None:
+            on_chunk(0, N)
+        return
+    if _POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _POOL = ThreadPoolExecutor(max_workers=T, thread_name_prefix="dash-gather")
+    cut = np.searchsorted(row_ptr, np.linspace(0, N, T + 1).astype(np.int64))
+    cut[0], cut[-1] = 0, len(arrs)
+    cut = np.unique(cut)
+    jobs = [(int(row_ptr[a]), int(row_ptr[b]), _POOL.submit(np.concatenate, arrs[a:b], 0,
+                                                             out[row_ptr[a]:row_ptr[b]]))
+            for a, b in zip(cut[:-1], cut[1:]) if b > a]
+    for lo, hi, f in jobs:
+        f.result()
+        if on_chunk is not None:
+            on_chunk(lo, hi)
 
 
 class StreamState:
@@ -411,29 +445,54 @@ class StreamState:
     # -- the update -----------------------------------------------------------
     def update(self, batch: UpdateBatch) -> UpdateResult:
         """Consume one batch (stream.py:251-370): same validation, same
-        registration order, same results within FP64 rounding."""
+        registration order, same results within FP64 rounding.  Accepts this
+        package's UpdateBatch or the reference's (anything with
+        ``existing_rows`` / ``new_slices``, or with ``items()``)."""
         with _on(self.device):
             if self._unchecked:  # report a failure latched by an earlier unchecked update first
                 self.check()
+            if hasattr(batch, "existing_rows") and hasattr(batch, "new_slices"):
+                ex = batch.existing_rows
+                return self._update_lists(list(ex.keys()), list(ex.values()),
+                                          [ns.slice_id for ns in batch.new_slices],
+                                          [ns.rows for ns in batch.new_slices])
             return self._update_items(batch.items())
 
     def _update_items(self, items, allreduce=None) -> UpdateResult:
-        started = time.perf_counter()
-        entries = []
+        """Generic form: (sid, rows, is_new) in items() order (existing first)."""
+        ex_ids, ex_rows, new_ids, new_rows = [], [], [], []
         for sid, rows, is_new in items:
-            if is_new and sid in self._row_of:
-                raise ValueError(f"batch declares known slice {sid!r} as new")
-            if not is_new and sid not in self._row_of:
-                raise ValueError(f"batch references unknown existing slice {sid!r}")
-            rows = np.asarray(rows, dtype=float)
-            if rows.ndim != 2 or rows.shape[1] != self.J:
-                raise ValueError(f"slice {sid!r}: rows must be (n, {self.J})")
-            entries.append((sid, rows, is_new))
-        new_ids = [sid for sid, _, is_new in entries if is_new]
-        M = len(entries)
-        counts = np.fromiter((r.shape[0] for _, r, _ in entries), dtype=np.int64, count=M)
-        # items() order: existing slices, then new ones (tensor.py:166-171)
-        existing_rows = np.fromiter((self._row_of[sid] for sid, _, n in entries if not n), dtype=np.int32)
+            if is_new:
+                new_ids.append(sid)
+                new_rows.append(rows)
+            else:
+                if new_ids:
+                    raise ValueError("batch items must list existing slices before new ones")
+                ex_ids.append(sid)
+                ex_rows.append(rows)
+        return self._update_lists(ex_ids, ex_rows, new_ids, new_rows, allreduce=allreduce)
+
+    def _update_lists(self, ex_ids, ex_rows, new_ids, new_rows, allreduce=None) -> UpdateResult:
+        started = time.perf_counter()
+        rowmap = self._row_of
+        J = self.J
+        # validation (stream.py:262-268), vectorised over the entries
+        bad = [sid for sid in new_ids if sid in rowmap]
+        if bad:
+            raise ValueError(f"batch declares known slice {bad[0]!r} as new")
+        bad = [sid for sid in ex_ids if sid not in rowmap]
+        if bad:
+            raise ValueError(f"batch references unknown existing slice {bad[0]!r}")
+        arrs = [r if (type(r) is np.ndarray and r.dtype == np.float64) else np.asarray(r, dtype=float)
+                for r in ex_rows + new_rows]
+        bad = [k for k, r in enumerate(arrs) if r.ndim != 2 or r.shape[1] != J]
+        if bad:
+            sid = (ex_ids + new_ids)[bad[0]]
+            raise ValueError(f"slice {sid!r}: rows must be (n, {J})")
+        ids = ex_ids + new_ids
+        M = len(ids)
+        counts = np.fromiter((r.shape[0] for r in arrs), dtype=np.int64, count=M)
+        existing_rows = np.fromiter((rowmap[sid] for sid in ex_ids), dtype=np.int32, count=len(ex_ids))
         N, row_ptr, meta = self._stage_meta(counts, existing_rows, len(new_ids))
         row_ptr = row_ptr.copy()  # kept by UpdateResult / local_error beyond the ring's lifetime
         # registration (stream.py:270-280): new rows appended in batch order
@@ -441,19 +500,19 @@ class StreamState:
 
         pin, X = self._stage_x(N)
         if N:
-            np.concatenate([r for _, r, _ in entries], axis=0, out=pin.numpy()[:N])
-            X[:N].copy_(pin[:N], non_blocking=True)
+            def upload(lo, hi):  # each share's H2D starts as soon as its rows are gathered
+                X[lo:hi].copy_(pin[lo:hi], non_blocking=True)
+            _gather_rows(arrs, row_ptr, pin.numpy()[:N], upload)
             ev = torch.cuda.Event()
             ev.record()
             self._pin_event = ev
-        ids = [sid for sid, _, _ in entries]
         U_dev, v_used = self._run(X, N, row_ptr, meta, check=True, ids=ids, allreduce=allreduce)
         self.update_index += 1
         self._last = (ids, row_ptr, meta, X, N, U_dev)
         return UpdateResult(
             update_index=self.update_index,
             u_new=_UNew(ids, row_ptr, U_dev),
-            new_slice_ids=new_ids,
+            new_slice_ids=list(new_ids),
             rows_new=N,
             seconds=time.perf_counter() - started,
             v_used=v_used.cpu().numpy(),
