@@ -59,6 +59,10 @@ def parse():
     ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--no-fp32", dest="fp32", action="store_false",
                     help="skip the FP32 data-mode measurement")
+    ap.add_argument("--dropin-steps", type=int, default=3,
+                    help="timed StreamState.update(UpdateBatch) calls on host batches (0: skip)")
+    ap.add_argument("--no-als", dest="als", action="store_false",
+                    help="skip the parafac2_als sweep timing (medium, daily)")
     return ap.parse_args()
 
 
@@ -453,6 +457,17 @@ def run_gpu(args):
         e2e_elems = float(te.item())
     e2e_value = e2e_elems / (e2e_ms / 1e3) if e2e_b else None
 
+    # the drop-in API a reference user calls: StreamState.update(UpdateBatch)
+    # with host batches of per-slice numpy arrays (gather into pinned memory,
+    # H2D, update, sync + SolveError check, v_used read back), like the
+    # reference's update() whose `seconds` include its staging (rank 0, N=1)
+    dropin = None
+    if world == 1 and args.dropin_steps > 0:
+        dropin = run_dropin(cfg, arrays, args.dropin_steps, dev)
+    als = None
+    if world == 1 and args.als:
+        als = {name: als_timing(name, dev) for name in ("medium", "daily")}
+
     # roofline of the dominant kernel
     phase_ms = {nat.PHASES[i]: ms_arr[i] for i in range(nph)}
     phase_n = {nat.PHASES[i]: cnt_arr[i] for i in range(nph)}
@@ -506,12 +521,94 @@ def run_gpu(args):
             "gpu_launches": launches,
             "lu_fallbacks": fallbacks,
             "fp32": fp32,
+            "e2e_dropin": dropin,
+            "als": als,
             "clocks": clocks,
         }
     del batches
     if world > 1:
         dist.barrier()
     return out, cfg
+
+
+def run_dropin(cfg, arrays, steps, dev):
+    """e2e through StreamState.update(UpdateBatch) on host batches (the
+    reference's call): wall time per update, synchronous like the reference."""
+    import torch
+
+    from paper_2305_18376_b200.stream import StreamState
+    st = StreamState.from_arrays(arrays, device=dev)
+    hb, gen = host_stream(cfg, steps + 1, seed_extra=1)
+    del hb
+    batches = [(b, N) for b, N in gen()]
+    st.reserve_u_history(sum(N for _, N in batches))
+    st.update(batches[0][0])  # warm-up (pinned staging buffers, thread pool)
+    torch.cuda.synchronize()
+    times, elems, h2d, d2h = [], 0, 0, 0
+    for b, N in batches[1:]:
+        t0 = time.perf_counter()
+        st.update(b)
+        times.append(time.perf_counter() - t0)
+        elems += N * cfg.J
+        h2d += N * cfg.J * 8 + (b.slice_count) * 13 + 8
+        d2h += cfg.J * cfg.R * 8 + 8
+    secs = sum(times)
+    return {"value": elems / secs, "unit": "elements/s", "ms_per_step": 1e3 * secs / len(times),
+            "steps": len(times), "h2d_bytes_per_step": h2d / len(times), "d2h_bytes_per_step": d2h / len(times),
+            "api": "StreamState.update(UpdateBatch) with host numpy rows (wall clock, synchronous)"}
+
+
+def als_timing(name, dev, iters=3):
+    """One parafac2_als sweep at a BASELINE shape (initialize's fit and the
+    baseline refit, tol=0 so every sweep runs), on a device-resident tensor of
+    that shape drawn from the planted generator; SURVEY 8(d) ALS roofline:
+    >= 2 x 8 x sum(I_k) x J bytes per sweep (target and projection passes)."""
+    import torch
+
+    from paper_2305_18376_b200 import workloads as wl
+    from paper_2305_18376_b200.als import parafac2_als
+    from paper_2305_18376_b200.history import DeviceTensor
+    cfg = wl.CONFIGS[name]
+    sch = wl.make_schedule(cfg)
+    counts = sch.init_len.astype(np.int64)
+    row_ptr = np.zeros(len(counts) + 1, dtype=np.int64)
+    np.cumsum(counts, out=row_ptr[1:])
+    N, J, R = int(row_ptr[-1]), cfg.J, cfg.R
+    H, V = wl.true_factors(cfg)
+    g = torch.Generator(device=dev)
+    g.manual_seed(cfg.seed)
+    scale = torch.as_tensor(np.repeat(1.0 / np.sqrt(counts), counts), device=dev)
+    w = torch.rand((len(counts), R), generator=g, device=dev, dtype=torch.float64)
+    q = torch.randn((N, R), generator=g, device=dev, dtype=torch.float64) * scale[:, None]
+    rows_of = torch.as_tensor(np.repeat(np.arange(len(counts)), counts), device=dev)
+    X = ((q @ torch.as_tensor(H, device=dev)) * w[rows_of]) @ torch.as_tensor(V, device=dev).T
+    X += 0.1 * torch.randn((N, J), generator=g, device=dev, dtype=torch.float64)
+    del q, rows_of, scale
+    dt = DeviceTensor([wl.slice_id(k) for k in range(len(counts))], row_ptr, X)
+    parafac2_als(dt, R, iters=1, seed=0, tol=0.0)  # warm-up
+    torch.cuda.synchronize()
+    fit = []
+    for n in (1, 1 + iters):  # per sweep = the difference: fit setup / host factor copies cancel
+        t0 = time.perf_counter()
+        parafac2_als(dt, R, iters=n, seed=1, tol=0.0)
+        torch.cuda.synchronize()
+        fit.append(time.perf_counter() - t0)
+    sweep = (fit[1] - fit[0]) / iters
+    by = 2 * 8 * N * J
+    peak, _ = peaks()
+    ref = ROOT / "tests" / "golden" / f"als_{name}.npz"
+    ref_sweep = None
+    if ref.exists():  # the reference's own 10-sweep fit of this shape, timed when the fixture was made
+        with np.load(ref) as g:
+            ref_sweep = 1e3 * float(g["fit_seconds"]) / len(g["losses"])
+    return {"slices": len(counts), "rows": N, "J": J, "R": R, "sweep_ms": 1e3 * sweep,
+            "alg_bytes_per_sweep": by, "achieved_gbs": by / sweep / 1e9, "frac_hbm": by / sweep / 1e9 / peak,
+            "reference_cpu_sweep_ms": ref_sweep,
+            "reference_cpu_note": "p2stream parafac2_als (numpy/OpenBLAS, 8 cores of the build container), "
+                                  "fit time / sweeps, from tests/golden/make_golden_als.py",
+            "fit_ms_1_sweep": 1e3 * fit[0],
+            "note": "per sweep = (fit with 1 + n sweeps - fit with 1 sweep) / n, wall clock incl. the per-sweep "
+                    "loss read-back for the early-exit test; fit_ms_1_sweep adds setup and the host factor copies"}
 
 
 def run_fp32_arm(args, arrays, batches, dev, stream, world, J, R, prof_steps, barrier):

@@ -536,9 +536,12 @@ int dash_als_sweep_f64(dash_ctx *ctx, void *stream, const dash_batch_f64 *t, int
     }
     // loss with the refreshed H, W, V (als.py:182-185): Z = (Q H) o w
     k_als_qh<<<std::max(qb, 1), 256, 0, st>>>(Q, H, W, row_slice, N, R, Z);
-    k_als_loss<<<std::max(1, std::min((K + 7) / 8, ctx->num_sms * 8)), 256, 0, st>>>(t->X, t->ldx, t->row_ptr, K, Z,
-                                                                                    V, J, R, per);
-    k_sum_ordered<<<1, 32, 0, st>>>(per, K, loss);
+    if (ensure(ctx->rerr, sizeof(double) * (size_t)N)) return DASH_E_CUDA;
+    launch_row_err<false>(ctx, st, t->X, t->ldx, N, (const double *)Z, R, V, J, (const int32_t *)nullptr,
+                          (const int32_t *)nullptr, (const double *)nullptr, (double *)ctx->rerr.p);
+    k_seg_sum<<<std::max(1, std::min((K + 7) / 8, ctx->num_sms * 8)), 256, 0, st>>>((const double *)ctx->rerr.p,
+                                                                                  t->row_ptr, K, J, 0, per);
+    k_tree_sum<<<1, 256, 0, st>>>(per, K, 0, loss);
     return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_E_CUDA;
 }
 

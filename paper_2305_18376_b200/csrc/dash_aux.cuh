@@ -275,17 +275,120 @@ int dash_init_helpers_f64(dash_ctx *ctx, void *stream, const dash_batch_f64 *t, 
 }  // extern "C"
 
 namespace {
+// ---------------------------------------------------------------------------
+// Row-parallel reconstruction error (local_error / slice_error and the ALS
+// loss): per row e = sum_j phi(X[row][j] - sum_r z_r V[j][r]) with
+// z = U[row] o W[state_row[slice(row)]] (local_error) or z = Z[row] (ALS:
+// (Q H) o w already formed), phi = |.| or (.)^2.  One warp per row, lanes over
+// the columns; V staged in shared memory (odd pitch) when it fits.  Then the
+// per-slice sums in row order (one warp per slice) and a fixed-order tree
+// over the slices: deterministic, and every X byte is read once at full
+// occupancy (the previous one-warp-per-slice loops were latency-bound).
+// ---------------------------------------------------------------------------
+constexpr int kRecVS = 6144;  // J * R doubles staged (48 KB)
+template <bool ABS, typename TX, typename TU>
+__global__ void __launch_bounds__(256) k_row_err(const TX *__restrict__ X, int64_t ldx, int64_t N,
+                                                 const TU *__restrict__ Z, int R, const double *__restrict__ V, int J,
+                                                 const int32_t *__restrict__ row_slice,
+                                                 const int32_t *__restrict__ state_row, const double *__restrict__ W,
+                                                 double *__restrict__ row_err) {
+    extern __shared__ double vs[];
+    __shared__ double zbuf[8][DASH_MAX_RANK];
+    const bool staged = (int64_t)J * R <= kRecVS;
+    const int P = R + 1;
+    if (staged)
+        for (int i = threadIdx.x; i < J * R; i += blockDim.x) vs[(i / R) * P + i % R] = V[i];
+    __syncthreads();
+    const int lane = lane_id(), w = warp_id();
+    double *zs = zbuf[w];
+    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + w, nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t row = gw; row < N; row += nw) {
+        const double *wr = W ? W + (int64_t)state_row[row_slice[row]] * R : nullptr;
+        for (int r = lane; r < R; r += 32) zs[r] = (double)Z[row * R + r] * (wr ? wr[r] : 1.0);
+        __syncwarp();
+        double acc = 0.0;
+        for (int j = lane; j < J; j += 32) {
+            double rec = 0.0;
+            if (staged) {
+                const double *vj = vs + j * P;
+                for (int r = 0; r < R; ++r) rec = fma(zs[r], vj[r], rec);
+            } else {
+                const double *vj = V + (int64_t)j * R;
+                for (int r = 0; r < R; ++r) rec = fma(zs[r], __ldg(vj + r), rec);
+            }
+            const double d = (double)X[row * ldx + j] - rec;
+            acc = ABS ? acc + fabs(d) : fma(d, d, acc);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(FULL_MASK, acc, off);
+        if (lane == 0) row_err[row] = acc;
+        __syncwarp();
+    }
+}
+
+// per-slice sum of the row errors (rows in order, lanes strided, fixed tree),
+// divided by n_k * J when `mean` (local_error's per-slice mean)
+__global__ void __launch_bounds__(256) k_seg_sum(const double *__restrict__ row_err,
+                                                 const int64_t *__restrict__ row_ptr, int K, int J, int mean,
+                                                 double *__restrict__ per) {
+    const int lane = lane_id();
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (int k = gw; k < K; k += nw) {
+        const int64_t r0 = row_ptr[k], r1 = row_ptr[k + 1];
+        double acc = 0.0;
+        for (int64_t i = r0 + lane; i < r1; i += 32) acc += row_err[i];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(FULL_MASK, acc, off);
+        if (lane == 0) per[k] = mean ? acc / ((double)(r1 - r0) * J) : acc;
+    }
+}
+
+// fixed-order sum (or mean) of n values by one block: strided partials, then a tree
+__global__ void __launch_bounds__(256) k_tree_sum(const double *__restrict__ v, int n, int mean,
+                                                  double *__restrict__ out) {
+    __shared__ double part[256];
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) acc += v[i];
+    part[threadIdx.x] = acc;
+    __syncthreads();
+    for (int h = 128; h > 0; h >>= 1) {
+        if ((int)threadIdx.x < h) part[threadIdx.x] += part[threadIdx.x + h];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = mean ? (n > 0 ? part[0] / n : 0.0) : part[0];
+}
+
+template <bool ABS, typename TX, typename TU>
+int launch_row_err(dash_ctx *ctx, cudaStream_t st, const TX *X, int64_t ldx, int64_t N, const TU *Z, int R,
+                   const double *V, int J, const int32_t *row_slice, const int32_t *state_row, const double *W,
+                   double *row_err) {
+    if (N <= 0) return 0;
+    const size_t smem = (int64_t)J * R <= kRecVS ? sizeof(double) * (size_t)J * (R + 1) : 0;
+    ensure_smem_attr(k_row_err<ABS, TX, TU>, smem);
+    const int blocks = (int)std::min<int64_t>((N + 7) / 8, (int64_t)ctx->num_sms * 8);
+    k_row_err<ABS, TX, TU><<<std::max(blocks, 1), 256, smem, st>>>(X, ldx, N, Z, R, V, J, row_slice, state_row, W,
+                                                                   row_err);
+    return 0;
+}
+
 template <class B, typename TX>
 int local_error_impl(dash_ctx *ctx, void *stream, const B *b, const TX *U, const double *W,
                          const double *V, int32_t J, int32_t R, double *slice_err, double *tensor_err) {
     if (!ctx || !b || R < 1 || R > DASH_MAX_RANK || J < 1) return DASH_E_ARG;
     cudaStream_t st = (cudaStream_t)stream;
-    if (b->M > 0) {
-        int blocks = std::max(1, std::min((b->M + 7) / 8, ctx->num_sms * 8));
-        k_local_error<<<blocks, 256, 0, st>>>(b->X, b->ldx, b->row_ptr, b->state_row, b->M, U, W, V, J, R,
-                                              slice_err);
+    const int M = b->M;
+    const int64_t N = b->N;
+    if (M > 0 && N > 0) {
+        if (ensure(ctx->row_slice, sizeof(int32_t) * (size_t)N) || ensure(ctx->rerr, sizeof(double) * (size_t)N))
+            return DASH_E_CUDA;
+        k_row_slice<<<std::min(ctx->num_sms * 4, (M + 7) / 8 + 1), 256, 0, st>>>(b->row_ptr, M,
+                                                                               (int32_t *)ctx->row_slice.p);
+        launch_row_err<true>(ctx, st, b->X, b->ldx, N, U, R, V, J, (const int32_t *)ctx->row_slice.p, b->state_row,
+                             W, (double *)ctx->rerr.p);
+        k_seg_sum<<<std::max(1, std::min((M + 7) / 8, ctx->num_sms * 8)), 256, 0, st>>>(
+            (const double *)ctx->rerr.p, b->row_ptr, M, J, 1, slice_err);
     }
-    k_mean<<<1, 32, 0, st>>>(slice_err, b->M, tensor_err);
+    k_tree_sum<<<1, 256, 0, st>>>(slice_err, M, 1, tensor_err);
     return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_E_CUDA;
 }
 

@@ -934,6 +934,7 @@ struct dash_ctx {
     };
     Buf xv, row_slice, items, gslots, fslots, vtv, fsnap, gsnap, fg, part, us, scratch, smeta, plan_hist, u64;
     Buf tflag, bx_ms, bx_toff, bx_parts;  // fused big-slice path
+    Buf rerr;                             // per-row reconstruction errors (local_error, ALS loss)
     unsigned long long *err = nullptr;
     unsigned int *fallbacks = nullptr;
     int4 *items_host[2] = {nullptr, nullptr};
@@ -1778,7 +1779,7 @@ void dash_ctx_destroy(dash_ctx *ctx) {
                              &ctx->vtv, &ctx->fsnap,     &ctx->gsnap, &ctx->fg,     &ctx->part, &ctx->us, &ctx->scratch,
                              &ctx->smeta, &ctx->plan_hist, &ctx->u64,
                              &ctx->tflag, &ctx->bx_ms, &ctx->bx_toff, &ctx->bx_parts,
-                             &ctx->sx_tmp, &ctx->sx_units, &ctx->sx_meta};
+                             &ctx->sx_tmp, &ctx->sx_units, &ctx->sx_meta, &ctx->rerr};
     for (auto *b : bufs)
         if (b->p) cudaFree(b->p);
     cudaFree(ctx->err);
