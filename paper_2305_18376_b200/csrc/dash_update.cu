@@ -544,6 +544,7 @@ int launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 #include "dash_big.cuh"
 #include "dash_bigx.cuh"
 #include "dash_smallx.cuh"
+#include "dash_slicesw.cuh"
 
 // ---------------------------------------------------------------------------
 // k_fgemm: F partial slot s = X[rows_s]^T (U o w)[rows_s], J-block of 64.
@@ -552,7 +553,10 @@ template <int RP, typename TX>
 __global__ void __launch_bounds__(256) k_fgemm(const TX *__restrict__ X, int64_t ldx, int64_t N, int J,
                                                const double *__restrict__ U, const int32_t *__restrict__ row_slice,
                                                const int32_t *__restrict__ state_row, const double *__restrict__ W,
-                                               int R, int64_t rows_per_split, double *__restrict__ F_slots) {
+                                               int R, int64_t rows_per_split, double *__restrict__ F_slots,
+                                               double *__restrict__ G_slots) {
+    // G_slots != null: the last column block computes US^T US (G's fresh term,
+    // sum_k gram_k o w_k w_k^T of _kernels.py:139-143 summed by rows) instead of X^T US
     constexpr int BJ = 64, BK = 32, LDXS = BJ + 8;
     constexpr int LDUS = (RP % 16 == 0) ? RP + 8 : RP;
     constexpr int NT = RP / 8;
@@ -560,7 +564,8 @@ __global__ void __launch_bounds__(256) k_fgemm(const TX *__restrict__ X, int64_t
     __shared__ double Ss[BK * LDUS];
     const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
     const int g = lane >> 2, t = lane & 3;
-    const int j0 = blockIdx.x * BJ;
+    const bool gblk = G_slots != nullptr && blockIdx.x == gridDim.x - 1;
+    const int j0 = gblk ? 0 : blockIdx.x * BJ;
     const int64_t rbeg = (int64_t)blockIdx.y * rows_per_split;
     const int64_t rend = min(N, rbeg + rows_per_split);
     double acc[NT][2];
@@ -573,7 +578,14 @@ __global__ void __launch_bounds__(256) k_fgemm(const TX *__restrict__ X, int64_t
             int r = i / BJ, c = i % BJ;
             int64_t row = k0 + r;
             int col = j0 + c;
-            Xs[r * LDXS + c] = (row < rend && col < J) ? (double)__ldg(X + row * ldx + col) : 0.0;
+            if (gblk) {
+                double v = 0.0;
+                if (row < rend && c < R)
+                    v = U[row * R + c] * W[(int64_t)state_row[row_slice[row]] * R + c];
+                Xs[r * LDXS + c] = v;
+            } else {
+                Xs[r * LDXS + c] = (row < rend && col < J) ? (double)__ldg(X + row * ldx + col) : 0.0;
+            }
         }
         for (int i = tid; i < BK * RP; i += 256) {
             int r = i / RP, c = i % RP;
@@ -597,9 +609,9 @@ __global__ void __launch_bounds__(256) k_fgemm(const TX *__restrict__ X, int64_t
         }
         __syncthreads();
     }
-    double *slot = F_slots + (int64_t)blockIdx.y * J * R;
+    double *slot = gblk ? G_slots + (int64_t)blockIdx.y * R * R : F_slots + (int64_t)blockIdx.y * J * R;
     const int j = j0 + w * 8 + g;
-    if (j < J) {
+    if (j < (gblk ? R : J)) {
 #pragma unroll
         for (int n = 0; n < NT; ++n)
 #pragma unroll
@@ -935,6 +947,8 @@ struct dash_ctx {
     Buf xv, row_slice, items, gslots, fslots, vtv, fsnap, gsnap, fg, part, us, scratch, smeta, plan_hist, u64;
     Buf tflag, bx_ms, bx_toff, bx_parts;  // fused big-slice path
     Buf rerr;                             // per-row reconstruction errors (local_error, ALS loss)
+    Buf sw_scr;                           // k_slicesw per-warp scratch (R in (16, 64])
+    bool swide = false;                   // R > 16 on k_slicesw (G's fresh term from the F GEMM)
     unsigned long long *err = nullptr;
     unsigned int *fallbacks = nullptr;
     int4 *items_host[2] = {nullptr, nullptr};
@@ -1098,7 +1112,14 @@ struct SlicePlan {
     int nbig = 0, g3 = 0, gbig = 0, nslots = 0;
     int64_t big_tiles = 0;  // 32-row tiles of the big slices (fused path grid split)
     bool split = false, big_dev = false;
+    bool wide = false;      // RB > 16 on k_slicesw: items = slice order, 4 positions per int4
 };
+
+// A/B switch: DASH_OLD_WIDE=1 keeps R > 16 on k_slices / k_slices_cta
+bool wide_kernel() {
+    static const bool v = getenv("DASH_OLD_WIDE") == nullptr;
+    return v;
+}
 
 // Big-slice statistics of the last row_ptr built by dash_host_row_ptr on this
 // thread: the planner reuses them instead of re-scanning row_ptr (M entries).
@@ -1111,6 +1132,23 @@ thread_local RowPtrStats g_rp_stats;
 
 SlicePlan make_plan(const int64_t *row_ptr, int M, int RB, int R, int num_sms) {
     SlicePlan pl;
+    if (RB > 16 && wide_kernel()) {
+        // k_slicesw order: multi-chunk slices first, longest first (stable), then the rest in
+        // batch order; the warps take it strided, so the long solves start in the first wave
+        std::vector<int32_t> ord;
+        ord.reserve(M);
+        for (int m = 0; m < M; ++m)
+            if (row_ptr[m + 1] - row_ptr[m] > kSmallRows) ord.push_back(m);
+        std::stable_sort(ord.begin(), ord.end(), [row_ptr](int a, int b) {
+            return row_ptr[a + 1] - row_ptr[a] > row_ptr[b + 1] - row_ptr[b];
+        });
+        for (int m = 0; m < M; ++m)
+            if (row_ptr[m + 1] - row_ptr[m] <= kSmallRows) ord.push_back(m);
+        pl.items.assign((M + 3) / 4, make_int4(0, 0, 0, 0));
+        if (M) memcpy(pl.items.data(), ord.data(), sizeof(int32_t) * M);
+        pl.wide = true;
+        return pl;
+    }
     if (RB > 16) {
         plan_items(row_ptr, M, pl.items, slices_per_item(RB));
         pl.nslots = (int)pl.items.size();
@@ -1180,8 +1218,28 @@ const int *plan_counts_of(dash_ctx *ctx, int M) {
     return (const int *)ctx->plan_hist.p + 2 * (size_t)nch * kPlanBuckets + kPlanBuckets;
 }
 
+template <int NB>
+int run_slicesw(dash_ctx *ctx, cudaStream_t st, SwParams q) {
+    using Cf = swk::Cfg<NB>;
+    const int grid = ctx->num_sms;
+    if (ensure(ctx->sw_scr, sizeof(double) * (size_t)grid * Cf::NW * Cf::scr_doubles)) return DASH_E_CUDA;
+    q.scratch = (double *)ctx->sw_scr.p;
+    ensure_smem_attr(k_slicesw<NB>, Cf::smem_bytes());
+    k_slicesw<NB><<<grid, Cf::NW * 32, Cf::smem_bytes(), st>>>(q);
+    return cudaGetLastError() == cudaSuccess ? 0 : DASH_E_CUDA;
+}
+
+int launch_slicesw(dash_ctx *ctx, cudaStream_t st, int RB, int M, const SliceParams &sp) {
+    SwParams q{reinterpret_cast<const int32_t *>(sp.items), M, sp.row_ptr, sp.state_row, sp.is_new, sp.XV, sp.U,
+               sp.W, sp.C, sp.D, sp.vtv, nullptr, sp.err, sp.fallbacks, sp.R, sp.lam, sp.eps, sp.pass,
+               sp.final_pass};
+    PhaseScope ps(ctx, st, PH_SLICES);
+    return RB <= 32 ? run_slicesw<4>(ctx, st, q) : run_slicesw<8>(ctx, st, q);
+}
+
 int launch_plan(dash_ctx *ctx, cudaStream_t st, int RB, const SlicePlan &pl, SliceParams sp, int M,
                 bool skip_big = false) {
+    if (pl.wide) return launch_slicesw(ctx, st, RB, M, sp);
     if (!pl.split) return dispatch_slices(ctx, st, RB, (int)pl.items.size(), sp);
     const int4 *meta = (const int4 *)ctx->smeta.p;
     const int *counts = plan_counts_of(ctx, M);
@@ -1231,20 +1289,23 @@ void launch_xv(dash_ctx *ctx, cudaStream_t st, const B *b, int J, const double *
 
 template <int RP, class B>
 void launch_fgemm_t(dash_ctx *ctx, cudaStream_t st, const B *b, int J, const double *U,
-                    const int32_t *row_slice, const double *W, int R, int64_t rps, int nsplit, double *F_slots) {
-    dim3 grid((J + 63) / 64, nsplit);
+                    const int32_t *row_slice, const double *W, int R, int64_t rps, int nsplit, double *F_slots,
+                    double *G_slots) {
+    dim3 grid((J + 63) / 64 + (G_slots ? 1 : 0), nsplit);
     PhaseScope ps(ctx, st, PH_FGEMM);
-    k_fgemm<RP><<<grid, 256, 0, st>>>(b->X, b->ldx, b->N, J, U, row_slice, b->state_row, W, R, rps, F_slots);
+    k_fgemm<RP><<<grid, 256, 0, st>>>(b->X, b->ldx, b->N, J, U, row_slice, b->state_row, W, R, rps, F_slots,
+                                      G_slots);
 }
 
 template <class B>
 void launch_fgemm(dash_ctx *ctx, cudaStream_t st, const B *b, int J, const double *U,
-                  const int32_t *row_slice, const double *W, int R, int64_t rps, int nsplit, double *F_slots) {
+                  const int32_t *row_slice, const double *W, int R, int64_t rps, int nsplit, double *F_slots,
+                  double *G_slots = nullptr) {
     switch (rank_bucket(R) < 8 ? 8 : rank_bucket(R)) {
-        case 8: launch_fgemm_t<8>(ctx, st, b, J, U, row_slice, W, R, rps, nsplit, F_slots); break;
-        case 16: launch_fgemm_t<16>(ctx, st, b, J, U, row_slice, W, R, rps, nsplit, F_slots); break;
-        case 32: launch_fgemm_t<32>(ctx, st, b, J, U, row_slice, W, R, rps, nsplit, F_slots); break;
-        default: launch_fgemm_t<64>(ctx, st, b, J, U, row_slice, W, R, rps, nsplit, F_slots); break;
+        case 8: launch_fgemm_t<8>(ctx, st, b, J, U, row_slice, W, R, rps, nsplit, F_slots, G_slots); break;
+        case 16: launch_fgemm_t<16>(ctx, st, b, J, U, row_slice, W, R, rps, nsplit, F_slots, G_slots); break;
+        case 32: launch_fgemm_t<32>(ctx, st, b, J, U, row_slice, W, R, rps, nsplit, F_slots, G_slots); break;
+        default: launch_fgemm_t<64>(ctx, st, b, J, U, row_slice, W, R, rps, nsplit, F_slots, G_slots); break;
     }
 }
 
@@ -1526,6 +1587,8 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
         }
         plan_fsplit(ctx, N, J, ctx->nsplit, ctx->rps);
         if (ctx->stream) ctx->nsplit = ctx->num_sms * (f32 ? TmaSmem32::row_groups(J) : 1);
+        ctx->swide = plan_of(ctx).wide;
+        if (ctx->swide) ctx->nitems = (int)ctx->nsplit;  // G slots: one per F-GEMM row split
         if constexpr (!f32) ctx->tma = ctx->stream && tma_ok(b, J, R);
         {
             static const bool no_bigx = getenv("DASH_NO_BIGX") != nullptr;  // A/B switch: the k_big path
@@ -1727,7 +1790,7 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
             }
         } else {
             launch_fgemm(ctx, st, b, J, Ud, (const int32_t *)ctx->row_slice.p, s->W, R, ctx->rps,
-                         (int)ctx->nsplit, Fsl);
+                         (int)ctx->nsplit, Fsl, ctx->swide ? Gsl : nullptr);
         }
         // big slices' S-row systems and F / G slots: beside the F GEMM (independent of it)
         if (ctx->bigx && launch_bigx_post(ctx, st, bp)) return DASH_E_CUDA;
