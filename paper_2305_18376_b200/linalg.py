@@ -1,7 +1,8 @@
 """Ridge constant, error type and symmetrisation shared with the reference
 (/root/reference/pkg/src/p2stream/linalg.py:7-22).
 
-The solves themselves run on the GPU (csrc/dash_solve.cuh); this module only
+The solves themselves run on the GPU (csrc/dash_common.cuh: the symmetric sweep and the
+LU fallback; csrc/dash_update.cu: k_vsolve2); this module only
 carries the constants and the exception users catch.
 """
 from __future__ import annotations
