@@ -21,7 +21,9 @@
 //
 // G's fresh term sum_k gram_k o w_k w_k^T equals US^T US over all rows
 // (US = U o w of the row's slice); the F GEMM forms it (k_fgemm's extra
-// column block), so this kernel writes no G slots.
+// column block / k_fgemmw's G tiles), so this kernel writes no G slots.  US
+// itself is written by k_us_rows after this kernel (an in-kernel pass cost 4-10x
+// more: the warp re-walks its rows behind a 255-register solver).
 //
 // Failure chain (reference semantics): a non-SPD / non-finite system is
 // re-solved by LU with partial pivoting (lane 0, per-warp global scratch);

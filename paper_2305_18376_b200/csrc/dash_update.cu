@@ -92,6 +92,18 @@ __global__ void k_row_slice(const int64_t *__restrict__ row_ptr, int M, int32_t 
     }
 }
 
+// US = U o w(slice of the row): the tensor-map F GEMM's operand when the slice kernel
+// (k_slicesw) does not write it itself.  One element per thread, W rows from L2.
+__global__ void k_us_rows(const double *__restrict__ U, const int32_t *__restrict__ row_slice,
+                          const int32_t *__restrict__ state_row, const double *__restrict__ W, int R, int64_t n,
+                          double *__restrict__ US) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = i / R;
+        const int r = (int)(i - row * R);
+        US[i] = U[i] * W[(int64_t)state_row[row_slice[row]] * R + r];
+    }
+}
+
 // ---------------------------------------------------------------------------
 // k_xv: XV (N x R) = X (N x J, ld ldx) . V (J x R).  64-row tiles, 8 warps,
 // warp w owns rows 8w..8w+7 of the tile and all RP/8 column tiles.
@@ -545,6 +557,7 @@ int launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 #include "dash_bigx.cuh"
 #include "dash_smallx.cuh"
 #include "dash_slicesw.cuh"
+#include "dash_widej.cuh"
 
 // ---------------------------------------------------------------------------
 // k_fgemm: F partial slot s = X[rows_s]^T (U o w)[rows_s], J-block of 64.
@@ -963,6 +976,8 @@ struct dash_ctx {
     bool stream = false;  // TMA-ring GEMM path for this update
     bool tma = false;     // ... with tensor-map (swizzled box) copies: k_xv3 / k_fgemm3
     bool bigx = false;    // big slices on the fused single-read path (dash_bigx.cuh)
+    bool wtma = false;    // wide-J tensor-map GEMMs (dash_widej.cuh): J > 128, FP64 batches
+    int wnj = 1;          // ... column blocks of the wide F GEMM
     int bigx_nbig = 0, bigx_grid = 0;
     bool smallx = false;  // small slices on the fused single-kernel path (dash_smallx.cuh)
     bool planned = false; // the device slice plan ran for this update
@@ -1516,6 +1531,58 @@ int launch_bigx_post(dash_ctx *ctx, cudaStream_t st, const BigxParams &bp) {
     return launch_k(pdl_site("bxpost"), k_bigx_post, ctx->bigx_nbig, 256, 0, st, bp);
 }
 
+// ---- wide-J tensor-map GEMMs (dash_widej.cuh)
+bool widej_ok(const dash_batch_f64 *b, int J, int R, const double *V) {
+    static const bool off = getenv("DASH_NO_WIDEJ") != nullptr;  // A/B switch: the generic register-staged GEMMs
+    return !off && J > 128 && !(R & 1) && R <= 64 && !(b->ldx & 1) && (reinterpret_cast<uintptr_t>(b->X) & 15) == 0 &&
+           (reinterpret_cast<uintptr_t>(V) & 15) == 0 && b->N < ((int64_t)1 << 31) - 64 && encode_fn() != nullptr;
+}
+
+template <int RP>
+int launch_xvw_t(dash_ctx *ctx, cudaStream_t st, const CUtensorMap &mx, const CUtensorMap &mv, int64_t N, int J, int R,
+                 double *XV) {
+    constexpr size_t smem = WideCfg<RP>::xv_bytes();
+    ensure_smem_attr(k_xvw<RP>, smem);
+    const int grid = (int)std::min<int64_t>(ctx->num_sms, (N + 63) / 64);
+    k_xvw<RP><<<grid, kCW * 32 + 32, smem, st>>>(mx, mv, N, J, R, XV);
+    return cudaGetLastError() == cudaSuccess ? 0 : DASH_E_CUDA;
+}
+
+int launch_xvw(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, const double *V, int R, double *XV) {
+    CUtensorMap mx, mv;
+    if (!make_box_map(&mx, b->X, J, b->N, b->ldx) || !make_box_map(&mv, V, R, J, R, 64)) return DASH_E_CUDA;
+    PhaseScope ps(ctx, st, PH_XV);
+    const int RB = rank_bucket(R);
+    return RB <= 16 ? launch_xvw_t<16>(ctx, st, mx, mv, b->N, J, R, XV)
+           : RB <= 32 ? launch_xvw_t<32>(ctx, st, mx, mv, b->N, J, R, XV)
+                      : launch_xvw_t<64>(ctx, st, mx, mv, b->N, J, R, XV);
+}
+
+template <int RP>
+int launch_fw_t(dash_ctx *ctx, cudaStream_t st, const CUtensorMap &mx, const CUtensorMap &mu, int64_t N, int J, int R,
+                double *F_slots, double *G_slots) {
+    constexpr size_t smem = WideCfg<RP>::f_bytes();
+    ensure_smem_attr(k_fgemmw<RP>, smem);
+    k_fgemmw<RP><<<(unsigned)(ctx->wnj * ctx->nsplit), kCW * 32 + 32, smem, st>>>(mx, mu, N, J, R, ctx->rps, ctx->wnj,
+                                                                                 F_slots, G_slots);
+    return cudaGetLastError() == cudaSuccess ? 0 : DASH_E_CUDA;
+}
+
+int launch_fw(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, const double *US, int R, double *F_slots,
+              double *G_slots) {
+    CUtensorMap mx, mu;
+    if (!make_box_map(&mx, b->X, J, b->N, b->ldx) || !make_box_map(&mu, US, R, b->N, R)) return DASH_E_CUDA;
+    PhaseScope ps(ctx, st, PH_FGEMM);
+    const int RB = rank_bucket(R);
+    return RB <= 16 ? launch_fw_t<16>(ctx, st, mx, mu, b->N, J, R, F_slots, G_slots)
+           : RB <= 32 ? launch_fw_t<32>(ctx, st, mx, mu, b->N, J, R, F_slots, G_slots)
+                      : launch_fw_t<64>(ctx, st, mx, mu, b->N, J, R, F_slots, G_slots);
+}
+int launch_xvw(dash_ctx *, cudaStream_t, const dash_batch_f32 *, int, const double *, int, double *) { return DASH_E_ARG; }
+int launch_fw(dash_ctx *, cudaStream_t, const dash_batch_f32 *, int, const double *, int, double *, double *) {
+    return DASH_E_ARG;
+}
+
 template <int RP>
 void launch_xv2_t(dash_ctx *ctx, cudaStream_t st, const dash_batch_f64 *b, int J, const double *V, int R, double *XV) {
     const size_t smem = StreamSmem<RP>::xv_bytes(J);
@@ -1587,6 +1654,21 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
         }
         plan_fsplit(ctx, N, J, ctx->nsplit, ctx->rps);
         if (ctx->stream) ctx->nsplit = ctx->num_sms * (f32 ? TmaSmem32::row_groups(J) : 1);
+        ctx->wtma = false;
+        if constexpr (!f32) {
+            if (!ctx->stream && N > 0 && widej_ok(b, J, R, s->V)) {
+                // column blocks x row ranges (multiples of 32 rows), about one CTA per SM
+                const int fc = RB <= 32 ? WideCfg<32>::FC : WideCfg<64>::FC;
+                ctx->wnj = (J + fc - 1) / fc;
+                // k_slicesw's G term rides on the F GEMM: 2 tiles per warp must cover the (RB/8)^2 tiles
+                ctx->wtma = !plan_of(ctx).wide || (RB / 8) * (RB / 8) <= 16 * ctx->wnj;
+            }
+            if (ctx->wtma) {
+                const int64_t nrow = std::max<int64_t>(1, ctx->num_sms / ctx->wnj);
+                ctx->rps = std::max<int64_t>(32, ((N + nrow - 1) / nrow + 31) / 32 * 32);
+                ctx->nsplit = (N + ctx->rps - 1) / ctx->rps;
+            }
+        }
         ctx->swide = plan_of(ctx).wide;
         if (ctx->swide) ctx->nitems = (int)ctx->nsplit;  // G slots: one per F-GEMM row split
         if constexpr (!f32) ctx->tma = ctx->stream && tma_ok(b, J, R);
@@ -1639,7 +1721,7 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
             ensure(ctx->fslots, sizeof(double) * (ctx->nsplit + ctx->bigx_nbig) * J * R) ||
             ensure(ctx->vtv, sizeof(double) * R * R) ||
             ensure(ctx->fsnap, sizeof(double) * J * R) || ensure(ctx->gsnap, sizeof(double) * R * R) ||
-            ((ctx->stream || ctx->smallx) && ensure(ctx->us, sizeof(double) * std::max<int64_t>(N, 1) * R)) ||
+            ((ctx->stream || ctx->smallx || ctx->wtma) && ensure(ctx->us, sizeof(double) * std::max<int64_t>(N, 1) * R)) ||
             (f32 && ensure(ctx->u64, sizeof(double) * std::max<int64_t>(N, 1) * R)))
             return DASH_E_CUDA;
         if (!items.empty() && stage_items(ctx, st, items)) return DASH_E_CUDA;
@@ -1647,7 +1729,7 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
         if (ctx->planned &&
             device_plan(ctx, st, b, ctx->bigx ? (uint32_t *)ctx->tflag.p : nullptr))
             return DASH_E_CUDA;
-        if (M > 0 && !ctx->stream) {  // row -> slice map: only the generic F GEMM needs it
+        if (M > 0 && !ctx->stream && (!ctx->wtma || ctx->swide)) {  // row -> slice map: the generic F GEMM, k_us_rows
             PhaseScope ps(ctx, st, PH_ROWSLICE);
             k_row_slice<<<std::min(ctx->num_sms * 4, (M + 7) / 8 + 1), 256, 0, st>>>(b->row_ptr, M,
                                                                                     (int32_t *)ctx->row_slice.p);
@@ -1715,6 +1797,8 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
                 if (rank_bucket(R) <= 8) launch_xv2_t<8>(ctx, st, b, J, s->V, R, XV);
                 else launch_xv2_t<16>(ctx, st, b, J, s->V, R, XV);
             }
+        } else if (ctx->wtma) {
+            if (launch_xvw(ctx, st, b, J, s->V, R, XV)) return DASH_E_CUDA;
         } else {
             launch_xv(ctx, st, b, J, s->V, R, XV);
         }
@@ -1725,7 +1809,7 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
         sp.is_new = b->is_new;
         sp.XV = XV;
         sp.U = Ud;
-        sp.US = ctx->stream ? (double *)ctx->us.p : nullptr;
+        sp.US = (ctx->stream || ctx->wtma) ? (double *)ctx->us.p : nullptr;
         sp.W = s->W;
         sp.C = s->C;
         sp.D = s->D;
@@ -1739,6 +1823,12 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
         sp.pass = pass;
         sp.final_pass = last;
         if (!ctx->smallx && launch_plan(ctx, st, RB, plan_of(ctx), sp, M, ctx->bigx)) return DASH_E_CUDA;
+        if (ctx->wtma && ctx->swide) {  // k_slicesw leaves US to this pass
+            PhaseScope ps(ctx, st, PH_SLICES);
+            const int64_t n = N * R;
+            k_us_rows<<<(int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->num_sms * 16), 256, 0, st>>>(
+                Ud, (const int32_t *)ctx->row_slice.p, b->state_row, s->W, R, n, (double *)ctx->us.p);
+        }
         BigxParams bp{};
         {
             if (ctx->bigx) {
@@ -1788,6 +1878,9 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
                 if (rank_bucket(R) <= 8) launch_f2_t<8>(ctx, st, b, J, (const double *)ctx->us.p, R, Fsl);
                 else launch_f2_t<16>(ctx, st, b, J, (const double *)ctx->us.p, R, Fsl);
             }
+        } else if (ctx->wtma) {
+            if (launch_fw(ctx, st, b, J, (const double *)ctx->us.p, R, Fsl, ctx->swide ? Gsl : nullptr))
+                return DASH_E_CUDA;
         } else {
             launch_fgemm(ctx, st, b, J, Ud, (const int32_t *)ctx->row_slice.p, s->W, R, ctx->rps,
                          (int)ctx->nsplit, Fsl, ctx->swide ? Gsl : nullptr);
