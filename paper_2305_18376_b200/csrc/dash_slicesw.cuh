@@ -28,8 +28,10 @@
 // Failure chain (reference semantics): a non-SPD / non-finite system is
 // re-solved by LU with partial pivoting (lane 0, per-warp global scratch);
 // an LU zero pivot or a non-finite result reports SolveError for the slice.
-// State (W, C, D) is written only after the slice's W solve is validated, so
-// the LU re-solve of B still sees the old D.
+// D_old is read once per slice (prefetched into L2 when the slice starts):
+// D_new = lam D_old + gram replaces the gram tiles in the warp's scratch, the B
+// system, its LU re-solve and the write-back all read it from there.  State
+// (W, C, D) is written only after the slice's W solve is validated.
 // (included inside dash_update.cu's anonymous namespace)
 #pragma once
 
@@ -127,6 +129,17 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// 1 / sqrt(d) to ~1 ulp for d > 0 (NaN / inf otherwise -- the caller's SPD test has
+// already failed then): rsqrt.approx (2^-22) + two Newton steps y += y (1 - d y^2) / 2
+__device__ __forceinline__ double rsqrt_nr(double d) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+    double e = fma(-d * y, y, 1.0);
+    y = fma(0.5 * y, e, y);
+    e = fma(-d * y, y, 1.0);
+    return fma(0.5 * y, e, y);
+}
+
 // Cholesky of the 8x8 SPD diagonal tile T (lower part), right-looking in the
 // reference's update order; writes L^{-1} (lower, zeros above) to Li.  Every
 // 8-lane group computes the same factor (warp-uniform result).
@@ -141,11 +154,12 @@ __device__ __forceinline__ bool diag_chol8(const double *T, double *Li) {
     for (int j = 0; j < 8; ++j) {
         const double d = __shfl_sync(FULL_MASK, row[j], j, 8);
         ok = ok && (d > 0.0) && finite_d(d);
-        const double piv = sqrt(d);
-        const double iv = 1.0 / piv;
+        // only 1 / sqrt(d) is needed (L_jj itself is never stored): hardware seed + two
+        // Newton steps instead of the IEEE sqrt and two divisions (35% of the kernel's
+        // stall samples sat on those three subroutines, profiles/r02s3_w64_ncu.md)
+        const double iv = rsqrt_nr(d);
         inv[j] = iv;
-        if (i == j) row[j] = piv;
-        else if (i > j) row[j] = row[j] / piv;
+        if (i > j) row[j] = row[j] * iv;
 #pragma unroll
         for (int k = j + 1; k < 8; ++k) {
             const double lkj = __shfl_sync(FULL_MASK, row[j], k, 8);
@@ -300,6 +314,8 @@ __global__ void __launch_bounds__(swk::Cfg<NB>::NW * 32, 1) k_slicesw(SwParams p
         const bool fresh = p.is_new[m] != 0;
         const bool boot = fresh && p.pass == 0;
         const double *Dold = p.D + (int64_t)wrow * R * R;
+        if (!fresh)  // D_old is needed after the A system and the row solves: start its trip from HBM now
+            for (int e = lane * 16; e < R * R; e += 512) asm volatile("prefetch.global.L2 [%0];" ::"l"(Dold + e));
         __syncwarp();
         for (int r = lane; r < RB; r += 32) sv[r] = r < R ? (boot ? 1.0 : p.W[(int64_t)wrow * R + r]) : 0.0;
         __syncwarp();
@@ -421,9 +437,11 @@ __global__ void __launch_bounds__(swk::Cfg<NB>::NW * 32, 1) k_slicesw(SwParams p
                     const int rr = row >= col ? row : col, cc = row >= col ? col : row;  // lower element
                     double dn = 0.0;
                     if (row < R && col < R) dn = p.lam * (fresh ? 0.0 : Dold[rr * R + cc]) + g2[e];
+                    g2[e] = dn;
                     bd[jb][e] = v[e] * dn;
                     if (row == col && row < R) sh2 += v[e] * dn;
                 }
+                stc(GR + 64 * t, g2, o);  // GR now holds D_new (D_old is read exactly once per slice)
             }
             sh2 = p.eps * warp_sum(sh2) / R;
 #pragma unroll
@@ -451,8 +469,10 @@ __global__ void __launch_bounds__(swk::Cfg<NB>::NW * 32, 1) k_slicesw(SwParams p
                     const int col = 8 * kb + o.c0 + e;
                     double dn = 0.0;
                     if (row < R && col < R) dn = p.lam * (fresh ? 0.0 : Dold[row * R + col]) + g2[e];
+                    g2[e] = dn;
                     v[e] *= dn;
                 }
+                stc(GR + 64 * t, g2, o);
                 stc(Lt + 64 * t, v, o);
             }
         __syncwarp();
@@ -469,19 +489,16 @@ __global__ void __launch_bounds__(swk::Cfg<NB>::NW * 32, 1) k_slicesw(SwParams p
 #pragma unroll
             for (int e = 0; e < 2; ++e) fin = fin && finite_d(wv[jb][e]);
         if (!(okB && __all_sync(FULL_MASK, fin))) {
-            // LU on the unpadded B system; D_new recomputed from GR and the untouched D_old
+            // LU on the unpadded B system from the D_new tiles in GR
             if (lane == 0) atomicAdd(p.fallbacks, 1u);
             double shb = 0.0;
-            for (int r = lane; r < R; r += 32) {
-                const double g2 = GR[64 * tri(r >> 3, r >> 3) + toff(r & 7, r & 7)];
-                shb += p.vtv[r * R + r] * (p.lam * (fresh ? 0.0 : Dold[r * R + r]) + g2);
-            }
+            for (int r = lane; r < R; r += 32)
+                shb += p.vtv[r * R + r] * GR[64 * tri(r >> 3, r >> 3) + toff(r & 7, r & 7)];
             shb = p.eps * warp_sum(shb) / R;
             for (int e = lane; e < R * R; e += 32) {
                 const int r = e / R, z = e % R;
                 const int rr = r >= z ? r : z, cc = r >= z ? z : r;
-                const double g2 = GR[64 * tri(rr >> 3, cc >> 3) + toff(rr & 7, cc & 7)];
-                const double dn = p.lam * (fresh ? 0.0 : Dold[rr * R + cc]) + g2;
+                const double dn = GR[64 * tri(rr >> 3, cc >> 3) + toff(rr & 7, cc & 7)];
                 LUm[r * RB + z] = p.vtv[r * R + z] * dn + (r == z ? shb : 0.0);
             }
             __syncwarp();
@@ -516,8 +533,7 @@ __global__ void __launch_bounds__(swk::Cfg<NB>::NW * 32, 1) k_slicesw(SwParams p
         }
         if (p.final_pass) {
             double *Dn = p.D + (int64_t)wrow * R * R;
-            // every lane rewrites only elements it read itself (same addresses), so
-            // no other lane's D_old read can be overtaken
+            // D_new from GR (each lane reads back the pairs it stored itself)
 #pragma unroll
             for (int ib = 0; ib < NB; ++ib)
 #pragma unroll
@@ -530,7 +546,7 @@ __global__ void __launch_bounds__(swk::Cfg<NB>::NW * 32, 1) k_slicesw(SwParams p
                     for (int e = 0; e < 2; ++e) {
                         const int col = 8 * kb + o.c0 + e;
                         if (row < R && col < R && row >= col) {
-                            const double dn = p.lam * (fresh ? 0.0 : Dn[row * R + col]) + g2[e];
+                            const double dn = g2[e];
                             Dn[row * R + col] = dn;
                             if (row != col) Dn[col * R + row] = dn;
                         }
