@@ -316,6 +316,11 @@ __global__ void __launch_bounds__(swk::Cfg<NB>::NW * 32, 1) k_slicesw(SwParams p
         const double *Dold = p.D + (int64_t)wrow * R * R;
         if (!fresh)  // D_old is needed after the A system and the row solves: start its trip from HBM now
             for (int e = lane * 16; e < R * R; e += 512) asm volatile("prefetch.global.L2 [%0];" ::"l"(Dold + e));
+        if (lane * 16 < R) {
+            if (!fresh) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.C + (int64_t)wrow * R + lane * 16));
+            for (int64_t i = 0; i < (n < 8 ? n : 8); ++i)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(p.XV + (r0 + i) * R + lane * 16));
+        }
         __syncwarp();
         for (int r = lane; r < RB; r += 32) sv[r] = r < R ? (boot ? 1.0 : p.W[(int64_t)wrow * R + r]) : 0.0;
         __syncwarp();
@@ -456,25 +461,38 @@ __global__ void __launch_bounds__(swk::Cfg<NB>::NW * 32, 1) k_slicesw(SwParams p
             }
         }
 #pragma unroll
-        for (int ib = 1; ib < NB; ++ib)
+        for (int ib = 1; ib < NB; ++ib) {
+            // the block row's D_old pairs first (independent loads in flight together; the
+            // stores below would otherwise fence each tile's loads behind the previous tile)
+            const int row = 8 * ib + gr;
+            double dd[NB - 1][2];
+#pragma unroll
+            for (int kb = 0; kb < ib; ++kb) {
+                const int col = 8 * kb + o.c0;  // even; R even -> 16-byte aligned pair
+                double2 d2 = make_double2(0.0, 0.0);
+                if (!fresh && row < R && col + 1 < R) d2 = __ldcg(reinterpret_cast<const double2 *>(Dold + row * R + col));
+                else if (!fresh && row < R && col < R) d2.x = __ldcg(Dold + row * R + col);
+                dd[kb][0] = d2.x;
+                dd[kb][1] = d2.y;
+            }
 #pragma unroll
             for (int kb = 0; kb < ib; ++kb) {
                 const int t = tri(ib, kb);
                 double g2[2], v[2];
                 ldc(g2, GR + 64 * t, o);
                 ldc(v, vtvT + 64 * t, o);
-                const int row = 8 * ib + gr;
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
                     const int col = 8 * kb + o.c0 + e;
                     double dn = 0.0;
-                    if (row < R && col < R) dn = p.lam * (fresh ? 0.0 : Dold[row * R + col]) + g2[e];
+                    if (row < R && col < R) dn = p.lam * dd[kb][e] + g2[e];
                     g2[e] = dn;
                     v[e] *= dn;
                 }
                 stc(GR + 64 * t, g2, o);
                 stc(Lt + 64 * t, v, o);
             }
+        }
         __syncwarp();
         const bool okB = chol_tiles<NB>(Lt, Li, o);
         double wv[NB][2];
@@ -542,13 +560,26 @@ __global__ void __launch_bounds__(swk::Cfg<NB>::NW * 32, 1) k_slicesw(SwParams p
                     double g2[2];
                     ldc(g2, GR + 64 * t, o);
                     const int row = 8 * ib + gr;
+                    if (ib == kb) {  // diagonal tile: GR holds it fully symmetric
 #pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        const int col = 8 * kb + o.c0 + e;
-                        if (row < R && col < R && row >= col) {
-                            const double dn = g2[e];
-                            Dn[row * R + col] = dn;
-                            if (row != col) Dn[col * R + row] = dn;
+                        for (int e = 0; e < 2; ++e) {
+                            const int col = 8 * kb + o.c0 + e;
+                            if (row < R && col < R) Dn[row * R + col] = g2[e];
+                        }
+                    } else {  // lower tile rows, then its transpose (through Cs) as rows of the upper tile
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int col = 8 * kb + o.c0 + e;
+                            if (row < R && col < R) Dn[row * R + col] = g2[e];
+                        }
+                        __syncwarp();
+                        stc(Cs, g2, o);
+                        __syncwarp();
+                        const int urow = 8 * kb + gr;
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int ucol = 8 * ib + o.c0 + e;
+                            if (urow < R && ucol < R) Dn[urow * R + ucol] = Cs[toff(o.c0 + e, gr)];
                         }
                     }
                 }
