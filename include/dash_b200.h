@@ -66,6 +66,34 @@ int dash_ctx_last_launches(const dash_ctx *ctx);
  * the device), *N_out = total rows.  DASH_E_ARG on a negative count. */
 int dash_host_row_ptr(const int64_t *counts, int64_t M, int64_t *row_ptr, int64_t *N_out);
 
+/* Batch index staging (the host half of stream.py:282-298, the reference's
+ * per-update grouping / staging): a ring of caller-owned slots, each a pinned
+ * host block and a device block of `cap` bytes.  dash_stage_meta packs
+ *   row_ptr (M+1) i64 | state_row (M) i32, padded to 8 bytes | is_new (M) u8
+ * for a batch of M_old existing slices (state rows `existing_rows`) followed by
+ * L new slices (state rows K_base ..) into the next slot's pinned block, copies
+ * it to the slot's device block on the context's side stream (overlapping the
+ * previous update's kernels) and makes `stream` wait for that copy; with
+ * keep_dev != NULL the packed block is also copied there (device to device, on
+ * `stream`) for the U history.  dash_stage_release records, on `stream`, that
+ * the update which read the last staged slot has been issued in full -- the slot's
+ * device block is rewritten only after that point.  The host blocks only when
+ * the ring wraps onto a copy still in flight. */
+typedef struct dash_staged {
+    int64_t N;               /* total rows of the batch */
+    int32_t M;               /* slices */
+    int32_t slot;            /* ring slot used */
+    const void *row_ptr;     /* device, int64 (M+1) */
+    const void *state_row;   /* device, int32 (M) */
+    const void *is_new;      /* device, uint8 (M) */
+    const void *row_ptr_host;/* pinned, valid until the ring wraps */
+    int64_t nbytes;          /* size of the packed block */
+} dash_staged;
+int dash_meta_ring_set(dash_ctx *ctx, int32_t nslots, void *const *pinned, void *const *device, int64_t cap);
+int dash_stage_meta(dash_ctx *ctx, void *stream, const int64_t *counts, int32_t M_old, const int32_t *existing_rows,
+                    int32_t L, int32_t K_base, void *keep_dev, dash_staged *out);
+int dash_stage_release(dash_ctx *ctx, void *stream);
+
 /* Kernel path chosen for the last update (for benchmarks): bit 0 = streaming
  * (TMA-ring) GEMMs, bit 1 = tensor-map boxes (k_xv3 / k_fgemm3 or the FP32
  * variants), bit 2 = fused big-slice path (k_bigx: big-slice rows read once). */

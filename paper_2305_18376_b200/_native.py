@@ -46,6 +46,15 @@ class DashState(ctypes.Structure):
     ]
 
 
+class DashStaged(ctypes.Structure):
+    """dash_staged: what dash_stage_meta reports about the slot it filled."""
+    _fields_ = [
+        ("N", ctypes.c_int64), ("M", ctypes.c_int32), ("slot", ctypes.c_int32),
+        ("row_ptr", _c_dp), ("state_row", _c_dp), ("is_new", _c_dp), ("row_ptr_host", _c_dp),
+        ("nbytes", ctypes.c_int64),
+    ]
+
+
 # exported symbol -> (restype, argtypes); tests check every one is present
 SIGNATURES = {
     "dash_ctx_create": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p)]),
@@ -54,6 +63,11 @@ SIGNATURES = {
     "dash_ctx_last_launches": (ctypes.c_int, [ctypes.c_void_p]),
     "dash_ctx_path_flags": (ctypes.c_int, [ctypes.c_void_p]),
     "dash_host_row_ptr": (ctypes.c_int, [_c_dp, ctypes.c_int64, _c_dp, ctypes.POINTER(ctypes.c_int64)]),
+    "dash_meta_ring_set": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(ctypes.c_void_p),
+                                          ctypes.POINTER(ctypes.c_void_p), ctypes.c_int64]),
+    "dash_stage_meta": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, _c_dp, ctypes.c_int32, _c_dp,
+                                       ctypes.c_int32, ctypes.c_int32, _c_dp, ctypes.POINTER(DashStaged)]),
+    "dash_stage_release": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
     "dash_update_f64": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(DashBatch),
                                        ctypes.POINTER(DashState), _c_dp, _c_dp, ctypes.c_double]),
     "dash_update_pass_begin_f64": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(DashBatch),

@@ -968,6 +968,17 @@ struct dash_ctx {
     size_t items_host_cap[2] = {0, 0};
     cudaEvent_t staged[2] = {nullptr, nullptr};
     int cur = 0;
+    // batch index staging ring (dash_stage_meta): caller-owned pinned / device blocks
+    struct MetaSlot {
+        uint8_t *pin = nullptr, *dev = nullptr;
+        cudaEvent_t copied = nullptr, done = nullptr;
+        bool copy_issued = false, upd_issued = false;
+    };
+    static constexpr int kMetaSlots = 4;
+    MetaSlot mring[kMetaSlots];
+    int mring_n = 0, mring_i = 0, mring_last = -1;
+    size_t mring_cap = 0;
+    cudaStream_t meta_stream = nullptr;
     int last_launches = 0;
     int num_sms = 148;
     // per-update plan, shared by the pass_begin calls of one update
@@ -1945,6 +1956,11 @@ void dash_ctx_destroy(dash_ctx *ctx) {
         cudaEventDestroy(ctx->staged[i]);
     }
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+    for (auto &m : ctx->mring) {
+        if (m.copied) cudaEventDestroy(m.copied);
+        if (m.done) cudaEventDestroy(m.done);
+    }
+    if (ctx->meta_stream) cudaStreamDestroy(ctx->meta_stream);
     delete reinterpret_cast<SlicePlan *>(ctx->plan_p);
     delete ctx;
 }
@@ -2005,6 +2021,73 @@ int dash_host_row_ptr(const int64_t *counts, int64_t M, int64_t *row_ptr, int64_
     g_rp_stats.N = acc;
     g_rp_stats.nbig = nbig;
     g_rp_stats.tiles = tiles;
+    return DASH_OK;
+}
+
+int dash_meta_ring_set(dash_ctx *ctx, int32_t nslots, void *const *pinned, void *const *device, int64_t cap) {
+    if (!ctx || nslots < 1 || nslots > dash_ctx::kMetaSlots || !pinned || !device || cap < 0) return DASH_E_ARG;
+    if (!ctx->meta_stream && cudaStreamCreateWithFlags(&ctx->meta_stream, cudaStreamNonBlocking) != cudaSuccess)
+        return DASH_E_CUDA;
+    for (int i = 0; i < nslots; ++i) {
+        dash_ctx::MetaSlot &s = ctx->mring[i];
+        s.pin = (uint8_t *)pinned[i];
+        s.dev = (uint8_t *)device[i];
+        if (!s.copied && (cudaEventCreateWithFlags(&s.copied, cudaEventDisableTiming) != cudaSuccess ||
+                          cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming) != cudaSuccess))
+            return DASH_E_CUDA;
+        s.copy_issued = s.upd_issued = false;
+    }
+    ctx->mring_n = nslots;
+    ctx->mring_i = 0;
+    ctx->mring_last = -1;
+    ctx->mring_cap = (size_t)cap;
+    return DASH_OK;
+}
+
+int dash_stage_meta(dash_ctx *ctx, void *stream, const int64_t *counts, int32_t M_old, const int32_t *existing_rows,
+                    int32_t L, int32_t K_base, void *keep_dev, dash_staged *out) {
+    if (!ctx || !out || ctx->mring_n < 1 || M_old < 0 || L < 0 || (M_old > 0 && !existing_rows)) return DASH_E_ARG;
+    const int64_t M = (int64_t)M_old + L;
+    const size_t o_sr = 8 * (size_t)(M + 1), o_nw = o_sr + ((4 * (size_t)M + 7) / 8) * 8, nbytes = o_nw + (size_t)M;
+    if (nbytes > ctx->mring_cap || (M > 0 && !counts)) return DASH_E_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int si = ctx->mring_i;
+    dash_ctx::MetaSlot &s = ctx->mring[si];
+    ctx->mring_i = (si + 1) % ctx->mring_n;
+    if (s.copy_issued && cudaEventSynchronize(s.copied) != cudaSuccess) return DASH_E_CUDA;  // pinned block free again
+    int64_t *row_ptr = reinterpret_cast<int64_t *>(s.pin);
+    int64_t N = 0;
+    const int rc = dash_host_row_ptr(counts, M, row_ptr, &N);
+    if (rc != DASH_OK) return rc;
+    int32_t *sr = reinterpret_cast<int32_t *>(s.pin + o_sr);
+    if (M_old) memcpy(sr, existing_rows, sizeof(int32_t) * (size_t)M_old);
+    for (int32_t j = 0; j < L; ++j) sr[M_old + j] = K_base + j;
+    if (M_old) memset(s.pin + o_nw, 0, (size_t)M_old);
+    if (L) memset(s.pin + o_nw + M_old, 1, (size_t)L);
+    if (s.upd_issued && cudaStreamWaitEvent(ctx->meta_stream, s.done, 0) != cudaSuccess) return DASH_E_CUDA;
+    if (cudaMemcpyAsync(s.dev, s.pin, nbytes, cudaMemcpyHostToDevice, ctx->meta_stream) != cudaSuccess ||
+        cudaEventRecord(s.copied, ctx->meta_stream) != cudaSuccess || cudaStreamWaitEvent(st, s.copied, 0) != cudaSuccess)
+        return DASH_E_CUDA;
+    s.copy_issued = true;
+    if (keep_dev && cudaMemcpyAsync(keep_dev, s.dev, nbytes, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        return DASH_E_CUDA;
+    ctx->mring_last = si;
+    out->N = N;
+    out->M = (int32_t)M;
+    out->slot = si;
+    out->row_ptr = s.dev;
+    out->state_row = s.dev + o_sr;
+    out->is_new = s.dev + o_nw;
+    out->row_ptr_host = s.pin;
+    out->nbytes = (int64_t)nbytes;
+    return DASH_OK;
+}
+
+int dash_stage_release(dash_ctx *ctx, void *stream) {
+    if (!ctx || ctx->mring_last < 0) return DASH_E_ARG;
+    dash_ctx::MetaSlot &s = ctx->mring[ctx->mring_last];
+    if (cudaEventRecord(s.done, (cudaStream_t)stream) != cudaSuccess) return DASH_E_CUDA;
+    s.upd_issued = true;
     return DASH_OK;
 }
 

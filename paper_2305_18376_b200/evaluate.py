@@ -20,7 +20,9 @@ def local_error(batch_items, u_new, state):
     if (last is not None and last[0] == ids and hasattr(u_new, "device_tensor")
             and u_new.device_tensor is last[5]):
         _, row_ptr, meta, X, N, U = last
-        state_row = meta[1][:len(row_ptr) - 1]  # device copy staged by the update
+        if row_ptr is None:
+            row_ptr = meta.host_row_ptr()
+        state_row = meta[1]  # device copy staged by the update
     else:
         counts = np.array([np.asarray(r).shape[0] for _, r in batch_items], dtype=np.int64)
         row_ptr = np.zeros(len(ids) + 1, dtype=np.int64)

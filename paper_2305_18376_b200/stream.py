@@ -199,6 +199,36 @@ def _gather_rows(arrs, row_ptr, out, on_chunk=None):
             on_chunk(lo, hi)
 
 
+class _Meta:
+    """One staged batch's index arrays (dash_stage_meta): raw pointers for the
+    launch, torch / numpy views built only when somebody asks (local_error)."""
+    __slots__ = ("M", "N", "rp", "sr", "nw", "rp_host", "nbytes", "_slot", "_keep")
+
+    def __init__(self, st: "nat.DashStaged", slot, keep):
+        self.M, self.N = int(st.M), int(st.N)
+        self.rp, self.sr, self.nw, self.rp_host = st.row_ptr, st.state_row, st.is_new, st.row_ptr_host
+        self.nbytes = int(st.nbytes)
+        self._slot = slot    # (pinned bytes, device bytes) of the ring slot
+        self._keep = keep    # (arena, lo) of the persistent device copy, or None
+
+    def _dev_bytes(self):
+        if self._keep is not None:  # outlives the ring
+            a, lo = self._keep
+            return a[lo:lo + self.nbytes]
+        return self._slot[1][:self.nbytes]
+
+    def __getitem__(self, i):  # (row_ptr, state_row, is_new) device views
+        M = self.M
+        o_sr = 8 * (M + 1)
+        o_nw = o_sr + ((4 * M + 7) // 8) * 8
+        db = self._dev_bytes()
+        return (db[:o_sr].view(torch.int64), db[o_sr:o_sr + 4 * M].view(torch.int32), db[o_nw:o_nw + M])[i]
+
+    def host_row_ptr(self) -> np.ndarray:
+        """Pinned host view of row_ptr: valid until the ring wraps (3 updates)."""
+        return self._slot[0].numpy()[:8 * (self.M + 1)].view(np.int64)
+
+
 class StreamState:
     """Factors plus helper summaries of a live stream, resident on one GPU
     (stream.py:184-247).  Exclusively owned during an update."""
@@ -493,8 +523,9 @@ class StreamState:
         M = len(ids)
         counts = np.fromiter((r.shape[0] for r in arrs), dtype=np.int64, count=M)
         existing_rows = np.fromiter((rowmap[sid] for sid in ex_ids), dtype=np.int32, count=len(ex_ids))
-        N, row_ptr, meta = self._stage_meta(counts, existing_rows, len(new_ids))
-        row_ptr = row_ptr.copy()  # kept by UpdateResult / local_error beyond the ring's lifetime
+        meta = self._stage_meta(counts, existing_rows, len(new_ids))
+        N = meta.N
+        row_ptr = meta.host_row_ptr().copy()  # kept by UpdateResult / local_error beyond the ring's lifetime
         # registration (stream.py:270-280): new rows appended in batch order
         self._register(new_ids)
 
@@ -506,7 +537,7 @@ class StreamState:
             ev = torch.cuda.Event()
             ev.record()
             self._pin_event = ev
-        U_dev, v_used = self._run(X, N, row_ptr, meta, check=True, ids=ids, allreduce=allreduce)
+        U_dev, v_used = self._run(X, meta, check=True, ids=ids, allreduce=allreduce)
         self.update_index += 1
         self._last = (ids, row_ptr, meta, X, N, U_dev)
         return UpdateResult(
@@ -525,11 +556,11 @@ class StreamState:
         ``len(new_ids)`` new slices; ``counts`` their row counts.  No host sync
         unless ``check``.  Returns (U_new (N, R), v_used (J, R)) device tensors."""
         with _on(self.device):
-            N, row_ptr, meta = self._stage_meta(counts, existing_rows, len(new_ids))
+            meta = self._stage_meta(counts, existing_rows, len(new_ids))
             self._register(new_ids)
-            U_dev, v_used = self._run(X, N, row_ptr, meta, check=check, ids=None, allreduce=allreduce)
+            U_dev, v_used = self._run(X, meta, check=check, ids=None, allreduce=allreduce)
         self.update_index += 1
-        self._last = (None, row_ptr, meta, X, N, U_dev)
+        self._last = (None, None, meta, X, meta.N, U_dev)  # row_ptr: meta.host_row_ptr() on demand
         return U_dev, v_used
 
     def _register(self, new_ids):
@@ -539,20 +570,18 @@ class StreamState:
         self.slice_ids.extend(new_ids)  # _row_of catches up lazily
         self._K += L
 
-    def _run(self, X, N, row_ptr, meta, check, ids, allreduce=None):
+    def _run(self, X, meta, check, ids, allreduce=None):
         dev = self.device
-        M = len(row_ptr) - 1
+        M, N = meta.M, meta.N
         if N and X.dtype != self.dtype:
             raise TypeError(f"batch X is {X.dtype}, the stream state runs in {self.dtype}")
         if N and X.shape[0] < N:
             raise ValueError(f"batch X has {X.shape[0]} rows, the counts sum to {N}")
         f32 = self.dtype == torch.float32
-        rp_d, sr_d, nw_d = meta
         U = self._alloc_u(N)
         v_used = torch.empty((self.J, self._R), dtype=F64, device=dev)
         b = nat.DashBatch(X=_ptr(X), ldx=int(X.stride(0)) if N else self.J, N=N, M=M,
-                          row_ptr=_ptr(rp_d), row_ptr_host=row_ptr.ctypes.data,
-                          state_row=_ptr(sr_d), is_new=_ptr(nw_d))
+                          row_ptr=meta.rp, row_ptr_host=meta.rp_host, state_row=meta.sr, is_new=meta.nw)
         s = nat.DashState(W=_ptr(self._Wd), C=_ptr(self._Cd), D=_ptr(self._Dd), V=_ptr(self._V),
                           F=_ptr(self._F), G=_ptr(self._G), J=self.J, R=self._R,
                           forgetting=self.forgetting, passes=self.passes)
@@ -576,9 +605,9 @@ class StreamState:
         # batch's index arrays; the per-slice refs are built on first read
         if self.keep_u_history:
             self._ustore.append(U)
-            self._ulog.append((len(self._ustore) - 1, self._keep_meta(self._meta_bytes), M))
-        self._meta_slot[3].record()  # this update no longer reads its meta slot after this point
-        self._meta_slot[4][1] = True
+            self._ulog.append((len(self._ustore) - 1, meta, M))
+        # this update no longer reads its ring slot after this point
+        nat.check(L.dash_stage_release(self._ctx, st), "dash_stage_release")
         self._cache.clear()
         self.last_launches = L.dash_ctx_last_launches(self._ctx)
         self._err_ids = ids
@@ -601,25 +630,25 @@ class StreamState:
         a = self._uarena
         need = max(N, 0)
         if a is None or a[1] + need > a[0].shape[0]:
-            self._new_u_chunk(max(need, 4 * need, 1 << 14))
+            # chunks double (up to ~2 GB) so a long stream allocates O(log) times, not every 4th update
+            prev = 0 if a is None else a[0].shape[0]
+            cap = (2 << 30) // (8 * R)
+            self._new_u_chunk(max(4 * need, min(2 * prev, cap), 1 << 14))
             a = self._uarena
         lo = a[1]
         a[1] = lo + (need + self._U_ALIGN - 1) // self._U_ALIGN * self._U_ALIGN
         return a[0][lo:lo + need]
 
-    def _keep_meta(self, mb: torch.Tensor) -> torch.Tensor:
-        """Device copy of this update's index arrays for the U history, carved
-        from a byte arena (no allocation per update: a fresh cudaMalloc can
-        stall the host behind the GPU)."""
-        n = int(mb.shape[0])
+    def _keep_room(self, n: int):
+        """(arena, lo): ``n`` bytes of the index-array arena for the U history
+        (dash_stage_meta copies the packed block there; no allocation per
+        update: a fresh cudaMalloc can stall the host behind the GPU)."""
         a = self._marena
         if a is None or a[1] + n > a[0].shape[0]:
             self._marena = a = [torch.empty(max(16 * n, 1 << 24), dtype=torch.uint8, device=self.device), 0]
         lo = a[1]
         a[1] = lo + (n + 255) // 256 * 256
-        out = a[0][lo:lo + n]
-        out.copy_(mb, non_blocking=True)
-        return out
+        return a[0], lo
 
     def _new_u_chunk(self, rows: int):
         self._uarena = [torch.empty((rows, self._R), dtype=self.dtype, device=self.device), 0]
@@ -639,8 +668,8 @@ class StreamState:
             return
         pending, self._ulog = self._ulog, []
         ids = self.slice_ids
-        for bi, mb, M in pending:
-            hb = mb.cpu().numpy()
+        for bi, meta, M in pending:
+            hb = meta._dev_bytes().cpu().numpy()
             o_sr = 8 * (M + 1)
             rp = hb[:o_sr].view(np.int64)
             sr = hb[o_sr:o_sr + 4 * M].view(np.int32)
@@ -649,67 +678,47 @@ class StreamState:
 
     _META_RING = 3  # updates whose index arrays stay valid (local_error reads the last one)
 
-    def _stage_meta(self, counts, existing_rows, L):
-        """Pack the batch's CSR index arrays -- row_ptr (M+1) i64 | state_row
-        (M) i32 | is_new (M) u8 -- into one pinned ring slot (the prefix sum is
-        written there by the library's host helper) and copy them to the
-        device in ONE transfer on a side stream, so the copy runs while the
-        previous update's kernels still execute and the update's first kernel
-        follows the previous one with only an event wait between them.  The
-        host never waits for the GPU unless the ring wraps onto a copy still
-        in flight; a device slot is rewritten only after the update that read
-        it has finished.  Returns (N, row_ptr host view, (row_ptr, state_row,
-        is_new) device views)."""
+    def _stage_meta(self, counts, existing_rows, L) -> _Meta:
+        """Stage the batch's CSR index arrays -- row_ptr (M+1) i64 | state_row
+        (M) i32 | is_new (M) u8 -- through the library's ring (dash_stage_meta):
+        prefix sum written straight into a pinned slot, ONE host-to-device copy
+        on a side stream (it runs while the previous update's kernels still
+        execute; the update's first kernel follows with only an event wait),
+        and, with the U history kept, a device copy into the history's index
+        arena.  The host never waits for the GPU unless the ring wraps onto a
+        copy still in flight; a device slot is rewritten only after the update
+        that read it has been issued (dash_stage_release).  One native call per
+        update: the Python-side ring this replaces cost ~90 us of interpreter
+        and torch-call overhead per update, more than a medium-sized update's
+        kernels."""
         counts = np.ascontiguousarray(counts, dtype=np.int64)
-        M_old = len(existing_rows)
+        existing_rows = np.ascontiguousarray(existing_rows, dtype=np.int32)
+        M_old = existing_rows.shape[0]
         M = M_old + L
         if counts.shape[0] != M:
             raise ValueError(f"{counts.shape[0]} counts for {M_old} existing + {L} new slices")
-        o_sr = 8 * (M + 1)
-        o_nw = o_sr + ((4 * M + 7) // 8) * 8
-        nbytes = o_nw + M
+        nbytes = 8 * (M + 1) + ((4 * M + 7) // 8) * 8 + M
         ring = getattr(self, "_meta_ring", None)
+        lib = nat.lib()
         if ring is None or ring[0][0].shape[0] < nbytes:
             cap = max(4096, int(nbytes * 1.25) + 64)
             if ring is not None:
                 torch.cuda.current_stream(self.device).synchronize()  # old slots may still be read
-            # slot: pinned bytes, device bytes, copy-done event, update-done event, [copy issued, update issued]
-            ring = [[torch.empty(cap, dtype=torch.uint8, pin_memory=True),
-                     torch.empty(cap, dtype=torch.uint8, device=self.device),
-                     torch.cuda.Event(), torch.cuda.Event(), [False, False]]
-                    for _ in range(self._META_RING)]
+            ring = [(torch.empty(cap, dtype=torch.uint8, pin_memory=True),
+                     torch.empty(cap, dtype=torch.uint8, device=self.device)) for _ in range(self._META_RING)]
+            pins = (ctypes.c_void_p * len(ring))(*[t[0].data_ptr() for t in ring])
+            devs = (ctypes.c_void_p * len(ring))(*[t[1].data_ptr() for t in ring])
+            nat.check(lib.dash_meta_ring_set(self._ctx, len(ring), pins, devs, cap), "dash_meta_ring_set")
             self._meta_ring = ring
-            self._meta_i = 0
-            if getattr(self, "_meta_stream", None) is None:
-                self._meta_stream = torch.cuda.Stream(self.device)
-        slot = ring[self._meta_i]
-        self._meta_i = (self._meta_i + 1) % self._META_RING
-        if slot[4][0]:
-            slot[2].synchronize()  # the pinned bytes' previous upload is done
-        hb = slot[0].numpy()
-        row_ptr = hb[:o_sr].view(np.int64)
-        Nout = ctypes.c_int64(0)
-        nat.check(nat.load_library().dash_host_row_ptr(counts.ctypes.data, M, row_ptr.ctypes.data,
-                                                       ctypes.byref(Nout)), "dash_host_row_ptr")
-        sr = hb[o_sr:o_sr + 4 * M].view(np.int32)
-        sr[:M_old] = existing_rows
-        sr[M_old:] = np.arange(self._K, self._K + L, dtype=np.int32)
-        nw = hb[o_nw:o_nw + M]
-        nw[:M_old] = 0
-        nw[M_old:] = 1
-        db = slot[1]
-        cs = self._meta_stream
-        with torch.cuda.stream(cs):
-            if slot[4][1]:
-                cs.wait_event(slot[3])  # the update that last read this device slot is done
-            db[:nbytes].copy_(slot[0][:nbytes], non_blocking=True)
-            slot[2].record(cs)
-        slot[4][0] = True
-        torch.cuda.current_stream(self.device).wait_event(slot[2])
-        self._meta_slot = slot
-        self._meta_bytes = db[:nbytes]
-        meta = (db[:o_sr].view(torch.int64), db[o_sr:o_sr + 4 * M].view(torch.int32), db[o_nw:o_nw + M])
-        return int(Nout.value), row_ptr, meta
+        keep = self._keep_room(nbytes) if self.keep_u_history else None
+        out = nat.DashStaged()
+        rc = lib.dash_stage_meta(self._ctx, nat.stream_ptr(), counts.ctypes.data, M_old,
+                                 existing_rows.ctypes.data if M_old else None, L, self._K,
+                                 keep[0].data_ptr() + keep[1] if keep is not None else None, ctypes.byref(out))
+        if rc == nat.DASH_E_ARG:
+            raise ValueError("row counts must be non-negative")
+        nat.check(rc, "dash_stage_meta")
+        return _Meta(out, ring[out.slot], keep)
 
     def check(self):
         """Synchronise and raise SolveError for a device-side solver failure."""
