@@ -83,8 +83,22 @@ class Schedule:
             active += L
 
 
-def owned(k, rank, world):
-    return k % world == rank
+def ownership(cfg, sched, world):
+    """Owner rank of every slice that will ever exist, by the engine's own
+    placement rule (distributed.Placement: initial slices by position, each
+    new slice to the rank with the least rows in the update that brings it).
+    Computed identically on every rank from the shared schedule."""
+    from paper_2305_18376_b200.distributed import owner_of_index, place_counts
+    n_all = cfg.K0 + sum(len(n) for n in sched.new_len)
+    owner = np.full(n_all, -1, dtype=np.int64)
+    owner[:cfg.K0] = [owner_of_index(k, world) for k in range(cfg.K0)]
+    n_owned = [int(v) for v in np.bincount(owner[:cfg.K0], minlength=world)]
+    active = cfg.K0
+    for add, new_len in zip(sched.adds, sched.new_len):
+        load = np.bincount(owner[:active], weights=add, minlength=world)
+        owner[active:active + len(new_len)] = place_counts(world, n_owned, load, new_len)
+        active += len(new_len)
+    return owner
 
 
 def algorithmic_bytes(N, J, R, M_old, L, b=8):
@@ -291,7 +305,8 @@ def run_gpu(args):
     n_all = cfg.K0 + sum(len(n) for n in sched.new_len)
     w_true = np.random.default_rng([cfg.seed, 12]).uniform(size=(n_all, R))
     # planted initial state (closed form, see workloads.planted_state) for owned slices
-    own0 = np.array([k for k in range(cfg.K0) if owned(k, rank, world)], dtype=np.int64)
+    owner = ownership(cfg, sched, world)
+    own0 = np.nonzero(owner[:cfg.K0] == rank)[0].astype(np.int64)
     D0 = H.T @ H
     vtv = V.T @ V
     Wl = w_true[own0]
@@ -318,10 +333,10 @@ def run_gpu(args):
     batches = []
     for t in range(total_steps):
         add = sched.adds[t]
-        ex = [k for k in active if owned(k, rank, world)]
+        ex = [k for k in active if owner[k] == rank]
         ex_counts = add[np.array(ex, dtype=np.int64)] if ex else np.zeros(0, np.int64)
         base = len(active)
-        new = [base + i for i in range(len(sched.new_len[t])) if owned(base + i, rank, world)]
+        new = [base + i for i in range(len(sched.new_len[t])) if owner[base + i] == rank]
         new_counts = sched.new_len[t][np.array(new, dtype=np.int64) - base] if new else np.zeros(0, np.int64)
         active.extend(range(base, base + len(sched.new_len[t])))
         ex_rows = np.array([local_row[k] for k in ex], dtype=np.int32)

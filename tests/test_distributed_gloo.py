@@ -125,3 +125,41 @@ def test_two_rank_sharded_update_equals_single_process():
     for sid, w in allw.items():
         want = ref.W[ref.row_of(sid)]
         assert np.abs(w - want).max() <= 1e-12 * max(1.0, np.abs(want).max())
+
+
+def test_new_slices_go_to_the_least_loaded_rank_deterministically():
+    """a new slice lands on the rank with the fewest rows in the update that brings it
+    (ties: fewer owned slices, then the lowest rank); every rank computes the same map."""
+    from paper_2305_18376_b200.distributed import Placement, place_counts
+    world = 4
+    ids = [f"s{k}" for k in range(10)]
+    rng = np.random.default_rng(0)
+    maps = []
+    for _ in range(2):  # two "ranks" replaying the same batches
+        pl = Placement(world, ids)
+        assert [pl.owner[s] for s in ids] == [k % world for k in range(10)]
+        r2 = np.random.default_rng(1)
+        known = list(ids)
+        for t in range(5):
+            ex = [(s, int(r2.integers(1, 9))) for s in known]
+            new = [(f"n{t}_{i}", int(r2.integers(200, 2001))) for i in range(6)]
+            owners = pl.place(ex, new)
+            # replay the rule by hand
+            load = [0] * world
+            for s, n in ex:
+                load[pl.owner[s]] += n
+            # (owners were appended in order; check each choice was a minimum at its time)
+            own_cnt = [sum(1 for s in known if pl.owner[s] == q) for q in range(world)]
+            for (s, n), r in zip(new, owners):
+                assert (load[r], own_cnt[r], r) == min((load[q], own_cnt[q], q) for q in range(world))
+                load[r] += n
+                own_cnt[r] += 1
+            known += [s for s, _ in new]
+            # per-update rows end up balanced to within one new slice
+            assert max(load) - min(load) <= 2000
+        maps.append(dict(pl.owner))
+    assert maps[0] == maps[1]
+    # index form used by bench.py agrees with the id form
+    pl = Placement(2, ["a", "b", "c"])
+    got = place_counts(2, list(pl.n_owned), [5, 1], [10, 3, 3])
+    assert list(got) == pl.place([("a", 3), ("b", 1), ("c", 2)], [("x", 10), ("y", 3), ("z", 3)])
