@@ -61,6 +61,8 @@ def parse():
                     help="skip the FP32 data-mode measurement")
     ap.add_argument("--dropin-steps", type=int, default=3,
                     help="timed StreamState.update(UpdateBatch) calls on host batches (0: skip)")
+    ap.add_argument("--parity-steps", type=int, default=2,
+                    help="full-size updates of this config checked against the CPU oracle (0: skip)")
     ap.add_argument("--no-als", dest="als", action="store_false",
                     help="skip the parafac2_als sweep timing (medium, daily)")
     return ap.parse_args()
@@ -479,6 +481,9 @@ def run_gpu(args):
     dropin = None
     if world == 1 and args.dropin_steps > 0:
         dropin = run_dropin(cfg, arrays, args.dropin_steps, dev)
+    parity = None
+    if world == 1 and args.parity_steps > 0:
+        parity = run_parity(cfg, args.parity_steps, dev)
     als = None
     if world == 1 and args.als:
         als = {name: als_timing(name, dev) for name in ("medium", "daily")}
@@ -537,6 +542,7 @@ def run_gpu(args):
             "lu_fallbacks": fallbacks,
             "fp32": fp32,
             "e2e_dropin": dropin,
+            "parity": parity,
             "als": als,
             "clocks": clocks,
         }
@@ -571,6 +577,47 @@ def run_dropin(cfg, arrays, steps, dev):
     return {"value": elems / secs, "unit": "elements/s", "ms_per_step": 1e3 * secs / len(times),
             "steps": len(times), "h2d_bytes_per_step": h2d / len(times), "d2h_bytes_per_step": d2h / len(times),
             "api": "StreamState.update(UpdateBatch) with host numpy rows (wall clock, synchronous)"}
+
+
+def run_parity(cfg, steps, dev):
+    """Parity of the timed configuration at its full size (the oracle as the
+    checker, outside every timed region): `steps` updates of this config
+    through StreamState.update on a fresh planted state (FP64, and the FP32
+    data mode), each compared with the CPU oracle on the same host batches --
+    max over the updates of max|a - b| / max|b| per array."""
+    import torch
+
+    from oracle import dash_oracle as orc
+    from paper_2305_18376_b200.evaluate import local_error
+    from paper_2305_18376_b200.stream import StreamState
+    orc.build_c()
+    arrays, gen = host_stream(cfg, steps, seed_extra=2)
+    gpu = StreamState.from_arrays(arrays, device=dev)
+    g32 = StreamState.from_arrays(arrays, device=dev, dtype=torch.float32)
+    cpu = oracle_state(arrays)
+
+    def rel(a, b):
+        return float(np.abs(np.asarray(a) - b).max() / max(float(np.abs(b).max()), 1e-300))
+
+    worst, worst32 = {}, {}
+    for batch, _ in gen():
+        ids = [sid for sid, _, _ in batch.items()]
+        res, r32, ref = gpu.update(batch), g32.update(batch), cpu.update(batch)
+        Uo = np.concatenate([ref["u_new"][s] for s in ids])
+        w_rows = {s: cpu.W[cpu.row_of(s)] for s in ids}
+        le_ref = orc.local_error([(s, r) for s, r, _ in batch.items()], ref["u_new"], w_rows, cpu.V)[0]
+        for eng, r, acc in ((gpu, res, worst), (g32, r32, worst32)):
+            errs = {"u_new": rel(r.u_new.device_tensor.cpu().numpy(), Uo), "v_used": rel(r.v_used, ref["v_used"])}
+            for name in ("W", "C", "D", "F", "G", "V"):
+                errs[name] = rel(getattr(eng, name), getattr(cpu, name))
+            le = local_error([(s, r_) for s, r_, _ in batch.items()], r.u_new, eng)[0]
+            errs["local_error"] = abs(le - le_ref) / max(abs(le_ref), 1e-300)
+            for k, v in errs.items():
+                acc[k] = max(acc.get(k, 0.0), v)
+    return {"updates": steps, "config": cfg.name, "K0": cfg.K0, "against": "CPU oracle (oracle/dash_oracle.py), same host batches",
+            "metric": "max over updates of max|gpu - oracle| / max|oracle| per array",
+            "fp64": {"tol": 1e-8, "max_err": worst, "ok": bool(max(worst.values()) <= 1e-8)},
+            "fp32_data_mode": {"tol": 1e-3, "max_err": worst32, "ok": bool(max(worst32.values()) <= 1e-3)}}
 
 
 def als_timing(name, dev, iters=3):

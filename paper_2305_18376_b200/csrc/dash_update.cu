@@ -979,6 +979,20 @@ struct dash_ctx {
     int mring_n = 0, mring_i = 0, mring_last = -1;
     size_t mring_cap = 0;
     cudaStream_t meta_stream = nullptr;
+    // Device slice plan on the staging side stream: the plan of update t+1 (k_plan_*: a pure
+    // function of the batch's index arrays, which arrive on that stream) runs while update t's
+    // kernels still execute.  Its outputs (smeta, plan_hist, tflag + tgen) are double-buffered:
+    // the fields above/below hold the current set, pset_alt the other one; pset_free fires when
+    // the update that read the current set has been issued in full.
+    struct PlanSet {
+        Buf smeta, plan_hist, tflag;
+        uint32_t tgen = 0;
+        cudaEvent_t free_ev = nullptr;
+        bool used = false;
+    } pset_alt;
+    cudaEvent_t pset_free = nullptr, plan_ev = nullptr;
+    bool pset_used = false, side_plan = false;
+    int cur_pass = 0;
     int last_launches = 0;
     int num_sms = 148;
     // per-update plan, shared by the pass_begin calls of one update
@@ -1650,7 +1664,10 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
     static const bool host_timing = getenv("DASH_HOST_TIMING") != nullptr;
     auto tnow = [] { return std::chrono::steady_clock::now(); };
     auto t0 = tnow();
+    ctx->cur_pass = pass;
+    cudaStream_t pst = st;  // stream of the plan kernels (the staging side stream when the plan runs ahead)
     if (pass == 0) {
+        ctx->side_plan = false;
         ctx->last_launches = 0;
         if (!ctx->plan_p) ctx->plan_p = new SlicePlan();
         plan_of(ctx) = make_plan(b->row_ptr_host, M, RB, R, ctx->num_sms);
@@ -1709,14 +1726,34 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
             ctx->bigx_nbig = ctx->bigx ? pl.gbig : 0;
             ctx->bigx_grid = ctx->bigx ? (int)std::min<int64_t>(ctx->num_sms, pl.big_tiles) : 0;
             if (ctx->smallx) ctx->nitems = ctx->sx_grid + pl.gbig;  // G slots: one per small-kernel CTA + big slice
+            {
+                // side-stream plan: only for batches staged by dash_stage_meta (their index arrays were
+                // copied on meta_stream, so the plan kernels there are ordered behind the copy)
+                static const bool side_off = getenv("DASH_NO_SIDE_PLAN") != nullptr;
+                // (small updates are host-bound: the three extra stream calls would cost more than they hide)
+                const bool will_plan = pl.split && M > 0 && N >= 32768 && !ctx->smallx;
+                ctx->side_plan = will_plan && !side_off && !ctx->prof && ctx->meta_stream && ctx->mring_last >= 0 &&
+                                 (const void *)b->row_ptr == (const void *)ctx->mring[ctx->mring_last].dev;
+                if (ctx->side_plan) {
+                    std::swap(ctx->smeta, ctx->pset_alt.smeta);
+                    std::swap(ctx->plan_hist, ctx->pset_alt.plan_hist);
+                    std::swap(ctx->tflag, ctx->pset_alt.tflag);
+                    std::swap(ctx->tgen, ctx->pset_alt.tgen);
+                    std::swap(ctx->pset_free, ctx->pset_alt.free_ev);
+                    std::swap(ctx->pset_used, ctx->pset_alt.used);
+                    pst = ctx->meta_stream;
+                    // the update that last read this set must have been issued in full
+                    if (ctx->pset_used && cudaStreamWaitEvent(pst, ctx->pset_free, 0) != cudaSuccess) return DASH_E_CUDA;
+                }
+            }
             if (ctx->bigx) {
                 const size_t tb = sizeof(uint32_t) * (size_t)((N + kTR - 1) / kTR + 16);
                 if (ctx->tflag.cap < tb) {  // zeroed once: marks are generation-tagged
                     if (ensure(ctx->tflag, tb)) return DASH_E_CUDA;
-                    cudaMemsetAsync(ctx->tflag.p, 0, ctx->tflag.cap, st);
+                    cudaMemsetAsync(ctx->tflag.p, 0, ctx->tflag.cap, pst);
                 }
                 if (++ctx->tgen == 0) {  // generation wrapped: clear, restart at 1
-                    cudaMemsetAsync(ctx->tflag.p, 0, ctx->tflag.cap, st);
+                    cudaMemsetAsync(ctx->tflag.p, 0, ctx->tflag.cap, pst);
                     ctx->tgen = 1;
                 }
             }
@@ -1738,7 +1775,10 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
         if (!items.empty() && stage_items(ctx, st, items)) return DASH_E_CUDA;
         ctx->planned = plan_of(ctx).split && M > 0 && N > 0 && (!ctx->smallx || ctx->bigx);
         if (ctx->planned &&
-            device_plan(ctx, st, b, ctx->bigx ? (uint32_t *)ctx->tflag.p : nullptr))
+            device_plan(ctx, pst, b, ctx->bigx ? (uint32_t *)ctx->tflag.p : nullptr))
+            return DASH_E_CUDA;
+        if (ctx->side_plan && (cudaEventRecord(ctx->plan_ev, pst) != cudaSuccess ||
+                               cudaStreamWaitEvent(st, ctx->plan_ev, 0) != cudaSuccess))
             return DASH_E_CUDA;
         if (M > 0 && !ctx->stream && (!ctx->wtma || ctx->swide)) {  // row -> slice map: the generic F GEMM, k_us_rows
             PhaseScope ps(ctx, st, PH_ROWSLICE);
@@ -1800,7 +1840,8 @@ int pass_begin_impl(dash_ctx *ctx, void *stream, const B *b, dash_state_f64 *s, 
             const FusedPrologue pro{(double *)ctx->vtv.p, s->F, s->G, (double *)ctx->fsnap.p, (double *)ctx->gsnap.p,
                                     v_used_out, pass == 0, last};
             // PDL only behind the plan kernels (pass 0); a later pass follows the V solve
-            if (launch_xv3(ctx, st, b, J, s->V, R, XV, pro, pass == 0,
+            // (not when the plan ran on the side stream: the kernel before this one is then the previous update's)
+            if (launch_xv3(ctx, st, b, J, s->V, R, XV, pro, pass == 0 && !ctx->side_plan,
                            ctx->bigx ? (const uint32_t *)ctx->tflag.p : nullptr))
                 return DASH_E_CUDA;
         } else if (ctx->stream) {
@@ -1961,6 +2002,10 @@ void dash_ctx_destroy(dash_ctx *ctx) {
         if (m.done) cudaEventDestroy(m.done);
     }
     if (ctx->meta_stream) cudaStreamDestroy(ctx->meta_stream);
+    for (auto e : {ctx->plan_ev, ctx->pset_free, ctx->pset_alt.free_ev})
+        if (e) cudaEventDestroy(e);
+    for (auto *b : {&ctx->pset_alt.smeta, &ctx->pset_alt.plan_hist, &ctx->pset_alt.tflag})
+        if (b->p) cudaFree(b->p);
     delete reinterpret_cast<SlicePlan *>(ctx->plan_p);
     delete ctx;
 }
@@ -2037,6 +2082,10 @@ int dash_meta_ring_set(dash_ctx *ctx, int32_t nslots, void *const *pinned, void 
             return DASH_E_CUDA;
         s.copy_issued = s.upd_issued = false;
     }
+    if (!ctx->plan_ev && (cudaEventCreateWithFlags(&ctx->plan_ev, cudaEventDisableTiming) != cudaSuccess ||
+                          cudaEventCreateWithFlags(&ctx->pset_free, cudaEventDisableTiming) != cudaSuccess ||
+                          cudaEventCreateWithFlags(&ctx->pset_alt.free_ev, cudaEventDisableTiming) != cudaSuccess))
+        return DASH_E_CUDA;
     ctx->mring_n = nslots;
     ctx->mring_i = 0;
     ctx->mring_last = -1;
@@ -2169,6 +2218,10 @@ int dash_update_pass_finish_f64(dash_ctx *ctx, void *stream, dash_state_f64 *s, 
                                                                s->F, s->G, s->V, ctx->err, ctx->fallbacks);
             break;
         }
+    }
+    if (ctx->pset_free && ctx->cur_pass == s->passes - 1) {  // the plan set of this update is free again
+        cudaEventRecord(ctx->pset_free, st);
+        ctx->pset_used = true;
     }
     return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_E_CUDA;
 }
