@@ -508,7 +508,30 @@ int dash_als_sweep_f64(dash_ctx *ctx, void *stream, const dash_batch_f64 *t, int
     dash_batch_f64 b = *t;
     b.state_row = ident;
     k_row_slice<<<std::min(ctx->num_sms * 4, (K + 7) / 8 + 1), 256, 0, st>>>(t->row_ptr, K, row_slice);
-    launch_xv(ctx, st, &b, J, V, R, XV);
+    // the two streaming contractions take the update path's tensor-map kernels when the shape allows
+    // (R bucket 16 and even, J <= 128: k_xv3 / k_fgemm3; J > 128: k_xvw / k_fgemmw), else the generic ones
+    const bool tma = N > 0 && tma_ok(&b, J, R) && !ensure(ctx->vtv, sizeof(double) * R * R) &&
+                     !ensure(ctx->fsnap, sizeof(double) * J * R) && !ensure(ctx->gsnap, sizeof(double) * R * R);
+    const bool wide = !tma && N > 0 && widej_ok(&b, J, R, V);
+    if (tma) {
+        nsplit = ctx->num_sms;  // one F slot per CTA
+    } else if (wide) {
+        const int fc = RB <= 32 ? WideCfg<32>::FC : WideCfg<64>::FC;
+        ctx->wnj = (J + fc - 1) / fc;
+        const int64_t nrow = std::max<int64_t>(1, ctx->num_sms / ctx->wnj);
+        ctx->rps = std::max<int64_t>(32, ((N + nrow - 1) / nrow + 31) / 32 * 32);
+        ctx->nsplit = nsplit = (N + ctx->rps - 1) / ctx->rps;
+    }
+    if ((tma || wide) && ensure(ctx->fslots, sizeof(double) * nsplit * J * R)) return DASH_E_CUDA;
+    if (tma) {
+        const FusedPrologue pro{(double *)ctx->vtv.p, V, V, (double *)ctx->fsnap.p, (double *)ctx->gsnap.p,
+                                (double *)ctx->fsnap.p, 0, 0};  // only vtv is produced (unused here)
+        if (launch_xv3(ctx, st, &b, J, V, R, XV, pro, false)) return DASH_E_CUDA;
+    } else if (wide) {
+        if (launch_xvw(ctx, st, &b, J, V, R, XV)) return DASH_E_CUDA;
+    } else {
+        launch_xv(ctx, st, &b, J, V, R, XV);
+    }
     switch (RB) {
         case 4: launch_als_polar<4>(ctx, st, t->row_ptr, K, XV, W, H, R, T, Q, yv); break;
         case 8: launch_als_polar<8>(ctx, st, t->row_ptr, K, XV, W, H, R, T, Q, yv); break;
@@ -522,9 +545,16 @@ int dash_als_sweep_f64(dash_ctx *ctx, void *stream, const dash_batch_f64 *t, int
         default: launch_als_cp<32>(st, yv, K, V, J, R, eps, H, W, lhs_v, ctx->err); break;
     }
     const int qb = (int)std::min<int64_t>((N * R + 255) / 256, (int64_t)ctx->num_sms * 16);
-    // rhs_v = X^T ((Q H) o w): the F GEMM multiplies "U" = Q H by W[state_row[slice]]
-    k_als_qh<<<std::max(qb, 1), 256, 0, st>>>(Q, H, nullptr, row_slice, N, R, Z);
-    launch_fgemm(ctx, st, &b, J, Z, row_slice, W, R, rps, (int)nsplit, (double *)ctx->fslots.p);
+    // rhs_v = X^T ((Q H) o w).  Tensor-map paths: Z = (Q H) o w once (the loss below reads the same Z);
+    // generic path: the F GEMM multiplies "U" = Q H by W[state_row[slice]] itself
+    k_als_qh<<<std::max(qb, 1), 256, 0, st>>>(Q, H, (tma || wide) ? W : nullptr, row_slice, N, R, Z);
+    if (tma) {
+        if (launch_f3(ctx, st, &b, J, Z, R, (double *)ctx->fslots.p)) return DASH_E_CUDA;
+    } else if (wide) {
+        if (launch_fw(ctx, st, &b, J, Z, R, (double *)ctx->fslots.p, nullptr)) return DASH_E_CUDA;
+    } else {
+        launch_fgemm(ctx, st, &b, J, Z, row_slice, W, R, rps, (int)nsplit, (double *)ctx->fslots.p);
+    }
     if (colsum(ctx, st, (double *)ctx->fslots.p, (int)nsplit, (int64_t)J * R, (double *)ctx->fg.p))
         return DASH_E_CUDA;
     // V = ridge(lhs_v, rhs_v^T)^T  (rhs_v^T (R x J): entry (r, j) = rhs_v[j][r])
@@ -535,7 +565,7 @@ int dash_als_sweep_f64(dash_ctx *ctx, void *stream, const dash_batch_f64 *t, int
         default: k_ridge<32><<<1, 32, 0, st>>>(lhs_v, (double *)ctx->fg.p, R, J, 1, R, eps, V, ctx->err); break;
     }
     // loss with the refreshed H, W, V (als.py:182-185): Z = (Q H) o w
-    k_als_qh<<<std::max(qb, 1), 256, 0, st>>>(Q, H, W, row_slice, N, R, Z);
+    if (!(tma || wide)) k_als_qh<<<std::max(qb, 1), 256, 0, st>>>(Q, H, W, row_slice, N, R, Z);
     if (ensure(ctx->rerr, sizeof(double) * (size_t)N)) return DASH_E_CUDA;
     launch_row_err<false>(ctx, st, t->X, t->ldx, N, (const double *)Z, R, V, J, (const int32_t *)nullptr,
                           (const int32_t *)nullptr, (const double *)nullptr, (double *)ctx->rerr.p);

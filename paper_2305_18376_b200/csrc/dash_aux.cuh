@@ -358,11 +358,88 @@ __global__ void __launch_bounds__(256) k_tree_sum(const double *__restrict__ v, 
     if (threadIdx.x == 0) *out = mean ? (n > 0 ? part[0] / n : 0.0) : part[0];
 }
 
+// Same row errors with the reconstruction on the FP64 tensor cores: a warp takes 8 rows, its A
+// fragments are the rows' Z (o w) values, B fragments come from V staged in shared memory (pitch
+// RB + 4: the fragment's 8 x 4 reads hit distinct banks), one 8 x 8 tile of Z V^T per 8 columns;
+// each lane then owns two reconstructed entries of one row, subtracts them from X and
+// accumulates; the four lanes of a row are summed in a fixed order.  ~10x fewer instructions
+// than the scalar loop above, which was shared-memory-issue bound at ~1 TB/s.
+template <bool ABS, typename TX, typename TU, int RB>
+__global__ void __launch_bounds__(256) k_row_err_mma(const TX *__restrict__ X, int64_t ldx, int64_t N,
+                                                     const TU *__restrict__ Z, int R, const double *__restrict__ V,
+                                                     int J, const int32_t *__restrict__ row_slice,
+                                                     const int32_t *__restrict__ state_row,
+                                                     const double *__restrict__ W, double *__restrict__ row_err) {
+    constexpr int P = RB == 4 ? 4 : RB + 4, KS = RB / 4;
+    extern __shared__ double vs[];  // J8 x P, zero padded
+    const int J8 = (J + 7) / 8 * 8;
+    for (int i = threadIdx.x; i < J8 * P; i += blockDim.x) {
+        const int j = i / P, r = i % P;
+        vs[i] = (j < J && r < R) ? V[(int64_t)j * R + r] : 0.0;
+    }
+    __syncthreads();
+    const int lane = lane_id(), g = lane >> 2, t = lane & 3;
+    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp_id(), nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int64_t nblk = (N + 7) / 8;
+    for (int64_t blk = gw; blk < nblk; blk += nw) {
+        const int64_t row = blk * 8 + g;
+        const bool valid = row < N;
+        const double *wr = (W && valid) ? W + (int64_t)state_row[row_slice[row]] * R : nullptr;
+        double a[KS];
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk) {
+            const int r = 4 * kk + t;
+            a[kk] = (valid && r < R) ? (double)Z[row * R + r] * (wr ? wr[r] : 1.0) : 0.0;
+        }
+        const TX *xrow = X + (valid ? row : 0) * ldx;
+        double acc = 0.0;
+        for (int j0 = 0; j0 < J8; j0 += 8) {
+            const int j = j0 + 2 * t;
+            const double x0 = (valid && j < J) ? (double)xrow[j] : 0.0;
+            const double x1 = (valid && j + 1 < J) ? (double)xrow[j + 1] : 0.0;
+            double c[2] = {0.0, 0.0};
+            const double *vb = vs + (j0 + g) * P + t;
+#pragma unroll
+            for (int kk = 0; kk < KS; ++kk) dmma884(c, a[kk], vb[4 * kk]);
+            const double d0 = x0 - c[0], d1 = x1 - c[1];  // padded columns: x = 0 and rec = 0
+            acc = ABS ? acc + fabs(d0) + fabs(d1) : fma(d1, d1, fma(d0, d0, acc));
+        }
+        acc += __shfl_xor_sync(FULL_MASK, acc, 1);
+        acc += __shfl_xor_sync(FULL_MASK, acc, 2);
+        if (t == 0 && valid) row_err[row] = acc;
+    }
+}
+
+template <bool ABS, typename TX, typename TU, int RB>
+void launch_row_err_mma(dash_ctx *ctx, cudaStream_t st, const TX *X, int64_t ldx, int64_t N, const TU *Z, int R,
+                        const double *V, int J, const int32_t *row_slice, const int32_t *state_row, const double *W,
+                        double *row_err, size_t smem) {
+    ensure_smem_attr(k_row_err_mma<ABS, TX, TU, RB>, smem);
+    const int blocks = (int)std::min<int64_t>((N + 63) / 64, (int64_t)ctx->num_sms * 8);
+    k_row_err_mma<ABS, TX, TU, RB><<<std::max(blocks, 1), 256, smem, st>>>(X, ldx, N, Z, R, V, J, row_slice,
+                                                                           state_row, W, row_err);
+}
+
 template <bool ABS, typename TX, typename TU>
 int launch_row_err(dash_ctx *ctx, cudaStream_t st, const TX *X, int64_t ldx, int64_t N, const TU *Z, int R,
                    const double *V, int J, const int32_t *row_slice, const int32_t *state_row, const double *W,
                    double *row_err) {
     if (N <= 0) return 0;
+    {
+        static const bool scalar = getenv("DASH_ROWERR_SCALAR") != nullptr;  // A/B switch
+        const int RB = rank_bucket(R), P = RB == 4 ? 4 : RB + 4;
+        const size_t sm = sizeof(double) * (size_t)((J + 7) / 8 * 8) * P;
+        if (!scalar && sm <= 96 * 1024) {
+            switch (RB) {
+                case 4: launch_row_err_mma<ABS, TX, TU, 4>(ctx, st, X, ldx, N, Z, R, V, J, row_slice, state_row, W, row_err, sm); break;
+                case 8: launch_row_err_mma<ABS, TX, TU, 8>(ctx, st, X, ldx, N, Z, R, V, J, row_slice, state_row, W, row_err, sm); break;
+                case 16: launch_row_err_mma<ABS, TX, TU, 16>(ctx, st, X, ldx, N, Z, R, V, J, row_slice, state_row, W, row_err, sm); break;
+                case 32: launch_row_err_mma<ABS, TX, TU, 32>(ctx, st, X, ldx, N, Z, R, V, J, row_slice, state_row, W, row_err, sm); break;
+                default: launch_row_err_mma<ABS, TX, TU, 64>(ctx, st, X, ldx, N, Z, R, V, J, row_slice, state_row, W, row_err, sm); break;
+            }
+            return 0;
+        }
+    }
     const size_t smem = (int64_t)J * R <= kRecVS ? sizeof(double) * (size_t)J * (R + 1) : 0;
     ensure_smem_attr(k_row_err<ABS, TX, TU>, smem);
     const int blocks = (int)std::min<int64_t>((N + 7) / 8, (int64_t)ctx->num_sms * 8);
