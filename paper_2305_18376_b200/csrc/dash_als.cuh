@@ -53,7 +53,11 @@ struct AlsSmem {
     static constexpr int NQ = RB * RB;
     // shared: H[RB*LD] + pair tables (NP + NQ) * 2 ints
     static constexpr int shared = RB * LD + (NP + NQ);
-    __host__ __device__ static constexpr size_t bytes(int nw) { return sizeof(double) * (shared + nw * per_warp); }
+    static constexpr int NRL = (NQ + 31) / 32;  // values per lane in the cross-warp reduction buffer
+    // + red[nw][32 * NRL]: per-warp Gram partials, summed in warp order by every warp
+    __host__ __device__ static constexpr size_t bytes(int nw) {
+        return sizeof(double) * (shared + nw * per_warp + nw * 32 * NRL);
+    }
 };
 
 template <int RB, int NW>
@@ -74,6 +78,21 @@ __global__ void __launch_bounds__(NW * 32) k_als_polar(const int64_t *__restrict
     double *rows = base, *rows2 = rows + 32 * LD;
     double *L1 = rows2 + 32 * LD, *L2 = L1 + RB * LD, *Ms = L2 + RB * LD, *Ss = Ms + RB * LD;
     double *d1 = Ss + RB * LD, *d2 = d1 + RB, *wv = d2 + RB;
+    double *red = sm + S::shared + NW * S::per_warp;
+    // Gram partials of the CTA's warps -> every warp holds the full sum (fixed warp order)
+    auto reduce = [&](auto &acc) {
+        constexpr int n = (int)(sizeof(acc) / sizeof(double));
+#pragma unroll
+        for (int q = 0; q < n; ++q) red[(w * S::NRL + q) * 32 + lane] = acc[q];
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < n; ++q) {
+            double t = 0.0;
+            for (int ww = 0; ww < NW; ++ww) t += red[(ww * S::NRL + q) * 32 + lane];
+            acc[q] = t;
+        }
+        __syncthreads();
+    };
     for (int i = threadIdx.x; i < RB * LD; i += blockDim.x) {
         int r = i / LD, z = i % LD;
         Hs[i] = (r < R && z < R) ? H[r * R + z] : 0.0;
@@ -90,8 +109,9 @@ __global__ void __launch_bounds__(NW * 32) k_als_polar(const int64_t *__restrict
         pc[i] = z;
     }
     __syncthreads();
-    const int gw = blockIdx.x * NW + w, nwarps = gridDim.x * NW;
-    for (int k = gw; k < K; k += nwarps) {
+    // one CTA per slice: its warps take the slice's 32-row chunks in turn (a single warp per slice
+    // made the kernel as slow as its longest slice: 4,000 rows = 375 serial chunk passes)
+    for (int k = blockIdx.x; k < K; k += gridDim.x) {
         const int64_t r0 = row_ptr[k], r1 = row_ptr[k + 1];
         if (lane < RB) wv[lane] = lane < R ? W[(int64_t)k * R + lane] : 0.0;
         __syncwarp();
@@ -99,7 +119,7 @@ __global__ void __launch_bounds__(NW * 32) k_als_polar(const int64_t *__restrict
         double g1[NPL];
 #pragma unroll
         for (int q = 0; q < NPL; ++q) g1[q] = 0.0;
-        for (int64_t c0 = r0; c0 < r1; c0 += 32) {
+        for (int64_t c0 = r0 + 32 * w; c0 < r1; c0 += 32 * NW) {
             const int64_t row = c0 + lane;
             const bool valid = row < r1;
             double xw[RB];
@@ -117,6 +137,7 @@ __global__ void __launch_bounds__(NW * 32) k_als_polar(const int64_t *__restrict
             pair_accum<NPL>(rows, rows, LD, pa, pc, NP, g1);
             __syncwarp();
         }
+        reduce(g1);
         // ---- S1 -> L1 (S1 = L1 L1^T, R1 = L1^T)
 #pragma unroll
         for (int q = 0; q < NPL; ++q) {
@@ -138,7 +159,7 @@ __global__ void __launch_bounds__(NW * 32) k_als_polar(const int64_t *__restrict
         double g2[NPL];
 #pragma unroll
         for (int q = 0; q < NPL; ++q) g2[q] = 0.0;
-        for (int64_t c0 = r0; c0 < r1; c0 += 32) {
+        for (int64_t c0 = r0 + 32 * w; c0 < r1; c0 += 32 * NW) {
             const int64_t row = c0 + lane;
             const bool valid = row < r1;
             double b[RB];
@@ -155,6 +176,7 @@ __global__ void __launch_bounds__(NW * 32) k_als_polar(const int64_t *__restrict
             pair_accum<NPL>(rows, rows, LD, pa, pc, NP, g2);
             __syncwarp();
         }
+        reduce(g2);
 #pragma unroll
         for (int q = 0; q < NPL; ++q) {
             const int pp = lane + 32 * q;
@@ -170,7 +192,7 @@ __global__ void __launch_bounds__(NW * 32) k_als_polar(const int64_t *__restrict
             for (int z = 0; z < RB; ++z) rr[z] = (lane < R && z < R) ? Ss[lane * LD + z] : (lane == z ? 1.0 : 0.0);
             ok = chol_regs<RB>(rr, L2, LD, d2) && ok;
         }
-        if (!ok && lane == 0) report_error(err, k, DASH_E_SINGULAR);
+        if (!ok && lane == 0 && w == 0) report_error(err, k, DASH_E_SINGULAR);
         // ---- Rt = R2 R1 = L2^T L1^T into Ms (row i by lane i); Va = I into Ss
         double *Rt = Ms, *Va = Ss;
         if (lane < RB) {
@@ -264,7 +286,7 @@ __global__ void __launch_bounds__(NW * 32) k_als_polar(const int64_t *__restrict
         double gy[NQL];
 #pragma unroll
         for (int q = 0; q < NQL; ++q) gy[q] = 0.0;
-        for (int64_t c0 = r0; c0 < r1; c0 += 32) {
+        for (int64_t c0 = r0 + 32 * w; c0 < r1; c0 += 32 * NW) {
             const int64_t row = c0 + lane;
             const bool valid = row < r1;
             double q1[RB];
@@ -284,10 +306,11 @@ __global__ void __launch_bounds__(NW * 32) k_als_polar(const int64_t *__restrict
             pair_accum<NQL>(rows, rows2, LD, pa + NP, pc + NP, NQ, gy);
             __syncwarp();
         }
+        reduce(gy);
 #pragma unroll
         for (int q = 0; q < NQL; ++q) {
             const int pp = lane + 32 * q;
-            if (pp < NQ) {
+            if (pp < NQ && w == 0) {
                 const int r = pa[NP + pp], z = pc[NP + pp];
                 if (r < R && z < R) yv[(int64_t)k * R * R + r * R + z] = gy[q];
             }
@@ -296,16 +319,26 @@ __global__ void __launch_bounds__(NW * 32) k_als_polar(const int64_t *__restrict
     }
 }
 
-// CP sweep on the projected tensor (als.py:166-176), one CTA:
+// CP sweep on the projected tensor (als.py:166-176), a cooperative grid:
 //   vtv = V^T V, wtw = W^T W, rhs_h = sum_k yv_k diag(W_k), H = ridge(vtv o wtw, rhs_h^T)^T,
 //   hth = H^T H, rhs_w[k] = sum_r yv[k][r][:] o H[r][:], W = ridge(hth o vtv, rhs_w^T)^T,
 //   wtw = W^T W.  Outputs H, W and lhs_v = hth o wtw (for the V solve).
+// Each CTA owns a contiguous range of slices: it forms that range's partial sums, the grid
+// syncs, and every CTA adds the partials in CTA order (identical bytes everywhere) and solves
+// the two R x R systems redundantly; the per-slice W solves and the second partial wtw are
+// again per range.  (One CTA looping over all K slices took 1.3 ms at the daily shape.)
 template <int RB>
 __global__ void __launch_bounds__(256) k_als_cp(const double *__restrict__ yv, int K, const double *__restrict__ V,
                                                 int J, int R, double eps, double *__restrict__ H,
                                                 double *__restrict__ W, double *__restrict__ lhs_v,
-                                                unsigned long long *err) {
+                                                double *__restrict__ part, unsigned long long *err) {
     constexpr int LD = RB + 1;
+    cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+    const int G = gridDim.x, RR = R * R;
+    const int kper = (K + G - 1) / G;
+    const int k0 = min(K, (int)blockIdx.x * kper), k1 = min(K, k0 + kper);
+    double *part1 = part;                        // [G][2][RR]: wtw, rhs_h partials
+    double *part2 = part + (size_t)G * 2 * RR;   // [G][RR]: new wtw partials
     __shared__ double vtv[RB * LD], wtw[RB * LD], rh[RB * LD], Hn[RB * LD];
     double *hth = rh;  // rhs_h is dead once H is solved
     __shared__ double Ls[RB * LD], dinv[RB];
@@ -316,9 +349,20 @@ __global__ void __launch_bounds__(256) k_als_cp(const double *__restrict__ yv, i
         const int r = p / R, z = p % R;
         double a = 0.0, b = 0.0, c = 0.0;
         for (int j = 0; j < J; ++j) a = fma(V[j * R + r], V[j * R + z], a);
-        for (int k = 0; k < K; ++k) b = fma(W[(int64_t)k * R + r], W[(int64_t)k * R + z], b);
-        for (int k = 0; k < K; ++k) c = fma(yv[(int64_t)k * R * R + r * R + z], W[(int64_t)k * R + z], c);
+        for (int k = k0; k < k1; ++k) b = fma(W[(int64_t)k * R + r], W[(int64_t)k * R + z], b);
+        for (int k = k0; k < k1; ++k) c = fma(yv[(int64_t)k * R * R + r * R + z], W[(int64_t)k * R + z], c);
         vtv[r * LD + z] = a;
+        part1[((size_t)blockIdx.x * 2 + 0) * RR + p] = b;
+        part1[((size_t)blockIdx.x * 2 + 1) * RR + p] = c;
+    }
+    grid.sync();
+    for (int p = tid; p < R * R; p += blockDim.x) {
+        const int r = p / R, z = p % R;
+        double b = 0.0, c = 0.0;
+        for (int g = 0; g < G; ++g) {
+            b += part1[((size_t)g * 2 + 0) * RR + p];
+            c += part1[((size_t)g * 2 + 1) * RR + p];
+        }
         wtw[r * LD + z] = b;
         rh[r * LD + z] = c;  // rhs_h[r][z]
     }
@@ -337,7 +381,7 @@ __global__ void __launch_bounds__(256) k_als_cp(const double *__restrict__ yv, i
             if (!ok && lane == 0) {
                 for (int r = 0; r < R; ++r)
                     for (int z = 0; z < R; ++z) Ls[r * LD + z] = lhs_of(r, z) + (r == z ? sh : 0.0);
-                if (!lu_factor_serial(Ls, LD, R, piv)) report_error(err, -1, DASH_E_SINGULAR);
+                if (!lu_factor_serial(Ls, LD, R, piv) && blockIdx.x == 0) report_error(err, -1, DASH_E_SINGULAR);
             }
             if (lane == 0) okflag = ok ? 1 : 0;
         }
@@ -369,7 +413,7 @@ __global__ void __launch_bounds__(256) k_als_cp(const double *__restrict__ yv, i
     __syncthreads();
     for (int p = tid; p < R * R; p += blockDim.x) {
         const int r = p / R, z = p % R;
-        H[p] = Hn[r * LD + z];
+        if (blockIdx.x == 0) H[p] = Hn[r * LD + z];
         double a = 0.0;
         for (int m = 0; m < R; ++m) a = fma(Hn[m * LD + r], Hn[m * LD + z], a);
         hth[r * LD + z] = a;
@@ -377,7 +421,7 @@ __global__ void __launch_bounds__(256) k_als_cp(const double *__restrict__ yv, i
     __syncthreads();
     // W = ridge(hth o vtv, rhs_w^T)^T, rhs_w[k][z] = sum_r yv[k][r][z] H[r][z]
     factor([&](int r, int z) { return hth[r * LD + z] * vtv[r * LD + z]; });
-    for (int k = tid; k < K; k += blockDim.x) {
+    for (int k = k0 + tid; k < k1; k += blockDim.x) {
         double b[RB];
 #pragma unroll
         for (int z = 0; z < RB; ++z) {
@@ -400,9 +444,17 @@ __global__ void __launch_bounds__(256) k_als_cp(const double *__restrict__ yv, i
     for (int p = tid; p < R * R; p += blockDim.x) {
         const int r = p / R, z = p % R;
         double b = 0.0;
-        for (int k = 0; k < K; ++k) b = fma(W[(int64_t)k * R + r], W[(int64_t)k * R + z], b);
-        lhs_v[p] = hth[r * LD + z] * b;
+        for (int k = k0; k < k1; ++k) b = fma(W[(int64_t)k * R + r], W[(int64_t)k * R + z], b);
+        part2[(size_t)blockIdx.x * RR + p] = b;
     }
+    grid.sync();
+    if (blockIdx.x == 0)
+        for (int p = tid; p < R * R; p += blockDim.x) {
+            const int r = p / R, z = p % R;
+            double b = 0.0;
+            for (int g = 0; g < G; ++g) b += part2[(size_t)g * RR + p];
+            lhs_v[p] = hth[r * LD + z] * b;
+        }
 }
 
 // Z[row] = (Q[row] H) o w_k  (and, with w == nullptr, U = Q H)
@@ -464,15 +516,22 @@ int launch_als_polar(dash_ctx *ctx, cudaStream_t st, const int64_t *row_ptr, int
     constexpr int NW = RB <= 16 ? 4 : 2;
     const size_t smem = AlsSmem<RB>::bytes(NW);
     ensure_smem_attr(k_als_polar<RB, NW>, smem);
-    const int blocks = std::max(1, std::min((K + NW - 1) / NW, ctx->num_sms * 8));
+    const int blocks = std::max(1, std::min(K, ctx->num_sms * 8));
     k_als_polar<RB, NW><<<blocks, NW * 32, smem, st>>>(row_ptr, K, XV, W, H, R, T, Q, yv, ctx->err);
     return 0;
 }
 
 template <int RB>
-void launch_als_cp(cudaStream_t st, const double *yv, int K, const double *V, int J, int R, double eps, double *H,
-                   double *W, double *lhs_v, unsigned long long *err) {
-    k_als_cp<RB><<<1, 256, 0, st>>>(yv, K, V, J, R, eps, H, W, lhs_v, err);
+int launch_als_cp(dash_ctx *ctx, cudaStream_t st, const double *yv, int K, const double *V, int J, int R, double eps,
+                  double *H, double *W, double *lhs_v, unsigned long long *err) {
+    // ranges of >= 32 slices, at most one CTA per SM (cooperative launch: all CTAs co-resident)
+    const int G = std::max(1, std::min(ctx->num_sms, (K + 31) / 32));
+    if (ensure(ctx->part, sizeof(double) * (size_t)G * 3 * R * R)) return DASH_E_CUDA;
+    double *part = (double *)ctx->part.p;
+    void *args[] = {(void *)&yv, (void *)&K, (void *)&V, (void *)&J, (void *)&R, (void *)&eps, (void *)&H,
+                    (void *)&W, (void *)&lhs_v, (void *)&part, (void *)&err};
+    return cudaLaunchCooperativeKernel((const void *)k_als_cp<RB>, dim3(G), dim3(256), args, 0, st) == cudaSuccess
+               ? 0 : DASH_E_CUDA;
 }
 
 }  // namespace
@@ -538,12 +597,14 @@ int dash_als_sweep_f64(dash_ctx *ctx, void *stream, const dash_batch_f64 *t, int
         case 16: launch_als_polar<16>(ctx, st, t->row_ptr, K, XV, W, H, R, T, Q, yv); break;
         default: launch_als_polar<32>(ctx, st, t->row_ptr, K, XV, W, H, R, T, Q, yv); break;
     }
+    int rc_cp;
     switch (RB) {
-        case 4: launch_als_cp<4>(st, yv, K, V, J, R, eps, H, W, lhs_v, ctx->err); break;
-        case 8: launch_als_cp<8>(st, yv, K, V, J, R, eps, H, W, lhs_v, ctx->err); break;
-        case 16: launch_als_cp<16>(st, yv, K, V, J, R, eps, H, W, lhs_v, ctx->err); break;
-        default: launch_als_cp<32>(st, yv, K, V, J, R, eps, H, W, lhs_v, ctx->err); break;
+        case 4: rc_cp = launch_als_cp<4>(ctx, st, yv, K, V, J, R, eps, H, W, lhs_v, ctx->err); break;
+        case 8: rc_cp = launch_als_cp<8>(ctx, st, yv, K, V, J, R, eps, H, W, lhs_v, ctx->err); break;
+        case 16: rc_cp = launch_als_cp<16>(ctx, st, yv, K, V, J, R, eps, H, W, lhs_v, ctx->err); break;
+        default: rc_cp = launch_als_cp<32>(ctx, st, yv, K, V, J, R, eps, H, W, lhs_v, ctx->err); break;
     }
+    if (rc_cp) return rc_cp;
     const int qb = (int)std::min<int64_t>((N * R + 255) / 256, (int64_t)ctx->num_sms * 16);
     // rhs_v = X^T ((Q H) o w).  Tensor-map paths: Z = (Q H) o w once (the loss below reads the same Z);
     // generic path: the F GEMM multiplies "U" = Q H by W[state_row[slice]] itself

@@ -19,6 +19,7 @@
 // criterion requires (test_acceptance.py:416-475).
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
