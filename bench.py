@@ -114,7 +114,7 @@ def algorithmic_flops(N, J, R, M):
     return 4 * N * J * R + N * (3 * R * R + 2 * R) + M * (4 * R ** 3 / 3 + 4 * R * R)
 
 
-SMALL_ROWS = 64  # csrc/dash_update.cu kSmallRows: slices with more rows go to k_big
+SMALL_ROWS = 32  # csrc/dash_update.cu kSmallRows: slices with more rows go to k_bigx / k_big
 
 
 def batch_stats(batches):
@@ -150,10 +150,13 @@ def kernel_bytes(phase, st, J, R, nsplit, b=8, bigx=False):
 
 
 def kernel_flops(phase, st, J, R, bigx=False):
-    """FP64 flops per launch of the DMMA-bound fused big-slice kernel: XV = X V,
-    P = X^T U (2 N J R each), U = XV Ms^T and U^T U (2 N R^2 each)."""
+    """FP64 flops per launch of the DMMA kernels: the fused big-slice kernel (XV = X V,
+    P = X^T U: 2 N J R each; U = XV Ms^T and U^T U: 2 N R^2 each) and the two
+    streaming contractions."""
     if phase == "big" and bigx:
         return 4 * st["Nb"] * J * R + 4 * st["Nb"] * R * R
+    if phase in ("xv", "fgemm"):  # one streaming contraction each (DMMA): binds at large R (wide32 / wide64)
+        return 2 * (st["Ns"] if bigx else st["N"]) * J * R
     return 0
 
 
