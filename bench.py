@@ -623,7 +623,7 @@ def run_parity(cfg, steps, dev):
             "fp32_data_mode": {"tol": 1e-3, "max_err": worst32, "ok": bool(max(worst32.values()) <= 1e-3)}}
 
 
-def als_timing(name, dev, iters=3):
+def als_timing(name, dev, iters=10):
     """One parafac2_als sweep at a BASELINE shape (initialize's fit and the
     baseline refit, tol=0 so every sweep runs), on a device-resident tensor of
     that shape drawn from the planted generator; SURVEY 8(d) ALS roofline:

@@ -44,5 +44,26 @@ def build_library(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+def build_host_ext(force: bool = False, verbose: bool = False) -> Path:
+    """The host-side gather helper (_dashhost, CPython extension, gcc): walks a
+    batch's per-slice arrays in C for StreamState.update(UpdateBatch)."""
+    import sysconfig
+    src = CSRC / "host_gather.c"
+    out = HERE / ("_dashhost" + sysconfig.get_config_var("EXT_SUFFIX"))
+    if not force and out.exists() and out.stat().st_mtime >= src.stat().st_mtime:
+        return out
+    cmd = [os.environ.get("CC", "gcc"), "-O3", "-shared", "-fPIC", "-pthread", "-I", sysconfig.get_paths()["include"],
+           str(src), "-o", str(out) + ".tmp"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stderr[-4000:])
+        raise RuntimeError("gcc failed on host_gather.c")
+    os.replace(str(out) + ".tmp", out)
+    if verbose:
+        print(f"built {out}")
+    return out
+
+
 if __name__ == "__main__":
+    build_host_ext(force="--force" in sys.argv, verbose=True)
     build_library(force="--force" in sys.argv, verbose=True)

@@ -168,6 +168,30 @@ class _UBlocks(Mapping):
 
 _POOL = None
 
+try:  # host-side gather in C (csrc/host_gather.c, built by build.py); numpy path if it is not built
+    from . import _dashhost
+except ImportError:  # pragma: no cover
+    _dashhost = None
+
+
+def _gather_plan(plan, row_ptr, out, on_chunk=None):
+    """_gather_rows through the C helper: the batch's blocks land in the pinned
+    buffer share by share (each share copied by several threads with the GIL
+    released); ``on_chunk(lo, hi)`` starts a share's upload behind the next
+    share's copy."""
+    M = len(row_ptr) - 1
+    N = int(row_ptr[M])
+    T = min(8, os.cpu_count() or 1)
+    shares = 1 if N * out.shape[1] < (1 << 22) else 4
+    cut = np.searchsorted(row_ptr, np.linspace(0, N, shares + 1).astype(np.int64))
+    cut[0], cut[-1] = 0, M
+    cut = np.unique(cut)
+    for a, b in zip(cut[:-1], cut[1:]):
+        lo, hi = int(row_ptr[a]), int(row_ptr[b])
+        _dashhost.copy(plan, int(a), int(b), out, lo, T, 1 if out.dtype == np.float32 else 0)
+        if on_chunk is not None:
+            on_chunk(lo, hi)
+
 
 def _gather_rows(arrs, row_ptr, out, on_chunk=None):
     """Concatenate the batch's per-slice row blocks into the pinned staging
@@ -513,15 +537,22 @@ class StreamState:
         bad = [sid for sid in ex_ids if sid not in rowmap]
         if bad:
             raise ValueError(f"batch references unknown existing slice {bad[0]!r}")
-        arrs = [r if (type(r) is np.ndarray and r.dtype == np.float64) else np.asarray(r, dtype=float)
-                for r in ex_rows + new_rows]
-        bad = [k for k, r in enumerate(arrs) if r.ndim != 2 or r.shape[1] != J]
-        if bad:
-            sid = (ex_ids + new_ids)[bad[0]]
-            raise ValueError(f"slice {sid!r}: rows must be (n, {J})")
         ids = ex_ids + new_ids
         M = len(ids)
-        counts = np.fromiter((r.shape[0] for r in arrs), dtype=np.int64, count=M)
+        arrs = ex_rows + new_rows
+        plan, counts = None, None
+        if _dashhost is not None:
+            # one C pass over the blocks: shape / dtype / layout check and the row counts
+            counts = np.empty(M, dtype=np.int64)
+            plan = _dashhost.scan(arrs, J, counts)
+        if plan is None or isinstance(plan, int):
+            # a block that is not a C-contiguous float64 (n, J) array: convert, re-check, report
+            arrs = [np.ascontiguousarray(r, dtype=float) for r in arrs]
+            bad = [k for k, r in enumerate(arrs) if r.ndim != 2 or r.shape[1] != J]
+            if bad:
+                raise ValueError(f"slice {ids[bad[0]]!r}: rows must be (n, {J})")
+            counts = np.fromiter((r.shape[0] for r in arrs), dtype=np.int64, count=M)
+            plan = _dashhost.scan(arrs, J, counts) if _dashhost is not None else None
         existing_rows = np.fromiter((rowmap[sid] for sid in ex_ids), dtype=np.int32, count=len(ex_ids))
         meta = self._stage_meta(counts, existing_rows, len(new_ids))
         N = meta.N
@@ -533,7 +564,10 @@ class StreamState:
         if N:
             def upload(lo, hi):  # each share's H2D starts as soon as its rows are gathered
                 X[lo:hi].copy_(pin[lo:hi], non_blocking=True)
-            _gather_rows(arrs, row_ptr, pin.numpy()[:N], upload)
+            if plan is not None and not isinstance(plan, int):
+                _gather_plan(plan, row_ptr, pin.numpy()[:N], upload)
+            else:
+                _gather_rows(arrs, row_ptr, pin.numpy()[:N], upload)
             ev = torch.cuda.Event()
             ev.record()
             self._pin_event = ev
