@@ -53,11 +53,7 @@ struct AlsSmem {
     static constexpr int NQ = RB * RB;
     // shared: H[RB*LD] + pair tables (NP + NQ) * 2 ints
     static constexpr int shared = RB * LD + (NP + NQ);
-    static constexpr int NRL = (NQ + 31) / 32;  // values per lane in the cross-warp reduction buffer
-    // + red[nw][32 * NRL]: per-warp Gram partials, summed in warp order by every warp
-    __host__ __device__ static constexpr size_t bytes(int nw) {
-        return sizeof(double) * (shared + nw * per_warp + nw * 32 * NRL);
-    }
+    __host__ __device__ static constexpr size_t bytes(int nw) { return sizeof(double) * (shared + nw * per_warp); }
 };
 
 template <int RB, int NW>
@@ -78,21 +74,6 @@ __global__ void __launch_bounds__(NW * 32) k_als_polar(const int64_t *__restrict
     double *rows = base, *rows2 = rows + 32 * LD;
     double *L1 = rows2 + 32 * LD, *L2 = L1 + RB * LD, *Ms = L2 + RB * LD, *Ss = Ms + RB * LD;
     double *d1 = Ss + RB * LD, *d2 = d1 + RB, *wv = d2 + RB;
-    double *red = sm + S::shared + NW * S::per_warp;
-    // Gram partials of the CTA's warps -> every warp holds the full sum (fixed warp order)
-    auto reduce = [&](auto &acc) {
-        constexpr int n = (int)(sizeof(acc) / sizeof(double));
-#pragma unroll
-        for (int q = 0; q < n; ++q) red[(w * S::NRL + q) * 32 + lane] = acc[q];
-        __syncthreads();
-#pragma unroll
-        for (int q = 0; q < n; ++q) {
-            double t = 0.0;
-            for (int ww = 0; ww < NW; ++ww) t += red[(ww * S::NRL + q) * 32 + lane];
-            acc[q] = t;
-        }
-        __syncthreads();
-    };
     for (int i = threadIdx.x; i < RB * LD; i += blockDim.x) {
         int r = i / LD, z = i % LD;
         Hs[i] = (r < R && z < R) ? H[r * R + z] : 0.0;
@@ -109,9 +90,11 @@ __global__ void __launch_bounds__(NW * 32) k_als_polar(const int64_t *__restrict
         pc[i] = z;
     }
     __syncthreads();
-    // one CTA per slice: its warps take the slice's 32-row chunks in turn (a single warp per slice
-    // made the kernel as slow as its longest slice: 4,000 rows = 375 serial chunk passes)
-    for (int k = blockIdx.x; k < K; k += gridDim.x) {
+    // one warp per slice.  (One CTA per slice with the warps sharing its chunks was measured
+    // slower -- 3.99 -> 5.05 ms at the daily shape: the kernel is bound by its scalar row passes,
+    // not by its longest slice, and the redundant per-warp factorisations cost SM time.)
+    const int gw = blockIdx.x * NW + w, nwarps = gridDim.x * NW;
+    for (int k = gw; k < K; k += nwarps) {
         const int64_t r0 = row_ptr[k], r1 = row_ptr[k + 1];
         if (lane < RB) wv[lane] = lane < R ? W[(int64_t)k * R + lane] : 0.0;
         __syncwarp();
@@ -119,7 +102,7 @@ __global__ void __launch_bounds__(NW * 32) k_als_polar(const int64_t *__restrict
         double g1[NPL];
 #pragma unroll
         for (int q = 0; q < NPL; ++q) g1[q] = 0.0;
-        for (int64_t c0 = r0 + 32 * w; c0 < r1; c0 += 32 * NW) {
+        for (int64_t c0 = r0; c0 < r1; c0 += 32) {
             const int64_t row = c0 + lane;
             const bool valid = row < r1;
             double xw[RB];
@@ -137,7 +120,6 @@ __global__ void __launch_bounds__(NW * 32) k_als_polar(const int64_t *__restrict
             pair_accum<NPL>(rows, rows, LD, pa, pc, NP, g1);
             __syncwarp();
         }
-        reduce(g1);
         // ---- S1 -> L1 (S1 = L1 L1^T, R1 = L1^T)
 #pragma unroll
         for (int q = 0; q < NPL; ++q) {
@@ -159,7 +141,7 @@ __global__ void __launch_bounds__(NW * 32) k_als_polar(const int64_t *__restrict
         double g2[NPL];
 #pragma unroll
         for (int q = 0; q < NPL; ++q) g2[q] = 0.0;
-        for (int64_t c0 = r0 + 32 * w; c0 < r1; c0 += 32 * NW) {
+        for (int64_t c0 = r0; c0 < r1; c0 += 32) {
             const int64_t row = c0 + lane;
             const bool valid = row < r1;
             double b[RB];
@@ -176,7 +158,6 @@ __global__ void __launch_bounds__(NW * 32) k_als_polar(const int64_t *__restrict
             pair_accum<NPL>(rows, rows, LD, pa, pc, NP, g2);
             __syncwarp();
         }
-        reduce(g2);
 #pragma unroll
         for (int q = 0; q < NPL; ++q) {
             const int pp = lane + 32 * q;
@@ -192,7 +173,7 @@ __global__ void __launch_bounds__(NW * 32) k_als_polar(const int64_t *__restrict
             for (int z = 0; z < RB; ++z) rr[z] = (lane < R && z < R) ? Ss[lane * LD + z] : (lane == z ? 1.0 : 0.0);
             ok = chol_regs<RB>(rr, L2, LD, d2) && ok;
         }
-        if (!ok && lane == 0 && w == 0) report_error(err, k, DASH_E_SINGULAR);
+        if (!ok && lane == 0) report_error(err, k, DASH_E_SINGULAR);
         // ---- Rt = R2 R1 = L2^T L1^T into Ms (row i by lane i); Va = I into Ss
         double *Rt = Ms, *Va = Ss;
         if (lane < RB) {
@@ -286,7 +267,7 @@ __global__ void __launch_bounds__(NW * 32) k_als_polar(const int64_t *__restrict
         double gy[NQL];
 #pragma unroll
         for (int q = 0; q < NQL; ++q) gy[q] = 0.0;
-        for (int64_t c0 = r0 + 32 * w; c0 < r1; c0 += 32 * NW) {
+        for (int64_t c0 = r0; c0 < r1; c0 += 32) {
             const int64_t row = c0 + lane;
             const bool valid = row < r1;
             double q1[RB];
@@ -306,17 +287,405 @@ __global__ void __launch_bounds__(NW * 32) k_als_polar(const int64_t *__restrict
             pair_accum<NQL>(rows, rows2, LD, pa + NP, pc + NP, NQ, gy);
             __syncwarp();
         }
-        reduce(gy);
 #pragma unroll
         for (int q = 0; q < NQL; ++q) {
             const int pp = lane + 32 * q;
-            if (pp < NQ && w == 0) {
+            if (pp < NQ) {
                 const int r = pa[NP + pp], z = pc[NP + pp];
                 if (r < R && z < R) yv[(int64_t)k * R * R + r * R + z] = gy[q];
             }
         }
         __syncwarp();
     }
+}
+
+// ---------------------------------------------------------------------------
+// k_als_polar_mma: the same per-slice polar factor (CholQR2 + Jacobi, als.py:156-160)
+// with the three row passes on the FP64 tensor cores.  Each pass is
+//     out (8 x RB) = in (8 x RB) . B (RB x RB)   per 8-row chunk,
+// followed by a Gram accumulation of the chunk:
+//   pass 1: in = XV o w,  B = H^T       -> T,   S1 += T^T T
+//   pass 2: in = T,       B = L1^{-T}   -> Q1 (in place), S2 += Q1^T Q1
+//   pass 3: in = Q1,      B = M         -> Q,   yv += Q^T XV
+// (L1^{-1} is formed explicitly, lane per column, instead of a forward
+// substitution per row; CholQR2's second pass absorbs the difference.)  Chunks
+// live in shared memory as swizzled 8 x 8 tiles (swk::toff), so the A / B /
+// transposed DMMA fragment patterns of dash_slicesw.cuh apply unchanged.  The
+// scalar kernel above spent ~600 FMA + as many LDS per row; this one ~14 DMMA
+// per 8 rows and pass.  One warp per slice; the R x R serial part (Cholesky
+// twice, the Jacobi SVD, M) is the scalar kernel's.
+// ---------------------------------------------------------------------------
+template <int NB>
+struct AlsMmaSmem {
+    static constexpr int RB = 8 * NB, LD = RB + 1;
+    // per warp: In[NB] | Out[NB] | Xt[NB] | Bm[NB*NB] tiles, L1, L2, Ms, Ss (RB x LD), d1, d2, wv
+    static constexpr int per_warp = (3 * NB + NB * NB) * 64 + 4 * RB * LD + 3 * RB;
+    static constexpr int shared = NB * NB * 64;  // H^T tiles
+    static constexpr int NRL = NB * NB * 2;      // Gram values per lane (the full yv block is the largest)
+    // + red[nw][NRL * 32]: per-warp Gram partials of the cooperative variant
+    __host__ __device__ static constexpr size_t bytes(int nw, bool coop) {
+        return sizeof(double) * (shared + nw * per_warp + (coop ? nw * NRL * 32 : 0));
+    }
+};
+
+// COOP = false: one warp per slice of `list` (short slices).  COOP = true: one CTA per slice -- its
+// warps take the slice's chunks in turn and add their Gram partials in warp order through shared
+// memory (long slices: a 4,000-row slice is 1,500 serial chunk passes for a single warp); the R x R
+// serial part is then repeated by every warp on identical inputs.
+template <int NB, int NW, bool COOP>
+__global__ void __launch_bounds__(NW * 32) k_als_polar_mma(const int64_t *__restrict__ row_ptr,
+                                                           const int32_t *__restrict__ list, int K,
+                                                           const double *__restrict__ XV, const double *__restrict__ W,
+                                                           const double *__restrict__ H, int R, double *__restrict__ T,
+                                                           double *__restrict__ Q, double *__restrict__ yv,
+                                                           unsigned long long *err) {
+    using namespace swk;
+    using S = AlsMmaSmem<NB>;
+    constexpr int RB = S::RB, LD = S::LD, NT = NB * (NB + 1) / 2;
+    extern __shared__ double sm[];
+    double *BH = sm;  // tile (kb, jb) element (k, n) = H[8 jb + n][8 kb + k]
+    const int lane = lane_id(), w = warp_id();
+    double *base = sm + S::shared + w * S::per_warp;
+    double *In = base, *Out = In + NB * 64, *Xt = Out + NB * 64, *Bm = Xt + NB * 64;
+    double *L1 = Bm + NB * NB * 64, *L2 = L1 + RB * LD, *Ms = L2 + RB * LD, *Ss = Ms + RB * LD;
+    double *d1 = Ss + RB * LD, *d2 = d1 + RB, *wv = d2 + RB;
+    for (int i = threadIdx.x; i < NB * NB * 64; i += blockDim.x) {
+        const int tl = i >> 6, e = i & 63, kb = tl / NB, jb = tl % NB;
+        const int k = e >> 3, n = (e & 7) ^ ((k & 2) << 1);  // inverse of toff(k, n) = 8 k + (n ^ ...)
+        const int hr = 8 * jb + n, hc = 8 * kb + k;
+        BH[i] = (hr < R && hc < R) ? H[hr * R + hc] : 0.0;
+    }
+    __syncthreads();
+    const LaneOff o = lane_offsets();
+    const int g = o.g, c0 = o.c0;
+    double *red = sm + S::shared + NW * S::per_warp;
+    // cooperative variant: Gram partials of the CTA's warps -> the full sum in every warp (warp order)
+    auto reduce = [&](auto &acc) {
+        if constexpr (COOP) {
+            constexpr int n = (int)(sizeof(acc) / sizeof(double));
+            double *flat = &acc[0][0];
+#pragma unroll
+            for (int q = 0; q < n; ++q) red[(w * S::NRL + q) * 32 + lane] = flat[q];
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < n; ++q) {
+                double t = 0.0;
+                for (int ww = 0; ww < NW; ++ww) t += red[(ww * S::NRL + q) * 32 + lane];
+                flat[q] = t;
+            }
+            __syncthreads();
+        }
+    };
+    const int cw = COOP ? w : 0, cs = COOP ? NW : 1;  // this warp's first chunk and the chunk stride
+    // out tiles (C layout, registers) = In . B, B given as NB x NB tiles
+    auto gemm = [&](const double *Bt, double (&out)[NB][2]) {
+#pragma unroll
+        for (int jb = 0; jb < NB; ++jb) {
+            out[jb][0] = out[jb][1] = 0.0;
+#pragma unroll
+            for (int kb = 0; kb < NB; ++kb) mma_xy(out[jb], In + 64 * kb, Bt + 64 * (kb * NB + jb), o);
+        }
+    };
+    // rows of a chunk (global, R columns) -> registers (optionally scaled by wv) -> tiles; the next
+    // chunk is fetched before the current one is worked on, so its latency hides behind the DMMAs
+    auto fetch = [&](double (&v)[NB][2], const double *src, int64_t row, bool valid, bool scale) {
+#pragma unroll
+        for (int kb = 0; kb < NB; ++kb)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int col = 8 * kb + c0 + e;
+                double x = (valid && col < R) ? src[row * R + col] : 0.0;
+                if (scale) x *= wv[col];
+                v[kb][e] = x;
+            }
+    };
+    auto put = [&](double *Tl, const double (&v)[NB][2]) {
+#pragma unroll
+        for (int kb = 0; kb < NB; ++kb) stc(Tl + 64 * kb, v[kb], o);
+    };
+    auto copy2 = [&](double (&d)[NB][2], const double (&a)[NB][2]) {
+#pragma unroll
+        for (int kb = 0; kb < NB; ++kb) d[kb][0] = a[kb][0], d[kb][1] = a[kb][1];
+    };
+    auto store_rows = [&](double *dst, int64_t row, bool valid, const double (&out)[NB][2]) {
+#pragma unroll
+        for (int jb = 0; jb < NB; ++jb) {
+            stc(Out + 64 * jb, out[jb], o);
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int col = 8 * jb + c0 + e;
+                if (valid && col < R) dst[row * R + col] = out[jb][e];
+            }
+        }
+    };
+    // symmetric Gram tiles -> the lower triangle of Ss (row-major)
+    auto gram_to_ss = [&](const double (&ga)[NT][2]) {
+#pragma unroll
+        for (int ib = 0; ib < NB; ++ib)
+#pragma unroll
+            for (int kb = 0; kb <= ib; ++kb)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int r = 8 * ib + g, c = 8 * kb + c0 + e;
+                    if (ib > kb || r >= c) Ss[r * LD + c] = ga[tri(ib, kb)][e];  // lower triangle only (one writer each)
+                }
+    };
+    const int gw = COOP ? blockIdx.x : blockIdx.x * NW + w, nwarps = COOP ? gridDim.x : gridDim.x * NW;
+    for (int ki = gw; ki < K; ki += nwarps) {
+        const int k = list[ki];
+        const int64_t r0 = row_ptr[k], r1 = row_ptr[k + 1];
+        const int nch = (int)((r1 - r0 + 7) >> 3);
+        __syncwarp();
+        for (int r = lane; r < RB; r += 32) wv[r] = r < R ? W[(int64_t)k * R + r] : 0.0;
+        __syncwarp();
+        // ---- pass 1
+        double ga[NT][2];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) ga[t][0] = ga[t][1] = 0.0;
+        double cur[NB][2], nxt[NB][2];
+        fetch(cur, XV, r0 + 8 * (int64_t)cw + g, r0 + 8 * (int64_t)cw + g < r1, true);
+        for (int ch = cw; ch < nch; ch += cs) {
+            const int64_t row = r0 + 8 * (int64_t)ch + g;
+            const bool valid = row < r1;
+            fetch(nxt, XV, row + 8 * cs, row + 8 * cs < r1, true);
+            put(In, cur);
+            __syncwarp();
+            double out[NB][2];
+            gemm(BH, out);
+            store_rows(T, row, valid, out);
+            __syncwarp();
+#pragma unroll
+            for (int ib = 0; ib < NB; ++ib)
+#pragma unroll
+                for (int kb = 0; kb <= ib; ++kb) mma_xty(ga[tri(ib, kb)], Out + 64 * ib, Out + 64 * kb, o);
+            __syncwarp();
+            copy2(cur, nxt);  // only now: the fetch had the whole chunk to land
+        }
+        reduce(ga);
+        gram_to_ss(ga);
+        __syncwarp();
+        bool ok;
+        {
+            double rr[RB];
+#pragma unroll
+            for (int z = 0; z < RB; ++z)
+                rr[z] = (lane < R && z < R) ? Ss[(lane >= z ? lane : z) * LD + (lane >= z ? z : lane)]
+                                            : (lane == z ? 1.0 : 0.0);
+            ok = chol_regs<RB>(rr, L1, LD, d1);
+        }
+        // ---- B = L1^{-T}: lane c solves L1 x = e_c; Bm (k = c, n = i) = x[i]
+        {
+            double x[RB];
+#pragma unroll
+            for (int i = 0; i < RB; ++i) x[i] = (i == lane) ? 1.0 : 0.0;
+            if (lane < RB) fwd_solve_lane<RB>(L1, LD, d1, x);
+            if (lane < RB) {
+#pragma unroll
+                for (int i = 0; i < RB; ++i) Bm[64 * ((lane >> 3) * NB + (i >> 3)) + toff(lane & 7, i & 7)] = x[i];
+            }
+        }
+        __syncwarp();
+        // ---- pass 2
+#pragma unroll
+        for (int t = 0; t < NT; ++t) ga[t][0] = ga[t][1] = 0.0;
+        fetch(cur, T, r0 + 8 * (int64_t)cw + g, r0 + 8 * (int64_t)cw + g < r1, false);
+        for (int ch = cw; ch < nch; ch += cs) {
+            const int64_t row = r0 + 8 * (int64_t)ch + g;
+            const bool valid = row < r1;
+            fetch(nxt, T, row + 8 * cs, row + 8 * cs < r1, false);
+            put(In, cur);
+            __syncwarp();
+            double out[NB][2];
+            gemm(Bm, out);
+            store_rows(T, row, valid, out);
+            __syncwarp();
+#pragma unroll
+            for (int ib = 0; ib < NB; ++ib)
+#pragma unroll
+                for (int kb = 0; kb <= ib; ++kb) mma_xty(ga[tri(ib, kb)], Out + 64 * ib, Out + 64 * kb, o);
+            __syncwarp();
+            copy2(cur, nxt);  // only now: the fetch had the whole chunk to land
+        }
+        reduce(ga);
+        gram_to_ss(ga);
+        __syncwarp();
+        {
+            double rr[RB];
+#pragma unroll
+            for (int z = 0; z < RB; ++z)
+                rr[z] = (lane < R && z < R) ? Ss[(lane >= z ? lane : z) * LD + (lane >= z ? z : lane)]
+                                            : (lane == z ? 1.0 : 0.0);
+            ok = chol_regs<RB>(rr, L2, LD, d2) && ok;
+        }
+        if (!ok && lane == 0 && cw == 0) report_error(err, k, DASH_E_SINGULAR);
+        // ---- Rt = L2^T L1^T into Ms (row i by lane i); Va = I into Ss
+        double *Rt = Ms, *Va = Ss;
+        if (lane < RB) {
+            for (int j = 0; j < RB; ++j) {
+                double acc = 0.0;
+                for (int m = 0; m < RB; ++m) acc = fma(L2[m * LD + lane], L1[j * LD + m], acc);
+                Rt[lane * LD + j] = acc;
+                Va[lane * LD + j] = (lane == j) ? 1.0 : 0.0;
+            }
+        }
+        __syncwarp();
+        // ---- one-sided Jacobi SVD of Rt (cyclic by rows): Rt V = U Sigma
+        for (int sweep = 0; sweep < 60; ++sweep) {
+            double offmax = 0.0;
+            for (int p = 0; p < R - 1; ++p) {
+                for (int q = p + 1; q < R; ++q) {
+                    const double a = lane < RB ? Rt[lane * LD + p] : 0.0;
+                    const double b = lane < RB ? Rt[lane * LD + q] : 0.0;
+                    double al = a * a, be = b * b, gm = a * b;
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) {
+                        al += __shfl_xor_sync(FULL_MASK, al, off);
+                        be += __shfl_xor_sync(FULL_MASK, be, off);
+                        gm += __shfl_xor_sync(FULL_MASK, gm, off);
+                    }
+                    const double nrm = sqrt(al * be);
+                    if (!(nrm > 0.0) || fabs(gm) <= 1e-16 * nrm) continue;  // warp-uniform
+                    offmax = fmax(offmax, fabs(gm) / nrm);
+                    const double zeta = (be - al) / (2.0 * gm);
+                    const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                    const double cs = 1.0 / sqrt(1.0 + tt * tt), sn = cs * tt;
+                    if (lane < RB) {
+                        Rt[lane * LD + p] = cs * a - sn * b;
+                        Rt[lane * LD + q] = sn * a + cs * b;
+                        const double vp = Va[lane * LD + p], vq = Va[lane * LD + q];
+                        Va[lane * LD + p] = cs * vp - sn * vq;
+                        Va[lane * LD + q] = sn * vp + cs * vq;
+                    }
+                    __syncwarp();
+                }
+            }
+            if (offmax <= 1e-15) break;
+        }
+        // ---- polar(Rt) = U V^T, M = L2^-T polar(Rt); Bm (k = i, n = lane) = M[i][lane]
+        {
+            double sig[RB];
+#pragma unroll
+            for (int m = 0; m < RB; ++m) {
+                const double v = lane < RB ? Rt[lane * LD + m] : 0.0;
+                sig[m] = v * v;
+            }
+            warp_allreduce<RB>(sig);
+#pragma unroll
+            for (int m = 0; m < RB; ++m) sig[m] = (m < R && sig[m] > 0.0) ? 1.0 / sqrt(sig[m]) : 0.0;
+            double prow[RB];
+#pragma unroll
+            for (int j = 0; j < RB; ++j) {
+                double acc = 0.0;
+                if (lane < RB) {
+#pragma unroll
+                    for (int m = 0; m < RB; ++m) acc = fma(Rt[lane * LD + m] * sig[m], Va[j * LD + m], acc);
+                }
+                prow[j] = (j < R && lane < R) ? acc : (j == lane ? 1.0 : 0.0);
+            }
+            __syncwarp();
+            if (lane < RB) {
+#pragma unroll
+                for (int j = 0; j < RB; ++j) Rt[lane * LD + j] = prow[j];  // Rt <- P (row-major)
+            }
+            __syncwarp();
+            double col[RB];
+#pragma unroll
+            for (int i = 0; i < RB; ++i) col[i] = lane < RB ? Rt[i * LD + lane] : 0.0;
+#pragma unroll
+            for (int kk = RB - 1; kk >= 0; --kk) {
+                col[kk] *= d2[kk];
+#pragma unroll
+                for (int i = 0; i < kk; ++i) col[i] = fma(-L2[kk * LD + i], col[kk], col[i]);
+            }
+            __syncwarp();
+            if (lane < RB) {
+#pragma unroll
+                for (int i = 0; i < RB; ++i) Bm[64 * ((i >> 3) * NB + (lane >> 3)) + toff(i & 7, lane & 7)] = col[i];
+            }
+            __syncwarp();
+        }
+        // ---- pass 3: Q = Q1 M, yv = Q^T XV (full RB x RB)
+        double gy[NB * NB][2];
+#pragma unroll
+        for (int t = 0; t < NB * NB; ++t) gy[t][0] = gy[t][1] = 0.0;
+        double curx[NB][2], nxtx[NB][2];
+        fetch(cur, T, r0 + 8 * (int64_t)cw + g, r0 + 8 * (int64_t)cw + g < r1, false);
+        fetch(curx, XV, r0 + 8 * (int64_t)cw + g, r0 + 8 * (int64_t)cw + g < r1, false);
+        for (int ch = cw; ch < nch; ch += cs) {
+            const int64_t row = r0 + 8 * (int64_t)ch + g;
+            const bool valid = row < r1;
+            fetch(nxt, T, row + 8 * cs, row + 8 * cs < r1, false);
+            fetch(nxtx, XV, row + 8 * cs, row + 8 * cs < r1, false);
+            put(In, cur);
+            put(Xt, curx);
+            __syncwarp();
+            double out[NB][2];
+            gemm(Bm, out);
+            store_rows(Q, row, valid, out);
+            __syncwarp();
+#pragma unroll
+            for (int ib = 0; ib < NB; ++ib)
+#pragma unroll
+                for (int kb = 0; kb < NB; ++kb) mma_xty(gy[ib * NB + kb], Out + 64 * ib, Xt + 64 * kb, o);
+            __syncwarp();
+            copy2(cur, nxt);
+            copy2(curx, nxtx);
+        }
+        reduce(gy);
+#pragma unroll
+        for (int ib = 0; ib < NB; ++ib)
+#pragma unroll
+            for (int kb = 0; kb < NB; ++kb)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int r = 8 * ib + g, z = 8 * kb + c0 + e;
+                    if (cw == 0 && r < R && z < R) yv[(int64_t)k * R * R + r * R + z] = gy[ib * NB + kb][e];
+                }
+        __syncwarp();
+    }
+}
+
+// slices with more than max(512, 2 x mean) rows take the cooperative (CTA per slice) variant: it repeats the
+// R x R serial part in every warp, so it only pays for the outliers that would otherwise set the kernel's tail
+constexpr int kAlsLongRows = 512;
+
+template <int NB>
+int launch_als_polar_mma(dash_ctx *ctx, cudaStream_t st, const int64_t *row_ptr, const int64_t *row_ptr_host, int K,
+                         const double *XV, const double *W, const double *H, int R, double *T, double *Q,
+                         double *yv) {
+    constexpr int NW = NB == 1 ? 8 : (NB == 2 ? 5 : 4);  // NB = 2: ~72 KB per CTA -> 3 CTAs = 15 warps per SM
+    // long slices first (longest first), then the short ones in tensor order
+    std::vector<int32_t> ord;
+    ord.reserve(K);
+    const int64_t long_rows = std::max<int64_t>(kAlsLongRows, 2 * (row_ptr_host[K] - row_ptr_host[0]) / std::max(K, 1));
+    for (int k = 0; k < K; ++k)
+        if (row_ptr_host[k + 1] - row_ptr_host[k] > long_rows) ord.push_back(k);
+    const int nlong = (int)ord.size();
+    std::stable_sort(ord.begin(), ord.end(), [row_ptr_host](int a, int b) {
+        return row_ptr_host[a + 1] - row_ptr_host[a] > row_ptr_host[b + 1] - row_ptr_host[b];
+    });
+    for (int k = 0; k < K; ++k)
+        if (row_ptr_host[k + 1] - row_ptr_host[k] <= long_rows) ord.push_back(k);
+    if (ensure(ctx->items, sizeof(int32_t) * (size_t)std::max(K, 1))) return DASH_E_CUDA;
+    int32_t *list = (int32_t *)ctx->items.p;
+    // pageable source: the call returns once `ord` has been read into the driver's staging buffer
+    cudaMemcpyAsync(list, ord.data(), sizeof(int32_t) * (size_t)K, cudaMemcpyHostToDevice, st);
+    auto per_sm = [&](size_t smem) { return std::max<int>(1, (int)std::min<size_t>(8, (size_t)(227 * 1024) / (smem + 1024))); };
+    if (nlong > 0) {
+        const size_t smem = AlsMmaSmem<NB>::bytes(NW, true);
+        ensure_smem_attr(k_als_polar_mma<NB, NW, true>, smem);
+        k_als_polar_mma<NB, NW, true><<<std::min(nlong, ctx->num_sms * per_sm(smem)), NW * 32, smem, st>>>(
+            row_ptr, list, nlong, XV, W, H, R, T, Q, yv, ctx->err);
+    }
+    if (K > nlong) {
+        const size_t smem = AlsMmaSmem<NB>::bytes(NW, false);
+        ensure_smem_attr(k_als_polar_mma<NB, NW, false>, smem);
+        const int ns = K - nlong;
+        k_als_polar_mma<NB, NW, false><<<std::max(1, std::min((ns + NW - 1) / NW, ctx->num_sms * per_sm(smem))),
+                                          NW * 32, smem, st>>>(row_ptr, list + nlong, ns, XV, W, H, R, T, Q, yv,
+                                                               ctx->err);
+    }
+    return cudaGetLastError() == cudaSuccess ? 0 : DASH_E_CUDA;
 }
 
 // CP sweep on the projected tensor (als.py:166-176), a cooperative grid:
@@ -516,7 +885,7 @@ int launch_als_polar(dash_ctx *ctx, cudaStream_t st, const int64_t *row_ptr, int
     constexpr int NW = RB <= 16 ? 4 : 2;
     const size_t smem = AlsSmem<RB>::bytes(NW);
     ensure_smem_attr(k_als_polar<RB, NW>, smem);
-    const int blocks = std::max(1, std::min(K, ctx->num_sms * 8));
+    const int blocks = std::max(1, std::min((K + NW - 1) / NW, ctx->num_sms * 8));
     k_als_polar<RB, NW><<<blocks, NW * 32, smem, st>>>(row_ptr, K, XV, W, H, R, T, Q, yv, ctx->err);
     return 0;
 }
@@ -591,6 +960,17 @@ int dash_als_sweep_f64(dash_ctx *ctx, void *stream, const dash_batch_f64 *t, int
     } else {
         launch_xv(ctx, st, &b, J, V, R, XV);
     }
+    static const bool polar_scalar = getenv("DASH_ALS_POLAR_SCALAR") != nullptr;  // A/B switch
+    if (!polar_scalar) {
+        int rc_p;
+        switch (RB) {
+            case 4:
+            case 8: rc_p = launch_als_polar_mma<1>(ctx, st, t->row_ptr, t->row_ptr_host, K, XV, W, H, R, T, Q, yv); break;
+            case 16: rc_p = launch_als_polar_mma<2>(ctx, st, t->row_ptr, t->row_ptr_host, K, XV, W, H, R, T, Q, yv); break;
+            default: rc_p = launch_als_polar_mma<4>(ctx, st, t->row_ptr, t->row_ptr_host, K, XV, W, H, R, T, Q, yv); break;
+        }
+        if (rc_p) return rc_p;
+    } else
     switch (RB) {
         case 4: launch_als_polar<4>(ctx, st, t->row_ptr, K, XV, W, H, R, T, Q, yv); break;
         case 8: launch_als_polar<8>(ctx, st, t->row_ptr, K, XV, W, H, R, T, Q, yv); break;
