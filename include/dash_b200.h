@@ -77,7 +77,9 @@ int dash_host_row_ptr(const int64_t *counts, int64_t M, int64_t *row_ptr, int64_
  * keep_dev != NULL the packed block is also copied there (device to device, on
  * `stream`) for the U history.  dash_stage_release records, on `stream`, that
  * the update which read the last staged slot has been issued in full -- the slot's
- * device block is rewritten only after that point.  The host blocks only when
+ * device block is rewritten only after that point; the final dash_update_pass_finish
+ * of an update (and so dash_update_f64 / _f32) does the same, so callers that run
+ * the staged batch through those entry points need not call it.  The host blocks only when
  * the ring wraps onto a copy still in flight. */
 typedef struct dash_staged {
     int64_t N;               /* total rows of the batch */

@@ -2223,6 +2223,12 @@ int dash_update_pass_finish_f64(dash_ctx *ctx, void *stream, dash_state_f64 *s, 
     if (ctx->pset_free && ctx->cur_pass == s->passes - 1) {  // the plan set of this update is free again
         cudaEventRecord(ctx->pset_free, st);
         ctx->pset_used = true;
+        // ... and so is the staging slot it read (what dash_stage_release does; the same event serves both)
+        if (ctx->mring_last >= 0) {
+            dash_ctx::MetaSlot &ms = ctx->mring[ctx->mring_last];
+            cudaEventRecord(ms.done, st);
+            ms.upd_issued = true;
+        }
     }
     return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_E_CUDA;
 }

@@ -597,6 +597,11 @@ class StreamState:
         self._last = (None, None, meta, X, meta.N, U_dev)  # row_ptr: meta.host_row_ptr() on demand
         return U_dev, v_used
 
+    @property
+    def last_launches(self) -> int:
+        """Library kernels launched by the last update (bench's gpu_launches)."""
+        return int(nat.lib().dash_ctx_last_launches(self._ctx))
+
     def _register(self, new_ids):
         """stream.py:270-280: new slices take the next state rows, in batch order."""
         L = len(new_ids)
@@ -614,11 +619,22 @@ class StreamState:
         f32 = self.dtype == torch.float32
         U = self._alloc_u(N)
         v_used = torch.empty((self.J, self._R), dtype=F64, device=dev)
-        b = nat.DashBatch(X=_ptr(X), ldx=int(X.stride(0)) if N else self.J, N=N, M=M,
-                          row_ptr=meta.rp, row_ptr_host=meta.rp_host, state_row=meta.sr, is_new=meta.nw)
-        s = nat.DashState(W=_ptr(self._Wd), C=_ptr(self._Cd), D=_ptr(self._Dd), V=_ptr(self._V),
-                          F=_ptr(self._F), G=_ptr(self._G), J=self.J, R=self._R,
-                          forgetting=self.forgetting, passes=self.passes)
+        # the two argument structs are reused across updates (building ctypes structs and reading six
+        # data pointers per update is measurable on a host-bound stream); the state struct is refreshed
+        # whenever a state tensor was replaced (capacity growth, a setter)
+        b = self.__dict__.get("_cbatch")
+        if b is None:
+            b = self._cbatch = nat.DashBatch()
+        b.X, b.ldx, b.N, b.M = _ptr(X), (int(X.stride(0)) if N else self.J), N, M
+        b.row_ptr, b.row_ptr_host, b.state_row, b.is_new = meta.rp, meta.rp_host, meta.sr, meta.nw
+        key = (self._Wd, self._Cd, self._Dd, self._V, self._F, self._G)
+        cs = self.__dict__.get("_cstate")
+        if cs is None or any(a is not c for a, c in zip(cs[1], key)):
+            cs = self._cstate = (nat.DashState(W=_ptr(self._Wd), C=_ptr(self._Cd), D=_ptr(self._Dd),
+                                               V=_ptr(self._V), F=_ptr(self._F), G=_ptr(self._G), J=self.J,
+                                               R=self._R, forgetting=self.forgetting, passes=self.passes), key)
+        s = cs[0]
+        s.forgetting, s.passes = self.forgetting, self.passes
         L = nat.lib()
         st = nat.stream_ptr()
         upd = L.dash_update_f32 if f32 else L.dash_update_f64
@@ -640,10 +656,8 @@ class StreamState:
         if self.keep_u_history:
             self._ustore.append(U)
             self._ulog.append((len(self._ustore) - 1, meta, M))
-        # this update no longer reads its ring slot after this point
-        nat.check(L.dash_stage_release(self._ctx, st), "dash_stage_release")
+        # (the update's last pass_finish released the staging slot: dash_b200.h)
         self._cache.clear()
-        self.last_launches = L.dash_ctx_last_launches(self._ctx)
         self._err_ids = ids
         if check:
             self.check()
