@@ -21,6 +21,7 @@
 #include <cudaTypedefs.h>
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -1034,7 +1035,15 @@ struct PhaseScope {
     cudaStream_t st;
     int id;
     cudaEvent_t a = nullptr;
+    // NVTX range per phase (host-side launch window; header-only NVTX3: a no-op unless a
+    // tool such as nsys / ncu --nvtx is attached), named like bench.py's phase keys
+    static const char *phase_name(int i) {
+        static const char *const names[PH_COUNT] = {"dash:row_slice", "dash:prologue", "dash:xv",      "dash:slices", "dash:fgemm",
+                                                    "dash:sum_fg",    "dash:vsolve",   "dash:big",     "dash:big_post"};
+        return (i >= 0 && i < PH_COUNT) ? names[i] : "dash:?";
+    }
     PhaseScope(dash_ctx *c, cudaStream_t s, int i) : ctx(c), st(s), id(i) {
+        nvtxRangePushA(phase_name(i));
         if (ctx->prof) {
             a = prof_event(ctx);
             cudaEventRecord(a, st);
@@ -1047,6 +1056,7 @@ struct PhaseScope {
             cudaEventRecord(b, st);
             ctx->ev_recs.push_back({id, {a, b}});
         }
+        nvtxRangePop();
     }
 };
 
