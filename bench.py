@@ -409,6 +409,29 @@ def run_gpu(args):
     L.dash_ctx_phase_ms(state._ctx, ms_arr, cnt_arr, nph)
     L.dash_ctx_set_profiling(state._ctx, 0)
     state.check()
+    # the per-update fitness (evaluate.local_error) on the device-resident batch the
+    # last profiled update just consumed: the reference's comment asks that it stay cheap next to
+    # the update it measures -- timed here (second pass over X: row errors on DMMA tiles + sums)
+    fitness = None
+    if profiled:
+        from paper_2305_18376_b200.evaluate import local_error_device
+        lb = profiled[-1]
+        _, _, meta, Xl, Nl, Ul = state._last
+        rp_h = meta.host_row_ptr().copy()
+        sr_d = meta[1]
+        local_error_device(Xl, Nl, rp_h, sr_d, Ul, state, row_ptr_dev=meta[0])  # warm-up
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 5
+        f0.record(stream)
+        for _ in range(reps):
+            local_error_device(Xl, Nl, rp_h, sr_d, Ul, state, row_ptr_dev=meta[0])
+        f1.record(stream)
+        torch.cuda.synchronize()
+        fit_ms = f0.elapsed_time(f1) / reps
+        fb = 8 * (lb["N"] * J + lb["N"] * R + J * R)
+        fitness = {"ms_per_update": fit_ms, "alg_bytes": fb, "gbs": fb / (fit_ms / 1e3) / 1e9,
+                   "what": "local_error of one update's batch (device-resident X, U_new; per-slice MAD + tensor mean)"}
     t_ms = e0.elapsed_time(e1)
     t_max = t_ms
     if world > 1:
@@ -546,6 +569,7 @@ def run_gpu(args):
             "fp32": fp32,
             "e2e_dropin": dropin,
             "parity": parity,
+            "fitness": fitness,
             "als": als,
             "clocks": clocks,
         }

@@ -393,6 +393,7 @@ __global__ void __launch_bounds__(256) k_row_err_mma(const TX *__restrict__ X, i
         }
         const TX *xrow = X + (valid ? row : 0) * ldx;
         double acc = 0.0;
+#pragma unroll 4
         for (int j0 = 0; j0 < J8; j0 += 8) {
             const int j = j0 + 2 * t;
             const double x0 = (valid && j < J) ? (double)xrow[j] : 0.0;
@@ -408,6 +409,72 @@ __global__ void __launch_bounds__(256) k_row_err_mma(const TX *__restrict__ X, i
         acc += __shfl_xor_sync(FULL_MASK, acc, 2);
         if (t == 0 && valid) row_err[row] = acc;
     }
+}
+
+// Wide-J form of k_row_err_mma (J x (RB + 4) doubles of V do not fit in shared memory: J = 1,024):
+// a CTA takes 64 rows at a time (8 rows per warp, A fragments kept in registers) and walks the
+// columns in chunks of JC, re-staging that chunk of V from L2 for every 64-row group (V traffic
+// ~ X traffic).  The scalar fallback this replaces ran at 0.9 TB/s at R = 10 and 33 GB/s at R = 64.
+template <bool ABS, typename TX, typename TU, int RB>
+__global__ void __launch_bounds__(256) k_row_err_mma_wide(const TX *__restrict__ X, int64_t ldx, int64_t N,
+                                                          const TU *__restrict__ Z, int R, const double *__restrict__ V,
+                                                          int J, int JC, const int32_t *__restrict__ row_slice,
+                                                          const int32_t *__restrict__ state_row,
+                                                          const double *__restrict__ W, double *__restrict__ row_err) {
+    constexpr int P = RB == 4 ? 4 : RB + 4, KS = RB / 4;
+    extern __shared__ double vs[];  // JC x P
+    const int lane = lane_id(), g = lane >> 2, t = lane & 3, w = warp_id();
+    const int64_t ngroups = (N + 63) / 64;
+    for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+        const int64_t row = grp * 64 + 8 * w + g;
+        const bool valid = row < N;
+        const double *wr = (W && valid) ? W + (int64_t)state_row[row_slice[row]] * R : nullptr;
+        double a[KS];
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk) {
+            const int r = 4 * kk + t;
+            a[kk] = (valid && r < R) ? (double)Z[row * R + r] * (wr ? wr[r] : 1.0) : 0.0;
+        }
+        const TX *xrow = X + (valid ? row : 0) * ldx;
+        double acc = 0.0;
+        for (int jc0 = 0; jc0 < J; jc0 += JC) {
+            __syncthreads();  // the previous chunk (or group) is no longer read
+            for (int i = threadIdx.x; i < JC * P; i += blockDim.x) {
+                const int j = jc0 + i / P, r = i % P;
+                vs[i] = (j < J && r < R) ? V[(int64_t)j * R + r] : 0.0;
+            }
+            __syncthreads();
+            const int jn = min(JC, (J - jc0 + 7) / 8 * 8);
+#pragma unroll 2
+            for (int j0 = 0; j0 < jn; j0 += 8) {
+                const int j = jc0 + j0 + 2 * t;
+                const double x0 = (valid && j < J) ? (double)xrow[j] : 0.0;
+                const double x1 = (valid && j + 1 < J) ? (double)xrow[j + 1] : 0.0;
+                double c[2] = {0.0, 0.0};
+                const double *vb = vs + (j0 + g) * P + t;
+#pragma unroll
+                for (int kk = 0; kk < KS; ++kk) dmma884(c, a[kk], vb[4 * kk]);
+                const double d0 = x0 - c[0], d1 = x1 - c[1];
+                acc = ABS ? acc + fabs(d0) + fabs(d1) : fma(d1, d1, fma(d0, d0, acc));
+            }
+        }
+        acc += __shfl_xor_sync(FULL_MASK, acc, 1);
+        acc += __shfl_xor_sync(FULL_MASK, acc, 2);
+        if (t == 0 && valid) row_err[row] = acc;
+    }
+}
+
+template <bool ABS, typename TX, typename TU, int RB>
+void launch_row_err_mma_wide(dash_ctx *ctx, cudaStream_t st, const TX *X, int64_t ldx, int64_t N, const TU *Z, int R,
+                             const double *V, int J, const int32_t *row_slice, const int32_t *state_row,
+                             const double *W, double *row_err) {
+    constexpr int P = RB == 4 ? 4 : RB + 4;
+    const int JC = RB <= 16 ? 512 : (RB <= 32 ? 256 : 128);
+    const size_t smem = sizeof(double) * (size_t)JC * P;
+    ensure_smem_attr(k_row_err_mma_wide<ABS, TX, TU, RB>, smem);
+    const int blocks = (int)std::min<int64_t>((N + 63) / 64, (int64_t)ctx->num_sms * 2);
+    k_row_err_mma_wide<ABS, TX, TU, RB><<<std::max(blocks, 1), 256, smem, st>>>(X, ldx, N, Z, R, V, J, JC, row_slice,
+                                                                                state_row, W, row_err);
 }
 
 template <bool ABS, typename TX, typename TU, int RB>
@@ -429,6 +496,16 @@ int launch_row_err(dash_ctx *ctx, cudaStream_t st, const TX *X, int64_t ldx, int
         static const bool scalar = getenv("DASH_ROWERR_SCALAR") != nullptr;  // A/B switch
         const int RB = rank_bucket(R), P = RB == 4 ? 4 : RB + 4;
         const size_t sm = sizeof(double) * (size_t)((J + 7) / 8 * 8) * P;
+        if (!scalar && sm > 96 * 1024) {  // wide J: V chunked through shared memory
+            switch (RB) {
+                case 4: launch_row_err_mma_wide<ABS, TX, TU, 4>(ctx, st, X, ldx, N, Z, R, V, J, row_slice, state_row, W, row_err); break;
+                case 8: launch_row_err_mma_wide<ABS, TX, TU, 8>(ctx, st, X, ldx, N, Z, R, V, J, row_slice, state_row, W, row_err); break;
+                case 16: launch_row_err_mma_wide<ABS, TX, TU, 16>(ctx, st, X, ldx, N, Z, R, V, J, row_slice, state_row, W, row_err); break;
+                case 32: launch_row_err_mma_wide<ABS, TX, TU, 32>(ctx, st, X, ldx, N, Z, R, V, J, row_slice, state_row, W, row_err); break;
+                default: launch_row_err_mma_wide<ABS, TX, TU, 64>(ctx, st, X, ldx, N, Z, R, V, J, row_slice, state_row, W, row_err); break;
+            }
+            return 0;
+        }
         if (!scalar && sm <= 96 * 1024) {
             switch (RB) {
                 case 4: launch_row_err_mma<ABS, TX, TU, 4>(ctx, st, X, ldx, N, Z, R, V, J, row_slice, state_row, W, row_err, sm); break;

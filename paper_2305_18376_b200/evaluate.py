@@ -22,7 +22,8 @@ def local_error(batch_items, u_new, state):
         _, row_ptr, meta, X, N, U = last
         if row_ptr is None:
             row_ptr = meta.host_row_ptr()
-        state_row = meta[1]  # device copy staged by the update
+        state_row = meta[1]  # device copies staged by the update
+        rp_dev = meta[0]
     else:
         counts = np.array([np.asarray(r).shape[0] for _, r in batch_items], dtype=np.int64)
         row_ptr = np.zeros(len(ids) + 1, dtype=np.int64)
@@ -34,24 +35,26 @@ def local_error(batch_items, u_new, state):
                             device=dev).to(dt)
         state_row = np.array([state.row_of(s) for s in ids], dtype=np.int32)
         N = int(row_ptr[-1])
-    slice_err, te = local_error_device(X, N, row_ptr, state_row, U, state)
+        rp_dev = None
+    slice_err, te = local_error_device(X, N, row_ptr, state_row, U, state, row_ptr_dev=rp_dev)
     se = slice_err.cpu().numpy()
     return float(te.item()), {sid: float(se[k]) for k, sid in enumerate(ids)}
 
 
-def local_error_device(X, N, row_ptr, state_row, U, state):
-    """Device tensors in, device (slice_err (M,), tensor_err ()) out."""
+def local_error_device(X, N, row_ptr, state_row, U, state, row_ptr_dev=None):
+    """Device tensors in, device (slice_err (M,), tensor_err ()) out.  ``row_ptr_dev``: the
+    update's own staged device copy of row_ptr (saves re-uploading it)."""
     return slice_errors_device(X, N, row_ptr, state_row, U, state.device_tensors["W"], state._V,
-                               state._ctx, state.device)
+                               state._ctx, state.device, row_ptr_dev=row_ptr_dev)
 
 
-def slice_errors_device(X, N, row_ptr, state_row, U, W, V, ctx=None, device=None):
+def slice_errors_device(X, N, row_ptr, state_row, U, W, V, ctx=None, device=None, row_ptr_dev=None):
     """Per-slice mean |X_k - (U_k o W[state_row[k]]) V^T| and their mean
     (anomaly.py:23-42 slice_error / tensor_error) on the device."""
     dev = X.device if device is None else device
     M = len(row_ptr) - 1
     J, R = V.shape
-    rp = torch.as_tensor(np.asarray(row_ptr, dtype=np.int64), device=dev)
+    rp = row_ptr_dev if row_ptr_dev is not None else torch.as_tensor(np.asarray(row_ptr, dtype=np.int64), device=dev)
     sr = (state_row if isinstance(state_row, torch.Tensor)
           else torch.as_tensor(np.asarray(state_row, dtype=np.int32), device=dev))
     slice_err = torch.empty(max(M, 1), dtype=torch.float64, device=dev)

@@ -27,13 +27,26 @@ def main(K0=20000, J=128, R=16, steps=4, n_new=300):
     gen.manual_seed(11)
     h = hashlib.sha256()
     K = K0
+    # "async": no host sync between updates (the results are read after the last one), so update
+    # t+1 is issued -- and its device plan runs on the staging side stream -- while update t executes
+    defer = "async" in sys.argv[1:]
+    batches, kept = [], []
     for t in range(steps):
         counts = np.concatenate([rng.integers(1, 9, K), rng.integers(65, 1500, n_new)]).astype(np.int64)
         X = torch.randn((int(counts.sum()), J), generator=gen, dtype=torch.float64, device="cuda") * 0.1
-        U, vu = st.update_packed(X, counts, np.arange(K, dtype=np.int32), [f"n{t}_{i}" for i in range(n_new)])
+        batches.append((X, counts, np.arange(K, dtype=np.int32), [f"n{t}_{i}" for i in range(n_new)]))
+        K += n_new
+    torch.cuda.synchronize()
+    for X, counts, ex, new in batches:
+        U, vu = st.update_packed(X, counts, ex, new)
+        if defer:
+            kept.append((U, vu))
+        else:
+            h.update(U.cpu().numpy().tobytes())
+            h.update(vu.cpu().numpy().tobytes())
+    for U, vu in kept:
         h.update(U.cpu().numpy().tobytes())
         h.update(vu.cpu().numpy().tobytes())
-        K += n_new
     st.check()
     for name in ("W", "C", "D", "F", "G", "V"):
         h.update(np.ascontiguousarray(getattr(st, name)).tobytes())
