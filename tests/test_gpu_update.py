@@ -351,3 +351,34 @@ def test_indefinite_G_takes_the_lu_path_like_the_reference():
     for name in ("V", "F", "G", "W"):
         assert rel(getattr(gpu, name), getattr(cpu, name)) < TOL, name
     assert nat.lib().dash_ctx_fallbacks(gpu._ctx, nat.stream_ptr(), 1) >= 1
+
+
+@pytest.mark.parametrize("name,kw", [
+    ("wide10", dict(K0=40, steps=2, new_slices=2, J=130)),             # just past the J <= 128 tensor-map path
+    ("wide10", dict(K0=40, steps=2, new_slices=2, J=257, R=16)),       # two column blocks, the second one column wide
+    ("wide10", dict(K0=30, steps=2, new_slices=2, J=1000, R=6)),       # J not a multiple of 16 / 64; R bucket 8
+    ("wide32", dict(K0=30, steps=2, new_slices=2, J=600, R=30)),       # R < 32: padded ranks in k_xvw / k_fgemmw / k_slicesw
+    ("wide64", dict(K0=24, steps=2, new_slices=2, J=1030, R=50)),      # 9 column blocks of 128, G tiles over 9 x 8 warps
+    ("wide64", dict(K0=24, steps=2, new_slices=2, J=300)),             # 3 column blocks: too few warps for the G tiles -> generic GEMMs
+    ("wide32", dict(K0=30, steps=2, new_slices=2, passes=2)),          # multi-pass: US / G recomputed per pass
+    ("wide10", dict(K0=1, steps=2, new_slices=0, add_rows=("fixed", 1))),  # one slice, one row per update
+    ("wide10", dict(K0=40, steps=2, new_slices=2, R=9)),               # odd R: generic register-staged GEMMs
+])
+def test_wide_j_path_edges_match_oracle(name, kw):
+    """The wide-J tensor-map GEMMs (dash_widej.cuh), k_us_rows and the wide row-error kernel at the
+    edges of their tilings; every case also checks local_error against the oracle."""
+    from oracle import dash_oracle as orc
+    from paper_2305_18376_b200 import workloads as wl
+    from paper_2305_18376_b200.evaluate import local_error
+    cfg = wl.scaled(wl.CONFIGS[name], **kw)
+    stream_parity(cfg)
+    stream = wl.make_stream(cfg)
+    ps = wl.planted_state(stream)
+    gpu, cpu = gpu_state_from_planted(ps, passes=cfg.passes), oracle_from_planted(ps, passes=cfg.passes)
+    batch = next(stream.batches())
+    res, ref = gpu.update(batch), cpu.update(batch)
+    items = [(s, r) for s, r, _ in batch.items()]
+    te, per = local_error(items, res.u_new, gpu)
+    te_o, per_o = orc.local_error(items, ref["u_new"], {s: cpu.W[cpu.row_of(s)] for s, _ in items}, cpu.V)
+    assert abs(te - te_o) <= TOL * abs(te_o)
+    assert max(abs(per[s] - per_o[s]) for s, _ in items) <= TOL * max(per_o.values())
