@@ -144,6 +144,51 @@ __device__ __forceinline__ double rsqrt_nr(double d) {
 // reference's update order; writes L^{-1} (lower, zeros above) to Li.  Every
 // 8-lane group computes the same factor (warp-uniform result).
 __device__ __forceinline__ bool diag_chol8(const double *T, double *Li) {
+    // Every lane factors the whole tile in registers (36 broadcast loads, ~150 DFMA / DMUL, 8 rsqrt;
+    // static indices throughout) and then solves for one column of L^{-1}.  The earlier version kept
+    // one row per lane and exchanged pivots and multipliers by shuffles: 33% of the kernel's stall
+    // samples and 45% of its instructions at R = 64 (profiles/r02s3_checkpoint/ncu_w64_slicesw_lines.txt).
+    const int l = lane_id(), i = l & 7;
+    double L[8][8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int k = 0; k <= r; ++k) L[r][k] = T[toff(r, k)];
+    double inv[8];
+    bool ok = true;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const double d = L[j][j];
+        ok = ok && (d > 0.0) && finite_d(d);
+        const double iv = rsqrt_nr(d);  // only 1 / sqrt(d) is needed (L_jj itself is never stored)
+        inv[j] = iv;
+#pragma unroll
+        for (int r = j + 1; r < 8; ++r) L[r][j] *= iv;
+#pragma unroll
+        for (int k = j + 1; k < 8; ++k)
+#pragma unroll
+            for (int r = k; r < 8; ++r) L[r][k] = fma(-L[r][j], L[k][j], L[r][k]);
+    }
+    // column i of L^{-1}:  L x = e_i
+    double x[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        double s = (r == i) ? 1.0 : 0.0;
+#pragma unroll
+        for (int k = 0; k < r; ++k) s = fma(-L[r][k], x[k], s);
+        x[r] = s * inv[r];
+    }
+    if (l < 8) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) Li[toff(r, i)] = x[r];
+    }
+    return ok;
+}
+
+// Row-per-lane variant (pivots and multipliers exchanged by shuffles), kept behind -DDASH_DIAG_SHFL
+// for A/B.  Same-box A/B at R = 64 (tools/ab_diag.sh, 3 runs each): 3.28-3.33 ms / update with
+// this variant, 3.09-3.13 ms with the register-resident factor above; R = 32: slices phase 610 -> 562 us.
+__device__ __forceinline__ bool diag_chol8_shfl(const double *T, double *Li) {
     const int l = lane_id(), i = l & 7;
     double row[8];
 #pragma unroll
@@ -205,7 +250,13 @@ __device__ __forceinline__ bool chol_tiles(double *Lt, double *Li, const LaneOff
 #pragma unroll
         for (int ib = jb; ib < NB; ++ib) stc(Lt + 64 * tri(ib, jb), c[ib], o);
         __syncwarp();
-        ok = diag_chol8(Lt + 64 * tri(jb, jb), Li + 64 * jb) && ok;
+#ifdef DASH_DIAG_SHFL  // A/B build knob: the row-per-lane shuffle variant
+        constexpr int kSerialMaxNB = 0;
+#else
+        constexpr int kSerialMaxNB = 8;
+#endif
+        ok = (NB <= kSerialMaxNB ? diag_chol8(Lt + 64 * tri(jb, jb), Li + 64 * jb)
+                      : diag_chol8_shfl(Lt + 64 * tri(jb, jb), Li + 64 * jb)) && ok;
         __syncwarp();
         if (jb + 1 < NB) {
 #pragma unroll
