@@ -529,32 +529,58 @@ __global__ void __launch_bounds__(NW * 32) k_als_polar_mma(const int64_t *__rest
             }
         }
         __syncwarp();
-        // ---- one-sided Jacobi SVD of Rt (cyclic by rows): Rt V = U Sigma
+        // ---- one-sided Jacobi SVD of Rt (cyclic by rows): Rt V = U Sigma.  Column norms are
+        // refreshed once per sweep (one batched warp reduction) and updated in closed form after
+        // each rotation (|a'|^2 = |a|^2 - t gamma, |b'|^2 = |b|^2 + t gamma), so a pair costs one
+        // warp reduction (gamma) instead of three; the rotation parameters come from rsqrt / rcp
+        // seeds + Newton steps instead of three IEEE sqrt and three divisions (together 46% of the
+        // kernel's stall samples at the daily shape, profiles/r02s3_als/ncu_polar_lines.txt).
+        double *nrm2 = wv;  // the slice's weights are dead after pass 1
         for (int sweep = 0; sweep < 60; ++sweep) {
+            {
+                double sig[RB];
+#pragma unroll
+                for (int m = 0; m < RB; ++m) {
+                    const double v = lane < RB ? Rt[lane * LD + m] : 0.0;
+                    sig[m] = v * v;
+                }
+                warp_allreduce<RB>(sig);
+                __syncwarp();
+#pragma unroll
+                for (int m = 0; m < RB; ++m)
+                    if (lane == 0) nrm2[m] = sig[m];
+                __syncwarp();
+            }
+            // (A round-robin ordering -- n / 2 independent rotations per round, batched reductions
+            // -- was measured slower: 168 -> 255 registers, 2 CTAs per SM; polar 2.20 -> 2.66 ms daily.)
             double offmax = 0.0;
             for (int p = 0; p < R - 1; ++p) {
                 for (int q = p + 1; q < R; ++q) {
                     const double a = lane < RB ? Rt[lane * LD + p] : 0.0;
                     const double b = lane < RB ? Rt[lane * LD + q] : 0.0;
-                    double al = a * a, be = b * b, gm = a * b;
+                    const double al = nrm2[p], be = nrm2[q];
+                    double gm = a * b;
 #pragma unroll
-                    for (int off = 16; off > 0; off >>= 1) {
-                        al += __shfl_xor_sync(FULL_MASK, al, off);
-                        be += __shfl_xor_sync(FULL_MASK, be, off);
-                        gm += __shfl_xor_sync(FULL_MASK, gm, off);
-                    }
-                    const double nrm = sqrt(al * be);
-                    if (!(nrm > 0.0) || fabs(gm) <= 1e-16 * nrm) continue;  // warp-uniform
-                    offmax = fmax(offmax, fabs(gm) / nrm);
-                    const double zeta = (be - al) / (2.0 * gm);
-                    const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                    const double cs = 1.0 / sqrt(1.0 + tt * tt), sn = cs * tt;
+                    for (int off = 16; off > 0; off >>= 1) gm += __shfl_xor_sync(FULL_MASK, gm, off);
+                    const double ab = al * be;
+                    if (!(ab > 0.0)) continue;                            // warp-uniform
+                    const double rel = fabs(gm) * rsqrt_nr(ab);           // |gamma| / (|a| |b|)
+                    if (rel <= 1e-16) continue;
+                    offmax = fmax(offmax, rel);
+                    const double zeta = (be - al) * 0.5 * rcp_nr(gm);
+                    const double z1 = 1.0 + zeta * zeta;
+                    const double tt = copysign(1.0, zeta) * rcp_nr(fabs(zeta) + z1 * rsqrt_nr(z1));
+                    const double cs = rsqrt_nr(1.0 + tt * tt), sn = cs * tt;
                     if (lane < RB) {
                         Rt[lane * LD + p] = cs * a - sn * b;
                         Rt[lane * LD + q] = sn * a + cs * b;
                         const double vp = Va[lane * LD + p], vq = Va[lane * LD + q];
                         Va[lane * LD + p] = cs * vp - sn * vq;
                         Va[lane * LD + q] = sn * vp + cs * vq;
+                    }
+                    if (lane == 0) {
+                        nrm2[p] = al - tt * gm;
+                        nrm2[q] = be + tt * gm;
                     }
                     __syncwarp();
                 }
