@@ -30,6 +30,28 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
+// 1/d to within 1 ulp: hardware reciprocal seed + two Newton steps (no IEEE
+// division subroutine on a solver's critical path)
+__device__ __forceinline__ double rcp_nr(double d) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+    double e = fma(-d, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-d, r, 1.0);
+    return fma(r, e, r);
+}
+
+// 1 / sqrt(d) to ~1 ulp for d > 0 (NaN / inf otherwise -- the caller's SPD test has
+// already failed then): rsqrt.approx (2^-22) + two Newton steps y += y (1 - d y^2) / 2
+__device__ __forceinline__ double rsqrt_nr(double d) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+    double e = fma(-d * y, y, 1.0);
+    y = fma(0.5 * y, e, y);
+    e = fma(-d * y, y, 1.0);
+    return fma(0.5 * y, e, y);
+}
+
 // Programmatic dependent launch (sm_90+): a kernel launched with the
 // programmatic-serialization attribute may start while its predecessor in the
 // stream is still running; pdl_wait() blocks until that predecessor has
@@ -68,8 +90,8 @@ __device__ __forceinline__ bool chol_regs(double (&row)[RB], double *Lsm, int ld
     for (int j = 0; j < RB; ++j) {
         double d = __shfl_sync(FULL_MASK, row[j], j);
         ok = ok && (d > 0.0) && finite_d(d);
-        double piv = sqrt(d);
-        double inv = 1.0 / piv;
+        const double inv = rsqrt_nr(d);  // no IEEE sqrt / division on the column chain
+        const double piv = d * inv;
         if (lane > j) row[j] = row[j] * inv;
         if (lane == j) row[j] = piv;
         if (lane == 0) dinv[j] = inv;

@@ -68,17 +68,6 @@ __device__ __forceinline__ void cp_async8(double *dst, const double *src) {
 }
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_all;\n" ::); }
 
-// 1/d to within 1 ulp: hardware reciprocal seed + two Newton steps (no IEEE
-// division subroutine on the sweep's critical path)
-__device__ __forceinline__ double rcp_nr(double d) {
-    double r;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
-    double e = fma(-d, r, 1.0);
-    r = fma(r, e, r);
-    e = fma(-d, r, 1.0);
-    return fma(r, e, r);
-}
-
 // In-place sweep of every pivot of the row-distributed symmetric matrix
 // (lane r holds row r in a[]): a <- -A^{-1}.  Returns false on a
 // non-positive or non-finite pivot.

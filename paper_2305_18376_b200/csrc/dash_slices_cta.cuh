@@ -27,7 +27,7 @@ __device__ __forceinline__ bool cta_sweep(double *M) {
         __syncthreads();
         const double d = M[k * LDM + k];
         ok = ok && (d > 0.0) && isfinite(d);
-        const double id = 1.0 / d;
+        const double id = rcp_nr(d);
         double nv[S::EPT];
 #pragma unroll
         for (int q = 0; q < S::EPT; ++q) {

@@ -129,17 +129,6 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-// 1 / sqrt(d) to ~1 ulp for d > 0 (NaN / inf otherwise -- the caller's SPD test has
-// already failed then): rsqrt.approx (2^-22) + two Newton steps y += y (1 - d y^2) / 2
-__device__ __forceinline__ double rsqrt_nr(double d) {
-    double y;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
-    double e = fma(-d * y, y, 1.0);
-    y = fma(0.5 * y, e, y);
-    e = fma(-d * y, y, 1.0);
-    return fma(0.5 * y, e, y);
-}
-
 // Cholesky of the 8x8 SPD diagonal tile T (lower part), right-looking in the
 // reference's update order; writes L^{-1} (lower, zeros above) to Li.  Every
 // 8-lane group computes the same factor (warp-uniform result).
