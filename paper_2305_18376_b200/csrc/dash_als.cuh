@@ -1038,7 +1038,7 @@ int dash_als_sweep_f64(dash_ctx *ctx, void *stream, const dash_batch_f64 *t, int
                           (const int32_t *)nullptr, (const double *)nullptr, (double *)ctx->rerr.p);
     k_seg_sum<<<std::max(1, std::min((K + 7) / 8, ctx->num_sms * 8)), 256, 0, st>>>((const double *)ctx->rerr.p,
                                                                                   t->row_ptr, K, J, 0, per);
-    k_tree_sum<<<1, 256, 0, st>>>(per, K, 0, loss);
+    k_tree_sum<<<1, kTreeThreads, 0, st>>>(per, K, 0, loss);
     return cudaGetLastError() == cudaSuccess ? DASH_OK : DASH_E_CUDA;
 }
 
