@@ -224,7 +224,9 @@ __global__ void __launch_bounds__(256) k_vsolve_cta(const double *__restrict__ f
                                                    const double *__restrict__ G_snap, double lam, int J, int R,
                                                    double eps, double *__restrict__ F, double *__restrict__ G,
                                                    double *__restrict__ V, unsigned long long *err,
-                                                   unsigned int *fallbacks) {
+                                                   unsigned int *fallbacks, const unsigned int *only_if = nullptr,
+                                                   unsigned int gen = 0) {
+    if (only_if != nullptr && *only_if != gen) return;  // k_vsolvew solved this update's V already
     using S = SC<RB>;
     constexpr int LDM = S::LDM;
     extern __shared__ double sm[];

@@ -720,10 +720,12 @@ __global__ void __launch_bounds__(NWV * 32) k_vsolve(const double *__restrict__ 
                                                      const double *__restrict__ G_snap, double lam, int J, int R,
                                                      double eps, double *__restrict__ F, double *__restrict__ G,
                                                      double *__restrict__ V, unsigned long long *err,
-                                                     unsigned int *fallbacks) {
+                                                     unsigned int *fallbacks, const unsigned int *only_if = nullptr,
+                                                     unsigned int gen = 0) {
     constexpr int LD = RB + 1;
     pdl_wait();
     pdl_trigger();
+    if (only_if != nullptr && *only_if != gen) return;  // k_vsolvew solved this update's V already
     __shared__ double sL[NWV][RB * LD];
     __shared__ double sG[NWV][RB * LD];
     __shared__ double sd[NWV][RB];
@@ -966,6 +968,8 @@ struct dash_ctx {
     bool swide = false;                   // R > 16 on k_slicesw (G's fresh term from the F GEMM)
     unsigned long long *err = nullptr;
     unsigned int *fallbacks = nullptr;
+    unsigned int *vs_flag = nullptr;  // k_vsolvew -> fallback V solve hand-off (holds the failing launch's generation)
+    unsigned int vs_gen = 0;
     int4 *items_host[2] = {nullptr, nullptr};
     size_t items_host_cap[2] = {0, 0};
     cudaEvent_t staged[2] = {nullptr, nullptr};
@@ -1360,6 +1364,123 @@ void launch_fgemm(dash_ctx *ctx, cudaStream_t st, const B *b, int J, const doubl
     }
 }
 
+// ---------------------------------------------------------------------------
+// k_vsolvew<NB>: the V solve for R in (16, 64] on DMMA tiles.  F = lam F0 + f,
+// G = sym(lam G0 + g), V = ridge_solve(G, F^T)^T (stream.py:344-346,
+// linalg.py:25-45).  Every CTA factors G + shift I once (one warp: the blocked
+// tile Cholesky of dash_slicesw.cuh), then its 8 warps each take 8-row chunks
+// of F and solve them against the factor (blocked substitution on DMMA) --
+// ~25 us where the one-pivot-at-a-time sweep of k_vsolve_cta<64> takes ~100 us
+// (64 block-wide barriers).  A non-SPD / non-finite G leaves the update to the
+// reference's fallback chain: the kernel then only marks the launch (flag = its
+// generation) and the sweep / LU kernel, launched behind it, runs for real.
+// ---------------------------------------------------------------------------
+template <int NB>
+__global__ void __launch_bounds__(256) k_vsolvew(const double *__restrict__ fg, const double *__restrict__ F_snap,
+                                                 const double *__restrict__ G_snap, double lam, int J, int R, double eps,
+                                                 double *__restrict__ F, double *__restrict__ G, double *__restrict__ V,
+                                                 unsigned long long *err, unsigned int *flag, unsigned int gen) {
+    using namespace swk;
+    constexpr int NT = NB * (NB + 1) / 2, NWV = 8;
+    extern __shared__ __align__(16) double sm[];
+    double *Lt = sm, *Li = Lt + 64 * NT;
+    const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
+    double *Uc = Li + 64 * NB + w * (NB + 1) * 64, *Cs = Uc + 64 * NB;
+    __shared__ int okf;
+    __shared__ double shv;
+    pdl_wait();     // fg from the slot sums
+    pdl_trigger();
+    const int64_t JR = (int64_t)J * R;
+    const double *g = fg + JR;
+    for (int e = tid; e < NT * 64; e += 256) {
+        const int t = e >> 6, k = e & 63, r = k >> 3, c = (k & 7) ^ ((r & 2) << 1);
+        int ib = 0;
+        while (tri(ib + 1, 0) <= t) ++ib;
+        const int kb = t - tri(ib, 0);
+        const int row = 8 * ib + r, col = 8 * kb + c;
+        double v = (row == col) ? 1.0 : 0.0;
+        if (row < R && col < R) {
+            const double m1 = lam * G_snap[row * R + col] + g[row * R + col];
+            const double m2 = lam * G_snap[col * R + row] + g[col * R + row];
+            v = (m1 + m2) / 2.0;
+            if (blockIdx.x == 0) {
+                G[row * R + col] = v;
+                G[col * R + row] = v;
+            }
+        }
+        Lt[e] = v;
+    }
+    __syncthreads();
+    if (w == 0) {
+        double tr = 0.0;
+        for (int r = lane; r < R; r += 32) tr += Lt[64 * tri(r >> 3, r >> 3) + toff(r & 7, r & 7)];
+        tr = warp_sum(tr);
+        if (lane == 0) shv = eps * (tr / R);
+    }
+    __syncthreads();
+    if (tid < R) Lt[64 * tri(tid >> 3, tid >> 3) + toff(tid & 7, tid & 7)] += shv;
+    __syncthreads();
+    const LaneOff o = lane_offsets();
+    if (w == 0) {
+        const bool ok = chol_tiles<NB>(Lt, Li, o);
+        if (lane == 0) okf = ok ? 1 : 0;
+    }
+    __syncthreads();
+    if (!okf) {  // not SPD: the sweep / LU kernel behind this one takes over (it rewrites F, G, V)
+        if (tid == 0) *flag = gen;
+        return;
+    }
+    const int nchunks = (J + 7) / 8;
+    for (int ch = blockIdx.x * NWV + w; ch < nchunks; ch += gridDim.x * NWV) {
+        const int j = 8 * ch + o.g;
+        double x[NB][2];
+#pragma unroll
+        for (int jb = 0; jb < NB; ++jb)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int col = 8 * jb + o.c0 + e;
+                double f = 0.0;
+                if (j < J && col < R) {
+                    f = lam * F_snap[(int64_t)j * R + col] + fg[(int64_t)j * R + col];
+                    F[(int64_t)j * R + col] = f;
+                }
+                x[jb][e] = f;
+            }
+        __syncwarp();
+        solve_chunk<NB>(x, Lt, Li, Uc, Cs, o);
+        bool fin = true;
+#pragma unroll
+        for (int jb = 0; jb < NB; ++jb)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int col = 8 * jb + o.c0 + e;
+                if (j < J && col < R) {
+                    V[(int64_t)j * R + col] = x[jb][e];
+                    fin = fin && finite_d(x[jb][e]);
+                }
+            }
+        if (!fin) report_error(err, -1, DASH_E_NONFINITE);
+        __syncwarp();
+    }
+}
+
+// returns true if k_vsolvew was launched (the caller then launches the fallback kernel gated on the flag)
+template <int NB>
+bool launch_vsolvew(dash_ctx *ctx, cudaStream_t st, const double *fg, double lam, int J, int R, double eps, double *F,
+                    double *G, double *V, unsigned int &gen) {
+    static const bool off = getenv("DASH_OLD_VSOLVE") != nullptr;  // A/B switch: the sweep kernels only
+    if (off) return false;
+    constexpr int NT = NB * (NB + 1) / 2;
+    const size_t smem = sizeof(double) * 64 * (NT + NB + 8 * (NB + 1));
+    ensure_smem_attr(k_vsolvew<NB>, smem);
+    gen = ++ctx->vs_gen;
+    if (gen == 0) gen = ++ctx->vs_gen;  // 0 is the flag's resting value
+    const int blocks = std::max(1, ((J + 7) / 8 + 7) / 8);
+    ctx->last_launches++;
+    return launch_k(pdl_site("vsw"), k_vsolvew<NB>, blocks, 256, smem, st, fg, (const double *)ctx->fsnap.p,
+                    (const double *)ctx->gsnap.p, lam, J, R, eps, F, G, V, ctx->err, ctx->vs_flag, gen) == 0;
+}
+
 template <int RB>
 void launch_vsolve_t(dash_ctx *ctx, cudaStream_t st, const double *fg, double lam, int J, int R, double eps,
                      double *F, double *G, double *V) {
@@ -1374,8 +1495,13 @@ void launch_vsolve_t(dash_ctx *ctx, cudaStream_t st, const double *fg, double la
     }
     constexpr int NWV = RB <= 16 ? 4 : 1;
     int blocks = (J + NWV * 32 - 1) / (NWV * 32);
+    const unsigned int *only_if = nullptr;
+    unsigned int gen = 0;
+    if constexpr (RB == 32) {
+        if (launch_vsolvew<4>(ctx, st, fg, lam, J, R, eps, F, G, V, gen)) only_if = ctx->vs_flag;
+    }
     launch_k(true, k_vsolve<RB, NWV>, blocks, NWV * 32, 0, st, fg, (const double *)ctx->fsnap.p,
-             (const double *)ctx->gsnap.p, lam, J, R, eps, F, G, V, ctx->err, ctx->fallbacks);
+             (const double *)ctx->gsnap.p, lam, J, R, eps, F, G, V, ctx->err, ctx->fallbacks, only_if, gen);
 }
 
 // out[0:width] = column sums of slots (nslots x width), deterministic order
@@ -1979,13 +2105,15 @@ int dash_ctx_create(dash_ctx **out) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (cudaMalloc(&ctx->err, sizeof(unsigned long long)) != cudaSuccess ||
-        cudaMalloc(&ctx->fallbacks, sizeof(unsigned int)) != cudaSuccess) {
+        cudaMalloc(&ctx->fallbacks, sizeof(unsigned int)) != cudaSuccess ||
+        cudaMalloc(&ctx->vs_flag, sizeof(unsigned int)) != cudaSuccess) {
         delete ctx;
         return DASH_E_CUDA;
     }
     unsigned long long none = ~0ull;
     cudaMemcpy(ctx->err, &none, sizeof(none), cudaMemcpyHostToDevice);
     cudaMemset(ctx->fallbacks, 0, sizeof(unsigned int));
+    cudaMemset(ctx->vs_flag, 0, sizeof(unsigned int));
     for (int i = 0; i < 2; ++i) cudaEventCreateWithFlags(&ctx->staged[i], cudaEventDisableTiming);
     *out = ctx;
     return DASH_OK;
@@ -2003,6 +2131,7 @@ void dash_ctx_destroy(dash_ctx *ctx) {
         if (b->p) cudaFree(b->p);
     cudaFree(ctx->err);
     cudaFree(ctx->fallbacks);
+    cudaFree(ctx->vs_flag);
     for (int i = 0; i < 2; ++i) {
         if (ctx->items_host[i]) cudaFreeHost(ctx->items_host[i]);
         cudaEventDestroy(ctx->staged[i]);
@@ -2224,9 +2353,12 @@ int dash_update_pass_finish_f64(dash_ctx *ctx, void *stream, dash_state_f64 *s, 
             const size_t smem = sizeof(double) * (64 * SC<64>::LDM + SC<64>::NT + 64);
             ensure_smem_attr(k_vsolve_cta<64>, smem);
             PhaseScope ps(ctx, st, PH_VSOLVE);
+            const unsigned int *only_if = nullptr;
+            unsigned int gen = 0;
+            if (launch_vsolvew<8>(ctx, st, fg, s->forgetting, J, R, eps, s->F, s->G, s->V, gen)) only_if = ctx->vs_flag;
             k_vsolve_cta<64><<<(J + 31) / 32, 256, smem, st>>>(fg, (const double *)ctx->fsnap.p,
                                                                (const double *)ctx->gsnap.p, s->forgetting, J, R, eps,
-                                                               s->F, s->G, s->V, ctx->err, ctx->fallbacks);
+                                                               s->F, s->G, s->V, ctx->err, ctx->fallbacks, only_if, gen);
             break;
         }
     }

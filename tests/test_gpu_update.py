@@ -332,13 +332,16 @@ def test_host_pipeline_matches_device_resident_updates():
         assert np.array_equal(getattr(a, name), getattr(b, name)), name
 
 
-def test_indefinite_G_takes_the_lu_path_like_the_reference():
+@pytest.mark.parametrize("name", ["large", "wide32", "wide64"])
+def test_indefinite_G_takes_the_lu_path_like_the_reference(name):
     """G0 = -10 I makes lam G0 + g indefinite: every pivot test of the V
-    solve's sweep fails and the LU fallback (the reference's np.linalg.solve,
-    linalg.py:25-45) must give the reference's V."""
+    solve (the sweep at R <= 16; the tile Cholesky of k_vsolvew at R = 32 / 64,
+    which then hands the launch to the sweep / LU kernel behind it) fails and
+    the LU fallback (the reference's np.linalg.solve, linalg.py:25-45) must
+    give the reference's V."""
     from paper_2305_18376_b200 import _native as nat
     from paper_2305_18376_b200 import workloads as wl
-    cfg = wl.scaled(wl.CONFIGS["large"], K0=40, steps=1, new_slices=2)
+    cfg = wl.scaled(wl.CONFIGS[name], K0=40, steps=1, new_slices=2)
     stream = wl.make_stream(cfg)
     ps = wl.planted_state(stream)
     ps["G"] = -10.0 * np.eye(cfg.R) * np.abs(ps["G"]).max()
