@@ -46,6 +46,7 @@ struct SwParams {
     double *W, *C, *D;
     const double *vtv;        // R x R
     double *scratch;          // per warp: SwScr<NB>::doubles
+    double *vtv_tiles;        // per CTA: NT x 64 doubles
     unsigned long long *err;
     unsigned int *fallbacks;
     int R;
@@ -62,10 +63,12 @@ template <int NB>
 struct Cfg {
     static constexpr int RB = 8 * NB;
     static constexpr int NT = NB * (NB + 1) / 2;  // lower tiles
-    static constexpr int NW = NB <= 4 ? 16 : 7;   // warps per CTA (one CTA per SM)
+    static constexpr int NW = NB <= 4 ? 16 : 8;   // warps per CTA (one CTA per SM; 8 x 255 registers x 32 = the register file)
     // per warp smem: Lt[NT] | Li[NB] | Uc[NB] | Cs[1] tiles | sv[RB]
     static constexpr int warp_doubles = (NT + 2 * NB + 1) * 64 + RB;
-    static constexpr int shared_doubles = NT * 64;  // vtv lower tiles
+    // vtv's lower tiles live in a per-CTA global scratch (L1-resident, read twice per slice): in shared
+    // memory they cost the R = 64 kernel its 8th warp (18 KB against 27.6 KB per warp)
+    static constexpr int shared_doubles = 0;
     static constexpr size_t smem_bytes() { return sizeof(double) * (shared_doubles + NW * warp_doubles); }
     // per warp global scratch: GR[NT tiles] | LU matrix RB x RB | row buffer 8 x RB | piv
     static constexpr int scr_doubles = NT * 64 + RB * RB + 8 * RB + RB;
@@ -324,7 +327,7 @@ __global__ void __launch_bounds__(swk::Cfg<NB>::NW * 32, 1) k_slicesw(SwParams p
     using Cf = Cfg<NB>;
     constexpr int RB = Cf::RB, NT = Cf::NT, NW = Cf::NW;
     extern __shared__ __align__(16) double sm[];
-    double *vtvT = sm;
+    double *vtvT = p.vtv_tiles + (size_t)blockIdx.x * NT * 64;
     const int w = warp_id(), lane = lane_id();
     double *wb = sm + Cf::shared_doubles + w * Cf::warp_doubles;
     double *Lt = wb, *Li = Lt + 64 * NT, *Uc = Li + 64 * NB, *Cs = Uc + 64 * NB, *sv = Cs + 64;

@@ -1277,8 +1277,9 @@ template <int NB>
 int run_slicesw(dash_ctx *ctx, cudaStream_t st, SwParams q) {
     using Cf = swk::Cfg<NB>;
     const int grid = ctx->num_sms;
-    if (ensure(ctx->sw_scr, sizeof(double) * (size_t)grid * Cf::NW * Cf::scr_doubles)) return DASH_E_CUDA;
+    if (ensure(ctx->sw_scr, sizeof(double) * (size_t)grid * (Cf::NW * Cf::scr_doubles + Cf::NT * 64))) return DASH_E_CUDA;
     q.scratch = (double *)ctx->sw_scr.p;
+    q.vtv_tiles = q.scratch + (size_t)grid * Cf::NW * Cf::scr_doubles;
     ensure_smem_attr(k_slicesw<NB>, Cf::smem_bytes());
     k_slicesw<NB><<<grid, Cf::NW * 32, Cf::smem_bytes(), st>>>(q);
     return cudaGetLastError() == cudaSuccess ? 0 : DASH_E_CUDA;
@@ -1286,7 +1287,7 @@ int run_slicesw(dash_ctx *ctx, cudaStream_t st, SwParams q) {
 
 int launch_slicesw(dash_ctx *ctx, cudaStream_t st, int RB, int M, const SliceParams &sp) {
     SwParams q{reinterpret_cast<const int32_t *>(sp.items), M, sp.row_ptr, sp.state_row, sp.is_new, sp.XV, sp.U,
-               sp.W, sp.C, sp.D, sp.vtv, nullptr, sp.err, sp.fallbacks, sp.R, sp.lam, sp.eps, sp.pass,
+               sp.W, sp.C, sp.D, sp.vtv, nullptr, nullptr, sp.err, sp.fallbacks, sp.R, sp.lam, sp.eps, sp.pass,
                sp.final_pass};
     PhaseScope ps(ctx, st, PH_SLICES);
     return RB <= 32 ? run_slicesw<4>(ctx, st, q) : run_slicesw<8>(ctx, st, q);
