@@ -333,7 +333,7 @@ struct AlsMmaSmem {
 // memory (long slices: a 4,000-row slice is 1,500 serial chunk passes for a single warp); the R x R
 // serial part is then repeated by every warp on identical inputs.
 template <int NB, int NW, bool COOP>
-__global__ void __launch_bounds__(NW * 32) k_als_polar_mma(const int64_t *__restrict__ row_ptr,
+__global__ void __launch_bounds__(NW * 32, NB == 2 ? 3 : 1) k_als_polar_mma(const int64_t *__restrict__ row_ptr,
                                                            const int32_t *__restrict__ list, int K,
                                                            const double *__restrict__ XV, const double *__restrict__ W,
                                                            const double *__restrict__ H, int R, double *__restrict__ T,
