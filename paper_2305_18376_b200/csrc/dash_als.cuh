@@ -683,7 +683,9 @@ int launch_als_polar_mma(dash_ctx *ctx, cudaStream_t st, const int64_t *row_ptr,
     // long slices first (longest first), then the short ones in tensor order
     std::vector<int32_t> ord;
     ord.reserve(K);
-    const int64_t long_rows = std::max<int64_t>(kAlsLongRows, 2 * (row_ptr_host[K] - row_ptr_host[0]) / std::max(K, 1));
+    static const char *long_env = getenv("DASH_ALS_LONG");  // A/B: rows above which a slice takes the cooperative variant
+    const int64_t long_rows = long_env ? atoll(long_env)
+                                       : std::max<int64_t>(kAlsLongRows, 2 * (row_ptr_host[K] - row_ptr_host[0]) / std::max(K, 1));
     for (int k = 0; k < K; ++k)
         if (row_ptr_host[k + 1] - row_ptr_host[k] > long_rows) ord.push_back(k);
     const int nlong = (int)ord.size();
@@ -697,11 +699,26 @@ int launch_als_polar_mma(dash_ctx *ctx, cudaStream_t st, const int64_t *row_ptr,
     // pageable source: the call returns once `ord` has been read into the driver's staging buffer
     cudaMemcpyAsync(list, ord.data(), sizeof(int32_t) * (size_t)K, cudaMemcpyHostToDevice, st);
     auto per_sm = [&](size_t smem) { return std::max<int>(1, (int)std::min<size_t>(8, (size_t)(227 * 1024) / (smem + 1024))); };
+    // the long-slice kernel runs beside the short-slice one (disjoint slices and rows): both end in a
+    // low-occupancy tail that the other can fill
+    bool forked = false;
     if (nlong > 0) {
         const size_t smem = AlsMmaSmem<NB>::bytes(NW, true);
         ensure_smem_attr(k_als_polar_mma<NB, NW, true>, smem);
-        k_als_polar_mma<NB, NW, true><<<std::min(nlong, ctx->num_sms * per_sm(smem)), NW * 32, smem, st>>>(
+        cudaStream_t ls = st;
+        if (K > nlong) {
+            if (!ctx->aux_stream && (cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking) != cudaSuccess ||
+                                     cudaEventCreateWithFlags(&ctx->aux_fork, cudaEventDisableTiming) != cudaSuccess ||
+                                     cudaEventCreateWithFlags(&ctx->aux_join, cudaEventDisableTiming) != cudaSuccess))
+                return DASH_E_CUDA;
+            cudaEventRecord(ctx->aux_fork, st);
+            cudaStreamWaitEvent(ctx->aux_stream, ctx->aux_fork, 0);
+            ls = ctx->aux_stream;
+            forked = true;
+        }
+        k_als_polar_mma<NB, NW, true><<<std::min(nlong, ctx->num_sms * per_sm(smem)), NW * 32, smem, ls>>>(
             row_ptr, list, nlong, XV, W, H, R, T, Q, yv, ctx->err);
+        if (forked) cudaEventRecord(ctx->aux_join, ls);
     }
     if (K > nlong) {
         const size_t smem = AlsMmaSmem<NB>::bytes(NW, false);
@@ -711,6 +728,7 @@ int launch_als_polar_mma(dash_ctx *ctx, cudaStream_t st, const int64_t *row_ptr,
                                           NW * 32, smem, st>>>(row_ptr, list + nlong, ns, XV, W, H, R, T, Q, yv,
                                                                ctx->err);
     }
+    if (forked) cudaStreamWaitEvent(st, ctx->aux_join, 0);
     return cudaGetLastError() == cudaSuccess ? 0 : DASH_E_CUDA;
 }
 

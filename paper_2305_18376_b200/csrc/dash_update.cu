@@ -997,6 +997,9 @@ struct dash_ctx {
         bool used = false;
     } pset_alt;
     cudaEvent_t pset_free = nullptr, plan_ev = nullptr;
+    // second stream + fork / join events for independent kernel pairs (ALS polar: long || short slices)
+    cudaStream_t aux_stream = nullptr;
+    cudaEvent_t aux_fork = nullptr, aux_join = nullptr;
     bool pset_used = false, side_plan = false;
     int cur_pass = 0;
     int last_launches = 0;
@@ -2143,6 +2146,9 @@ void dash_ctx_destroy(dash_ctx *ctx) {
         if (m.done) cudaEventDestroy(m.done);
     }
     if (ctx->meta_stream) cudaStreamDestroy(ctx->meta_stream);
+    if (ctx->aux_stream) cudaStreamDestroy(ctx->aux_stream);
+    for (auto e : {ctx->aux_fork, ctx->aux_join})
+        if (e) cudaEventDestroy(e);
     for (auto e : {ctx->plan_ev, ctx->pset_free, ctx->pset_alt.free_ev})
         if (e) cudaEventDestroy(e);
     for (auto *b : {&ctx->pset_alt.smeta, &ctx->pset_alt.plan_hist, &ctx->pset_alt.tflag})
