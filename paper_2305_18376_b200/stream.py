@@ -181,7 +181,7 @@ def _gather_plan(plan, row_ptr, out, on_chunk=None):
     share's copy."""
     M = len(row_ptr) - 1
     N = int(row_ptr[M])
-    T = min(8, os.cpu_count() or 1)
+    T = min(int(os.environ.get("DASH_GATHER_THREADS", "8")), os.cpu_count() or 1)
     shares = 1 if N * out.shape[1] < (1 << 22) else 4
     cut = np.searchsorted(row_ptr, np.linspace(0, N, shares + 1).astype(np.int64))
     cut[0], cut[-1] = 0, M
