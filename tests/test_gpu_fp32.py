@@ -143,3 +143,30 @@ def test_fp32_rejects_fp64_batch():
     X = torch.zeros((3, cfg.J), dtype=torch.float64, device="cuda")
     with pytest.raises(TypeError):
         st.update_packed(X, np.array([3]), np.array([0], dtype=np.int32), [])
+
+
+@pytest.mark.parametrize("name,kw", [
+    ("wide10", dict(K0=40, steps=2, new_slices=2)),            # J = 1,024: k_row_err_mma_wide on float X / U
+    ("wide64", dict(K0=24, steps=1, new_slices=2, J=520)),     # R = 64, 5 column chunks of 128, the last one short
+])
+def test_fp32_local_error_at_wide_j(name, kw):
+    """local_error in the FP32 data mode where V does not fit in shared memory (chunked DMMA kernel)."""
+    from paper_2305_18376_b200 import workloads as wl
+    from paper_2305_18376_b200.evaluate import local_error
+    from paper_2305_18376_b200.stream import StreamState
+    cfg = wl.scaled(wl.CONFIGS[name], **kw)
+    stream = wl.make_stream(cfg)
+    ps = wl.planted_state(stream)
+    gpu = StreamState.from_arrays(ps, dtype=torch.float32)
+    cpu = _oracle(ps, 1)
+    for bt in stream.batches():
+        res = gpu.update(bt)
+        rb = _round_batch(bt)
+        ref = cpu.update(rb)
+        items = [(sid, rows) for sid, rows, _ in bt.items()]
+        te, per = local_error(items, res.u_new, gpu)
+        W_rows = {sid: cpu.W[cpu.row_of(sid)] for sid, _ in items}
+        te_o, per_o = orc.local_error([(sid, rows) for sid, rows, _ in rb.items()], ref["u_new"], W_rows, cpu.V)
+        assert abs(te - te_o) <= TOL_ROUNDED * abs(te_o)
+        ids = [s for s, _ in items]
+        assert rel(np.array([per[s] for s in ids]), np.array([per_o[s] for s in ids])) < TOL_ROUNDED
